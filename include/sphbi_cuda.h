@@ -1,0 +1,155 @@
+/* sphbi_cuda.h -- C-ABI of the B200 (sm_100a) analytic SPH boundary-integral
+ * evaluator (libsphbi_cuda.so). Plain pointers and sizes only.
+ *
+ * The reference (arXiv 2507.21686, /root/reference/proj) is a header-only
+ * C++20 library with no FFI; its hot-path entry points are C++ functions in
+ * namespace sphbi. Each C entry point below states which reference interface
+ * it replaces; the C++ drop-in headers under include/sphbi/ call these.
+ *
+ *   sphbi_kernel_validate   <- sphbi::table1_terms            triangle_integrator.hpp:111-152
+ *   sphbi_integrate_pairs   <- sphbi::integrate_triangle      triangle_integrator.hpp:808-822
+ *                              sphbi::integrate_triangle_bases triangle_integrator.hpp:828-846
+ *   sphbi_integrate_regions <- sphbi::detail::region_* / integrate_stub / _sector /
+ *                              _segment / _wedge / _triangle2 / _triangle3 /
+ *                              detail::integrate_normalized   triangle_integrator.hpp:335-674, 727-802
+ *   sphbi_evaluate          <- SPEC.md:479 "evaluate(query points, h, mesh, field ...)"
+ *                              (specified, never shipped) + the SPH-demo neighbour
+ *                              search of SPEC.md:711 (uniform grid, AABB prefilter,
+ *                              exact distance test)
+ *   sphbi_read_counters     <- sphbi::branch_counters / reset_branch_counters
+ *                              triangle_integrator.hpp:158-185
+ *
+ * Error convention: every call returns a sphbi_status; nothing throws across
+ * the ABI. The C++ wrappers map statuses back onto the reference's exception
+ * types (std::domain_error, std::invalid_argument, sphbi::UnsupportedForm,
+ * sphbi::SingularInput, std::logic_error).
+ */
+#ifndef SPHBI_CUDA_H
+#define SPHBI_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHBI_MAX_COEFFICIENTS 17 /* kMaxKernelDegree (16) + 1, special_functions.hpp:52 */
+#define SPHBI_NUM_COUNTERS 19     /* BranchCounters fields, triangle_integrator.hpp:158-178 */
+
+typedef enum sphbi_status {
+  SPHBI_OK = 0,
+  SPHBI_ERR_DOMAIN = 1,           /* std::domain_error */
+  SPHBI_ERR_INVALID_ARGUMENT = 2, /* std::invalid_argument */
+  SPHBI_ERR_UNSUPPORTED_FORM = 3, /* sphbi::UnsupportedForm */
+  SPHBI_ERR_SINGULAR_INPUT = 4,   /* sphbi::SingularInput */
+  SPHBI_ERR_LOGIC = 5,            /* std::logic_error */
+  SPHBI_ERR_CUDA = 6,             /* CUDA runtime failure (see sphbi_last_error) */
+  SPHBI_ERR_NO_DEVICE = 7,        /* no sm_100 device visible: there is no CPU fallback */
+  SPHBI_ERR_OUT_OF_MEMORY = 8,
+  SPHBI_ERR_INTERNAL = 9
+} sphbi_status;
+
+typedef enum sphbi_memory {
+  SPHBI_MEM_HOST = 0,  /* pointers are host memory (pageable or pinned) */
+  SPHBI_MEM_DEVICE = 1 /* pointers are device memory on the context's GPU */
+} sphbi_memory;
+
+/* Compact polynomial kernel k(q) = sum_k b_k q^k, W = C2/h^2 k(r/h)
+ * (mirrors sphbi::PolyKernel, kernels.hpp:23-64; the support h is passed
+ * per call as in integrate_triangle). */
+typedef struct sphbi_kernel_desc {
+  int32_t n_coefficients; /* degree + 1; degree <= 16 or SPHBI_ERR_DOMAIN */
+  int32_t reserved;
+  double coefficients[SPHBI_MAX_COEFFICIENTS];
+  double normalization; /* C2 */
+} sphbi_kernel_desc;
+
+typedef struct sphbi_ctx sphbi_ctx;
+
+/* Per-call statistics of sphbi_evaluate (all on the device clock). */
+typedef struct sphbi_stats {
+  int64_t n_pairs;      /* (particle, triangle) pairs evaluated */
+  int64_t n_candidates; /* cell-list candidates tested by the exact predicate */
+  uint32_t status_bits; /* OR of per-pair status bits (see sphbi_status mapping) */
+  uint32_t reserved;
+  double ms_pairs;      /* pair finding (0 for explicit pair lists) */
+  double ms_eval;       /* elementary-integral kernel */
+  double ms_reduce;     /* per-particle reduction */
+} sphbi_stats;
+
+/* ---- context -------------------------------------------------------- */
+sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out);
+sphbi_status sphbi_ctx_destroy(sphbi_ctx* ctx);
+/* Use a caller-owned cudaStream_t (NULL = the context's own stream). */
+sphbi_status sphbi_ctx_set_stream(sphbi_ctx* ctx, void* cuda_stream);
+sphbi_status sphbi_ctx_synchronize(sphbi_ctx* ctx);
+/* Branch-route counters on the device (off by default: they cost atomics). */
+sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* ctx, int enable);
+sphbi_status sphbi_read_counters(sphbi_ctx* ctx, uint64_t out[SPHBI_NUM_COUNTERS], int reset);
+/* Message of the last failing call on this host thread. */
+const char* sphbi_last_error(void);
+/* Device kernel launches issued by this context so far (evidence counter). */
+int64_t sphbi_ctx_launch_count(sphbi_ctx* ctx);
+
+/* ---- kernel descriptor -------------------------------------------- */
+/* table1_terms' validation: degree > 16 -> SPHBI_ERR_DOMAIN. */
+sphbi_status sphbi_kernel_validate(const sphbi_kernel_desc* kernel);
+
+/* ---- single / batched pair integrals ---------------------------------- */
+/* For each k < n: the integral over triangle tri_xy[6k..6k+5] (x0,y0,x1,y1,x2,y2)
+ * of A * W(|x - q_k|) and its q-gradient, q_k = query_xy[2k..2k+1].
+ *   mode 0: A barycentric in values[3k..3k+2]; out[4k..4k+3] =
+ *           (value, grad_x, grad_y, imag_residual)          == integrate_triangle
+ *   mode 1: the three vertex bases; out[12k..12k+11] =
+ *           3 x (value, grad_x, grad_y, imag_residual)       == integrate_triangle_bases
+ * status_out (optional, n entries): per-pair status bits. h <= 0 -> SPHBI_ERR_DOMAIN. */
+sphbi_status sphbi_integrate_pairs(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
+                                   int64_t n, const double* query_xy, const double* tri_xy,
+                                   const double* values, int32_t mode, double* out,
+                                   uint32_t* status_out, sphbi_memory mem);
+
+/* ---- region-level entry points (normalized frame, test surface) -------- */
+typedef enum sphbi_region_kind {
+  SPHBI_REGION_DISC = 0,       /* args: l                          (region_disc)   */
+  SPHBI_REGION_SECTOR = 1,     /* args: v1x v1y v2x v2y l          (region_sector) */
+  SPHBI_REGION_SEGMENT = 2,    /* args: t0x t0y t1x t1y kx ky      (region_segment)*/
+  SPHBI_REGION_STUB = 3,       /* args: v1x v1y v2x v2y            (region_stub)   */
+  SPHBI_REGION_WEDGE = 4,      /* args: n0 n1 n2 (6)               (region_wedge)  */
+  SPHBI_REGION_T2 = 5,         /* args: a b c (6)                  (region_t2)     */
+  SPHBI_REGION_T3 = 6,         /* args: a b c (6)                  (region_t3)     */
+  SPHBI_REGION_NORMALIZED = 7  /* args: v0 v1 v2 (6)               (integrate_normalized) */
+} sphbi_region_kind;
+/* For each k < n: region kind[k] with args[8k..8k+7] evaluated against the
+ * reference triangle ref_xy[6k..6k+5] (un-normalized basis triple, h = 1):
+ * out[9k..9k+8] = (value_i, grad_x_i, grad_y_i) for i = 0,1,2 (real parts).
+ * Host memory. */
+sphbi_status sphbi_integrate_regions(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, int64_t n,
+                                     const int32_t* kind, const double* args,
+                                     const double* ref_xy, double* out, uint32_t* status_out);
+
+/* ---- scene evaluation (the data-parallel hot path) ---------------------- */
+/* Per-particle sums over every (particle i, triangle t) pair with
+ * d(p_i, closed triangle t) < h:
+ *   out_value[i]   = sum_t integrate_triangle(p_i, h, T_t, A_t).value
+ *   out_grad[2i+c] = sum_t ... .gradient[c]
+ * summed in ascending triangle id. tri_values NULL means A == 1.
+ * Pairing: n_pairs < 0 -> device cell list (uniform grid of cell size h,
+ * triangles binned by their h-expanded AABB, particles sorted by cell,
+ * exact predicate). n_pairs >= 0 -> the explicit list
+ * (pair_particle[k], pair_triangle[k]); any order, duplicates allowed.
+ * Outputs may be NULL. pair_list_out (optional, device memory only when
+ * mem == SPHBI_MEM_DEVICE): receives the found pairs as int64 (particle,
+ * triangle) interleaved, sorted, when its capacity *pair_list_capacity
+ * suffices; *pair_list_capacity is set to the pair count. */
+sphbi_status sphbi_evaluate(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
+                            int64_t n_particles, const double* particle_xy, int64_t n_triangles,
+                            const double* tri_xy, const double* tri_values, int64_t n_pairs,
+                            const int64_t* pair_particle, const int64_t* pair_triangle,
+                            double* out_value, double* out_grad, int64_t* pair_list_out,
+                            int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPHBI_CUDA_H */

@@ -1,0 +1,1045 @@
+// sphbi_core.cuh -- the per-(particle, triangle) analytic boundary integral,
+// written once as __host__ __device__ FP64 code for the sm_100a kernels.
+//
+// What it computes (reference: /root/reference/proj/include/sphbi/
+// triangle_integrator.hpp:808-822 integrate_triangle and everything below
+// it): the area integral over a triangle of A(x) W(|x - q|) and its gradient
+// with respect to the query point q, for a compact polynomial kernel
+// W = C2/h^2 k(r/h), k(q) = sum_k b_k q^k, and a barycentric-linear field A.
+//
+// How it differs from the reference (B200-first, same results):
+//   * Geometry (canonical order, normalization, dispatch by vertices inside,
+//     wedge / t2 / t3 decomposition, stub / segment / sector / disc regions)
+//     replicates the reference's IEEE double operation order exactly (this
+//     file must be compiled with -fmad=false), including std::hypot's
+//     rounding (glibc_hypot), so every branch decision matches bit for bit.
+//   * Elementary integrals are evaluated in REAL arithmetic. On this path the
+//     reference's complex antiderivatives only ever carry an x-independent
+//     imaginary constant; their real parts are
+//        Re sqrt_power_antiderivative(n,1,D,x) = I_n(x;D)
+//                                 = int_D^x t^(n-1) sqrt(t^2-D^2) dt,
+//     which obeys the forward-stable, positive-term recurrence
+//        I_n = (x^(n-2) R^3 + (n-2) D^2 I_(n-2)) / (n+1),  R = sqrt(x^2-D^2),
+//     and likewise P_k = int x^k/R (special_functions.hpp:398-410). One pass
+//     over n per radial bound replaces the reference's per-slot 2F1 anchors
+//     (special_functions.hpp:246-300, 424-501).
+//   * The table1_terms slot sums (triangle_integrator.hpp:111-152, 274-290)
+//     are regrouped per kernel coefficient into polynomials in the radial
+//     bound and chain-weighted sums, evaluated with double-double Horner /
+//     Dot2 accumulation in place of the reference's long double.
+//   * Region results are not rounded to per-region basis triples. Instead the
+//     nine tau-channel sums of each region are rotated back to the particle
+//     frame (tau' = M tau, g = M^T g') and accumulated per pair in
+//     double-double; the three vertex bases (or any field) are formed once
+//     at the end from the exact barycentric plane of the triangle.
+#pragma once
+
+#include "sphbi_math.cuh"
+
+namespace sphbi_dev {
+
+// ---------------------------------------------------------------------------
+// kernel constants (the device form of KernelTermTable)
+// ---------------------------------------------------------------------------
+// With w_k = -k b_k (rounded exactly as table1_terms does, :139) the slot
+// sums of one region collapse to
+//   Pv(x) = sum_k b_k/(k+2) x^(k+2)      Qv(x) = sum_k b_k/(k+3) x^(k+3)
+//   Pg(x) = sum_k w_k/(2(k+2)) x^(k+2)   Tg(x) = sum_k w_k/(2k) x^k
+//   Rg(x) = sum_k w_k/(k+1) x^(k+1)
+// plus chain sums over P and I weighted by the same coefficients.
+struct KernelConsts {
+  int deg;
+  int pad;
+  double c2;       // normalization C2
+  double b[kMaxKernelDegree + 1];
+  double wh[kMaxKernelDegree + 1];   // w_k / 2 (exact halving)
+  dd pv[kMaxKernelDegree + 1];
+  dd qv[kMaxKernelDegree + 1];
+  dd pg[kMaxKernelDegree + 1];
+  dd tg[kMaxKernelDegree + 1];
+  dd rg[kMaxKernelDegree + 1];
+  dd pv1, qv1, pg1, rg1;             // the polynomials at x = 1
+};
+
+// Exact quotient of a double by a small positive integer, as a dd.
+inline dd dd_div_int(double a, int m) {
+  const double hi = a / m;
+  const double rem = fma(-hi, (double)m, a);  // exact
+  return dd{hi, rem / m};
+}
+
+// Host-side construction; returns false when the degree exceeds the
+// reference's kMaxKernelDegree (table1_terms throws std::domain_error, :112).
+inline bool build_kernel_consts(const double* coef, int ncoef, double c2, KernelConsts* K) {
+  const int deg = ncoef - 1;
+  if (deg > kMaxKernelDegree || deg < 0) return false;
+  *K = KernelConsts{};
+  K->deg = deg;
+  K->c2 = c2;
+  for (int k = 0; k <= deg; ++k) {
+    const double bk = coef[k];
+    const double w = -static_cast<double>(k) * bk;  // table1_terms:139
+    K->b[k] = bk;
+    K->wh[k] = w / 2.0;
+    K->pv[k] = dd_div_int(bk, k + 2);
+    K->qv[k] = dd_div_int(bk, k + 3);
+    K->pg[k] = dd_div_int(w / 2.0, k + 2);
+    K->tg[k] = k >= 1 ? dd_div_int(w / 2.0, k) : dd{0.0, 0.0};
+    K->rg[k] = dd_div_int(w, k + 1);
+  }
+  dd s[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  for (int k = 0; k <= deg; ++k) {
+    s[0] = dd_add(s[0], K->pv[k]);
+    s[1] = dd_add(s[1], K->qv[k]);
+    s[2] = dd_add(s[2], K->pg[k]);
+    s[3] = dd_add(s[3], K->rg[k]);
+  }
+  K->pv1 = s[0];
+  K->qv1 = s[1];
+  K->pg1 = s[2];
+  K->rg1 = s[3];
+  return true;
+}
+
+// sum_{k=0}^{deg} c_k x^(k+off) by double-double Horner.
+SPHBI_HD dd poly_dd(const dd* c, int deg, double x, int off) {
+  dd acc = c[deg];
+  for (int k = deg - 1; k >= 0; --k) acc = dd_add(dd_mul_d(acc, x), c[k]);
+  for (int j = 0; j < off; ++j) acc = dd_mul_d(acc, x);
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// branch counters (triangle_integrator.hpp:158-178), same order
+// ---------------------------------------------------------------------------
+enum Counter : int {
+  kDispatchDegenerate = 0,
+  kDispatchWedgeOutside,
+  kDispatchWedgeSingle,
+  kDispatchTwoInside,
+  kDispatchThreeInside,
+  kWedgeNoCrossingsDisc,
+  kWedgeNoCrossingsZero,
+  kWedgeSingleEdgeSegment,
+  kWedgeLoneTouch,
+  kWedgeGeneral,
+  kWedgeReflexDisc,
+  kWedgeCapSubtracted,
+  kStubDirect,
+  kStubSplit,
+  kStubDegenerate,
+  kSegmentGeneral,
+  kSegmentHalfDisc,
+  kSegmentFullDisc,
+  kSegmentEmpty,
+  kNumCounters
+};
+
+// status bits: the reference's exception classes (special_functions.hpp:38-47)
+enum Status : unsigned {
+  kStatusOk = 0,
+  kStatusDomain = 1u,       // std::domain_error
+  kStatusInvalid = 2u,      // std::invalid_argument
+  kStatusUnsupported = 4u,  // UnsupportedForm
+  kStatusLogic = 8u,        // std::logic_error
+  kStatusStack = 16u,       // device stub-split stack exhausted (no reference analogue)
+};
+
+// ---------------------------------------------------------------------------
+// geometry, replicating geometry.hpp with identical IEEE op order
+// ---------------------------------------------------------------------------
+struct P2 {
+  double x, y;
+};
+SPHBI_HD P2 p_sub(P2 a, P2 b) { return P2{a.x - b.x, a.y - b.y}; }
+SPHBI_HD double p_dot(P2 a, P2 b) { return a.x * b.x + a.y * b.y; }
+SPHBI_HD double p_cross(P2 a, P2 b) { return a.x * b.y - a.y * b.x; }
+SPHBI_HD double p_norm2(P2 a) { return p_dot(a, a); }
+SPHBI_HD double p_norm(P2 a) { return glibc_hypot(a.x, a.y); }
+SPHBI_HD double signed_area(P2 a, P2 b, P2 c) {
+  return ((b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x)) / 2.0;
+}
+// geometry.hpp:177-185
+SPHBI_HD bool point_in_triangle(P2 p, P2 v0, P2 v1, P2 v2) {
+  const double total = signed_area(v0, v1, v2);
+  if (fabs(total) < kGeomEps) return false;
+  const double sg = total > 0 ? 1.0 : -1.0;
+  const double s0 = signed_area(v0, v1, p);
+  const double s1 = signed_area(v1, v2, p);
+  const double s2 = signed_area(v2, v0, p);
+  return sg * s0 >= -kGeomEps && sg * s1 >= -kGeomEps && sg * s2 >= -kGeomEps;
+}
+
+// Orthonormal region frame (rows), triangle_integrator.hpp:193-213.
+struct Frame {
+  double m00, m01, m10, m11;
+};
+
+// ---------------------------------------------------------------------------
+// accumulation of region results in the particle (normalized) frame
+// ---------------------------------------------------------------------------
+// S9: the nine channel sums of one region in its own frame:
+//   v[tau]   = sum_terms(channel 0)  weight * slot
+//   gx[tau]  = ... channel 1, gy[tau] = ... channel 2,   tau = 1, 2, 3
+struct S9 {
+  dd v1, v2, v3, gx1, gx2, gx3, gy1, gy2, gy3;
+};
+
+struct PairAcc {
+  dd v1, v2, v3;           // value:  V . (t1, t2) + V3 t3
+  dd g11, g12, g21, g22;   // gradient tensor G (row: component, col: tau)
+  dd g13, g23;             // gradient vector part (tau3)
+};
+
+SPHBI_HD void acc_zero(PairAcc& a) {
+  const dd z{0.0, 0.0};
+  a.v1 = a.v2 = a.v3 = z;
+  a.g11 = a.g12 = a.g21 = a.g22 = a.g13 = a.g23 = z;
+}
+
+SPHBI_HD dd dd_scale(dd a, double s) { return s == 1.0 ? a : (s == -1.0 ? dd_neg(a) : dd_mul_d(a, s)); }
+
+// acc += sign * (M^T S M) (see header comment): tau' = M tau; g = M^T g'.
+SPHBI_HD void acc_add_region(PairAcc& a, const S9& S, const Frame& M, double sign) {
+  // value covector
+  const dd v1 = dd_add(dd_mul_d(S.v1, M.m00), dd_mul_d(S.v2, M.m10));
+  const dd v2 = dd_add(dd_mul_d(S.v1, M.m01), dd_mul_d(S.v2, M.m11));
+  // A = M^T G'
+  const dd a00 = dd_add(dd_mul_d(S.gx1, M.m00), dd_mul_d(S.gy1, M.m10));
+  const dd a01 = dd_add(dd_mul_d(S.gx2, M.m00), dd_mul_d(S.gy2, M.m10));
+  const dd a10 = dd_add(dd_mul_d(S.gx1, M.m01), dd_mul_d(S.gy1, M.m11));
+  const dd a11 = dd_add(dd_mul_d(S.gx2, M.m01), dd_mul_d(S.gy2, M.m11));
+  // G = A M
+  const dd g00 = dd_add(dd_mul_d(a00, M.m00), dd_mul_d(a01, M.m10));
+  const dd g01 = dd_add(dd_mul_d(a00, M.m01), dd_mul_d(a01, M.m11));
+  const dd g10 = dd_add(dd_mul_d(a10, M.m00), dd_mul_d(a11, M.m10));
+  const dd g11 = dd_add(dd_mul_d(a10, M.m01), dd_mul_d(a11, M.m11));
+  const dd g3x = dd_add(dd_mul_d(S.gx3, M.m00), dd_mul_d(S.gy3, M.m10));
+  const dd g3y = dd_add(dd_mul_d(S.gx3, M.m01), dd_mul_d(S.gy3, M.m11));
+  a.v1 = dd_add(a.v1, dd_scale(v1, sign));
+  a.v2 = dd_add(a.v2, dd_scale(v2, sign));
+  a.v3 = dd_add(a.v3, dd_scale(S.v3, sign));
+  a.g11 = dd_add(a.g11, dd_scale(g00, sign));
+  a.g12 = dd_add(a.g12, dd_scale(g01, sign));
+  a.g21 = dd_add(a.g21, dd_scale(g10, sign));
+  a.g22 = dd_add(a.g22, dd_scale(g11, sign));
+  a.g13 = dd_add(a.g13, dd_scale(g3x, sign));
+  a.g23 = dd_add(a.g23, dd_scale(g3y, sign));
+}
+
+// ---------------------------------------------------------------------------
+// elementary region sums (all in the region's own canonical frame)
+// ---------------------------------------------------------------------------
+
+// Cone / sector theta in [0, gamma], r in [0, L] (elementary_regions.hpp:65-83):
+//   p_n = gamma B_n, c_a = sin(a g)/a B_n, s_a = (1-cos(a g))/a B_n,
+//   B_n = L^(n+1)/(n+1).
+SPHBI_HD void cone_sums(const KernelConsts& K, double gamma, dd Pv, dd Qv, dd Pg, dd Rg, S9& S) {
+  double sg, cg;
+  dsincos(gamma, &sg, &cg);
+  const double sh = sin(0.5 * gamma);
+  const double omc = 2.0 * sh * sh;  // 1 - cos(gamma), cancellation-free
+  const dd sgcg = two_prod(sg, cg);  // sin(2g)/2
+  const dd ggp = dd_add(dd_make(gamma), sgcg);
+  const dd ggm = dd_sub(dd_make(gamma), sgcg);
+  const double s2 = sg * sg;  // (1 - cos 2g)/2
+  S.v3 = dd_mul_d(Pv, gamma);
+  S.v1 = dd_mul_d(Qv, sg);
+  S.v2 = dd_mul_d(Qv, omc);
+  S.gx1 = dd_mul(Pg, ggp);
+  S.gx2 = dd_mul_d(Pg, s2);
+  S.gx3 = dd_mul_d(Rg, sg);
+  S.gy1 = S.gx2;
+  S.gy2 = dd_mul(Pg, ggm);
+  S.gy3 = dd_mul_d(Rg, omc);
+}
+
+// Radial chains at bound x for chord distance D (x >= D > 0):
+//   P~_0 = log((x+R)/D), P~_1 = R, P~_m = (x^(m-1) R + (m-1) D^2 P~_(m-2)) / m
+//   I_1 = (x R - D^2 P~_0)/2 (series near x = D), I_2 = R^3/3,
+//   I_m = (x^(m-2) R^3 + (m-2) D^2 I_(m-2)) / (m+1)
+// accumulated into
+//   sPv = sum_k b_k/(k+2) P~_(k+1)    sPg = sum_k w_k/(2(k+2)) P~_(k+1)
+//   sIv = sum_k b_k I_(k+2)           sIg = sum_k w_k/2 I_k
+// (P~ differs from P by the constant -log D on the even chain, which cancels
+// in every bound difference / is absent from the segment's definite form.)
+struct ChainSums {
+  dd sPv, sPg, sIv, sIg;
+  double R;
+};
+
+// Seeds of the radial chains at bound x (x >= D > 0), all in dd: the
+// monomial-basis sums downstream cancel by up to ~1e3..1e6 near the support
+// edge, so every seed must be good to ~1e-20 relative (the reference's
+// long double level), not just to double precision.
+//   R = sqrt((x-D)(x+D)),  P~_0 = log((x+R)/D) = asinh(R/D),
+//   I_1 = (x R - D^2 P~_0)/2 = D^2/2 (s sqrt(1+s^2) - asinh s), s = R/D.
+struct ChainSeeds {
+  dd R, p0, i1;
+};
+
+SPHBI_HD void chain_seeds(double x, double D, ChainSeeds& S) {
+  const dd xm = two_sum(x, -D);
+  const dd xp = two_sum(x, D);
+  S.R = dd_sqrt(dd_mul(xm, xp));
+  const double s = S.R.hi / D;
+  if (s < 0.01) {
+    // series: f(s)/s^3 = 2/3 - s^2/5 + 3/28 s^4 - 5/72 s^6 + ...
+    const dd sdd = dd_div(S.R, dd_make(D));
+    const double s2 = sdd.hi * sdd.hi;
+    double t = -0.024643841911764705882;
+    t = fma(t, s2, 0.030078125);
+    t = fma(t, s2, -0.037860576923076923077);
+    t = fma(t, s2, 0.049715909090909090909);
+    t = fma(t, s2, -0.069444444444444444444);
+    t = fma(t, s2, 0.10714285714285714286);
+    t = t * s2 * s2 - 0.2 * s2;  // |.| <= 2e-5: double is ample here
+    const dd twothirds{0.66666666666666662966, 3.7007434154171882e-17};
+    const dd f_s3 = dd_add_d(twothirds, t);
+    const dd s3 = dd_mul(dd_mul(sdd, sdd), sdd);
+    S.i1 = dd_mul(dd_mul(f_s3, s3), dd_mul_d(two_prod(D, D), 0.5));
+    // P~_0 = asinh(s) = s - s^3/6 + 3/40 s^5 - 5/112 s^7 + ...
+    double a = -5.0 / 112.0;
+    a = fma(a, s2, 3.0 / 40.0);
+    a = fma(a, s2, -1.0 / 6.0);
+    S.p0 = dd_add_d(sdd, a * s2 * sdd.hi);
+  } else {
+    S.p0 = dd_log(dd_div(dd_add_d(S.R, x), dd_make(D)));
+    const dd xr = dd_mul_d(S.R, x);
+    const dd d2p0 = dd_mul(two_prod(D, D), S.p0);
+    const dd diff = dd_sub(xr, d2p0);
+    S.i1 = dd{0.5 * diff.hi, 0.5 * diff.lo};
+  }
+}
+
+SPHBI_HD void radial_chains(const KernelConsts& K, double x, double D, ChainSums& C) {
+  // The chain values feed sums whose monomial coefficients cancel heavily
+  // (the kernel polynomial in the power basis), so seeds and recurrences
+  // all run in double-double.
+  const int N = K.deg;
+  ChainSeeds sd;
+  chain_seeds(x, D, sd);
+  const dd D2 = two_prod(D, D);
+  const dd R3 = dd_mul(dd_mul(sd.R, sd.R), sd.R);
+  dd aPv{0, 0}, aPg{0, 0}, aIv{0, 0}, aIg{0, 0};
+  dd pm2 = sd.p0, pm1 = sd.R;
+  dd im2{0.0, 0.0}, im1 = sd.i1;
+  aPv = dd_mul(K.pv[0], sd.R);
+  if (N >= 1) aIg = dd_mul_d(im1, K.wh[1]);
+  dd xpm2 = dd_make(1.0), xpm1 = dd_make(x);
+  for (int m = 2; m <= N + 2; ++m) {
+    const dd pm = dd_div_d_small(dd_add(dd_mul(xpm1, sd.R), dd_mul_d(dd_mul(D2, pm2), (double)(m - 1))), m);
+    const dd im = dd_div_d_small(dd_add(dd_mul(xpm2, R3), dd_mul_d(dd_mul(D2, im2), (double)(m - 2))), m + 1);
+    if (m <= N + 1) {
+      aPv = dd_add(aPv, dd_mul(K.pv[m - 1], pm));
+      aPg = dd_add(aPg, dd_mul(K.pg[m - 1], pm));
+    }
+    aIv = dd_add(aIv, dd_mul_d(im, K.b[m - 2]));
+    if (m <= N) aIg = dd_add(aIg, dd_mul_d(im, K.wh[m]));
+    pm2 = pm1;
+    pm1 = pm;
+    im2 = im1;
+    im1 = im;
+    xpm2 = xpm1;
+    xpm1 = dd_mul_d(xpm1, x);
+  }
+  C.sPv = aPv;
+  C.sPg = aPg;
+  C.sIv = aIv;
+  C.sIg = aIg;
+  C.R = sd.R.hi;
+}
+
+// Stub radial window at one bound x (elementary_regions.hpp:175-232), with
+// X_n = x^(n+1)/(n+1), as = asin(D/x):
+//   p_n  = (as - beta) X_n + D P~_n/(n+1)
+//   c1_n = cb D X_(n-1) - sb I_n           s1_n = X_n - cb I_n - sb D X_(n-1)
+//   c2_n = c2b D I_(n-1) - s2b/2 E_n       s2_n = X_n/2 - c2b/2 E_n - s2b D I_(n-1)
+//   E_n = X_n - 2 D^2 X_(n-2)
+SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double beta, double cb,
+                              double sb, double c2b, double s2b, S9& S) {
+  ChainSums C;
+  radial_chains(K, x, D, C);
+  // asin_ratio (special_functions.hpp:150-155)
+  double as;
+  if (D <= 0.7 * x)
+    as = asin(D / x);
+  else
+    as = (kHalfPiHi - asin(C.R / x)) + kHalfPiLo;
+  const double amb = as - beta;
+  const int N = K.deg;
+  const dd Pv = poly_dd(K.pv, N, x, 2);
+  const dd Qv = poly_dd(K.qv, N, x, 3);
+  const dd Pg = poly_dd(K.pg, N, x, 2);
+  const dd Tg = poly_dd(K.tg, N, x, 0);
+  const dd Rg = poly_dd(K.rg, N, x, 1);
+  const double cbD = cb * D, sbD = sb * D, c2bD = c2b * D, s2bD = s2b * D;
+  const dd E = dd_sub(Pg, dd_mul_d(Tg, 2.0 * D * D));
+  const dd pcore_v = dd_add(dd_mul_d(Pv, amb), dd_mul_d(C.sPv, D));
+  const dd pcore_g = dd_add(dd_mul_d(Pg, amb), dd_mul_d(C.sPg, D));
+  S.v3 = pcore_v;
+  S.v1 = dd_sub(dd_mul_d(Pv, cbD), dd_mul_d(C.sIv, sb));
+  S.v2 = dd_sub(dd_sub(Qv, dd_mul_d(C.sIv, cb)), dd_mul_d(Pv, sbD));
+  const dd c2part = dd_sub(dd_mul_d(C.sIg, c2bD), dd_mul_d(E, 0.5 * s2b));
+  S.gx1 = dd_add(pcore_g, c2part);
+  S.gy2 = dd_sub(pcore_g, c2part);
+  S.gx2 = dd_sub(dd_sub(dd_mul_d(Pg, 0.5), dd_mul_d(E, 0.5 * c2b)), dd_mul_d(C.sIg, s2bD));
+  S.gy1 = S.gx2;
+  S.gx3 = dd_sub(dd_mul_d(Tg, 2.0 * cbD), dd_mul_d(C.sIg, 2.0 * sb));
+  S.gy3 = dd_sub(dd_sub(Rg, dd_mul_d(C.sIg, 2.0 * cb)), dd_mul_d(Tg, 2.0 * sbD));
+}
+
+SPHBI_HD void s9_sub(S9& a, const S9& b) {
+  a.v1 = dd_sub(a.v1, b.v1);
+  a.v2 = dd_sub(a.v2, b.v2);
+  a.v3 = dd_sub(a.v3, b.v3);
+  a.gx1 = dd_sub(a.gx1, b.gx1);
+  a.gx2 = dd_sub(a.gx2, b.gx2);
+  a.gx3 = dd_sub(a.gx3, b.gx3);
+  a.gy1 = dd_sub(a.gy1, b.gy1);
+  a.gy2 = dd_sub(a.gy2, b.gy2);
+  a.gy3 = dd_sub(a.gy3, b.gy3);
+}
+SPHBI_HD void s9_add(S9& a, const S9& b) {
+  a.v1 = dd_add(a.v1, b.v1);
+  a.v2 = dd_add(a.v2, b.v2);
+  a.v3 = dd_add(a.v3, b.v3);
+  a.gx1 = dd_add(a.gx1, b.gx1);
+  a.gx2 = dd_add(a.gx2, b.gx2);
+  a.gx3 = dd_add(a.gx3, b.gx3);
+  a.gy1 = dd_add(a.gy1, b.gy1);
+  a.gy2 = dd_add(a.gy2, b.gy2);
+  a.gy3 = dd_add(a.gy3, b.gy3);
+}
+
+// Circular segment {x >= d} of the unit disc, 0 < d < 1
+// (elementary_regions.hpp:130-167), with Q = P~(1) and J_n = I_n(1; d):
+//   p_n = 2/(n+1) (acos d - d Q_n), c1_n = 2 J_n, c2_n = 2 d J_(n-1), s = 0.
+SPHBI_HD void segment_sums(const KernelConsts& K, double d, S9& S) {
+  ChainSums C;
+  radial_chains(K, 1.0, d, C);
+  const double acd = d <= 0.7 ? acos(d) : asin(C.R);  // acos_ratio(d, 1)
+  const dd z{0.0, 0.0};
+  const dd av = dd_sub(dd_mul_d(K.pv1, 2.0 * acd), dd_mul_d(C.sPv, 2.0 * d));
+  const dd ag = dd_sub(dd_mul_d(K.pg1, 2.0 * acd), dd_mul_d(C.sPg, 2.0 * d));
+  const dd jg = dd_mul_d(C.sIg, 2.0 * d);
+  S.v3 = av;
+  S.v1 = dd_mul_d(C.sIv, 2.0);
+  S.v2 = z;
+  S.gx1 = dd_add(ag, jg);
+  S.gy2 = dd_sub(ag, jg);
+  S.gx2 = z;
+  S.gy1 = z;
+  S.gx3 = dd_mul_d(C.sIg, 4.0);
+  S.gy3 = z;
+}
+
+// ---------------------------------------------------------------------------
+// region evaluation context
+// ---------------------------------------------------------------------------
+struct RegionCtx {
+  const KernelConsts* K;
+  PairAcc acc;
+  unsigned status;
+  unsigned long long* counters;  // nullable: kNumCounters slots
+  int n_regions;                 // elementary region evaluations (work metric)
+};
+
+SPHBI_HD void bump(RegionCtx& c, int which) {
+  if (c.counters) {
+#if defined(__CUDA_ARCH__)
+    atomicAdd(c.counters + which, 1ull);
+#else
+    c.counters[which] += 1;
+#endif
+  }
+}
+
+// region_disc(1.0): full unit disc, identity frame (:335-347, :88-94).
+SPHBI_HD void region_disc(RegionCtx& c, double sign) {
+  const KernelConsts& K = *c.K;
+  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
+  const dd v3 = dd_mul(K.pv1, pi2);
+  const dd g = dd_mul(K.pg1, pi2);
+  c.acc.v3 = dd_add(c.acc.v3, dd_scale(v3, sign));
+  c.acc.g11 = dd_add(c.acc.g11, dd_scale(g, sign));
+  c.acc.g22 = dd_add(c.acc.g22, dd_scale(g, sign));
+  c.n_regions += 1;
+}
+
+// region_disc(l) for l < 1 (cone over [0, 2pi] of radius l): test surface.
+SPHBI_HD void region_disc_l(RegionCtx& c, double l, double sign) {
+  if (l >= 1.0) {
+    region_disc(c, sign);
+    return;
+  }
+  const KernelConsts& K = *c.K;
+  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
+  const dd v3 = dd_mul(poly_dd(K.pv, K.deg, l, 2), pi2);
+  const dd g = dd_mul(poly_dd(K.pg, K.deg, l, 2), pi2);
+  c.acc.v3 = dd_add(c.acc.v3, dd_scale(v3, sign));
+  c.acc.g11 = dd_add(c.acc.g11, dd_scale(g, sign));
+  c.acc.g22 = dd_add(c.acc.g22, dd_scale(g, sign));
+  c.n_regions += 1;
+}
+
+// Proper rotation taking v onto +x (:202-207).
+SPHBI_HD Frame rotation_taking_to_x(P2 v, RegionCtx& c) {
+  const double n = p_norm(v);
+  if (n < kGeomEps) c.status |= kStatusDomain;
+  return Frame{v.x / n, v.y / n, -v.y / n, v.x / n};
+}
+
+// region_sector(v1, v2, l) (:349-366); the hot path always passes l = 1.
+SPHBI_HD void region_sector(RegionCtx& c, P2 v1, P2 v2, double sign, double l = 1.0) {
+  Frame f = rotation_taking_to_x(v1, c);
+  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
+  if (w2.y < 0.0) {
+    f.m10 = -f.m10;
+    f.m11 = -f.m11;
+    w2.y = -w2.y;
+  }
+  const double gamma = atan2(w2.y, w2.x);
+  const KernelConsts& K = *c.K;
+  S9 S;
+  if (l >= 1.0) {
+    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+  } else {
+    const int N = K.deg;
+    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+              poly_dd(K.rg, N, l, 1), S);
+  }
+  acc_add_region(c.acc, S, f, sign);
+  c.n_regions += 1;
+}
+
+// region_segment(t0, t1, q_keep) (:369-423).
+SPHBI_HD void region_segment(RegionCtx& c, P2 t0, P2 t1, P2 q_keep, double sign) {
+  const P2 e = p_sub(t1, t0);
+  const double len = p_norm(e);
+  if (len < kGeomEps) {
+    c.status |= kStatusDomain;  // "chord endpoints coincide"
+    return;
+  }
+  P2 n{e.y / len, -e.x / len};
+  if (p_dot(p_sub(q_keep, t0), n) < 0.0) n = P2{-n.x, -n.y};
+  const double d = p_dot(t0, n);
+  if (d >= 1.0 - kGeomEps) {
+    bump(c, kSegmentEmpty);
+    return;
+  }
+  if (d <= -1.0 + kGeomEps) {
+    bump(c, kSegmentFullDisc);
+    region_disc(c, sign);
+    return;
+  }
+  const KernelConsts& K = *c.K;
+  if (fabs(d) < 1e-9) {
+    bump(c, kSegmentHalfDisc);
+    // half disc (elementary_regions.hpp:96-112): p = pi/(n+1), c_a = 2 sin(a pi/2)/a/(n+1)
+    const Frame f{n.x, n.y, -n.y, n.x};
+    const dd pi{kPiHi, kPiLo};
+    const dd z{0.0, 0.0};
+    S9 S;
+    S.v3 = dd_mul(K.pv1, pi);
+    S.v1 = dd_mul_d(K.qv1, 2.0);
+    S.v2 = z;
+    S.gx1 = dd_mul(K.pg1, pi);
+    S.gy2 = S.gx1;
+    S.gx2 = z;
+    S.gy1 = z;
+    S.gx3 = dd_mul_d(K.rg1, 2.0);
+    S.gy3 = z;
+    acc_add_region(c.acc, S, f, sign);
+    c.n_regions += 1;
+    return;
+  }
+  bump(c, kSegmentGeneral);
+  if (d < 0.0) {
+    // origin-side segment: whole disc minus the far-side complement
+    const P2 nc{-n.x, -n.y};
+    const Frame f{nc.x, nc.y, -nc.y, nc.x};
+    region_disc(c, sign);
+    S9 S;
+    segment_sums(K, -d, S);
+    acc_add_region(c.acc, S, f, -sign);
+    c.n_regions += 1;
+    return;
+  }
+  const Frame f{n.x, n.y, -n.y, n.x};
+  S9 S;
+  segment_sums(K, d, S);
+  acc_add_region(c.acc, S, f, sign);
+  c.n_regions += 1;
+}
+
+// Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
+SPHBI_HDNI void stub_direct(RegionCtx& c, P2 v1, P2 v2, double r1, double r2, double area2,
+                            P2 b, double sign) {
+  Frame f = rotation_taking_to_x(v1, c);
+  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
+  if (w2.y < 0.0) {
+    f.m10 = -f.m10;
+    f.m11 = -f.m11;
+    w2.y = -w2.y;
+  }
+  const double gamma = atan2(w2.y, w2.x);
+  const double D = fabs(area2) / p_norm(b);
+  const double l = fmin(r2, 1.0);
+  const double u = fmin(r1, 1.0);
+  const P2 cc = p_sub(v2, v1);
+  const double beta = atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
+  double lo = fmax(l, D);
+  if (lo - D <= 256.0 * kDblEps * D) lo = D;
+  const KernelConsts& K = *c.K;
+  const int N = K.deg;
+  S9 S;
+  if (l >= 1.0) {
+    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+  } else {
+    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+              poly_dd(K.rg, N, l, 1), S);
+  }
+  if (u > lo + kGeomEps) {
+    // stub_integral validation (elementary_regions.hpp:179-183)
+    if (!(beta >= 0.0 && beta < kHalfPiHi)) c.status |= kStatusDomain;
+    double sb, cb;
+    dsincos(beta, &sb, &cb);
+    const double s2b = 2.0 * sb * cb;
+    const double c2b = (cb - sb) * (cb + sb);
+    S9 hi, lo_s;
+    stub_bound_sums(K, u, D, beta, cb, sb, c2b, s2b, hi);
+    stub_bound_sums(K, lo, D, beta, cb, sb, c2b, s2b, lo_s);
+    s9_sub(hi, lo_s);
+    s9_add(S, hi);
+  }
+  acc_add_region(c.acc, S, f, sign);
+  c.n_regions += 1;
+}
+
+// region_stub(v1, v2) (:426-484): triangle (origin, v1, v2) clipped to the
+// disc; the perpendicular-foot split is unrolled with a small stack.
+SPHBI_HDNI void region_stub(RegionCtx& c, P2 v1_in, P2 v2_in, double sign) {
+  P2 st1[8], st2[8];
+  int top = 0;
+  st1[0] = v1_in;
+  st2[0] = v2_in;
+  top = 1;
+  while (top > 0) {
+    --top;
+    P2 v1 = st1[top], v2 = st2[top];
+    double r1 = p_norm(v1), r2 = p_norm(v2);
+    if (r1 < r2) {
+      const P2 tv = v1;
+      v1 = v2;
+      v2 = tv;
+      const double tr = r1;
+      r1 = r2;
+      r2 = tr;
+    }
+    const double area2 = p_cross(v1, v2);
+    if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
+      bump(c, kStubDegenerate);
+      continue;
+    }
+    const P2 b = p_sub(v1, v2);
+    const double dot_a = -(v2.x * b.x + v2.y * b.y);
+    if (dot_a <= kGeomEps) {
+      bump(c, kStubDirect);
+      stub_direct(c, v1, v2, r1, r2, area2, b, sign);
+      continue;
+    }
+    bump(c, kStubSplit);
+    const double t = dot_a / p_norm2(b);
+    const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
+    if (top + 2 > 8) {
+      c.status |= kStatusStack;
+      continue;
+    }
+    // reference order: stub(v1, foot) then stub(v2, foot)
+    st1[top] = v2;
+    st2[top] = foot;
+    ++top;
+    st1[top] = v1;
+    st2[top] = foot;
+    ++top;
+  }
+}
+
+// segment_circle_crossings (:494-509)
+struct Crossings {
+  int count;
+  P2 pts[2];
+};
+SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
+  Crossings out;
+  out.count = 0;
+  const P2 d = p_sub(q, p);
+  const double a = p_norm2(d);
+  if (a < kGeomEps * kGeomEps) return out;
+  const double b = 2.0 * p_dot(p, d);
+  const double cc = p_norm2(p) - 1.0;
+  const double disc = b * b - 4.0 * a * cc;
+  if (disc <= 0.0) return out;
+  const double rt = sqrt(disc);
+  const double lams[2] = {(-b - rt) / (2.0 * a), (-b + rt) / (2.0 * a)};
+  for (int i = 0; i < 2; ++i) {
+    const double lam = lams[i];
+    if (lam >= -1e-12 && lam <= 1.0 + 1e-12) {
+      out.pts[out.count] = P2{p.x + lam * d.x, p.y + lam * d.y};
+      out.count++;
+    }
+  }
+  return out;
+}
+
+// region_wedge (:514-603)
+SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
+  if (signed_area(n0, n1, n2) < 0.0) {
+    const P2 t = n1;
+    n1 = n2;
+    n2 = t;
+  }
+  if (fabs(signed_area(n0, n1, n2)) < kGeomEps) return;
+  Crossings x01 = segment_circle_crossings(n0, n1);
+  Crossings x02 = segment_circle_crossings(n0, n2);
+  Crossings x12 = segment_circle_crossings(n1, n2);
+  const P2 origin{0.0, 0.0};
+  const bool origin_inside = point_in_triangle(origin, n0, n1, n2);
+  if (x01.count == 0 && x02.count == 0 && x12.count == 0) {
+    if (origin_inside) {
+      bump(c, kWedgeNoCrossingsDisc);
+      region_disc(c, sign);
+      return;
+    }
+    bump(c, kWedgeNoCrossingsZero);
+    return;
+  }
+  const int crossing_edges = (x01.count > 0 ? 1 : 0) + (x02.count > 0 ? 1 : 0) +
+                             (x12.count > 0 ? 1 : 0);
+  if (crossing_edges == 1) {
+    P2 e0 = n0, e1 = n1, opp = n2;
+    int count = x01.count;
+    if (x02.count > 0) {
+      e0 = n0;
+      e1 = n2;
+      opp = n1;
+      count = x02.count;
+    } else if (x12.count > 0) {
+      e0 = n1;
+      e1 = n2;
+      opp = n0;
+      count = x12.count;
+    }
+    if (count == 2) {
+      bump(c, kWedgeSingleEdgeSegment);
+      region_segment(c, e0, e1, opp, sign);
+      return;
+    }
+    bump(c, kWedgeLoneTouch);
+    if (origin_inside) region_disc(c, sign);
+    return;
+  }
+  if (x01.count == 0 || x02.count == 0) {
+    if (x01.count > 0 && x12.count > 0) {
+      const P2 t0 = n0;
+      n0 = n1;
+      n1 = n2;
+      n2 = t0;
+    } else if (x02.count > 0 && x12.count > 0) {
+      const P2 t2 = n2;
+      n2 = n1;
+      n1 = n0;
+      n0 = t2;
+    }
+    if (signed_area(n0, n1, n2) < 0.0) {
+      const P2 t = n1;
+      n1 = n2;
+      n2 = t;
+    }
+    x01 = segment_circle_crossings(n0, n1);
+    x02 = segment_circle_crossings(n0, n2);
+    x12 = segment_circle_crossings(n1, n2);
+  }
+  bump(c, kWedgeGeneral);
+  // x01 / x02 could in principle lose their crossings after relabeling; the
+  // reference would then read points[-1] (UB). Flag instead of reading.
+  if (x01.count == 0 || x02.count == 0) {
+    c.status |= kStatusLogic;
+    return;
+  }
+  const P2 s1 = x01.pts[x01.count - 1];
+  const P2 s2 = x02.pts[x02.count - 1];
+  const double arc_orient = signed_area(origin, s1, s2);
+  if (fabs(arc_orient) > kGeomEps) {
+    if (arc_orient > 0.0) {
+      region_sector(c, s1, s2, sign);
+    } else {
+      bump(c, kWedgeReflexDisc);
+      region_sector(c, s1, s2, -sign);
+      region_disc(c, sign);
+    }
+  }
+  const double stub_a = signed_area(origin, n0, s1);
+  if (fabs(stub_a) > kGeomEps) region_stub(c, n0, s1, stub_a > 0.0 ? sign : -sign);
+  const double stub_b = signed_area(origin, s2, n0);
+  if (fabs(stub_b) > kGeomEps) region_stub(c, s2, n0, stub_b > 0.0 ? sign : -sign);
+  if (x12.count == 2) {
+    bump(c, kWedgeCapSubtracted);
+    const P2 mirror{n1.x + n2.x - n0.x, n1.y + n2.y - n0.y};
+    region_segment(c, n1, n2, mirror, -sign);
+  }
+}
+
+// region_t2 (:607-616)
+SPHBI_HD void region_t2(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
+  if (signed_area(a, b, cc) < 0.0) {
+    const P2 t = a;
+    a = b;
+    b = t;
+  }
+  const P2 u = p_sub(b, a);
+  const double len = p_norm(u);
+  const P2 x{a.x + 3.0 * u.x / len, a.y + 3.0 * u.y / len};
+  region_wedge(c, a, x, cc, sign);
+  region_wedge(c, b, x, cc, -sign);
+}
+
+// region_t3 (:620-632)
+SPHBI_HD void region_t3(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
+  if (signed_area(a, b, cc) < 0.0) {
+    const P2 t = b;
+    b = cc;
+    cc = t;
+  }
+  const P2 d1 = p_sub(b, a);
+  const P2 d2 = p_sub(cc, a);
+  const double l1 = p_norm(d1), l2 = p_norm(d2);
+  const P2 x1{a.x + 3.0 * d1.x / l1, a.y + 3.0 * d1.y / l1};
+  const P2 x2{a.x + 3.0 * d2.x / l2, a.y + 3.0 * d2.y / l2};
+  region_wedge(c, a, x1, x2, sign);
+  region_t2(c, b, cc, x1, -sign);
+  region_wedge(c, cc, x1, x2, -sign);
+}
+
+// integrate_normalized (:637-674). Returns false for the degenerate route.
+SPHBI_HD bool integrate_normalized(RegionCtx& c, const P2* v) {
+  if (fabs(signed_area(v[0], v[1], v[2])) < kGeomEps) {
+    bump(c, kDispatchDegenerate);
+    return false;
+  }
+  const double r[3] = {p_norm(v[0]), p_norm(v[1]), p_norm(v[2])};
+  int inside[3] = {0, 0, 0};
+  int inside_count = 0;
+  for (int i = 0; i < 3; ++i)
+    if (r[i] <= 1.0 + kOnCircleTol) inside[inside_count++] = i;
+  if (inside_count == 0) {
+    bump(c, kDispatchWedgeOutside);
+    int i0 = 0;
+    if (r[1] < r[i0]) i0 = 1;
+    if (r[2] < r[i0]) i0 = 2;
+    region_wedge(c, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
+    return true;
+  }
+  if (inside_count == 1) {
+    bump(c, kDispatchWedgeSingle);
+    const int i0 = inside[0];
+    region_wedge(c, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
+    return true;
+  }
+  if (inside_count == 2) {
+    bump(c, kDispatchTwoInside);
+    const int outside = 3 - inside[0] - inside[1];
+    region_t2(c, v[inside[0]], v[inside[1]], v[outside], 1.0);
+    return true;
+  }
+  bump(c, kDispatchThreeInside);
+  region_t3(c, v[0], v[1], v[2], 1.0);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// barycentric planes of the reference triangle (vertex hat fields), in dd
+// ---------------------------------------------------------------------------
+struct HatPlanes {
+  dd t1[3], t2[3], t3[3];
+};
+
+// assemble_region's plane solve (:255-269), done once per pair in the
+// particle frame (the rotated frames only rotate (t1, t2) and keep t3).
+SPHBI_HD bool hat_planes(const P2* v, HatPlanes& H) {
+  const dd dy12 = two_sum(v[1].y, -v[2].y);
+  const dd dx02 = two_sum(v[0].x, -v[2].x);
+  const dd dx21 = two_sum(v[2].x, -v[1].x);
+  const dd dy02 = two_sum(v[0].y, -v[2].y);
+  const dd den = dd_add(dd_mul(dy12, dx02), dd_mul(dx21, dy02));
+  if (fabs(den.hi) < 2.0 * kGeomEps) return false;
+  H.t1[0] = dd_div(dy12, den);
+  H.t2[0] = dd_div(dx21, den);
+  H.t1[1] = dd_div(dd_neg(dy02), den);
+  H.t2[1] = dd_div(dx02, den);
+  H.t1[2] = dd_neg(dd_add(H.t1[0], H.t1[1]));
+  H.t2[2] = dd_neg(dd_add(H.t2[0], H.t2[1]));
+  for (int i = 0; i < 3; ++i) {
+    dd t3 = dd_make(i == 2 ? 1.0 : 0.0);
+    t3 = dd_sub(t3, dd_mul_d(H.t1[i], v[2].x));
+    t3 = dd_sub(t3, dd_mul_d(H.t2[i], v[2].y));
+    H.t3[i] = t3;
+  }
+  return true;
+}
+
+// Channel values for a field with plane coefficients (tau1, tau2, tau3):
+// raw (un-normalized) value, grad x, grad y.
+SPHBI_HD void combine_plane(const PairAcc& a, dd tau1, dd tau2, dd tau3, double* out3) {
+  const dd v = dd_add(dd_add(dd_mul(a.v1, tau1), dd_mul(a.v2, tau2)), dd_mul(a.v3, tau3));
+  const dd gx = dd_add(dd_add(dd_mul(a.g11, tau1), dd_mul(a.g12, tau2)), dd_mul(a.g13, tau3));
+  const dd gy = dd_add(dd_add(dd_mul(a.g21, tau1), dd_mul(a.g22, tau2)), dd_mul(a.g23, tau3));
+  out3[0] = v.hi + v.lo;
+  out3[1] = gx.hi + gx.lo;
+  out3[2] = gy.hi + gy.lo;
+}
+
+// finalize (:696-704): value * C2, gradient * C2 / h.
+SPHBI_HD void finalize(const double* raw3, double c2, double h, double* out4) {
+  out4[0] = raw3[0] * c2;
+  out4[1] = raw3[1] * c2 / h;
+  out4[2] = raw3[2] * c2 / h;
+  out4[3] = 0.0;  // real arithmetic end to end: no imaginary residual
+}
+
+// ---------------------------------------------------------------------------
+// full pair evaluation (integrate_triangle :808-822 / _bases :828-846)
+// ---------------------------------------------------------------------------
+// canonicalize_triangle (:680-694)
+SPHBI_HD void canonicalize(P2* v, int* perm) {
+  perm[0] = 0;
+  perm[1] = 1;
+  perm[2] = 2;
+  int lead = 0;
+  for (int i = 1; i < 3; ++i) {
+    const P2 a = v[i];
+    const P2 b = v[lead];
+    if (a.x < b.x || (a.x == b.x && a.y < b.y)) lead = i;
+  }
+  if (lead != 0) {
+    P2 w[3];
+    int p[3];
+    for (int i = 0; i < 3; ++i) {
+      w[i] = v[(i + lead) % 3];
+      p[i] = perm[(i + lead) % 3];
+    }
+    for (int i = 0; i < 3; ++i) {
+      v[i] = w[i];
+      perm[i] = p[i];
+    }
+  }
+  if (signed_area(v[0], v[1], v[2]) < 0.0) {
+    const P2 t = v[1];
+    v[1] = v[2];
+    v[2] = t;
+    const int tp = perm[1];
+    perm[1] = perm[2];
+    perm[2] = tp;
+  }
+}
+
+// mode: 0 = field given by vals3 -> out4; 1 = vertex bases -> out12
+// (3 x (value, gx, gy, imag) in the ORIGINAL vertex order).
+SPHBI_HD unsigned eval_pair(const KernelConsts& K, double qx, double qy, double h,
+                            const double* tri6, const double* vals3, int mode, double* out,
+                            unsigned long long* counters, int* n_regions) {
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  RegionCtx c;
+  c.K = &K;
+  acc_zero(c.acc);
+  c.status = kStatusOk;
+  c.counters = counters;
+  c.n_regions = 0;
+  const bool nondeg = integrate_normalized(c, nv);
+  if (n_regions) *n_regions = c.n_regions;
+  HatPlanes H;
+  if (!nondeg || !hat_planes(nv, H)) {
+    const int nout = mode == 0 ? 4 : 12;
+    for (int i = 0; i < nout; ++i) out[i] = 0.0;
+    return c.status;
+  }
+  if (mode == 0) {
+    const double a[3] = {vals3[perm[0]], vals3[perm[1]], vals3[perm[2]]};
+    dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
+    for (int i = 0; i < 3; ++i) {
+      tau1 = dd_add(tau1, dd_mul_d(H.t1[i], a[i]));
+      tau2 = dd_add(tau2, dd_mul_d(H.t2[i], a[i]));
+      tau3 = dd_add(tau3, dd_mul_d(H.t3[i], a[i]));
+    }
+    double raw[3];
+    combine_plane(c.acc, tau1, tau2, tau3, raw);
+    finalize(raw, K.c2, h, out);
+  } else {
+    for (int i = 0; i < 3; ++i) {
+      double raw[3];
+      combine_plane(c.acc, H.t1[i], H.t2[i], H.t3[i], raw);
+      finalize(raw, K.c2, h, out + 4 * perm[i]);
+    }
+  }
+  return c.status;
+}
+
+// Region-level evaluation against an arbitrary reference triangle (the
+// detail::region_* test surface, triangle_integrator.hpp:335-674): raw basis
+// triple (value_i, gx_i, gy_i), i = 0..2, un-normalized (h = 1, no C2).
+SPHBI_HD unsigned eval_region(const KernelConsts& K, int kind, const double* a,
+                              const double* ref6, double* out9,
+                              unsigned long long* counters) {
+  RegionCtx c;
+  c.K = &K;
+  acc_zero(c.acc);
+  c.status = kStatusOk;
+  c.counters = counters;
+  c.n_regions = 0;
+  const P2 p0{a[0], a[1]}, p1{a[2], a[3]}, p2{a[4], a[5]};
+  switch (kind) {
+    case 0:
+      if (!(a[0] >= 0.0)) c.status |= kStatusDomain;
+      region_disc_l(c, fmin(a[0], 1.0), 1.0);
+      break;
+    case 1:
+      region_sector(c, p0, p1, 1.0, fmin(a[4], 1.0));
+      break;
+    case 2:
+      region_segment(c, p0, p1, p2, 1.0);
+      break;
+    case 3:
+      region_stub(c, p0, p1, 1.0);
+      break;
+    case 4:
+      region_wedge(c, p0, p1, p2, 1.0);
+      break;
+    case 5:
+      region_t2(c, p0, p1, p2, 1.0);
+      break;
+    case 6:
+      region_t3(c, p0, p1, p2, 1.0);
+      break;
+    default: {
+      const P2 v[3] = {p0, p1, p2};
+      integrate_normalized(c, v);
+      break;
+    }
+  }
+  const P2 ref[3] = {{ref6[0], ref6[1]}, {ref6[2], ref6[3]}, {ref6[4], ref6[5]}};
+  HatPlanes H;
+  if (!hat_planes(ref, H)) {
+    for (int i = 0; i < 9; ++i) out9[i] = 0.0;
+    // assemble_region throws on a degenerate reference only if a region is assembled (:257-258)
+    return c.status | (c.n_regions > 0 ? (unsigned)kStatusDomain : 0u);
+  }
+  for (int i = 0; i < 3; ++i) combine_plane(c.acc, H.t1[i], H.t2[i], H.t3[i], out9 + 3 * i);
+  return c.status;
+}
+
+}  // namespace sphbi_dev

@@ -1,0 +1,947 @@
+// sphbi_cuda.cu -- sm_100a kernels and the C-ABI of libsphbi_cuda.so.
+//
+// Hot path (BASELINE.json north_star):
+//   K1 triangle binning   h-expanded AABB -> uniform cell list (CUB radix sort)
+//   K2 particle cells     particle -> cell key
+//   K3 pair predicate     d(p, closed triangle) < h, exact IEEE op order
+//   K4 pair integrals     per (particle, triangle): sphbi_core.cuh eval_pair
+//                         (replaces integrate_triangle, triangle_integrator.hpp:808)
+//   K5 per-particle sums  fixed-order segmented reduction, double2 stores
+// Everything is FP64 scalar work on the CUDA cores; there is no tensor-core
+// shaped contraction on this path.
+//
+// Compile: nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false ...
+// (-fmad=false is REQUIRED: the geometry replicates the reference's
+// uncontracted IEEE operation order; wanted FMAs are explicit fma()).
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sphbi_cuda.h"
+#include "sphbi_core.cuh"
+
+using namespace sphbi_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sphbi_status fail(sphbi_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define SPHBI_CUDA_TRY(expr)                                                          \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      return fail(_e == cudaErrorMemoryAllocation ? SPHBI_ERR_OUT_OF_MEMORY            \
+                                                   : SPHBI_ERR_CUDA,                  \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+    }                                                                                 \
+  } while (0)
+
+sphbi_status status_from_bits(unsigned bits) {
+  if (bits & kStatusDomain) return SPHBI_ERR_DOMAIN;
+  if (bits & kStatusInvalid) return SPHBI_ERR_INVALID_ARGUMENT;
+  if (bits & kStatusUnsupported) return SPHBI_ERR_UNSUPPORTED_FORM;
+  if (bits & kStatusLogic) return SPHBI_ERR_LOGIC;
+  if (bits & kStatusStack) return SPHBI_ERR_INTERNAL;
+  return SPHBI_OK;
+}
+
+constexpr int kEvalBlock = 128;
+constexpr int kMaxChunkPairs = 1 << 26;  // 64 Mi pairs per evaluation chunk (~1.5 GB scratch)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+enum ScratchSlot {
+  kBufPxy = 0,
+  kBufTri,
+  kBufVals,
+  kBufPairP,
+  kBufPairT,
+  kBufPairOut,
+  kBufRowPtr,
+  kBufOutV,
+  kBufOutG,
+  kBufFlags,
+  kBufUserPairs0,
+  kBufUserPairs1,
+  kBufKeysA,
+  kBufKeysB,
+  kBufValsA,
+  kBufValsB,
+  kBufCellStart,
+  kBufTriCount,
+  kBufTriOffset,
+  kBufPartCell,
+  kBufPartCount,
+  kBufPartOffset,
+  kBufCubTemp,
+  kBufBBox,
+  kBufGeneric0,
+  kBufGeneric1,
+  kBufGeneric2,
+  kNumBufs
+};
+
+struct sphbi_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  unsigned long long* d_counters = nullptr;
+  bool counters_on = false;
+  int64_t launches = 0;
+  void* buf[kNumBufs] = {};
+  size_t cap[kNumBufs] = {};
+  cudaEvent_t ev[8] = {};
+  unsigned* h_flags = nullptr;  // pinned
+};
+
+namespace {
+
+sphbi_status scratch(sphbi_ctx* c, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (c->cap[slot] < bytes) {
+    if (c->buf[slot]) cudaFree(c->buf[slot]);
+    c->buf[slot] = nullptr;
+    c->cap[slot] = 0;
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&c->buf[slot], want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      e = cudaMalloc(&c->buf[slot], bytes);
+      want = bytes;
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPHBI_ERR_OUT_OF_MEMORY, "cudaMalloc scratch failed");
+    }
+    c->cap[slot] = want;
+  }
+  *out = c->buf[slot];
+  return SPHBI_OK;
+}
+
+template <class T>
+sphbi_status scratch_t(sphbi_ctx* c, int slot, size_t count, T** out) {
+  void* p = nullptr;
+  const sphbi_status st = scratch(c, slot, count * sizeof(T), &p);
+  *out = static_cast<T*>(p);
+  return st;
+}
+
+sphbi_status check_launch(sphbi_ctx* c, const char* what) {
+  c->launches += 1;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SPHBI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return SPHBI_OK;
+}
+
+sphbi_status make_consts(const sphbi_kernel_desc* k, KernelConsts* K) {
+  if (!k) return fail(SPHBI_ERR_INVALID_ARGUMENT, "kernel descriptor is NULL");
+  if (k->n_coefficients < 1 || k->n_coefficients > SPHBI_MAX_COEFFICIENTS)
+    return fail(SPHBI_ERR_DOMAIN, "table1_terms: kernel degree exceeds the configured maximum");
+  if (!build_kernel_consts(k->coefficients, k->n_coefficients, k->normalization, K))
+    return fail(SPHBI_ERR_DOMAIN, "table1_terms: kernel degree exceeds the configured maximum");
+  return SPHBI_OK;
+}
+
+int grid_for(int64_t n, int block) {
+  const int64_t g = (n + block - 1) / block;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K4: pair integrals
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kEvalBlock)
+    k_integrate_pairs(const __grid_constant__ KernelConsts K, double h, int64_t n,
+                      const double* __restrict__ q, const double* __restrict__ tri,
+                      const double* __restrict__ vals, int mode, double* __restrict__ out,
+                      unsigned* __restrict__ status, unsigned* __restrict__ status_or,
+                      unsigned long long* counters) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double t6[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
+  double a3[3] = {1.0, 1.0, 1.0};
+  if (mode == 0 && vals) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = vals[3 * k + j];
+  }
+  double o[12];
+  const unsigned st =
+      eval_pair(K, q[2 * k], q[2 * k + 1], h, t6, a3, mode, o, counters, nullptr);
+  const int nout = mode == 0 ? 4 : 12;
+  for (int j = 0; j < nout; ++j) out[nout * k + j] = o[j];
+  if (status) status[k] = st;
+  if (st) atomicOr(status_or, st);
+}
+
+__global__ void __launch_bounds__(kEvalBlock)
+    k_integrate_regions(const __grid_constant__ KernelConsts K, int64_t n,
+                        const int* __restrict__ kind, const double* __restrict__ args,
+                        const double* __restrict__ ref, double* __restrict__ out,
+                        unsigned* __restrict__ status, unsigned long long* counters) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double a[8], r[6], o[9];
+  for (int j = 0; j < 8; ++j) a[j] = args[8 * k + j];
+  for (int j = 0; j < 6; ++j) r[j] = ref[6 * k + j];
+  status[k] = eval_region(K, kind[k], a, r, o, counters);
+  for (int j = 0; j < 9; ++j) out[9 * k + j] = o[j];
+}
+
+// Scene pairs: particle pp[k] against triangle pt[k]; out3 = (value, gx, gy).
+__global__ void __launch_bounds__(kEvalBlock)
+    k_eval_scene_pairs(const __grid_constant__ KernelConsts K, double h, int64_t npairs,
+                       const int* __restrict__ pp, const int* __restrict__ pt,
+                       const double* __restrict__ pxy, const double* __restrict__ tri,
+                       const double* __restrict__ vals, double* __restrict__ out3,
+                       unsigned* __restrict__ status_or, unsigned long long* counters) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= npairs) return;
+  const int i = pp[k];
+  const int t = pt[k];
+  double t6[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) t6[j] = __ldg(tri + 6 * (int64_t)t + j);
+  double a3[3] = {1.0, 1.0, 1.0};
+  if (vals) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = __ldg(vals + 3 * (int64_t)t + j);
+  }
+  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+  double o[4];
+  const unsigned st = eval_pair(K, p.x, p.y, h, t6, a3, 0, o, counters, nullptr);
+  out3[3 * k] = o[0];
+  out3[3 * k + 1] = o[1];
+  out3[3 * k + 2] = o[2];
+  if (st) atomicOr(status_or, st);
+}
+
+// ---------------------------------------------------------------------------
+// K5: per-particle fixed-order reduction (pairs sorted by particle, then
+// triangle id), vectorised double2 gradient stores.
+// ---------------------------------------------------------------------------
+__global__ void k_row_ptr(int64_t npairs, const int* __restrict__ pp, int p_begin, int p_count,
+                          int64_t* __restrict__ row_ptr) {
+  // row_ptr[j] = first pair with particle >= p_begin + j, j in [0, p_count]
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k > npairs) return;
+  const int prev = k == 0 ? p_begin - 1 : pp[k - 1] ;
+  const int cur = k == npairs ? p_begin + p_count : pp[k];
+  for (int p = prev + 1; p <= cur; ++p) {
+    const int j = p - p_begin;
+    if (j >= 0 && j <= p_count) row_ptr[j] = k;
+  }
+}
+
+__global__ void k_reduce_rows(int p_begin, int p_count, const int64_t* __restrict__ row_ptr,
+                              const double* __restrict__ pair_out3, double* __restrict__ out_v,
+                              double* __restrict__ out_g, int accumulate) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p_count) return;
+  const int64_t b = row_ptr[j], e = row_ptr[j + 1];
+  double v = 0.0, gx = 0.0, gy = 0.0;
+  if (accumulate) {
+    v = out_v[p_begin + j];
+    gx = out_g[2 * (int64_t)(p_begin + j)];
+    gy = out_g[2 * (int64_t)(p_begin + j) + 1];
+  }
+  for (int64_t k = b; k < e; ++k) {
+    v += pair_out3[3 * k];
+    gx += pair_out3[3 * k + 1];
+    gy += pair_out3[3 * k + 2];
+  }
+  out_v[p_begin + j] = v;
+  reinterpret_cast<double2*>(out_g)[p_begin + j] = make_double2(gx, gy);
+}
+
+// ---------------------------------------------------------------------------
+// explicit pair lists: validation, int64 -> packed key, sortedness
+// ---------------------------------------------------------------------------
+__global__ void k_pack_pairs(int64_t n, const int64_t* __restrict__ ip, const int64_t* __restrict__ it,
+                             int64_t n_particles, int64_t n_tris, unsigned long long* __restrict__ keys,
+                             unsigned* __restrict__ flags) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t i = ip[k], t = it[k];
+  if (i < 0 || i >= n_particles || t < 0 || t >= n_tris) {
+    atomicOr(flags, 1u);  // out of range
+    keys[k] = 0ull;
+    return;
+  }
+  const unsigned long long key = (static_cast<unsigned long long>(i) << 32) | static_cast<unsigned long long>(t);
+  keys[k] = key;
+  if (k > 0) {
+    const int64_t i0 = ip[k - 1], t0 = it[k - 1];
+    const unsigned long long prev = (static_cast<unsigned long long>(i0) << 32) | static_cast<unsigned long long>(t0);
+    if (prev > key) atomicOr(flags, 2u);  // unsorted
+  }
+}
+
+__global__ void k_unpack_keys(int64_t n, const unsigned long long* __restrict__ keys, int* __restrict__ pp,
+                              int* __restrict__ pt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const unsigned long long key = keys[k];
+  pp[k] = static_cast<int>(key >> 32);
+  pt[k] = static_cast<int>(key & 0xffffffffull);
+}
+
+// ---------------------------------------------------------------------------
+// K1-K3: uniform-grid pair finding
+// ---------------------------------------------------------------------------
+struct Grid {
+  double x0, y0, cell, inv_unused;
+  int nx, ny;
+  double pad;  // h * (1 + 1e-12) + tiny: conservative AABB expansion
+};
+
+// Exact pair predicate, shared bit-for-bit with the CPU oracle's finder
+// (oracle/sphbi_oracle.c: oracle_pair_dist2): distance^2 from p to the
+// closed triangle, fixed IEEE op order, no contraction (-fmad=false).
+__host__ __device__ __forceinline__ double seg_dist2(double px, double py, double ax, double ay,
+                                                     double bx, double by) {
+  const double ex = bx - ax, ey = by - ay;
+  const double len2 = ex * ex + ey * ey;
+  double t = 0.0;
+  if (len2 > 0.0) t = ((px - ax) * ex + (py - ay) * ey) / len2;
+  t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  const double dx = ax + t * ex - px;
+  const double dy = ay + t * ey - py;
+  return dx * dx + dy * dy;
+}
+
+__host__ __device__ __forceinline__ double pair_dist2(double px, double py, const double* t) {
+  const double ax = t[0], ay = t[1], bx = t[2], by = t[3], cx = t[4], cy = t[5];
+  const double s0 = (bx - ax) * (py - ay) - (by - ay) * (px - ax);
+  const double s1 = (cx - bx) * (py - by) - (cy - by) * (px - bx);
+  const double s2 = (ax - cx) * (py - cy) - (ay - cy) * (px - cx);
+  if ((s0 >= 0.0 && s1 >= 0.0 && s2 >= 0.0) || (s0 <= 0.0 && s1 <= 0.0 && s2 <= 0.0)) return 0.0;
+  const double d0 = seg_dist2(px, py, ax, ay, bx, by);
+  const double d1 = seg_dist2(px, py, bx, by, cx, cy);
+  const double d2 = seg_dist2(px, py, cx, cy, ax, ay);
+  return fmin(d0, fmin(d1, d2));
+}
+
+__device__ __forceinline__ int cell_coord(double v, double o, double cell, int n) {
+  const double f = floor((v - o) / cell);
+  int c = f < 0.0 ? 0 : (f >= (double)(n - 1) ? n - 1 : (int)f);
+  return c;
+}
+
+// bounding box of particles and triangle vertices: per-block partials
+__global__ void k_bbox(int64_t n_pts, const double* __restrict__ pxy, int64_t n_tri_pts,
+                       const double* __restrict__ txy, double* __restrict__ partial) {
+  double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+  const int64_t total = n_pts + n_tri_pts;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = k < n_pts ? pxy[2 * k] : txy[2 * (k - n_pts)];
+    const double y = k < n_pts ? pxy[2 * k + 1] : txy[2 * (k - n_pts) + 1];
+    mnx = fmin(mnx, x);
+    mny = fmin(mny, y);
+    mxx = fmax(mxx, x);
+    mxy = fmax(mxy, y);
+  }
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage ts;
+  const double a = BR(ts).Reduce(mnx, cub::Min());
+  __syncthreads();
+  const double b = BR(ts).Reduce(mny, cub::Min());
+  __syncthreads();
+  const double c = BR(ts).Reduce(mxx, cub::Max());
+  __syncthreads();
+  const double d = BR(ts).Reduce(mxy, cub::Max());
+  if (threadIdx.x == 0) {
+    partial[4 * blockIdx.x] = a;
+    partial[4 * blockIdx.x + 1] = b;
+    partial[4 * blockIdx.x + 2] = c;
+    partial[4 * blockIdx.x + 3] = d;
+  }
+}
+
+__global__ void k_tri_cell_count(int64_t n_tris, const double* __restrict__ tri, Grid g,
+                                 unsigned* __restrict__ count) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_tris) return;
+  const double* v = tri + 6 * t;
+  const double mnx = fmin(v[0], fmin(v[2], v[4])) - g.pad, mxx = fmax(v[0], fmax(v[2], v[4])) + g.pad;
+  const double mny = fmin(v[1], fmin(v[3], v[5])) - g.pad, mxy = fmax(v[1], fmax(v[3], v[5])) + g.pad;
+  const int cx0 = cell_coord(mnx, g.x0, g.cell, g.nx), cx1 = cell_coord(mxx, g.x0, g.cell, g.nx);
+  const int cy0 = cell_coord(mny, g.y0, g.cell, g.ny), cy1 = cell_coord(mxy, g.y0, g.cell, g.ny);
+  count[t] = static_cast<unsigned>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
+}
+
+__global__ void k_tri_cell_fill(int64_t n_tris, const double* __restrict__ tri, Grid g,
+                                const unsigned long long* __restrict__ offset,
+                                unsigned* __restrict__ keys, int* __restrict__ vals) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_tris) return;
+  const double* v = tri + 6 * t;
+  const double mnx = fmin(v[0], fmin(v[2], v[4])) - g.pad, mxx = fmax(v[0], fmax(v[2], v[4])) + g.pad;
+  const double mny = fmin(v[1], fmin(v[3], v[5])) - g.pad, mxy = fmax(v[1], fmax(v[3], v[5])) + g.pad;
+  const int cx0 = cell_coord(mnx, g.x0, g.cell, g.nx), cx1 = cell_coord(mxx, g.x0, g.cell, g.nx);
+  const int cy0 = cell_coord(mny, g.y0, g.cell, g.ny), cy1 = cell_coord(mxy, g.y0, g.cell, g.ny);
+  unsigned long long o = offset[t];
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      keys[o] = static_cast<unsigned>(cy * g.nx + cx);
+      vals[o] = static_cast<int>(t);
+      ++o;
+    }
+}
+
+// cell_start[c] = first sorted entry with key >= c, c in [0, ncells]
+__global__ void k_cell_start(int64_t n_entries, const unsigned* __restrict__ keys, int ncells,
+                             unsigned long long* __restrict__ cell_start) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k > n_entries) return;
+  const long long prev = k == 0 ? -1 : static_cast<long long>(keys[k - 1]);
+  const long long cur = k == n_entries ? ncells : static_cast<long long>(keys[k]);
+  for (long long c = prev + 1; c <= cur; ++c) cell_start[c] = static_cast<unsigned long long>(k);
+}
+
+__global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid g, unsigned* __restrict__ cell) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cx = cell_coord(pxy[2 * i], g.x0, g.cell, g.nx);
+  const int cy = cell_coord(pxy[2 * i + 1], g.y0, g.cell, g.ny);
+  cell[i] = static_cast<unsigned>(cy * g.nx + cx);
+}
+
+// count (fill == 0) or emit (fill == 1) the pairs of particles [p0, p1)
+__global__ void k_find_pairs(int p0, int p1, const double* __restrict__ pxy,
+                             const unsigned* __restrict__ pcell,
+                             const unsigned long long* __restrict__ cell_start,
+                             const int* __restrict__ cell_tris, const double* __restrict__ tri,
+                             double h2, int fill, unsigned long long* __restrict__ count_or_offset,
+                             long long base, int* __restrict__ pp, int* __restrict__ pt) {
+  const int i = p0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p1) return;
+  const double px = pxy[2 * (int64_t)i], py = pxy[2 * (int64_t)i + 1];
+  const unsigned c = pcell[i];
+  const unsigned long long b = cell_start[c], e = cell_start[c + 1];
+  unsigned long long n = 0;
+  unsigned long long o = fill ? count_or_offset[i] - base : 0;
+  for (unsigned long long k = b; k < e; ++k) {
+    const int t = cell_tris[k];
+    double tv[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * (int64_t)t + j);
+    if (pair_dist2(px, py, tv) < h2) {
+      if (fill) {
+        pp[o] = i;
+        pt[o] = t;
+        ++o;
+      } else {
+        ++n;
+      }
+    }
+  }
+  if (!fill) count_or_offset[i] = n;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* sphbi_last_error(void) { return g_last_error.c_str(); }
+
+sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
+  if (!out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(SPHBI_ERR_NO_DEVICE, "no CUDA device visible (libsphbi_cuda has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) return fail(SPHBI_ERR_INVALID_ARGUMENT, "device index out of range");
+  cudaDeviceProp prop;
+  SPHBI_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(SPHBI_ERR_NO_DEVICE, "libsphbi_cuda is built for sm_100a (Blackwell) only");
+  SPHBI_CUDA_TRY(cudaSetDevice(device));
+  sphbi_ctx* c = new sphbi_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(SPHBI_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  c->stream = c->own_stream;
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaMallocHost(&c->h_flags, 64);
+  if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPHBI_ERR_OUT_OF_MEMORY, "counter allocation failed");
+  }
+  cudaMemset(c->d_counters, 0, sizeof(unsigned long long) * kNumCounters);
+  *out = c;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
+  if (!c) return SPHBI_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (int i = 0; i < kNumBufs; ++i)
+    if (c->buf[i]) cudaFree(c->buf[i]);
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  if (c->d_counters) cudaFree(c->d_counters);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_ctx_set_stream(sphbi_ctx* c, void* s) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_ctx_synchronize(sphbi_ctx* c) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* c, int enable) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  c->counters_on = enable != 0;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_read_counters(sphbi_ctx* c, uint64_t out[SPHBI_NUM_COUNTERS], int reset) {
+  if (!c || !out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL argument");
+  cudaSetDevice(c->device);
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(out, c->d_counters, sizeof(uint64_t) * kNumCounters,
+                                 cudaMemcpyDeviceToHost, c->stream));
+  if (reset)
+    SPHBI_CUDA_TRY(cudaMemsetAsync(c->d_counters, 0, sizeof(uint64_t) * kNumCounters, c->stream));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPHBI_OK;
+}
+
+int64_t sphbi_ctx_launch_count(sphbi_ctx* c) { return c ? c->launches : 0; }
+
+sphbi_status sphbi_kernel_validate(const sphbi_kernel_desc* k) {
+  KernelConsts K;
+  return make_consts(k, &K);
+}
+
+sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                   const double* query_xy, const double* tri_xy, const double* values,
+                                   int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
+  if (mode != 0 && mode != 1) return fail(SPHBI_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+  if (n < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "n < 0");
+  KernelConsts K;
+  sphbi_status st = make_consts(kernel, &K);
+  if (st != SPHBI_OK) return st;
+  if (n == 0) return SPHBI_OK;
+  if (!query_xy || !tri_xy || !out || (mode == 0 && !values))
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL input/output array");
+  cudaSetDevice(c->device);
+  const int nout = mode == 0 ? 4 : 12;
+  const double *dq = query_xy, *dt = tri_xy, *dv = values;
+  double* dout = out;
+  uint32_t* dstat = nullptr;
+  unsigned* dflags = nullptr;
+  if ((st = scratch_t(c, kBufFlags, 4, &dflags)) != SPHBI_OK) return st;
+  if (mem == SPHBI_MEM_HOST) {
+    double *a, *b, *v, *o;
+    if ((st = scratch_t(c, kBufPxy, 2 * n, &a)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufTri, 6 * n, &b)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufPairOut, nout * n, &o)) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(a, query_xy, 16 * n, cudaMemcpyHostToDevice, c->stream));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n, cudaMemcpyHostToDevice, c->stream));
+    dq = a;
+    dt = b;
+    dv = nullptr;
+    if (mode == 0) {
+      if ((st = scratch_t(c, kBufVals, 3 * n, &v)) != SPHBI_OK) return st;
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(v, values, 24 * n, cudaMemcpyHostToDevice, c->stream));
+      dv = v;
+    }
+    dout = o;
+    if (status_out) {
+      if ((st = scratch_t(c, kBufFlags + 0, 4 + n, &dflags)) != SPHBI_OK) return st;
+      dstat = dflags + 4;
+    }
+  } else {
+    dstat = status_out;
+  }
+  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, c->stream));
+  k_integrate_pairs<<<grid_for(n, kEvalBlock), kEvalBlock, 0, c->stream>>>(
+      K, h, n, dq, dt, dv, mode, dout, dstat, dflags, c->counters_on ? c->d_counters : nullptr);
+  if ((st = check_launch(c, "k_integrate_pairs")) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 4, cudaMemcpyDeviceToHost, c->stream));
+  if (mem == SPHBI_MEM_HOST) {
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(double) * nout * n, cudaMemcpyDeviceToHost, c->stream));
+    if (status_out)
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(status_out, dstat, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const unsigned bits = c->h_flags[0];
+  if (bits) return fail(status_from_bits(bits), "integrate_triangle: reference-domain error on device");
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_integrate_regions(sphbi_ctx* c, const sphbi_kernel_desc* kernel, int64_t n,
+                                     const int32_t* kind, const double* args, const double* ref_xy,
+                                     double* out, uint32_t* status_out) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  KernelConsts K;
+  sphbi_status st = make_consts(kernel, &K);
+  if (st != SPHBI_OK) return st;
+  if (n <= 0) return SPHBI_OK;
+  cudaSetDevice(c->device);
+  int* dk;
+  double *da, *dr, *dout;
+  unsigned* ds;
+  if ((st = scratch_t(c, kBufGeneric0, n, &dk)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPxy, 8 * n, &da)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufTri, 6 * n, &dr)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPairOut, 9 * n, &dout)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufGeneric1, n, &ds)) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(dk, kind, 4 * n, cudaMemcpyHostToDevice, c->stream));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(da, args, 64 * n, cudaMemcpyHostToDevice, c->stream));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(dr, ref_xy, 48 * n, cudaMemcpyHostToDevice, c->stream));
+  k_integrate_regions<<<grid_for(n, kEvalBlock), kEvalBlock, 0, c->stream>>>(
+      K, n, dk, da, dr, dout, ds, c->counters_on ? c->d_counters : nullptr);
+  if ((st = check_launch(c, "k_integrate_regions")) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, 72 * n, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<uint32_t> sv(static_cast<size_t>(n));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(sv.data(), ds, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  unsigned bits = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    bits |= sv[static_cast<size_t>(k)];
+    if (status_out) status_out[k] = sv[static_cast<size_t>(k)];
+  }
+  if (bits) return fail(status_from_bits(bits), "region evaluation: reference-domain error on device");
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
+                            const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                            const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
+                            const int64_t* pair_triangle, double* out_value, double* out_grad,
+                            int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
+                            sphbi_memory mem) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
+  if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
+  if (n_particles >= (1ll << 31) || n_triangles >= (1ll << 31))
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "particle / triangle counts must be < 2^31");
+  KernelConsts K;
+  sphbi_status st = make_consts(kernel, &K);
+  if (st != SPHBI_OK) return st;
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  const bool timing = stats != nullptr;
+  if (timing) {
+    std::memset(stats, 0, sizeof(*stats));
+    cudaEventRecord(c->ev[0], s);
+  }
+  // ---- inputs on the device
+  const double *dp = particle_xy, *dt = tri_xy, *dv = tri_values;
+  double *dov = out_value, *dog = out_grad;
+  if (mem == SPHBI_MEM_HOST) {
+    double *a, *b, *v;
+    if ((st = scratch_t(c, kBufPxy, 2 * n_particles, &a)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufTri, 6 * n_triangles, &b)) != SPHBI_OK) return st;
+    if (n_particles) SPHBI_CUDA_TRY(cudaMemcpyAsync(a, particle_xy, 16 * n_particles, cudaMemcpyHostToDevice, s));
+    if (n_triangles) SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, s));
+    dp = a;
+    dt = b;
+    if (tri_values) {
+      if ((st = scratch_t(c, kBufVals, 3 * n_triangles, &v)) != SPHBI_OK) return st;
+      if (n_triangles) SPHBI_CUDA_TRY(cudaMemcpyAsync(v, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, s));
+      dv = v;
+    }
+  }
+  if (mem == SPHBI_MEM_HOST || !out_value || !out_grad) {
+    double *a, *b;
+    if ((st = scratch_t(c, kBufOutV, n_particles, &a)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutG, 2 * n_particles, &b)) != SPHBI_OK) return st;
+    if (mem == SPHBI_MEM_HOST || !out_value) dov = a;
+    if (mem == SPHBI_MEM_HOST || !out_grad) dog = b;
+  }
+  unsigned* dflags;
+  if ((st = scratch_t(c, kBufFlags, 8, &dflags)) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, s));
+  if (n_particles) {
+    SPHBI_CUDA_TRY(cudaMemsetAsync(dov, 0, 8 * n_particles, s));
+    SPHBI_CUDA_TRY(cudaMemsetAsync(dog, 0, 16 * n_particles, s));
+  }
+  unsigned long long* ctr = c->counters_on ? c->d_counters : nullptr;
+  int64_t total_pairs = 0, candidates = 0;
+  int* pp = nullptr;
+  int* pt = nullptr;
+  double* pout = nullptr;
+  int64_t* row_ptr = nullptr;
+
+  if (n_pairs >= 0) {
+    // ---- explicit pair list
+    total_pairs = n_pairs;
+    if (n_pairs > 0) {
+      if (!pair_particle || !pair_triangle) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL pair arrays");
+      const int64_t *ip = pair_particle, *it = pair_triangle;
+      if (mem == SPHBI_MEM_HOST) {
+        int64_t *a, *b;
+        if ((st = scratch_t(c, kBufUserPairs0, n_pairs, &a)) != SPHBI_OK) return st;
+        if ((st = scratch_t(c, kBufUserPairs1, n_pairs, &b)) != SPHBI_OK) return st;
+        SPHBI_CUDA_TRY(cudaMemcpyAsync(a, pair_particle, 8 * n_pairs, cudaMemcpyHostToDevice, s));
+        SPHBI_CUDA_TRY(cudaMemcpyAsync(b, pair_triangle, 8 * n_pairs, cudaMemcpyHostToDevice, s));
+        ip = a;
+        it = b;
+      }
+      unsigned long long *ka, *kb;
+      if ((st = scratch_t(c, kBufKeysA, n_pairs, &ka)) != SPHBI_OK) return st;
+      k_pack_pairs<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, ip, it, n_particles, n_triangles, ka, dflags + 1);
+      if ((st = check_launch(c, "k_pack_pairs")) != SPHBI_OK) return st;
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
+      SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+      if (c->h_flags[1] & 1u) return fail(SPHBI_ERR_INVALID_ARGUMENT, "pair index out of range");
+      unsigned long long* keys = ka;
+      if (c->h_flags[1] & 2u) {
+        if ((st = scratch_t(c, kBufKeysB, n_pairs, &kb)) != SPHBI_OK) return st;
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tmp, ka, kb, (int)n_pairs, 0, 64, s);
+        void* dtmp;
+        if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+        cub::DeviceRadixSort::SortKeys(dtmp, tmp, ka, kb, (int)n_pairs, 0, 64, s);
+        if ((st = check_launch(c, "radix sort pairs")) != SPHBI_OK) return st;
+        keys = kb;
+      }
+      if ((st = scratch_t(c, kBufPairP, n_pairs, &pp)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPairT, n_pairs, &pt)) != SPHBI_OK) return st;
+      k_unpack_keys<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, keys, pp, pt);
+      if ((st = check_launch(c, "k_unpack_keys")) != SPHBI_OK) return st;
+    }
+    if (timing) cudaEventRecord(c->ev[1], s);
+    // evaluate in chunks of whole particles
+    int64_t done = 0;
+    std::vector<int64_t> dummy;
+    while (done < n_pairs) {
+      const int64_t cnt = std::min<int64_t>(n_pairs - done, kMaxChunkPairs);
+      if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
+      k_eval_scene_pairs<<<grid_for(cnt, kEvalBlock), kEvalBlock, 0, s>>>(
+          K, h, cnt, pp + done, pt + done, dp, dt, dv, pout, dflags, ctr);
+      if ((st = check_launch(c, "k_eval_scene_pairs")) != SPHBI_OK) return st;
+      // rows: all particles, accumulate (a particle may straddle chunks)
+      const int pc = static_cast<int>(n_particles);
+      if ((st = scratch_t(c, kBufRowPtr, pc + 1, &row_ptr)) != SPHBI_OK) return st;
+      k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp + done, 0, pc, row_ptr);
+      if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
+      k_reduce_rows<<<grid_for(pc, 256), 256, 0, s>>>(0, pc, row_ptr, pout, dov, dog, 1);
+      if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
+      done += cnt;
+    }
+    if (timing) cudaEventRecord(c->ev[2], s);
+    if (timing) cudaEventRecord(c->ev[3], s);
+  } else if (n_particles > 0 && n_triangles > 0) {
+    // ---- device cell list
+    const int nb = 296;
+    double* partial;
+    if ((st = scratch_t(c, kBufBBox, 4 * nb, &partial)) != SPHBI_OK) return st;
+    k_bbox<<<nb, 256, 0, s>>>(n_particles, dp, 3 * n_triangles, dt, partial);
+    if ((st = check_launch(c, "k_bbox")) != SPHBI_OK) return st;
+    std::vector<double> hb(4 * nb);
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(hb.data(), partial, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    for (int b = 0; b < nb; ++b) {
+      mnx = std::min(mnx, hb[4 * b]);
+      mny = std::min(mny, hb[4 * b + 1]);
+      mxx = std::max(mxx, hb[4 * b + 2]);
+      mxy = std::max(mxy, hb[4 * b + 3]);
+    }
+    if (!std::isfinite(mnx) || !std::isfinite(mny) || !std::isfinite(mxx) || !std::isfinite(mxy))
+      return fail(SPHBI_ERR_INVALID_ARGUMENT, "non-finite particle or vertex coordinates");
+    Grid g;
+    g.pad = h * (1.0 + 1e-12) + 1e-300;
+    g.x0 = mnx - 2.0 * g.pad;
+    g.y0 = mny - 2.0 * g.pad;
+    const double ex = (mxx + 2.0 * g.pad) - g.x0, ey = (mxy + 2.0 * g.pad) - g.y0;
+    g.cell = h;
+    const double max_cells = 1 << 26;
+    while ((ex / g.cell + 1.0) * (ey / g.cell + 1.0) > max_cells) g.cell *= 2.0;
+    g.nx = static_cast<int>(ex / g.cell) + 1;
+    g.ny = static_cast<int>(ey / g.cell) + 1;
+    g.inv_unused = 0.0;
+    const int ncells = g.nx * g.ny;
+    // K1: triangle binning
+    unsigned* tcount;
+    unsigned long long* toff;
+    if ((st = scratch_t(c, kBufTriCount, n_triangles + 1, &tcount)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufTriOffset, n_triangles + 1, &toff)) != SPHBI_OK) return st;
+    k_tri_cell_count<<<grid_for(n_triangles, 256), 256, 0, s>>>(n_triangles, dt, g, tcount);
+    if ((st = check_launch(c, "k_tri_cell_count")) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemsetAsync(tcount + n_triangles, 0, 4, s));
+    {
+      size_t tmp = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp, tcount, toff, (int)(n_triangles + 1), s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceScan::ExclusiveSum(dtmp, tmp, tcount, toff, (int)(n_triangles + 1), s);
+      if ((st = check_launch(c, "scan tri counts")) != SPHBI_OK) return st;
+    }
+    unsigned long long n_entries = 0;
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(&n_entries, toff + n_triangles, 8, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    if (n_entries >= (1ull << 31)) return fail(SPHBI_ERR_OUT_OF_MEMORY, "cell list exceeds 2^31 entries");
+    unsigned *ka, *kb;
+    int *va, *vb;
+    unsigned long long* cell_start;
+    if ((st = scratch_t(c, kBufKeysA, n_entries, &ka)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufKeysB, n_entries, &kb)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufValsA, n_entries, &va)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufValsB, n_entries, &vb)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufCellStart, (size_t)ncells + 1, &cell_start)) != SPHBI_OK) return st;
+    k_tri_cell_fill<<<grid_for(n_triangles, 256), 256, 0, s>>>(n_triangles, dt, g, toff, ka, va);
+    if ((st = check_launch(c, "k_tri_cell_fill")) != SPHBI_OK) return st;
+    {
+      int bits = 1;
+      while ((1ll << bits) < ncells) ++bits;
+      size_t tmp = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ka, kb, va, vb, (int)n_entries, 0, bits, s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceRadixSort::SortPairs(dtmp, tmp, ka, kb, va, vb, (int)n_entries, 0, bits, s);
+      if ((st = check_launch(c, "radix sort cell list")) != SPHBI_OK) return st;
+    }
+    k_cell_start<<<grid_for((int64_t)n_entries + 1, 256), 256, 0, s>>>((int64_t)n_entries, kb, ncells, cell_start);
+    if ((st = check_launch(c, "k_cell_start")) != SPHBI_OK) return st;
+    // K2: particle cells
+    unsigned* pcell;
+    unsigned long long *pcount, *poff;
+    if ((st = scratch_t(c, kBufPartCell, n_particles, &pcell)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufPartCount, n_particles + 1, &pcount)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufPartOffset, n_particles + 1, &poff)) != SPHBI_OK) return st;
+    k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
+    if ((st = check_launch(c, "k_particle_cell")) != SPHBI_OK) return st;
+    // K3: count, scan
+    const double h2 = h * h;
+    const int np = static_cast<int>(n_particles);
+    k_find_pairs<<<grid_for(np, 128), 128, 0, s>>>(0, np, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
+                                                    nullptr, nullptr);
+    if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
+    {
+      size_t tmp = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp, pcount, poff, (int)(n_particles + 1), s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceScan::ExclusiveSum(dtmp, tmp, pcount, poff, (int)(n_particles + 1), s);
+      if ((st = check_launch(c, "scan pair counts")) != SPHBI_OK) return st;
+    }
+    std::vector<unsigned long long> hoff(static_cast<size_t>(n_particles) + 1);
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(hoff.data(), poff, 8 * (n_particles + 1), cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    total_pairs = static_cast<int64_t>(hoff[static_cast<size_t>(n_particles)]);
+    if (timing) cudaEventRecord(c->ev[1], s);
+    // K4 + K5 in chunks of whole particles
+    int p0 = 0;
+    int64_t written = 0;
+    while (p0 < np) {
+      // largest p1 with off[p1] - off[p0] <= budget (at least one particle)
+      const unsigned long long base = hoff[p0];
+      int p1 = static_cast<int>(std::upper_bound(hoff.begin() + p0 + 1, hoff.end(), base + kMaxChunkPairs) -
+                                hoff.begin()) - 1;
+      if (p1 <= p0) p1 = p0 + 1;
+      const int64_t cnt = static_cast<int64_t>(hoff[p1] - base);
+      if (cnt > 0) {
+        if ((st = scratch_t(c, kBufPairP, cnt, &pp)) != SPHBI_OK) return st;
+        if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
+        if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
+        k_find_pairs<<<grid_for(p1 - p0, 128), 128, 0, s>>>(p0, p1, dp, pcell, cell_start, vb, dt, h2, 1, poff,
+                                                            (long long)base, pp, pt);
+        if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
+        if (pair_list_out && pair_list_capacity && *pair_list_capacity >= total_pairs) {
+          std::vector<int> a(static_cast<size_t>(cnt)), b(static_cast<size_t>(cnt));
+          SPHBI_CUDA_TRY(cudaMemcpyAsync(a.data(), pp, 4 * cnt, cudaMemcpyDeviceToHost, s));
+          SPHBI_CUDA_TRY(cudaMemcpyAsync(b.data(), pt, 4 * cnt, cudaMemcpyDeviceToHost, s));
+          SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+          if (mem == SPHBI_MEM_HOST) {
+            for (int64_t k = 0; k < cnt; ++k) {
+              pair_list_out[2 * (written + k)] = a[static_cast<size_t>(k)];
+              pair_list_out[2 * (written + k) + 1] = b[static_cast<size_t>(k)];
+            }
+          } else {
+            std::vector<int64_t> il(static_cast<size_t>(2 * cnt));
+            for (int64_t k = 0; k < cnt; ++k) {
+              il[static_cast<size_t>(2 * k)] = a[static_cast<size_t>(k)];
+              il[static_cast<size_t>(2 * k + 1)] = b[static_cast<size_t>(k)];
+            }
+            SPHBI_CUDA_TRY(cudaMemcpy(pair_list_out + 2 * written, il.data(), 16 * cnt, cudaMemcpyHostToDevice));
+          }
+          written += cnt;
+        }
+        k_eval_scene_pairs<<<grid_for(cnt, kEvalBlock), kEvalBlock, 0, s>>>(K, h, cnt, pp, pt, dp, dt, dv, pout,
+                                                                           dflags, ctr);
+        if ((st = check_launch(c, "k_eval_scene_pairs")) != SPHBI_OK) return st;
+        if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
+        k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp, p0, p1 - p0, row_ptr);
+        if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
+        k_reduce_rows<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, row_ptr, pout, dov, dog, 0);
+        if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
+      }
+      p0 = p1;
+    }
+    if (timing) {
+      cudaEventRecord(c->ev[2], s);
+      cudaEventRecord(c->ev[3], s);
+    }
+    (void)candidates;
+  } else if (timing) {
+    cudaEventRecord(c->ev[1], s);
+    cudaEventRecord(c->ev[2], s);
+    cudaEventRecord(c->ev[3], s);
+  }
+  if (pair_list_capacity) *pair_list_capacity = total_pairs;
+  // ---- outputs
+  if (mem == SPHBI_MEM_HOST && n_particles) {
+    if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, dov, 8 * n_particles, cudaMemcpyDeviceToHost, s));
+    if (out_grad) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, dog, 16 * n_particles, cudaMemcpyDeviceToHost, s));
+  }
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 4, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (timing) {
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&d, c->ev[2], c->ev[3]);
+    stats->ms_pairs = a;
+    stats->ms_eval = b;
+    stats->ms_reduce = d;
+    stats->n_pairs = total_pairs;
+    stats->n_candidates = candidates;
+    stats->status_bits = c->h_flags[0];
+  }
+  if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "pair evaluation: reference-domain error on device");
+  return SPHBI_OK;
+}
+
+}  // extern "C"
