@@ -148,6 +148,12 @@ sphbi_status sphbi_evaluate(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, dou
                             double* out_value, double* out_grad, int64_t* pair_list_out,
                             int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
 
+/* ---- measurement utility ----------------------------------------------- */
+/* FP64 (DFMA-pipe) peak of the context's GPU at the current clocks: a
+ * dependent-chain-free DFMA loop over all SMs, timed with CUDA events.
+ * *tflops = 2 * DFMA / s / 1e12 (the roofline denominator for the FP64 path). */
+sphbi_status sphbi_measure_fp64_peak(sphbi_ctx* ctx, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,372 @@
+"""GPU tier: the product path (libsphbi_cuda.so on the B200, through the C-ABI)
+against the oracle and the reference's own outputs / frozen values.
+
+Tolerance (BASELINE.json, literal reading, SURVEY.md §0 finding 3):
+|gpu - cpu| <= max(1e-11 max(|gpu|,|cpu|), 1e-13 C/h^2) per particle & channel;
+pair lists bit-exact.
+"""
+import ctypes
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib as OL
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+FROZEN = json.loads((GOLD / "reference_frozen.json").read_text())
+OUTS = np.load(GOLD / "reference_outputs.npz")
+REGION_KIND = {"disc": 0, "sector": 1, "segment": 2, "stub": 3, "wedge": 4, "t2": 5, "t3": 6}
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2507_21686_b200 import sphbi
+    return sphbi
+
+
+@pytest.fixture(scope="module")
+def ctx(S):
+    c = S.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def O():
+    return OL.oracle()
+
+
+def table_of(S, k):
+    return S.table1_terms(S.PolyKernel(list(k.coefficients), k.normalization))
+
+
+# ---------------------------------------------------------------------------
+# frozen known-answer values of the reference suite, through the product path
+# ---------------------------------------------------------------------------
+def test_full_physical_frozen_value(S):
+    f = FROZEN["triangle_integrator"]["full"][0]
+    ti = FROZEN["triangle_integrator"]
+    v = ti["ref_verts"]
+    tri = S.Triangle(S.Point2(v[0], v[1]), S.Point2(v[2], v[3]), S.Point2(v[4], v[5]))
+    r = S.integrate_triangle(S.Point2(*f["query"]), f["h"], tri, ti["ref_vals"], S.table1_terms(S.wendland4()))
+    for got, want in zip([r.value, *r.gradient], f["want"]):
+        assert abs(got - want) <= 5e-12 * max(abs(want), 0.21)
+    assert r.imag_residual <= 1e-10
+
+
+def test_region_and_dispatch_frozen_values(S):
+    ti = FROZEN["triangle_integrator"]
+    tab = S.table1_terms(S.wendland4())
+    kinds, args, refs, wants, floors, vals = [], [], [], [], [], []
+    for r in ti["regions"]:
+        kinds.append(REGION_KIND[r["kind"]]); args.append(r["args"] + [0] * (8 - len(r["args"])))
+        refs.append(ti["ref_verts"]); wants.append(r["want"]); floors.append(1e-3); vals.append(ti["ref_vals"])
+    for c in ti["dispatch"]:
+        kinds.append(7); args.append(c["verts"] + [0, 0]); refs.append(c["verts"]); wants.append(c["want"])
+        floors.append(2e-2); vals.append(ti["dispatch_values"])
+    raw = S.integrate_regions(kinds, args, refs, tab)
+    for k in range(len(kinds)):
+        got = [sum(vals[k][i] * raw[k][i][ch] for i in range(3)) for ch in range(3)]
+        for g, w in zip(got, wants[k]):
+            assert abs(g - w) <= 5e-12 * max(floors[k], abs(w)), (k, g, w)
+
+
+# ---------------------------------------------------------------------------
+# random configurations (the reference invariant-suite distribution)
+# ---------------------------------------------------------------------------
+def test_random_configs_vs_reference_outputs(S, ctx):
+    Q, T, V, H, R = (OUTS[k] for k in ("rand_q", "rand_tri", "rand_vals", "rand_h", "rand_out"))
+    tab = S.table1_terms(S.wendland4())
+    worst = 0.0
+    # evaluate each config at its own h through the batched API (n=1 calls)
+    got = np.zeros((Q.shape[0], 4))
+    for k in range(Q.shape[0]):
+        got[k] = S.integrate_pairs(Q[k], H[k], T[k], V[k], tab, ctx=ctx)[0]
+        worst = max(worst, OL.parity_ratio(got[k, :3], R[k, :3], OL.C4, H[k]))
+    assert worst <= 1.0, worst
+    assert np.all(got[:, 3] == 0.0)
+
+
+@pytest.mark.parametrize("h", [0.25, 0.8, 1.0, 2.0])
+def test_random_configs_fixed_h_vs_oracle(S, ctx, O, h):
+    rng = np.random.default_rng(int(h * 1000))
+    n = 20000
+    Q = np.zeros((n, 2)); T = np.zeros((n, 6)); V = np.zeros((n, 3))
+    for k in range(n):
+        T[k], V[k], Q[k], _ = OL.random_config(rng)
+    got = S.integrate_pairs(Q, h, T, V, S.table1_terms(S.wendland4()), ctx=ctx)
+    st, want = OL.oracle_pairs(O, np.arange(n), np.arange(n), Q, T, V, OL.W4, OL.C4, h)
+    assert st == 0
+    assert OL.parity_ratio(got[:, :3], want[:, :3], OL.C4, h) <= 1.0
+
+
+def test_bases_vs_oracle_and_combination(S, ctx, O):
+    rng = np.random.default_rng(9)
+    n = 4000
+    Q = np.zeros((n, 2)); T = np.zeros((n, 6)); V = np.zeros((n, 3))
+    for k in range(n):
+        T[k], V[k], Q[k], _ = OL.random_config(rng)
+    tab = S.table1_terms(S.wendland4())
+    B = S.integrate_pairs(Q, 0.9, T, None, tab, mode=1, ctx=ctx)
+    F = S.integrate_pairs(Q, 0.9, T, V, tab, ctx=ctx)
+    comb = np.einsum("ni,nic->nc", V, B[:, :, :3])
+    assert OL.parity_ratio(comb, F[:, :3], OL.C4, 0.9) <= 1.0
+    c = OL.arr(OL.W4)
+    for k in range(0, n, 40):
+        out = np.zeros(12)
+        assert O.oracle_integrate_bases(Q[k, 0], Q[k, 1], 0.9, OL.ptr(T[k]), OL.ptr(c), 9, OL.C4, OL.ptr(out)) == 0
+        assert OL.parity_ratio(B[k, :, :3], out.reshape(3, 4)[:, :3], OL.C4, 0.9) <= 1.0
+
+
+def test_orientation_independence_is_exact(S, ctx):
+    """test_triangle_integrator.cpp:523-548: all 6 vertex orders -> bitwise identical."""
+    rng = np.random.default_rng(90210)
+    n = 5000
+    Q = np.zeros((n, 2)); T = np.zeros((n, 6)); V = np.zeros((n, 3))
+    for k in range(n):
+        T[k], V[k], Q[k], _ = OL.random_config(rng)
+    tab = S.table1_terms(S.wendland4())
+    base = S.integrate_pairs(Q, 1.1, T, V, tab, ctx=ctx)
+    for perm in ([1, 2, 0], [2, 0, 1], [0, 2, 1], [2, 1, 0], [1, 0, 2]):
+        Tp = T.reshape(n, 3, 2)[:, perm].reshape(n, 6)
+        Vp = V[:, perm]
+        got = S.integrate_pairs(Q, 1.1, Tp, Vp, tab, ctx=ctx)
+        assert np.array_equal(got, base)
+
+
+# ---------------------------------------------------------------------------
+# benchmark configs
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("lin", [False, True])
+def test_cfg1_all_particles_vs_reference(S, ctx, lin):
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg1(linear_field=lin)
+    k = sc.kernels[0]
+    v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), tri_values=sc.values, ctx=ctx)
+    R = OUTS[f"cfg1_{'lin' if lin else 'one'}"]
+    got = np.concatenate([v[:, None], g], axis=1)
+    assert OL.parity_ratio(got, R[:, :3], k.normalization, sc.h) <= 1.0
+    assert int(np.sum(np.any(R[:, :3] != 0, axis=1))) <= st.n_pairs <= sc.particles.shape[0]
+
+
+@pytest.mark.parametrize("lin", [False, True])
+def test_cfg2_sample_vs_reference(S, ctx, lin):
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg2(linear_field=lin)
+    idx = OUTS[f"cfg2_{'lin' if lin else 'one'}_idx"]
+    R = OUTS[f"cfg2_{'lin' if lin else 'one'}"]
+    k = sc.kernels[0]
+    pp, pt = sc.pairs[0][idx], sc.pairs[1][idx]
+    vals = sc.values[pt] if sc.values is not None else np.ones((idx.shape[0], 3))
+    got = S.integrate_pairs(sc.particles[pp], sc.h, sc.triangles[pt], vals, table_of(S, k), ctx=ctx)
+    assert OL.parity_ratio(got[:, :3], R[:, :3], k.normalization, sc.h) <= 1.0
+
+
+def test_cfg2_full_scene_vs_oracle_sample_and_properties(S, ctx, O):
+    """All 4,194,304 own-triangle pairs on the GPU; a 65,536-pair seeded sample
+    against the oracle; size-independent properties at full size: determinism
+    (bitwise repeatability) and exact vertex-order invariance."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg2(linear_field=True)
+    k = sc.kernels[0]
+    tab = table_of(S, k)
+    v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, tab, tri_values=sc.values, pairs=sc.pairs, ctx=ctx)
+    assert st.n_pairs == 4194304 and st.status_bits == 0
+    v2, g2, _ = S.evaluate(sc.particles, sc.h, sc.triangles, tab, tri_values=sc.values, pairs=sc.pairs, ctx=ctx)
+    assert np.array_equal(v, v2) and np.array_equal(g, g2)
+    n = sc.particles.shape[0]
+    idx = np.sort(np.random.default_rng(2).choice(n, 65536, replace=False))
+    st_o, want = OL.oracle_pairs(O, idx, sc.pairs[1][idx], sc.particles, sc.triangles, sc.values, k.coefficients,
+                                 k.normalization, sc.h, threads=16)
+    assert st_o == 0
+    got = np.concatenate([v[idx, None], g[idx]], axis=1)
+    assert OL.parity_ratio(got, want[:, :3], k.normalization, sc.h) <= 1.0
+    # reversed vertex order of every triangle (values permuted alike): bitwise identical
+    Tr = sc.triangles.reshape(-1, 3, 2)[:, [0, 2, 1]].reshape(-1, 6)
+    Vr = sc.values[:, [0, 2, 1]]
+    v3, g3, _ = S.evaluate(sc.particles, sc.h, Tr, tab, tri_values=Vr, pairs=sc.pairs, ctx=ctx)
+    assert np.array_equal(v3, v) and np.array_equal(g3, g)
+
+
+def test_explicit_pairs_unsorted_and_duplicated(S, ctx):
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg2(T=512, per_tri=8)
+    tab = table_of(S, sc.kernels[0])
+    v, g, _ = S.evaluate(sc.particles, sc.h, sc.triangles, tab, pairs=sc.pairs, ctx=ctx)
+    perm = np.random.default_rng(4).permutation(sc.pairs[0].shape[0])
+    pp = np.concatenate([sc.pairs[0][perm], sc.pairs[0][:7]])
+    pt = np.concatenate([sc.pairs[1][perm], sc.pairs[1][:7]])
+    v2, g2, _ = S.evaluate(sc.particles, sc.h, sc.triangles, tab, pairs=(pp, pt), ctx=ctx)
+    expect_v = v.copy()
+    expect_g = g.copy()
+    expect_v[:7] *= 2
+    expect_g[:7] *= 2
+    assert np.allclose(v2, expect_v, rtol=1e-15, atol=0) and np.allclose(g2, expect_g, rtol=1e-15, atol=0)
+    with pytest.raises(S.InvalidArgument):
+        S.evaluate(sc.particles, sc.h, sc.triangles, tab, pairs=(np.array([0]), np.array([10 ** 6])), ctx=ctx)
+
+
+def _cpu_pairs(O, P, T, h):
+    cap = 4_000_000
+    buf = np.zeros((cap, 2), dtype=np.int64)
+    n = O.oracle_find_pairs(0, P.shape[0], OL.ptr(OL.arr(P)), T.shape[0], OL.ptr(OL.arr(T)), h, OL.ptr(buf), cap)
+    assert n <= cap
+    return buf[:n]
+
+
+def test_cfg3_cell_list_pairs_bit_exact_and_parity(S, ctx, O):
+    """Star-shaped boundary strip (8,192 triangles), Wendland C6, h = 0.01: the
+    device cell list must find exactly the brute-force pair list (exact
+    predicate), and the per-particle sums must match the oracle. Run on the
+    particles of a seeded window (the full 1M-particle scene runs in the bench)."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg3()
+    # particles within 3h of the wall, plus 2000 deep interior ones
+    r = np.hypot(sc.particles[:, 0], sc.particles[:, 1])
+    near = np.argsort(-r)[:30000]
+    far = np.random.default_rng(0).choice(sc.particles.shape[0], 2000, replace=False)
+    P = sc.particles[np.unique(np.concatenate([near, far]))]
+    k = sc.kernels[0]
+    v, g, st, plist = S.evaluate(P, sc.h, sc.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
+    ref_pairs = _cpu_pairs(O, P, sc.triangles, sc.h)
+    assert plist.shape == ref_pairs.shape and np.array_equal(plist, ref_pairs)
+    st_o, vo, go = OL.oracle_scene_sums(O, P, sc.triangles, None, k.coefficients, k.normalization, sc.h,
+                                        ref_pairs[:, 0], ref_pairs[:, 1], threads=16)
+    assert st_o == 0
+    got = np.concatenate([v[:, None], g], axis=1)
+    want = np.concatenate([vo[:, None], go], axis=1)
+    assert OL.parity_ratio(got, want, k.normalization, sc.h) <= 1.0
+
+
+def test_cfg3_full_scene_runs_and_interior_is_zero(S, ctx):
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg3()
+    k = sc.kernels[0]
+    v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), ctx=ctx)
+    assert st.status_bits == 0 and st.n_pairs > 10000
+    r = np.hypot(sc.particles[:, 0], sc.particles[:, 1])
+    deep = r < 0.8 * sc.info["r0"]
+    assert np.all(v[deep] == 0.0) and np.all(g[deep] == 0.0)
+    assert np.all(v >= -1e-12) and np.all(v <= 1.0 + 1e-12)
+
+
+@pytest.mark.parametrize("kernel", ["wendland_c2", "cubic_spline"])
+def test_cfg5_reduced_scene(S, ctx, O, kernel):
+    """cfg5 structure (Delaunay obstacle discs, uniform particles, h = 0.1) at
+    reduced size: pair list bit-exact and per-particle parity, for Wendland C2
+    and the 2-piece cubic spline (two passes, outer at h + inner at h/2)."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5(n_particles=60_000, n_discs=6, target_tris=20_000, domain=12.0)
+    kernels = [sc.kernels[0]] if kernel == "wendland_c2" else sc.kernels[1:]
+    tv = np.zeros(sc.particles.shape[0])
+    tg = np.zeros((sc.particles.shape[0], 2))
+    wv = np.zeros_like(tv)
+    wg = np.zeros_like(tg)
+    for k in kernels:
+        h = sc.h * k.support_scale
+        v, g, st, plist = S.evaluate(sc.particles, h, sc.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
+        ref_pairs = _cpu_pairs(O, sc.particles, sc.triangles, h)
+        assert np.array_equal(plist, ref_pairs)
+        st_o, vo, go = OL.oracle_scene_sums(O, sc.particles, sc.triangles, None, k.coefficients, k.normalization, h,
+                                            ref_pairs[:, 0], ref_pairs[:, 1], threads=16)
+        assert st_o == 0
+        tv += v; tg += g; wv += vo; wg += go
+    k0 = kernels[0]
+    got = np.concatenate([tv[:, None], tg], axis=1)
+    want = np.concatenate([wv[:, None], wg], axis=1)
+    assert OL.parity_ratio(got, want, k0.normalization, sc.h) <= 1.0
+
+
+def test_generic_degree12_kernel_linear_field(S, ctx, O):
+    """cfg4's kernel (sum_{k<=12} c_k q^k, c_k ~ N(0,1), normalised) on the
+    cfg3 mesh with a linear field (the P3 field is not in the reference)."""
+    from paper_2507_21686_b200 import scenes
+    rng = np.random.default_rng(scenes.SEED_BASE + 4)
+    k = scenes.generic_deg12(rng)
+    sc = scenes.cfg3(target_particles=200_000)
+    vals = rng.standard_normal((sc.triangles.shape[0], 3))
+    r = np.hypot(sc.particles[:, 0], sc.particles[:, 1])
+    P = sc.particles[np.argsort(-r)[:20000]]
+    v, g, st, plist = S.evaluate(P, sc.h, sc.triangles, table_of(S, k), tri_values=vals, ctx=ctx, return_pairs=True)
+    st_o, vo, go = OL.oracle_scene_sums(O, P, sc.triangles, vals, k.coefficients, k.normalization, sc.h,
+                                        plist[:, 0], plist[:, 1], threads=16)
+    assert st_o == 0
+    got = np.concatenate([v[:, None], g], axis=1)
+    want = np.concatenate([vo[:, None], go], axis=1)
+    assert OL.parity_ratio(got, want, k.normalization, sc.h) <= 1.0
+
+
+# ---------------------------------------------------------------------------
+# error contracts, counters, edge cases
+# ---------------------------------------------------------------------------
+def test_error_contracts(S, ctx):
+    tab = S.table1_terms(S.wendland4())
+    tri = S.Triangle(S.Point2(0.31, -0.12), S.Point2(1.1, 0.55), S.Point2(-0.2, 0.9))
+    with pytest.raises(S.DomainError):
+        S.integrate_triangle(S.Point2(0, 0), 0.0, tri, [1, 1, 1], tab)
+    with pytest.raises(S.DomainError):
+        S.integrate_triangle(S.Point2(0, 0), -1.0, tri, [1, 1, 1], tab)
+    with pytest.raises(S.InvalidArgument):
+        S.integrate_triangle(S.Point2(0, 0), 0.8, tri, tab)
+    tri.values = [2.0, -0.5, 1.3]
+    a = S.integrate_triangle(S.Point2(0.05, -0.03), 0.8, tri, tab)
+    b = S.integrate_triangle(S.Point2(0.05, -0.03), 0.8, tri, [2.0, -0.5, 1.3], tab)
+    assert a.value == b.value
+    with pytest.raises(S.DomainError):
+        S.integrate_segment(S.Point2(0, 0), S.Point2(0.5, 0.5), S.Point2(0.5, 0.5), tri, [1, 1, 1], tab)
+    with pytest.raises(S.DomainError):
+        S.integrate_sector(S.Point2(0, 0), S.Point2(0, 1), 1.0, tri, [1, 1, 1], tab)
+
+
+def test_empty_and_edge_inputs(S, ctx):
+    tab = S.table1_terms(S.wendland4())
+    out = S.integrate_pairs(np.zeros((0, 2)), 1.0, np.zeros((0, 6)), np.zeros((0, 3)), tab, ctx=ctx)
+    assert out.shape == (0, 4)
+    v, g, st = S.evaluate(np.zeros((0, 2)), 0.1, np.zeros((5, 6)), tab, ctx=ctx)
+    assert v.shape == (0,) and st.n_pairs == 0
+    v, g, st = S.evaluate(np.array([[0.5, 0.5]]), 0.1, np.zeros((0, 6)), tab, ctx=ctx)
+    assert v[0] == 0.0
+    # degenerate (collinear) triangle: exactly zero; far triangle: exactly zero
+    r = S.integrate_pairs([[0, 0], [0, 0]], 1.0, [[0, 0, 0.5, 0.5, 1, 1], [5, 5, 7, 5.5, 5.5, 7]],
+                          [[1, 2, 3], [1, 2, 3]], tab, ctx=ctx)
+    assert np.all(r == 0.0)
+    # enclosing triangle == full disc: unit mass for field 1
+    r = S.integrate_pairs([[0, 0]], 1.0, [[-9, -7, 9, -7, 0, 11]], [[1, 1, 1]], tab, ctx=ctx)
+    assert abs(r[0, 0] - 1.0) < 5e-15 and abs(r[0, 1]) < 1e-15 and abs(r[0, 2]) < 1e-15
+
+
+def test_branch_coverage_all_routes(S, ctx):
+    """Every BranchCounters route fires on the device over the reference
+    suite's own configurations (test_triangle_integrator.cpp:704-727)."""
+    c = S.Context(0)
+    c.enable_counters(True)
+    c.read_counters(reset=True)
+    tab = S.table1_terms(S.wendland4())
+    ti = FROZEN["triangle_integrator"]
+    kinds, args, refs = [], [], []
+    for cfg in ti["dispatch"]:
+        kinds.append(7); args.append(cfg["verts"] + [0, 0]); refs.append(cfg["verts"])
+    for r in ti["regions"]:
+        kinds.append(REGION_KIND[r["kind"]]); args.append(r["args"] + [0] * (8 - len(r["args"]))); refs.append(ti["ref_verts"])
+    ref = ti["ref_verts"]
+    for k, a in ((2, [0.0, -1.5, 0.0, 1.5, -0.7, 0.0]), (2, [-1.0, -2.0, -1.0, 2.0, 1.0, 0.0]),
+                 (2, [1.0, -2.0, 1.0, 2.0, 2.0, 0.0]), (3, [0.8, 0.4, 0.4, 0.2])):
+        kinds.append(k); args.append(a + [0] * (8 - len(a))); refs.append(ref)
+    S.integrate_regions(kinds, args, refs, tab, ctx=c)
+    Q = [[0, 0]] * 4
+    T = [[0, 0, 0.5, 0.5, 1, 1], [-9, -7, 9, -7, 0, 11], [5, 5, 7, 5.5, 5.5, 7], [1.0 + 1.2e-12, 0, 5, 0, 1.5, 0.5]]
+    S.integrate_pairs(Q, 1.0, T, [[1, 1, 1]] * 4, tab, ctx=c)
+    rng = np.random.default_rng(1)
+    n = 400
+    Qr = np.zeros((n, 2)); Tr = np.zeros((n, 6)); Vr = np.zeros((n, 3))
+    for i in range(n):
+        Tr[i], Vr[i], Qr[i], _ = OL.random_config(rng)
+    S.integrate_pairs(Qr, 1.0, Tr, Vr, tab, ctx=c)
+    counts = c.read_counters(reset=True)
+    c.close()
+    assert all(int(x) > 0 for x in counts), dict(zip(S.COUNTER_NAMES, counts))
