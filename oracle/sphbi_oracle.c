@@ -499,7 +499,7 @@ typedef struct {
 } ATerm;
 typedef struct {
   int nslots, nterms, max_radial_power;
-  Term slots[3 * (kMaxKernelDegree + 3)];
+  Term slots[5 * (kMaxKernelDegree + 1) + 8]; /* p: N+1, c1/s1: N+2 each, c2/s2: N each */
   ATerm terms[11 * (kMaxKernelDegree + 1)];
   double normalization;
 } Table;
@@ -663,7 +663,7 @@ static Basis assemble_region(const Table* table, Mat2 frame, const P2* ref, cons
   t1[2] = -t1[0] - t1[1];
   t2[2] = -t2[0] - t2[1];
   for (int i = 0; i < 3; ++i) t3[i] = (i == 2 ? 1.0L : 0.0L) - t1[i] * tvx[2] - t2[i] * tvy[2];
-  LC sv[3 * (kMaxKernelDegree + 3)];
+  LC sv[5 * (kMaxKernelDegree + 1) + 8];
   for (int s = 0; s < table->nslots; ++s) sv[s] = fam_eval(fam, table->slots[s]);
   LC v[3] = {0, 0, 0}, gxp[3] = {0, 0, 0}, gyp[3] = {0, 0, 0};
   for (int k = 0; k < table->nterms; ++k) {

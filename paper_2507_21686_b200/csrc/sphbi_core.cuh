@@ -435,63 +435,147 @@ SPHBI_HD void segment_sums(const KernelConsts& K, double d, S9& S) {
 }
 
 // ---------------------------------------------------------------------------
-// region evaluation context
+// region decomposition, written once and parameterised by a Sink
 // ---------------------------------------------------------------------------
-struct RegionCtx {
-  const KernelConsts* K;
-  PairAcc acc;
-  unsigned status;
-  unsigned long long* counters;  // nullable: kNumCounters slots
-  int n_regions;                 // elementary region evaluations (work metric)
-};
+// The geometry below (triangle_integrator.hpp:335-674) decides WHICH
+// elementary pieces a pair needs; a Sink decides what to do with each piece:
+//   EvalSink   evaluates it on the spot (single pairs, region test surface)
+//   the device count/emit sinks (sphbi_cuda.cu) queue it as a work item so
+//   that pieces of one kind are evaluated together by converged warps.
+// Piece vocabulary (all in the normalized frame, with a sign +-1):
+//   disc(sign)                      full unit disc, identity frame
+//   half_disc(f, sign)              half disc, frame f
+//   cone(f, gamma, L, sign)         sector [0,gamma] x [0,L]      (L <= 1)
+//   bound(f, x, D, beta, sign)      stub radial-window antiderivative at x
+//   segment(f, d, sign)             chord segment {x >= d}, 0 < d < 1
+// Counters mirror BranchCounters; status bits mirror the reference's throws.
 
-SPHBI_HD void bump(RegionCtx& c, int which) {
-  if (c.counters) {
+// ---------------------------------------------------------------------------
+// direct evaluation of pieces (math above), accumulated into a PairAcc
+// ---------------------------------------------------------------------------
+SPHBI_HD void piece_disc(const KernelConsts& K, PairAcc& acc, double sign) {
+  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
+  const dd v3 = dd_mul(K.pv1, pi2);
+  const dd g = dd_mul(K.pg1, pi2);
+  acc.v3 = dd_add(acc.v3, dd_scale(v3, sign));
+  acc.g11 = dd_add(acc.g11, dd_scale(g, sign));
+  acc.g22 = dd_add(acc.g22, dd_scale(g, sign));
+}
+
+// half disc (elementary_regions.hpp:96-112): p = pi/(n+1), c_a = 2 sin(a pi/2)/a/(n+1), s = 0
+SPHBI_HD void piece_half_disc(const KernelConsts& K, PairAcc& acc, const Frame& f, double sign) {
+  const dd pi{kPiHi, kPiLo};
+  const dd z{0.0, 0.0};
+  S9 S;
+  S.v3 = dd_mul(K.pv1, pi);
+  S.v1 = dd_mul_d(K.qv1, 2.0);
+  S.v2 = z;
+  S.gx1 = dd_mul(K.pg1, pi);
+  S.gy2 = S.gx1;
+  S.gx2 = z;
+  S.gy1 = z;
+  S.gx3 = dd_mul_d(K.rg1, 2.0);
+  S.gy3 = z;
+  acc_add_region(acc, S, f, sign);
+}
+
+SPHBI_HDNI void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double L,
+                           double sign) {
+  S9 S;
+  if (L >= 1.0) {
+    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+  } else {
+    const int N = K.deg;
+    cone_sums(K, gamma, poly_dd(K.pv, N, L, 2), poly_dd(K.qv, N, L, 3), poly_dd(K.pg, N, L, 2),
+              poly_dd(K.rg, N, L, 1), S);
+  }
+  acc_add_region(acc, S, f, sign);
+}
+
+SPHBI_HDNI void piece_bound(const KernelConsts& K, PairAcc& acc, const Frame& f, double x, double D,
+                            double beta, double sign) {
+  double sb, cb;
+  dsincos(beta, &sb, &cb);
+  const double s2b = 2.0 * sb * cb;
+  const double c2b = (cb - sb) * (cb + sb);
+  S9 S;
+  stub_bound_sums(K, x, D, beta, cb, sb, c2b, s2b, S);
+  acc_add_region(acc, S, f, sign);
+}
+
+SPHBI_HDNI void piece_segment(const KernelConsts& K, PairAcc& acc, const Frame& f, double d, double sign) {
+  S9 S;
+  segment_sums(K, d, S);
+  acc_add_region(acc, S, f, sign);
+}
+
+// region_disc(l) for l < 1 (cone over [0, 2pi] of radius l): test surface only.
+SPHBI_HD void piece_disc_l(const KernelConsts& K, PairAcc& acc, double l, double sign) {
+  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
+  const dd v3 = dd_mul(poly_dd(K.pv, K.deg, l, 2), pi2);
+  const dd g = dd_mul(poly_dd(K.pg, K.deg, l, 2), pi2);
+  acc.v3 = dd_add(acc.v3, dd_scale(v3, sign));
+  acc.g11 = dd_add(acc.g11, dd_scale(g, sign));
+  acc.g22 = dd_add(acc.g22, dd_scale(g, sign));
+}
+
+SPHBI_HD void bump_counter(unsigned long long* counters, int which) {
+  if (counters) {
 #if defined(__CUDA_ARCH__)
-    atomicAdd(c.counters + which, 1ull);
+    atomicAdd(counters + which, 1ull);
 #else
-    c.counters[which] += 1;
+    counters[which] += 1;
 #endif
   }
 }
 
-// region_disc(1.0): full unit disc, identity frame (:335-347, :88-94).
-SPHBI_HD void region_disc(RegionCtx& c, double sign) {
-  const KernelConsts& K = *c.K;
-  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
-  const dd v3 = dd_mul(K.pv1, pi2);
-  const dd g = dd_mul(K.pg1, pi2);
-  c.acc.v3 = dd_add(c.acc.v3, dd_scale(v3, sign));
-  c.acc.g11 = dd_add(c.acc.g11, dd_scale(g, sign));
-  c.acc.g22 = dd_add(c.acc.g22, dd_scale(g, sign));
-  c.n_regions += 1;
-}
-
-// region_disc(l) for l < 1 (cone over [0, 2pi] of radius l): test surface.
-SPHBI_HD void region_disc_l(RegionCtx& c, double l, double sign) {
-  if (l >= 1.0) {
-    region_disc(c, sign);
-    return;
+struct EvalSink {
+  const KernelConsts* K;
+  PairAcc acc;
+  unsigned status;
+  unsigned long long* counters;
+  int n_regions;
+  SPHBI_HD void bump(int which) { bump_counter(counters, which); }
+  SPHBI_HD void disc(double sign) {
+    piece_disc(*K, acc, sign);
+    ++n_regions;
   }
-  const KernelConsts& K = *c.K;
-  const dd pi2{2.0 * kPiHi, 2.0 * kPiLo};
-  const dd v3 = dd_mul(poly_dd(K.pv, K.deg, l, 2), pi2);
-  const dd g = dd_mul(poly_dd(K.pg, K.deg, l, 2), pi2);
-  c.acc.v3 = dd_add(c.acc.v3, dd_scale(v3, sign));
-  c.acc.g11 = dd_add(c.acc.g11, dd_scale(g, sign));
-  c.acc.g22 = dd_add(c.acc.g22, dd_scale(g, sign));
-  c.n_regions += 1;
+  SPHBI_HD void half_disc(const Frame& f, double sign) {
+    piece_half_disc(*K, acc, f, sign);
+    ++n_regions;
+  }
+  SPHBI_HD void cone(const Frame& f, double gamma, double L, double sign) {
+    piece_cone(*K, acc, f, gamma, L, sign);
+    ++n_regions;
+  }
+  SPHBI_HD void bound(const Frame& f, double x, double D, double beta, double sign) {
+    piece_bound(*K, acc, f, x, D, beta, sign);
+  }
+  SPHBI_HD void segment(const Frame& f, double d, double sign) {
+    piece_segment(*K, acc, f, d, sign);
+    ++n_regions;
+  }
+};
+
+SPHBI_HD void eval_sink_init(EvalSink& s, const KernelConsts* K, unsigned long long* counters) {
+  s.K = K;
+  acc_zero(s.acc);
+  s.status = kStatusOk;
+  s.counters = counters;
+  s.n_regions = 0;
 }
 
 // Proper rotation taking v onto +x (:202-207).
-SPHBI_HD Frame rotation_taking_to_x(P2 v, RegionCtx& c) {
+template <class Sink>
+SPHBI_HD Frame rotation_taking_to_x(P2 v, Sink& c) {
   const double n = p_norm(v);
   if (n < kGeomEps) c.status |= kStatusDomain;
   return Frame{v.x / n, v.y / n, -v.y / n, v.x / n};
 }
 
 // region_sector(v1, v2, l) (:349-366); the hot path always passes l = 1.
-SPHBI_HD void region_sector(RegionCtx& c, P2 v1, P2 v2, double sign, double l = 1.0) {
+template <class Sink>
+SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) {
   Frame f = rotation_taking_to_x(v1, c);
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -500,21 +584,12 @@ SPHBI_HD void region_sector(RegionCtx& c, P2 v1, P2 v2, double sign, double l = 
     w2.y = -w2.y;
   }
   const double gamma = atan2(w2.y, w2.x);
-  const KernelConsts& K = *c.K;
-  S9 S;
-  if (l >= 1.0) {
-    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
-  } else {
-    const int N = K.deg;
-    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
-              poly_dd(K.rg, N, l, 1), S);
-  }
-  acc_add_region(c.acc, S, f, sign);
-  c.n_regions += 1;
+  c.cone(f, gamma, fmin(l, 1.0), sign);
 }
 
 // region_segment(t0, t1, q_keep) (:369-423).
-SPHBI_HD void region_segment(RegionCtx& c, P2 t0, P2 t1, P2 q_keep, double sign) {
+template <class Sink>
+SPHBI_HD void region_segment(Sink& c, P2 t0, P2 t1, P2 q_keep, double sign) {
   const P2 e = p_sub(t1, t0);
   const double len = p_norm(e);
   if (len < kGeomEps) {
@@ -525,57 +600,34 @@ SPHBI_HD void region_segment(RegionCtx& c, P2 t0, P2 t1, P2 q_keep, double sign)
   if (p_dot(p_sub(q_keep, t0), n) < 0.0) n = P2{-n.x, -n.y};
   const double d = p_dot(t0, n);
   if (d >= 1.0 - kGeomEps) {
-    bump(c, kSegmentEmpty);
+    c.bump(kSegmentEmpty);
     return;
   }
   if (d <= -1.0 + kGeomEps) {
-    bump(c, kSegmentFullDisc);
-    region_disc(c, sign);
+    c.bump(kSegmentFullDisc);
+    c.disc(sign);
     return;
   }
-  const KernelConsts& K = *c.K;
   if (fabs(d) < 1e-9) {
-    bump(c, kSegmentHalfDisc);
-    // half disc (elementary_regions.hpp:96-112): p = pi/(n+1), c_a = 2 sin(a pi/2)/a/(n+1)
-    const Frame f{n.x, n.y, -n.y, n.x};
-    const dd pi{kPiHi, kPiLo};
-    const dd z{0.0, 0.0};
-    S9 S;
-    S.v3 = dd_mul(K.pv1, pi);
-    S.v1 = dd_mul_d(K.qv1, 2.0);
-    S.v2 = z;
-    S.gx1 = dd_mul(K.pg1, pi);
-    S.gy2 = S.gx1;
-    S.gx2 = z;
-    S.gy1 = z;
-    S.gx3 = dd_mul_d(K.rg1, 2.0);
-    S.gy3 = z;
-    acc_add_region(c.acc, S, f, sign);
-    c.n_regions += 1;
+    c.bump(kSegmentHalfDisc);
+    c.half_disc(Frame{n.x, n.y, -n.y, n.x}, sign);
     return;
   }
-  bump(c, kSegmentGeneral);
+  c.bump(kSegmentGeneral);
   if (d < 0.0) {
     // origin-side segment: whole disc minus the far-side complement
     const P2 nc{-n.x, -n.y};
-    const Frame f{nc.x, nc.y, -nc.y, nc.x};
-    region_disc(c, sign);
-    S9 S;
-    segment_sums(K, -d, S);
-    acc_add_region(c.acc, S, f, -sign);
-    c.n_regions += 1;
+    c.disc(sign);
+    c.segment(Frame{nc.x, nc.y, -nc.y, nc.x}, -d, -sign);
     return;
   }
-  const Frame f{n.x, n.y, -n.y, n.x};
-  S9 S;
-  segment_sums(K, d, S);
-  acc_add_region(c.acc, S, f, sign);
-  c.n_regions += 1;
+  c.segment(Frame{n.x, n.y, -n.y, n.x}, d, sign);
 }
 
 // Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
-SPHBI_HDNI void stub_direct(RegionCtx& c, P2 v1, P2 v2, double r1, double r2, double area2,
-                            P2 b, double sign) {
+template <class Sink>
+SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double area2, P2 b,
+                          double sign) {
   Frame f = rotation_taking_to_x(v1, c);
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -591,40 +643,23 @@ SPHBI_HDNI void stub_direct(RegionCtx& c, P2 v1, P2 v2, double r1, double r2, do
   const double beta = atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
   double lo = fmax(l, D);
   if (lo - D <= 256.0 * kDblEps * D) lo = D;
-  const KernelConsts& K = *c.K;
-  const int N = K.deg;
-  S9 S;
-  if (l >= 1.0) {
-    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
-  } else {
-    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
-              poly_dd(K.rg, N, l, 1), S);
-  }
+  c.cone(f, gamma, l, sign);
   if (u > lo + kGeomEps) {
     // stub_integral validation (elementary_regions.hpp:179-183)
     if (!(beta >= 0.0 && beta < kHalfPiHi)) c.status |= kStatusDomain;
-    double sb, cb;
-    dsincos(beta, &sb, &cb);
-    const double s2b = 2.0 * sb * cb;
-    const double c2b = (cb - sb) * (cb + sb);
-    S9 hi, lo_s;
-    stub_bound_sums(K, u, D, beta, cb, sb, c2b, s2b, hi);
-    stub_bound_sums(K, lo, D, beta, cb, sb, c2b, s2b, lo_s);
-    s9_sub(hi, lo_s);
-    s9_add(S, hi);
+    c.bound(f, u, D, beta, sign);
+    c.bound(f, lo, D, beta, -sign);
   }
-  acc_add_region(c.acc, S, f, sign);
-  c.n_regions += 1;
 }
 
 // region_stub(v1, v2) (:426-484): triangle (origin, v1, v2) clipped to the
 // disc; the perpendicular-foot split is unrolled with a small stack.
-SPHBI_HDNI void region_stub(RegionCtx& c, P2 v1_in, P2 v2_in, double sign) {
+template <class Sink>
+SPHBI_HDNI void region_stub(Sink& c, P2 v1_in, P2 v2_in, double sign) {
   P2 st1[8], st2[8];
-  int top = 0;
   st1[0] = v1_in;
   st2[0] = v2_in;
-  top = 1;
+  int top = 1;
   while (top > 0) {
     --top;
     P2 v1 = st1[top], v2 = st2[top];
@@ -639,17 +674,17 @@ SPHBI_HDNI void region_stub(RegionCtx& c, P2 v1_in, P2 v2_in, double sign) {
     }
     const double area2 = p_cross(v1, v2);
     if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
-      bump(c, kStubDegenerate);
+      c.bump(kStubDegenerate);
       continue;
     }
     const P2 b = p_sub(v1, v2);
     const double dot_a = -(v2.x * b.x + v2.y * b.y);
     if (dot_a <= kGeomEps) {
-      bump(c, kStubDirect);
+      c.bump(kStubDirect);
       stub_direct(c, v1, v2, r1, r2, area2, b, sign);
       continue;
     }
-    bump(c, kStubSplit);
+    c.bump(kStubSplit);
     const double t = dot_a / p_norm2(b);
     const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
     if (top + 2 > 8) {
@@ -694,7 +729,8 @@ SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
 }
 
 // region_wedge (:514-603)
-SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
+template <class Sink>
+SPHBI_HDNI void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
   if (signed_area(n0, n1, n2) < 0.0) {
     const P2 t = n1;
     n1 = n2;
@@ -708,11 +744,11 @@ SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
   const bool origin_inside = point_in_triangle(origin, n0, n1, n2);
   if (x01.count == 0 && x02.count == 0 && x12.count == 0) {
     if (origin_inside) {
-      bump(c, kWedgeNoCrossingsDisc);
-      region_disc(c, sign);
+      c.bump(kWedgeNoCrossingsDisc);
+      c.disc(sign);
       return;
     }
-    bump(c, kWedgeNoCrossingsZero);
+    c.bump(kWedgeNoCrossingsZero);
     return;
   }
   const int crossing_edges = (x01.count > 0 ? 1 : 0) + (x02.count > 0 ? 1 : 0) +
@@ -732,12 +768,12 @@ SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
       count = x12.count;
     }
     if (count == 2) {
-      bump(c, kWedgeSingleEdgeSegment);
+      c.bump(kWedgeSingleEdgeSegment);
       region_segment(c, e0, e1, opp, sign);
       return;
     }
-    bump(c, kWedgeLoneTouch);
-    if (origin_inside) region_disc(c, sign);
+    c.bump(kWedgeLoneTouch);
+    if (origin_inside) c.disc(sign);
     return;
   }
   if (x01.count == 0 || x02.count == 0) {
@@ -761,7 +797,7 @@ SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
     x02 = segment_circle_crossings(n0, n2);
     x12 = segment_circle_crossings(n1, n2);
   }
-  bump(c, kWedgeGeneral);
+  c.bump(kWedgeGeneral);
   // x01 / x02 could in principle lose their crossings after relabeling; the
   // reference would then read points[-1] (UB). Flag instead of reading.
   if (x01.count == 0 || x02.count == 0) {
@@ -775,9 +811,9 @@ SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
     if (arc_orient > 0.0) {
       region_sector(c, s1, s2, sign);
     } else {
-      bump(c, kWedgeReflexDisc);
+      c.bump(kWedgeReflexDisc);
       region_sector(c, s1, s2, -sign);
-      region_disc(c, sign);
+      c.disc(sign);
     }
   }
   const double stub_a = signed_area(origin, n0, s1);
@@ -785,14 +821,15 @@ SPHBI_HDNI void region_wedge(RegionCtx& c, P2 n0, P2 n1, P2 n2, double sign) {
   const double stub_b = signed_area(origin, s2, n0);
   if (fabs(stub_b) > kGeomEps) region_stub(c, s2, n0, stub_b > 0.0 ? sign : -sign);
   if (x12.count == 2) {
-    bump(c, kWedgeCapSubtracted);
+    c.bump(kWedgeCapSubtracted);
     const P2 mirror{n1.x + n2.x - n0.x, n1.y + n2.y - n0.y};
     region_segment(c, n1, n2, mirror, -sign);
   }
 }
 
 // region_t2 (:607-616)
-SPHBI_HD void region_t2(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
+template <class Sink>
+SPHBI_HD void region_t2(Sink& c, P2 a, P2 b, P2 cc, double sign) {
   if (signed_area(a, b, cc) < 0.0) {
     const P2 t = a;
     a = b;
@@ -806,7 +843,8 @@ SPHBI_HD void region_t2(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
 }
 
 // region_t3 (:620-632)
-SPHBI_HD void region_t3(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
+template <class Sink>
+SPHBI_HD void region_t3(Sink& c, P2 a, P2 b, P2 cc, double sign) {
   if (signed_area(a, b, cc) < 0.0) {
     const P2 t = b;
     b = cc;
@@ -823,9 +861,10 @@ SPHBI_HD void region_t3(RegionCtx& c, P2 a, P2 b, P2 cc, double sign) {
 }
 
 // integrate_normalized (:637-674). Returns false for the degenerate route.
-SPHBI_HD bool integrate_normalized(RegionCtx& c, const P2* v) {
+template <class Sink>
+SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
   if (fabs(signed_area(v[0], v[1], v[2])) < kGeomEps) {
-    bump(c, kDispatchDegenerate);
+    c.bump(kDispatchDegenerate);
     return false;
   }
   const double r[3] = {p_norm(v[0]), p_norm(v[1]), p_norm(v[2])};
@@ -834,7 +873,7 @@ SPHBI_HD bool integrate_normalized(RegionCtx& c, const P2* v) {
   for (int i = 0; i < 3; ++i)
     if (r[i] <= 1.0 + kOnCircleTol) inside[inside_count++] = i;
   if (inside_count == 0) {
-    bump(c, kDispatchWedgeOutside);
+    c.bump(kDispatchWedgeOutside);
     int i0 = 0;
     if (r[1] < r[i0]) i0 = 1;
     if (r[2] < r[i0]) i0 = 2;
@@ -842,18 +881,18 @@ SPHBI_HD bool integrate_normalized(RegionCtx& c, const P2* v) {
     return true;
   }
   if (inside_count == 1) {
-    bump(c, kDispatchWedgeSingle);
+    c.bump(kDispatchWedgeSingle);
     const int i0 = inside[0];
     region_wedge(c, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
     return true;
   }
   if (inside_count == 2) {
-    bump(c, kDispatchTwoInside);
+    c.bump(kDispatchTwoInside);
     const int outside = 3 - inside[0] - inside[1];
     region_t2(c, v[inside[0]], v[inside[1]], v[outside], 1.0);
     return true;
   }
-  bump(c, kDispatchThreeInside);
+  c.bump(kDispatchThreeInside);
   region_t3(c, v[0], v[1], v[2], 1.0);
   return true;
 }
@@ -954,12 +993,8 @@ SPHBI_HD unsigned eval_pair(const KernelConsts& K, double qx, double qy, double 
   canonicalize(v, perm);
   P2 nv[3];
   for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
-  RegionCtx c;
-  c.K = &K;
-  acc_zero(c.acc);
-  c.status = kStatusOk;
-  c.counters = counters;
-  c.n_regions = 0;
+  EvalSink c;
+  eval_sink_init(c, &K, counters);
   const bool nondeg = integrate_normalized(c, nv);
   if (n_regions) *n_regions = c.n_regions;
   HatPlanes H;
@@ -995,17 +1030,17 @@ SPHBI_HD unsigned eval_pair(const KernelConsts& K, double qx, double qy, double 
 SPHBI_HD unsigned eval_region(const KernelConsts& K, int kind, const double* a,
                               const double* ref6, double* out9,
                               unsigned long long* counters) {
-  RegionCtx c;
-  c.K = &K;
-  acc_zero(c.acc);
-  c.status = kStatusOk;
-  c.counters = counters;
-  c.n_regions = 0;
+  EvalSink c;
+  eval_sink_init(c, &K, counters);
   const P2 p0{a[0], a[1]}, p1{a[2], a[3]}, p2{a[4], a[5]};
   switch (kind) {
     case 0:
       if (!(a[0] >= 0.0)) c.status |= kStatusDomain;
-      region_disc_l(c, fmin(a[0], 1.0), 1.0);
+      if (a[0] >= 1.0)
+        c.disc(1.0);
+      else
+        piece_disc_l(K, c.acc, a[0], 1.0);
+      c.n_regions += 1;
       break;
     case 1:
       region_sector(c, p0, p1, 1.0, fmin(a[4], 1.0));

@@ -58,7 +58,7 @@ sphbi_status status_from_bits(unsigned bits) {
 }
 
 constexpr int kEvalBlock = 128;
-constexpr int kMaxChunkPairs = 1 << 26;  // 64 Mi pairs per evaluation chunk (~1.5 GB scratch)
+constexpr int kMaxChunkPairs = 1 << 23;  // 8 Mi pairs per evaluation chunk (pipeline scratch ~ a few GB)
 
 }  // namespace
 
@@ -93,6 +93,15 @@ enum ScratchSlot {
   kBufGeneric0,
   kBufGeneric1,
   kBufGeneric2,
+  kBufPipeCnt,
+  kBufPipeOff,
+  kBufItemsC,
+  kBufItemsB,
+  kBufItemsS,
+  kBufOutC,
+  kBufOutB,
+  kBufOutS,
+  kBufPartial,
   kNumBufs
 };
 
@@ -169,31 +178,6 @@ int grid_for(int64_t n, int block) {
 // K4: pair integrals
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kEvalBlock)
-    k_integrate_pairs(const __grid_constant__ KernelConsts K, double h, int64_t n,
-                      const double* __restrict__ q, const double* __restrict__ tri,
-                      const double* __restrict__ vals, int mode, double* __restrict__ out,
-                      unsigned* __restrict__ status, unsigned* __restrict__ status_or,
-                      unsigned long long* counters) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double t6[6];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
-  double a3[3] = {1.0, 1.0, 1.0};
-  if (mode == 0 && vals) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) a3[j] = vals[3 * k + j];
-  }
-  double o[12];
-  const unsigned st =
-      eval_pair(K, q[2 * k], q[2 * k + 1], h, t6, a3, mode, o, counters, nullptr);
-  const int nout = mode == 0 ? 4 : 12;
-  for (int j = 0; j < nout; ++j) out[nout * k + j] = o[j];
-  if (status) status[k] = st;
-  if (st) atomicOr(status_or, st);
-}
-
-__global__ void __launch_bounds__(kEvalBlock)
     k_integrate_regions(const __grid_constant__ KernelConsts K, int64_t n,
                         const int* __restrict__ kind, const double* __restrict__ args,
                         const double* __restrict__ ref, double* __restrict__ out,
@@ -207,32 +191,262 @@ __global__ void __launch_bounds__(kEvalBlock)
   for (int j = 0; j < 9; ++j) out[9 * k + j] = o[j];
 }
 
-// Scene pairs: particle pp[k] against triangle pt[k]; out3 = (value, gx, gy).
-__global__ void __launch_bounds__(kEvalBlock)
-    k_eval_scene_pairs(const __grid_constant__ KernelConsts K, double h, int64_t npairs,
-                       const int* __restrict__ pp, const int* __restrict__ pt,
-                       const double* __restrict__ pxy, const double* __restrict__ tri,
-                       const double* __restrict__ vals, double* __restrict__ out3,
-                       unsigned* __restrict__ status_or, unsigned long long* counters) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= npairs) return;
-  const int i = pp[k];
-  const int t = pt[k];
-  double t6[6];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) t6[j] = __ldg(tri + 6 * (int64_t)t + j);
-  double a3[3] = {1.0, 1.0, 1.0};
-  if (vals) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) a3[j] = __ldg(vals + 3 * (int64_t)t + j);
+// ---------------------------------------------------------------------------
+// K4 as a work-item pipeline (divergence-aware evaluation)
+// ---------------------------------------------------------------------------
+// A thread-per-pair kernel diverges badly (a pair decomposes into 1..~20
+// pieces of 5 kinds with a 20x cost spread) and its fully inlined code
+// overflows the instruction cache. Instead:
+//   count : thread per pair runs the (cheap, exact) geometry with a counting
+//           sink -> number of cone / bound / segment pieces per pair
+//   scan  : CUB exclusive sums -> per-pair item offsets (deterministic order)
+//   emit  : the same geometry with an emitting sink writes one work item per
+//           piece; full/half discs (kernel constants) are accumulated inline
+//   eval  : one kernel per piece kind, thread per item: every warp runs the
+//           same straight-line FP64 / double-double code (converged)
+//   combine: thread per pair sums its items in the particle frame (fixed
+//           order, double-double) and applies the barycentric field.
+struct PieceItem {
+  int pair;
+  int pad;
+  double sign, m00, m01, m10, m11;
+  double a, b, c;  // cone: gamma, L | bound: x, D, beta | segment: d
+};
+
+struct AccOut {  // one piece's rotated contribution (9 dd)
+  double v[18];
+};
+
+SPHBI_HD void acc_to_out(const PairAcc& a, AccOut& o) {
+  const dd x[9] = {a.v1, a.v2, a.v3, a.g11, a.g12, a.g21, a.g22, a.g13, a.g23};
+  for (int i = 0; i < 9; ++i) {
+    o.v[2 * i] = x[i].hi;
+    o.v[2 * i + 1] = x[i].lo;
   }
-  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
-  double o[4];
-  const unsigned st = eval_pair(K, p.x, p.y, h, t6, a3, 0, o, counters, nullptr);
-  out3[3 * k] = o[0];
-  out3[3 * k + 1] = o[1];
-  out3[3 * k + 2] = o[2];
-  if (st) atomicOr(status_or, st);
+}
+__device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
+  dd* x[9] = {&a.v1, &a.v2, &a.v3, &a.g11, &a.g12, &a.g21, &a.g22, &a.g13, &a.g23};
+#pragma unroll
+  for (int i = 0; i < 9; ++i) *x[i] = dd_add(*x[i], dd{o[2 * i], o[2 * i + 1]});
+}
+
+struct CountSink {
+  unsigned n_cone, n_bound, n_seg, status;
+  unsigned long long* counters;
+  __device__ void bump(int w) { bump_counter(counters, w); }
+  __device__ void disc(double) {}
+  __device__ void half_disc(const Frame&, double) {}
+  __device__ void cone(const Frame&, double, double, double) { ++n_cone; }
+  __device__ void bound(const Frame&, double, double, double, double) { ++n_bound; }
+  __device__ void segment(const Frame&, double, double) { ++n_seg; }
+};
+
+struct EmitSink {
+  const KernelConsts* K;
+  PairAcc acc;
+  unsigned status;
+  int pair;
+  PieceItem *cone_items, *bound_items, *seg_items;
+  __device__ void bump(int) {}
+  __device__ void put(PieceItem*& dst, const Frame& f, double sign, double a, double b, double c) {
+    PieceItem it;
+    it.pair = pair;
+    it.pad = 0;
+    it.sign = sign;
+    it.m00 = f.m00;
+    it.m01 = f.m01;
+    it.m10 = f.m10;
+    it.m11 = f.m11;
+    it.a = a;
+    it.b = b;
+    it.c = c;
+    *dst++ = it;
+  }
+  __device__ void disc(double sign) { piece_disc(*K, acc, sign); }
+  __device__ void half_disc(const Frame& f, double sign) { piece_half_disc(*K, acc, f, sign); }
+  __device__ void cone(const Frame& f, double gamma, double L, double sign) {
+    put(cone_items, f, sign, gamma, L, 0.0);
+  }
+  __device__ void bound(const Frame& f, double x, double D, double beta, double sign) {
+    put(bound_items, f, sign, x, D, beta);
+  }
+  __device__ void segment(const Frame& f, double d, double sign) { put(seg_items, f, sign, d, 0.0, 0.0); }
+};
+
+// pair sources
+struct SceneSrc {  // particle pp[k] vs triangle pt[k]
+  const int* pp;
+  const int* pt;
+  const double* pxy;
+  const double* tri;
+  const double* vals;  // nullable: field == 1
+  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* a3) const {
+    const int i = pp[k], t = pt[k];
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    qx = p.x;
+    qy = p.y;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) t6[j] = __ldg(tri + 6 * (int64_t)t + j);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = vals ? __ldg(vals + 3 * (int64_t)t + j) : 1.0;
+  }
+};
+struct DirectSrc {  // query, triangle, values per item
+  const double* q;
+  const double* tri;
+  const double* vals;  // nullable
+  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* a3) const {
+    qx = q[2 * k];
+    qy = q[2 * k + 1];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = vals ? vals[3 * k + j] : 1.0;
+  }
+};
+
+__device__ __forceinline__ void normalized_pair(double qx, double qy, double h, const double* t6, P2* nv,
+                                                int* perm) {
+  P2 v[3] = {{t6[0], t6[1]}, {t6[2], t6[3]}, {t6[4], t6[5]}};
+  canonicalize(v, perm);
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+}
+
+template <class Src>
+__global__ void __launch_bounds__(128) k_pipe_count(Src src, int64_t n, double h, unsigned* __restrict__ cnt,
+                                                    unsigned long long* counters, unsigned* status_or) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) {
+    if (k == n) cnt[k] = cnt[n + 1 + k] = cnt[2 * (n + 1) + k] = 0;  // scan tails
+    return;
+  }
+  double qx, qy, t6[6], a3[3];
+  src.load(k, qx, qy, t6, a3);
+  P2 nv[3];
+  int perm[3];
+  normalized_pair(qx, qy, h, t6, nv, perm);
+  CountSink c{0u, 0u, 0u, 0u, counters};
+  integrate_normalized(c, nv);
+  cnt[k] = c.n_cone;
+  cnt[n + 1 + k] = c.n_bound;
+  cnt[2 * (n + 1) + k] = c.n_seg;
+  if (c.status) atomicOr(status_or, c.status);
+}
+
+template <class Src>
+__global__ void __launch_bounds__(128)
+    k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
+                const unsigned long long* __restrict__ off, PieceItem* __restrict__ cone_items,
+                PieceItem* __restrict__ bound_items, PieceItem* __restrict__ seg_items,
+                AccOut* __restrict__ partial, unsigned* status_or) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6], a3[3];
+  src.load(k, qx, qy, t6, a3);
+  P2 nv[3];
+  int perm[3];
+  normalized_pair(qx, qy, h, t6, nv, perm);
+  EmitSink e;
+  e.K = &K;
+  acc_zero(e.acc);
+  e.status = 0;
+  e.pair = static_cast<int>(k);
+  e.cone_items = cone_items + off[k];
+  e.bound_items = bound_items + off[n + 1 + k];
+  e.seg_items = seg_items + off[2 * (n + 1) + k];
+  integrate_normalized(e, nv);
+  acc_to_out(e.acc, partial[k]);
+  if (e.status) atomicOr(status_or, e.status);
+}
+
+__global__ void __launch_bounds__(128)
+    k_pipe_cone(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                AccOut* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PieceItem it = items[k];
+  PairAcc a;
+  acc_zero(a);
+  piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.b, it.sign);
+  acc_to_out(a, out[k]);
+}
+
+__global__ void __launch_bounds__(128)
+    k_pipe_bound(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                 AccOut* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PieceItem it = items[k];
+  PairAcc a;
+  acc_zero(a);
+  piece_bound(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.b, it.c, it.sign);
+  acc_to_out(a, out[k]);
+}
+
+__global__ void __launch_bounds__(128)
+    k_pipe_segment(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                   AccOut* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PieceItem it = items[k];
+  PairAcc a;
+  acc_zero(a);
+  piece_segment(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.sign);
+  acc_to_out(a, out[k]);
+}
+
+// combine: out3 = (value, gx, gy) per pair (mode 0; `stride` doubles per
+// pair, imag residual 0 written when stride == 4) or the three vertex bases
+// (mode 1, 12 doubles per pair, original vertex order).
+template <class Src>
+__global__ void __launch_bounds__(128)
+    k_pipe_combine(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
+                   const AccOut* __restrict__ partial, const unsigned long long* __restrict__ off,
+                   const AccOut* __restrict__ cone_out, const AccOut* __restrict__ bound_out,
+                   const AccOut* __restrict__ seg_out, int mode, int stride, double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6], a3[3];
+  src.load(k, qx, qy, t6, a3);
+  P2 nv[3];
+  int perm[3];
+  normalized_pair(qx, qy, h, t6, nv, perm);
+  PairAcc a;
+  acc_zero(a);
+  acc_add_out(a, partial[k].v);
+  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, cone_out[j].v);
+  for (unsigned long long j = off[n + 1 + k]; j < off[n + 1 + k + 1]; ++j) acc_add_out(a, bound_out[j].v);
+  for (unsigned long long j = off[2 * (n + 1) + k]; j < off[2 * (n + 1) + k + 1]; ++j)
+    acc_add_out(a, seg_out[j].v);
+  HatPlanes H;
+  const bool nondeg = !(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes(nv, H);
+  if (mode == 0) {
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    if (nondeg) {
+      const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
+      dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
+      for (int i = 0; i < 3; ++i) {
+        tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
+        tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
+        tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
+      }
+      double raw[3];
+      combine_plane(a, tau1, tau2, tau3, raw);
+      finalize(raw, K.c2, h, o);
+    }
+    for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
+  } else {
+    double o[12];
+    for (int j = 0; j < 12; ++j) o[j] = 0.0;
+    if (nondeg) {
+      for (int i = 0; i < 3; ++i) {
+        double raw[3];
+        combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
+        finalize(raw, K.c2, h, o + 4 * perm[i]);
+      }
+    }
+    for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -479,6 +693,75 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, double seed) {
 }
 
 // ---------------------------------------------------------------------------
+// host driver of the K4 pipeline
+// ---------------------------------------------------------------------------
+namespace {
+
+struct PipeStats {
+  unsigned long long n_cone = 0, n_bound = 0, n_seg = 0;
+};
+
+template <class Src>
+sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
+                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps) {
+  if (n <= 0) return SPHBI_OK;
+  cudaStream_t s = c->stream;
+  sphbi_status st;
+  unsigned* cnt;
+  unsigned long long* off;
+  const int64_t m = n + 1;
+  if ((st = scratch_t(c, kBufPipeCnt, 3 * m, &cnt)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPipeOff, 3 * m, &off)) != SPHBI_OK) return st;
+  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(src, n, h, cnt, ctr, dflags);
+  if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
+  void* dtmp;
+  if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+  for (int j = 0; j < 3; ++j) {
+    cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
+    if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
+  }
+  unsigned long long tot[3];
+  for (int j = 0; j < 3; ++j)
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(tot + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  PieceItem *ic, *ib, *is;
+  AccOut *oc, *ob, *os, *part;
+  if ((st = scratch_t(c, kBufItemsC, tot[0], &ic)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, tot[1], &ib)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, tot[2], &is)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutC, tot[0], &oc)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutB, tot[1], &ob)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutS, tot[2], &os)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPartial, n, &part)) != SPHBI_OK) return st;
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, ic, ib, is, part, dflags);
+  if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
+  if (tot[1]) {
+    k_pipe_bound<<<grid_for(tot[1], 128), 128, 0, s>>>(K, (int64_t)tot[1], ib, ob);
+    if ((st = check_launch(c, "k_pipe_bound")) != SPHBI_OK) return st;
+  }
+  if (tot[0]) {
+    k_pipe_cone<<<grid_for(tot[0], 128), 128, 0, s>>>(K, (int64_t)tot[0], ic, oc);
+    if ((st = check_launch(c, "k_pipe_cone")) != SPHBI_OK) return st;
+  }
+  if (tot[2]) {
+    k_pipe_segment<<<grid_for(tot[2], 128), 128, 0, s>>>(K, (int64_t)tot[2], is, os);
+    if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
+  }
+  k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, part, off, oc, ob, os, mode, stride, dout);
+  if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
+  if (ps) {
+    ps->n_cone += tot[0];
+    ps->n_bound += tot[1];
+    ps->n_seg += tot[2];
+  }
+  return SPHBI_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // C-ABI
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -635,14 +918,19 @@ sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel
     dstat = status_out;
   }
   SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, c->stream));
-  k_integrate_pairs<<<grid_for(n, kEvalBlock), kEvalBlock, 0, c->stream>>>(
-      K, h, n, dq, dt, dv, mode, dout, dstat, dflags, c->counters_on ? c->d_counters : nullptr);
-  if ((st = check_launch(c, "k_integrate_pairs")) != SPHBI_OK) return st;
+  (void)dstat;
+  if (status_out && mem == SPHBI_MEM_DEVICE)
+    SPHBI_CUDA_TRY(cudaMemsetAsync(status_out, 0, 4 * n, c->stream));
+  {
+    const DirectSrc src{dq, dt, mode == 0 ? dv : nullptr};
+    st = run_pipeline(c, K, h, src, n, mode, nout, dout, dflags, c->counters_on ? c->d_counters : nullptr,
+                      nullptr);
+    if (st != SPHBI_OK) return st;
+  }
   SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 4, cudaMemcpyDeviceToHost, c->stream));
   if (mem == SPHBI_MEM_HOST) {
     SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(double) * nout * n, cudaMemcpyDeviceToHost, c->stream));
-    if (status_out)
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(status_out, dstat, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (status_out) std::memset(status_out, 0, 4 * n);  // per-call status is reported as a whole
   }
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
   const unsigned bits = c->h_flags[0];
@@ -790,9 +1078,10 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
     while (done < n_pairs) {
       const int64_t cnt = std::min<int64_t>(n_pairs - done, kMaxChunkPairs);
       if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
-      k_eval_scene_pairs<<<grid_for(cnt, kEvalBlock), kEvalBlock, 0, s>>>(
-          K, h, cnt, pp + done, pt + done, dp, dt, dv, pout, dflags, ctr);
-      if ((st = check_launch(c, "k_eval_scene_pairs")) != SPHBI_OK) return st;
+      {
+        const SceneSrc src{pp + done, pt + done, dp, dt, dv};
+        if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
+      }
       if (timing && done + cnt >= n_pairs) cudaEventRecord(c->ev[2], s);
       // rows: all particles, accumulate (a particle may straddle chunks)
       const int pc = static_cast<int>(n_particles);
@@ -949,9 +1238,10 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
           written += cnt;
         }
         if (timing && p0 == 0) cudaEventRecord(c->ev[1], s);
-        k_eval_scene_pairs<<<grid_for(cnt, kEvalBlock), kEvalBlock, 0, s>>>(K, h, cnt, pp, pt, dp, dt, dv, pout,
-                                                                           dflags, ctr);
-        if ((st = check_launch(c, "k_eval_scene_pairs")) != SPHBI_OK) return st;
+        {
+          const SceneSrc src{pp, pt, dp, dt, dv};
+          if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
+        }
         if (timing && p1 >= np) cudaEventRecord(c->ev[2], s);
         if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
         k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp, p0, p1 - p0, row_ptr);
