@@ -437,6 +437,13 @@ SPHBI_HD void segment_sums(const KernelConsts& K, double d, S9& S) {
 // ---------------------------------------------------------------------------
 // region decomposition, written once and parameterised by a Sink
 // ---------------------------------------------------------------------------
+// NOTE: every device function on this path is force-inlined. With nvcc 12.9
+// (sm_100a, -fmad=false) the scene-pair instantiation of the emit/count
+// kernels received a corrupted vertex argument when region_wedge was an
+// out-of-line (ABI) call taking the sink by reference; the inlined build is
+// correct and is covered by tests/test_gpu_parity.py (cfg1 / cfg3 / cfg5
+// scene paths against the oracle).
+// ---------------------------------------------------------------------------
 // The geometry below (triangle_integrator.hpp:335-674) decides WHICH
 // elementary pieces a pair needs; a Sink decides what to do with each piece:
 //   EvalSink   evaluates it on the spot (single pairs, region test surface)
@@ -479,7 +486,7 @@ SPHBI_HD void piece_half_disc(const KernelConsts& K, PairAcc& acc, const Frame& 
   acc_add_region(acc, S, f, sign);
 }
 
-SPHBI_HDNI void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double L,
+SPHBI_HD void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double L,
                            double sign) {
   S9 S;
   if (L >= 1.0) {
@@ -492,7 +499,7 @@ SPHBI_HDNI void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, 
   acc_add_region(acc, S, f, sign);
 }
 
-SPHBI_HDNI void piece_bound(const KernelConsts& K, PairAcc& acc, const Frame& f, double x, double D,
+SPHBI_HD void piece_bound(const KernelConsts& K, PairAcc& acc, const Frame& f, double x, double D,
                             double beta, double sign) {
   double sb, cb;
   dsincos(beta, &sb, &cb);
@@ -503,7 +510,7 @@ SPHBI_HDNI void piece_bound(const KernelConsts& K, PairAcc& acc, const Frame& f,
   acc_add_region(acc, S, f, sign);
 }
 
-SPHBI_HDNI void piece_segment(const KernelConsts& K, PairAcc& acc, const Frame& f, double d, double sign) {
+SPHBI_HD void piece_segment(const KernelConsts& K, PairAcc& acc, const Frame& f, double d, double sign) {
   S9 S;
   segment_sums(K, d, S);
   acc_add_region(acc, S, f, sign);
@@ -655,7 +662,7 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
 // region_stub(v1, v2) (:426-484): triangle (origin, v1, v2) clipped to the
 // disc; the perpendicular-foot split is unrolled with a small stack.
 template <class Sink>
-SPHBI_HDNI void region_stub(Sink& c, P2 v1_in, P2 v2_in, double sign) {
+SPHBI_HD void region_stub(Sink& c, P2 v1_in, P2 v2_in, double sign) {
   P2 st1[8], st2[8];
   st1[0] = v1_in;
   st2[0] = v2_in;
@@ -730,7 +737,7 @@ SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
 
 // region_wedge (:514-603)
 template <class Sink>
-SPHBI_HDNI void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
+SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
   if (signed_area(n0, n1, n2) < 0.0) {
     const P2 t = n1;
     n1 = n2;
