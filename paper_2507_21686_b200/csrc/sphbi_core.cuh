@@ -594,43 +594,6 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
   c.cone(f, gamma, fmin(l, 1.0), sign);
 }
 
-// region_segment(t0, t1, q_keep) (:369-423).
-template <class Sink>
-SPHBI_HD void region_segment(Sink& c, P2 t0, P2 t1, P2 q_keep, double sign) {
-  const P2 e = p_sub(t1, t0);
-  const double len = p_norm(e);
-  if (len < kGeomEps) {
-    c.status |= kStatusDomain;  // "chord endpoints coincide"
-    return;
-  }
-  P2 n{e.y / len, -e.x / len};
-  if (p_dot(p_sub(q_keep, t0), n) < 0.0) n = P2{-n.x, -n.y};
-  const double d = p_dot(t0, n);
-  if (d >= 1.0 - kGeomEps) {
-    c.bump(kSegmentEmpty);
-    return;
-  }
-  if (d <= -1.0 + kGeomEps) {
-    c.bump(kSegmentFullDisc);
-    c.disc(sign);
-    return;
-  }
-  if (fabs(d) < 1e-9) {
-    c.bump(kSegmentHalfDisc);
-    c.half_disc(Frame{n.x, n.y, -n.y, n.x}, sign);
-    return;
-  }
-  c.bump(kSegmentGeneral);
-  if (d < 0.0) {
-    // origin-side segment: whole disc minus the far-side complement
-    const P2 nc{-n.x, -n.y};
-    c.disc(sign);
-    c.segment(Frame{nc.x, nc.y, -nc.y, nc.x}, -d, -sign);
-    return;
-  }
-  c.segment(Frame{n.x, n.y, -n.y, n.x}, d, sign);
-}
-
 // Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
 template <class Sink>
 SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double area2, P2 b,
@@ -659,53 +622,95 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
   }
 }
 
-// region_stub(v1, v2) (:426-484): triangle (origin, v1, v2) clipped to the
-// disc; the perpendicular-foot split is unrolled with a small stack.
+// ---------------------------------------------------------------------------
+// Flattened decomposition. The reference recurses (t3 -> wedge + t2 + wedge,
+// wedge -> stubs -> split stubs, wedge -> segments). Here each routine exists
+// ONCE in the generated code: decomposition queues wedge / segment / stub
+// tasks and three loops drain them. Branch decisions, signs and constants are
+// the reference's; only the order in which pieces reach the sink differs
+// (immaterial: pieces are summed in double-double).
+// ---------------------------------------------------------------------------
+struct WedgeTask {
+  P2 n0, n1, n2;
+  double sign;
+};
+struct SegTask {
+  P2 t0, t1, keep;
+  double sign;
+};
+struct StubTask {
+  P2 v1, v2;
+  double sign;
+};
+constexpr int kMaxWedges = 4;   // t3 -> 4 wedges
+constexpr int kMaxSegs = 4;     // <= 1 per wedge
+constexpr int kMaxStubs = 16;   // <= 2 per wedge, + 1 per split (LIFO)
+
+struct Tasks {
+  WedgeTask w[kMaxWedges];
+  SegTask sg[kMaxSegs];
+  StubTask st[kMaxStubs];
+  int nw, nsg, nst;
+};
+
+SPHBI_HD void tasks_init(Tasks& T) { T.nw = T.nsg = T.nst = 0; }
+
 template <class Sink>
-SPHBI_HD void region_stub(Sink& c, P2 v1_in, P2 v2_in, double sign) {
-  P2 st1[8], st2[8];
-  st1[0] = v1_in;
-  st2[0] = v2_in;
-  int top = 1;
-  while (top > 0) {
-    --top;
-    P2 v1 = st1[top], v2 = st2[top];
-    double r1 = p_norm(v1), r2 = p_norm(v2);
-    if (r1 < r2) {
-      const P2 tv = v1;
-      v1 = v2;
-      v2 = tv;
-      const double tr = r1;
-      r1 = r2;
-      r2 = tr;
-    }
-    const double area2 = p_cross(v1, v2);
-    if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
-      c.bump(kStubDegenerate);
-      continue;
-    }
-    const P2 b = p_sub(v1, v2);
-    const double dot_a = -(v2.x * b.x + v2.y * b.y);
-    if (dot_a <= kGeomEps) {
-      c.bump(kStubDirect);
-      stub_direct(c, v1, v2, r1, r2, area2, b, sign);
-      continue;
-    }
-    c.bump(kStubSplit);
-    const double t = dot_a / p_norm2(b);
-    const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
-    if (top + 2 > 8) {
-      c.status |= kStatusStack;
-      continue;
-    }
-    // reference order: stub(v1, foot) then stub(v2, foot)
-    st1[top] = v2;
-    st2[top] = foot;
-    ++top;
-    st1[top] = v1;
-    st2[top] = foot;
-    ++top;
+SPHBI_HD void push_wedge(Sink& c, Tasks& T, P2 n0, P2 n1, P2 n2, double sign) {
+  if (T.nw >= kMaxWedges) {
+    c.status |= kStatusStack;
+    return;
   }
+  T.w[T.nw++] = WedgeTask{n0, n1, n2, sign};
+}
+template <class Sink>
+SPHBI_HD void push_seg(Sink& c, Tasks& T, P2 t0, P2 t1, P2 keep, double sign) {
+  if (T.nsg >= kMaxSegs) {
+    c.status |= kStatusStack;
+    return;
+  }
+  T.sg[T.nsg++] = SegTask{t0, t1, keep, sign};
+}
+template <class Sink>
+SPHBI_HD void push_stub(Sink& c, Tasks& T, P2 v1, P2 v2, double sign) {
+  if (T.nst >= kMaxStubs) {
+    c.status |= kStatusStack;
+    return;
+  }
+  T.st[T.nst++] = StubTask{v1, v2, sign};
+}
+
+// region_t2 (:607-616): two wedges about the auxiliary point at distance 3.
+template <class Sink>
+SPHBI_HD void tasks_t2(Sink& c, Tasks& T, P2 a, P2 b, P2 cc, double sign) {
+  if (signed_area(a, b, cc) < 0.0) {
+    const P2 t = a;
+    a = b;
+    b = t;
+  }
+  const P2 u = p_sub(b, a);
+  const double len = p_norm(u);
+  const P2 x{a.x + 3.0 * u.x / len, a.y + 3.0 * u.y / len};
+  push_wedge(c, T, a, x, cc, sign);
+  push_wedge(c, T, b, x, cc, -sign);
+}
+
+// region_t3 (:620-632): wedge - t2 - wedge.
+template <class Sink>
+SPHBI_HD void tasks_t3(Sink& c, Tasks& T, P2 a, P2 b, P2 cc, double sign) {
+  if (signed_area(a, b, cc) < 0.0) {
+    const P2 t = b;
+    b = cc;
+    cc = t;
+  }
+  const P2 d1 = p_sub(b, a);
+  const P2 d2 = p_sub(cc, a);
+  const double l1 = p_norm(d1), l2 = p_norm(d2);
+  const P2 x1{a.x + 3.0 * d1.x / l1, a.y + 3.0 * d1.y / l1};
+  const P2 x2{a.x + 3.0 * d2.x / l2, a.y + 3.0 * d2.y / l2};
+  push_wedge(c, T, a, x1, x2, sign);
+  tasks_t2(c, T, b, cc, x1, -sign);
+  push_wedge(c, T, cc, x1, x2, -sign);
 }
 
 // segment_circle_crossings (:494-509)
@@ -716,6 +721,8 @@ struct Crossings {
 SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
   Crossings out;
   out.count = 0;
+  out.pts[0] = P2{0.0, 0.0};
+  out.pts[1] = P2{0.0, 0.0};
   const P2 d = p_sub(q, p);
   const double a = p_norm2(d);
   if (a < kGeomEps * kGeomEps) return out;
@@ -724,20 +731,23 @@ SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
   const double disc = b * b - 4.0 * a * cc;
   if (disc <= 0.0) return out;
   const double rt = sqrt(disc);
-  const double lams[2] = {(-b - rt) / (2.0 * a), (-b + rt) / (2.0 * a)};
-  for (int i = 0; i < 2; ++i) {
-    const double lam = lams[i];
-    if (lam >= -1e-12 && lam <= 1.0 + 1e-12) {
-      out.pts[out.count] = P2{p.x + lam * d.x, p.y + lam * d.y};
-      out.count++;
-    }
+  const double lam0 = (-b - rt) / (2.0 * a), lam1 = (-b + rt) / (2.0 * a);
+  if (lam0 >= -1e-12 && lam0 <= 1.0 + 1e-12) {
+    out.pts[out.count] = P2{p.x + lam0 * d.x, p.y + lam0 * d.y};
+    out.count++;
+  }
+  if (lam1 >= -1e-12 && lam1 <= 1.0 + 1e-12) {
+    out.pts[out.count] = P2{p.x + lam1 * d.x, p.y + lam1 * d.y};
+    out.count++;
   }
   return out;
 }
+SPHBI_HD P2 last_crossing(const Crossings& x) { return x.count == 2 ? x.pts[1] : x.pts[0]; }
 
-// region_wedge (:514-603)
+// region_wedge body (:514-603): emits discs / the arc sector directly and
+// queues its stubs and segments.
 template <class Sink>
-SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
+SPHBI_HD void wedge_body(Sink& c, Tasks& T, P2 n0, P2 n1, P2 n2, double sign) {
   if (signed_area(n0, n1, n2) < 0.0) {
     const P2 t = n1;
     n1 = n2;
@@ -776,7 +786,7 @@ SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
     }
     if (count == 2) {
       c.bump(kWedgeSingleEdgeSegment);
-      region_segment(c, e0, e1, opp, sign);
+      push_seg(c, T, e0, e1, opp, sign);
       return;
     }
     c.bump(kWedgeLoneTouch);
@@ -811,60 +821,110 @@ SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
     c.status |= kStatusLogic;
     return;
   }
-  const P2 s1 = x01.pts[x01.count - 1];
-  const P2 s2 = x02.pts[x02.count - 1];
+  const P2 s1 = last_crossing(x01);
+  const P2 s2 = last_crossing(x02);
   const double arc_orient = signed_area(origin, s1, s2);
   if (fabs(arc_orient) > kGeomEps) {
-    if (arc_orient > 0.0) {
-      region_sector(c, s1, s2, sign);
-    } else {
+    double sector_sign = sign;
+    if (!(arc_orient > 0.0)) {
+      // reflex arc: negated sector plus the full disc
       c.bump(kWedgeReflexDisc);
-      region_sector(c, s1, s2, -sign);
+      sector_sign = -sign;
       c.disc(sign);
     }
+    region_sector(c, s1, s2, sector_sign);
   }
   const double stub_a = signed_area(origin, n0, s1);
-  if (fabs(stub_a) > kGeomEps) region_stub(c, n0, s1, stub_a > 0.0 ? sign : -sign);
+  if (fabs(stub_a) > kGeomEps) push_stub(c, T, n0, s1, stub_a > 0.0 ? sign : -sign);
   const double stub_b = signed_area(origin, s2, n0);
-  if (fabs(stub_b) > kGeomEps) region_stub(c, s2, n0, stub_b > 0.0 ? sign : -sign);
+  if (fabs(stub_b) > kGeomEps) push_stub(c, T, s2, n0, stub_b > 0.0 ? sign : -sign);
   if (x12.count == 2) {
     c.bump(kWedgeCapSubtracted);
     const P2 mirror{n1.x + n2.x - n0.x, n1.y + n2.y - n0.y};
-    region_segment(c, n1, n2, mirror, -sign);
+    push_seg(c, T, n1, n2, mirror, -sign);
   }
 }
 
-// region_t2 (:607-616)
+// region_segment body (:369-423).
 template <class Sink>
-SPHBI_HD void region_t2(Sink& c, P2 a, P2 b, P2 cc, double sign) {
-  if (signed_area(a, b, cc) < 0.0) {
-    const P2 t = a;
-    a = b;
-    b = t;
+SPHBI_HD void segment_body(Sink& c, P2 t0, P2 t1, P2 q_keep, double sign) {
+  const P2 e = p_sub(t1, t0);
+  const double len = p_norm(e);
+  if (len < kGeomEps) {
+    c.status |= kStatusDomain;  // "chord endpoints coincide"
+    return;
   }
-  const P2 u = p_sub(b, a);
-  const double len = p_norm(u);
-  const P2 x{a.x + 3.0 * u.x / len, a.y + 3.0 * u.y / len};
-  region_wedge(c, a, x, cc, sign);
-  region_wedge(c, b, x, cc, -sign);
+  P2 n{e.y / len, -e.x / len};
+  if (p_dot(p_sub(q_keep, t0), n) < 0.0) n = P2{-n.x, -n.y};
+  const double d = p_dot(t0, n);
+  if (d >= 1.0 - kGeomEps) {
+    c.bump(kSegmentEmpty);
+    return;
+  }
+  if (d <= -1.0 + kGeomEps) {
+    c.bump(kSegmentFullDisc);
+    c.disc(sign);
+    return;
+  }
+  if (fabs(d) < 1e-9) {
+    c.bump(kSegmentHalfDisc);
+    c.half_disc(Frame{n.x, n.y, -n.y, n.x}, sign);
+    return;
+  }
+  c.bump(kSegmentGeneral);
+  if (d < 0.0) {
+    // origin-side segment: whole disc minus the far-side complement
+    c.disc(sign);
+    c.segment(Frame{-n.x, -n.y, n.y, -n.x}, -d, -sign);
+    return;
+  }
+  c.segment(Frame{n.x, n.y, -n.y, n.x}, d, sign);
 }
 
-// region_t3 (:620-632)
+// region_stub body (:426-484): a direct stub is emitted (cone + window
+// bounds); an acute one is split at the perpendicular foot (LIFO, in the
+// reference's order: stub(v1, foot) then stub(v2, foot)).
 template <class Sink>
-SPHBI_HD void region_t3(Sink& c, P2 a, P2 b, P2 cc, double sign) {
-  if (signed_area(a, b, cc) < 0.0) {
-    const P2 t = b;
-    b = cc;
-    cc = t;
+SPHBI_HD void stub_body(Sink& c, Tasks& T, P2 v1, P2 v2, double sign) {
+  double r1 = p_norm(v1), r2 = p_norm(v2);
+  if (r1 < r2) {
+    const P2 tv = v1;
+    v1 = v2;
+    v2 = tv;
+    const double tr = r1;
+    r1 = r2;
+    r2 = tr;
   }
-  const P2 d1 = p_sub(b, a);
-  const P2 d2 = p_sub(cc, a);
-  const double l1 = p_norm(d1), l2 = p_norm(d2);
-  const P2 x1{a.x + 3.0 * d1.x / l1, a.y + 3.0 * d1.y / l1};
-  const P2 x2{a.x + 3.0 * d2.x / l2, a.y + 3.0 * d2.y / l2};
-  region_wedge(c, a, x1, x2, sign);
-  region_t2(c, b, cc, x1, -sign);
-  region_wedge(c, cc, x1, x2, -sign);
+  const double area2 = p_cross(v1, v2);
+  if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
+    c.bump(kStubDegenerate);
+    return;
+  }
+  const P2 b = p_sub(v1, v2);
+  const double dot_a = -(v2.x * b.x + v2.y * b.y);
+  if (dot_a <= kGeomEps) {
+    c.bump(kStubDirect);
+    stub_direct(c, v1, v2, r1, r2, area2, b, sign);
+    return;
+  }
+  c.bump(kStubSplit);
+  const double t = dot_a / p_norm2(b);
+  const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
+  push_stub(c, T, v2, foot, sign);
+  push_stub(c, T, v1, foot, sign);
+}
+
+// Drain the queues: wedges first (they queue segments and stubs), then
+// segments, then stubs (LIFO, splits push back).
+template <class Sink>
+SPHBI_HD void run_tasks(Sink& c, Tasks& T) {
+  for (int i = 0; i < T.nw; ++i) wedge_body(c, T, T.w[i].n0, T.w[i].n1, T.w[i].n2, T.w[i].sign);
+  for (int i = 0; i < T.nsg; ++i) segment_body(c, T.sg[i].t0, T.sg[i].t1, T.sg[i].keep, T.sg[i].sign);
+  while (T.nst > 0) {
+    --T.nst;
+    const StubTask s = T.st[T.nst];
+    stub_body(c, T, s.v1, s.v2, s.sign);
+  }
 }
 
 // integrate_normalized (:637-674). Returns false for the degenerate route.
@@ -874,34 +934,71 @@ SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
     c.bump(kDispatchDegenerate);
     return false;
   }
+  Tasks T;
+  tasks_init(T);
   const double r[3] = {p_norm(v[0]), p_norm(v[1]), p_norm(v[2])};
-  int inside[3] = {0, 0, 0};
-  int inside_count = 0;
+  int inside_count = 0, in0 = 0, in1 = 0;
   for (int i = 0; i < 3; ++i)
-    if (r[i] <= 1.0 + kOnCircleTol) inside[inside_count++] = i;
-  if (inside_count == 0) {
-    c.bump(kDispatchWedgeOutside);
-    int i0 = 0;
-    if (r[1] < r[i0]) i0 = 1;
-    if (r[2] < r[i0]) i0 = 2;
-    region_wedge(c, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
-    return true;
-  }
-  if (inside_count == 1) {
-    c.bump(kDispatchWedgeSingle);
-    const int i0 = inside[0];
-    region_wedge(c, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
-    return true;
-  }
-  if (inside_count == 2) {
+    if (r[i] <= 1.0 + kOnCircleTol) {
+      if (inside_count == 0) in0 = i;
+      if (inside_count == 1) in1 = i;
+      ++inside_count;
+    }
+  if (inside_count <= 1) {
+    int i0 = in0;
+    if (inside_count == 0) {
+      c.bump(kDispatchWedgeOutside);
+      i0 = 0;
+      if (r[1] < r[i0]) i0 = 1;
+      if (r[2] < r[i0]) i0 = 2;
+    } else {
+      c.bump(kDispatchWedgeSingle);
+    }
+    push_wedge(c, T, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
+  } else if (inside_count == 2) {
     c.bump(kDispatchTwoInside);
-    const int outside = 3 - inside[0] - inside[1];
-    region_t2(c, v[inside[0]], v[inside[1]], v[outside], 1.0);
-    return true;
+    tasks_t2(c, T, v[in0], v[in1], v[3 - in0 - in1], 1.0);
+  } else {
+    c.bump(kDispatchThreeInside);
+    tasks_t3(c, T, v[0], v[1], v[2], 1.0);
   }
-  c.bump(kDispatchThreeInside);
-  region_t3(c, v[0], v[1], v[2], 1.0);
+  run_tasks(c, T);
   return true;
+}
+
+// Region-level entry points (test surface): the reference's region_* with a
+// single task queued.
+template <class Sink>
+SPHBI_HD void region_segment(Sink& c, P2 t0, P2 t1, P2 keep, double sign) {
+  segment_body(c, t0, t1, keep, sign);
+}
+template <class Sink>
+SPHBI_HD void region_stub(Sink& c, P2 v1, P2 v2, double sign) {
+  Tasks T;
+  tasks_init(T);
+  push_stub(c, T, v1, v2, sign);
+  run_tasks(c, T);
+}
+template <class Sink>
+SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
+  Tasks T;
+  tasks_init(T);
+  push_wedge(c, T, n0, n1, n2, sign);
+  run_tasks(c, T);
+}
+template <class Sink>
+SPHBI_HD void region_t2(Sink& c, P2 a, P2 b, P2 cc, double sign) {
+  Tasks T;
+  tasks_init(T);
+  tasks_t2(c, T, a, b, cc, sign);
+  run_tasks(c, T);
+}
+template <class Sink>
+SPHBI_HD void region_t3(Sink& c, P2 a, P2 b, P2 cc, double sign) {
+  Tasks T;
+  tasks_init(T);
+  tasks_t3(c, T, a, b, cc, sign);
+  run_tasks(c, T);
 }
 
 // ---------------------------------------------------------------------------
