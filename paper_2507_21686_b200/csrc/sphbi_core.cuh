@@ -350,6 +350,13 @@ SPHBI_HD void radial_chains(const KernelConsts& K, double x, double D, ChainSums
   C.R = sd.R.hi;
 }
 
+SPHBI_HD void s9_put(dd& dst, dd v, double sgn) {
+  if (sgn == 0.0)
+    dst = v;
+  else
+    dst = dd_add(dst, sgn > 0.0 ? v : dd_neg(v));
+}
+
 // Stub radial window at one bound x (elementary_regions.hpp:175-232), with
 // X_n = x^(n+1)/(n+1), as = asin(D/x):
 //   p_n  = (as - beta) X_n + D P~_n/(n+1)
@@ -357,9 +364,18 @@ SPHBI_HD void radial_chains(const KernelConsts& K, double x, double D, ChainSums
 //   c2_n = c2b D I_(n-1) - s2b/2 E_n       s2_n = X_n/2 - c2b/2 E_n - s2b D I_(n-1)
 //   E_n = X_n - 2 D^2 X_(n-2)
 SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double beta, double cb,
-                              double sb, double c2b, double s2b, S9& S) {
+                              double sb, double c2b, double s2b, S9& S, double sgn = 0.0) {
+  // sgn == 0: S = sums at x; sgn = +-1: S += sgn * sums at x
   ChainSums C;
-  radial_chains(K, x, D, C);
+  if (x == D) {
+    // right-limit bound (the snapped lo = D of every right stub): R = 0, so
+    // every chain term vanishes exactly and asin_ratio(D, D) = pi/2.
+    const dd z{0.0, 0.0};
+    C.sPv = C.sPg = C.sIv = C.sIg = z;
+    C.R = 0.0;
+  } else {
+    radial_chains(K, x, D, C);
+  }
   // asin_ratio (special_functions.hpp:150-155)
   double as;
   if (D <= 0.7 * x)
@@ -377,16 +393,17 @@ SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double 
   const dd E = dd_sub(Pg, dd_mul_d(Tg, 2.0 * D * D));
   const dd pcore_v = dd_add(dd_mul_d(Pv, amb), dd_mul_d(C.sPv, D));
   const dd pcore_g = dd_add(dd_mul_d(Pg, amb), dd_mul_d(C.sPg, D));
-  S.v3 = pcore_v;
-  S.v1 = dd_sub(dd_mul_d(Pv, cbD), dd_mul_d(C.sIv, sb));
-  S.v2 = dd_sub(dd_sub(Qv, dd_mul_d(C.sIv, cb)), dd_mul_d(Pv, sbD));
+  s9_put(S.v3, pcore_v, sgn);
+  s9_put(S.v1, dd_sub(dd_mul_d(Pv, cbD), dd_mul_d(C.sIv, sb)), sgn);
+  s9_put(S.v2, dd_sub(dd_sub(Qv, dd_mul_d(C.sIv, cb)), dd_mul_d(Pv, sbD)), sgn);
   const dd c2part = dd_sub(dd_mul_d(C.sIg, c2bD), dd_mul_d(E, 0.5 * s2b));
-  S.gx1 = dd_add(pcore_g, c2part);
-  S.gy2 = dd_sub(pcore_g, c2part);
-  S.gx2 = dd_sub(dd_sub(dd_mul_d(Pg, 0.5), dd_mul_d(E, 0.5 * c2b)), dd_mul_d(C.sIg, s2bD));
-  S.gy1 = S.gx2;
-  S.gx3 = dd_sub(dd_mul_d(Tg, 2.0 * cbD), dd_mul_d(C.sIg, 2.0 * sb));
-  S.gy3 = dd_sub(dd_sub(Rg, dd_mul_d(C.sIg, 2.0 * cb)), dd_mul_d(Tg, 2.0 * sbD));
+  s9_put(S.gx1, dd_add(pcore_g, c2part), sgn);
+  s9_put(S.gy2, dd_sub(pcore_g, c2part), sgn);
+  const dd gx2_val = dd_sub(dd_sub(dd_mul_d(Pg, 0.5), dd_mul_d(E, 0.5 * c2b)), dd_mul_d(C.sIg, s2bD));
+  s9_put(S.gx2, gx2_val, sgn);
+  s9_put(S.gy1, gx2_val, sgn);
+  s9_put(S.gx3, dd_sub(dd_mul_d(Tg, 2.0 * cbD), dd_mul_d(C.sIg, 2.0 * sb)), sgn);
+  s9_put(S.gy3, dd_sub(dd_sub(Rg, dd_mul_d(C.sIg, 2.0 * cb)), dd_mul_d(Tg, 2.0 * sbD)), sgn);
 }
 
 SPHBI_HD void s9_sub(S9& a, const S9& b) {
@@ -499,6 +516,29 @@ SPHBI_HD void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, do
   acc_add_region(acc, S, f, sign);
 }
 
+// Direct stub: cone [0,gamma] x [0,l] plus (when u > lo + eps) the radial
+// window [lo, u] at chord distance D and far-edge angle beta, in ONE frame.
+SPHBI_HD void piece_stub(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double l, double D,
+                         double beta, double lo, double u, bool window, double sign) {
+  S9 S;
+  if (l >= 1.0) {
+    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+  } else {
+    const int N = K.deg;
+    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+              poly_dd(K.rg, N, l, 1), S);
+  }
+  if (window) {
+    double sb, cb;
+    dsincos(beta, &sb, &cb);
+    const double s2b = 2.0 * sb * cb;
+    const double c2b = (cb - sb) * (cb + sb);
+    stub_bound_sums(K, u, D, beta, cb, sb, c2b, s2b, S, 1.0);
+    stub_bound_sums(K, lo, D, beta, cb, sb, c2b, s2b, S, -1.0);
+  }
+  acc_add_region(acc, S, f, sign);
+}
+
 SPHBI_HD void piece_bound(const KernelConsts& K, PairAcc& acc, const Frame& f, double x, double D,
                             double beta, double sign) {
   double sb, cb;
@@ -551,12 +591,14 @@ struct EvalSink {
     piece_half_disc(*K, acc, f, sign);
     ++n_regions;
   }
-  SPHBI_HD void cone(const Frame& f, double gamma, double L, double sign) {
+  SPHBI_HD void sector(const Frame& f, double gamma, double L, double sign) {
     piece_cone(*K, acc, f, gamma, L, sign);
     ++n_regions;
   }
-  SPHBI_HD void bound(const Frame& f, double x, double D, double beta, double sign) {
-    piece_bound(*K, acc, f, x, D, beta, sign);
+  SPHBI_HD void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
+                     bool window, double sign) {
+    piece_stub(*K, acc, f, gamma, l, D, beta, lo, u, window, sign);
+    ++n_regions;
   }
   SPHBI_HD void segment(const Frame& f, double d, double sign) {
     piece_segment(*K, acc, f, d, sign);
@@ -591,7 +633,7 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
     w2.y = -w2.y;
   }
   const double gamma = atan2(w2.y, w2.x);
-  c.cone(f, gamma, fmin(l, 1.0), sign);
+  c.sector(f, gamma, fmin(l, 1.0), sign);
 }
 
 // Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
@@ -613,13 +655,10 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
   const double beta = atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
   double lo = fmax(l, D);
   if (lo - D <= 256.0 * kDblEps * D) lo = D;
-  c.cone(f, gamma, l, sign);
-  if (u > lo + kGeomEps) {
-    // stub_integral validation (elementary_regions.hpp:179-183)
-    if (!(beta >= 0.0 && beta < kHalfPiHi)) c.status |= kStatusDomain;
-    c.bound(f, u, D, beta, sign);
-    c.bound(f, lo, D, beta, -sign);
-  }
+  const bool window = u > lo + kGeomEps;
+  // stub_integral validation (elementary_regions.hpp:179-183)
+  if (window && !(beta >= 0.0 && beta < kHalfPiHi)) c.status |= kStatusDomain;
+  c.stub(f, gamma, l, D, beta, lo, u, window, sign);
 }
 
 // ---------------------------------------------------------------------------
@@ -643,8 +682,8 @@ struct StubTask {
   double sign;
 };
 constexpr int kMaxWedges = 4;   // t3 -> 4 wedges
-constexpr int kMaxSegs = 4;     // <= 1 per wedge
-constexpr int kMaxStubs = 16;   // <= 2 per wedge, + 1 per split (LIFO)
+constexpr int kMaxSegs = 2;     // <= 1 per wedge (drained per wedge)
+constexpr int kMaxStubs = 8;    // <= 2 per wedge, + 1 per split (LIFO, drained per wedge)
 
 struct Tasks {
   WedgeTask w[kMaxWedges];
@@ -917,13 +956,21 @@ SPHBI_HD void stub_body(Sink& c, Tasks& T, P2 v1, P2 v2, double sign) {
 // Drain the queues: wedges first (they queue segments and stubs), then
 // segments, then stubs (LIFO, splits push back).
 template <class Sink>
-SPHBI_HD void run_tasks(Sink& c, Tasks& T) {
-  for (int i = 0; i < T.nw; ++i) wedge_body(c, T, T.w[i].n0, T.w[i].n1, T.w[i].n2, T.w[i].sign);
+SPHBI_HD void drain_pieces(Sink& c, Tasks& T) {
   for (int i = 0; i < T.nsg; ++i) segment_body(c, T.sg[i].t0, T.sg[i].t1, T.sg[i].keep, T.sg[i].sign);
+  T.nsg = 0;
   while (T.nst > 0) {
     --T.nst;
     const StubTask s = T.st[T.nst];
     stub_body(c, T, s.v1, s.v2, s.sign);
+  }
+}
+template <class Sink>
+SPHBI_HD void run_tasks(Sink& c, Tasks& T) {
+  drain_pieces(c, T);  // pieces queued directly (region-level entry points)
+  for (int i = 0; i < T.nw; ++i) {
+    wedge_body(c, T, T.w[i].n0, T.w[i].n1, T.w[i].n2, T.w[i].sign);
+    drain_pieces(c, T);
   }
 }
 

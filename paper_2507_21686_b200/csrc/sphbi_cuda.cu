@@ -206,11 +206,17 @@ __global__ void __launch_bounds__(kEvalBlock)
 //           same straight-line FP64 / double-double code (converged)
 //   combine: thread per pair sums its items in the particle frame (fixed
 //           order, double-double) and applies the barycentric field.
-struct PieceItem {
+struct PieceItem {  // sector (a = gamma) / segment (a = d)
   int pair;
   int pad;
   double sign, m00, m01, m10, m11;
-  double a, b, c;  // cone: gamma, L | bound: x, D, beta | segment: d
+  double a;
+};
+struct StubItem {  // direct stub: cone (gamma, l) + radial window [lo, u] (D, beta)
+  int pair;
+  int window;
+  double sign, m00, m01, m10, m11;
+  double gamma, l, D, beta, lo, u;
 };
 
 struct AccOut {  // one piece's rotated contribution (9 dd)
@@ -231,13 +237,13 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
 }
 
 struct CountSink {
-  unsigned n_cone, n_bound, n_seg, status;
+  unsigned n_sector, n_stub, n_seg, status;
   unsigned long long* counters;
   __device__ void bump(int w) { bump_counter(counters, w); }
   __device__ void disc(double) {}
   __device__ void half_disc(const Frame&, double) {}
-  __device__ void cone(const Frame&, double, double, double) { ++n_cone; }
-  __device__ void bound(const Frame&, double, double, double, double) { ++n_bound; }
+  __device__ void sector(const Frame&, double, double, double) { ++n_sector; }
+  __device__ void stub(const Frame&, double, double, double, double, double, double, bool, double) { ++n_stub; }
   __device__ void segment(const Frame&, double, double) { ++n_seg; }
 };
 
@@ -246,9 +252,10 @@ struct EmitSink {
   PairAcc acc;
   unsigned status;
   int pair;
-  PieceItem *cone_items, *bound_items, *seg_items;
+  PieceItem *sector_items, *seg_items;
+  StubItem* stub_items;
   __device__ void bump(int) {}
-  __device__ void put(PieceItem*& dst, const Frame& f, double sign, double a, double b, double c) {
+  __device__ void put(PieceItem*& dst, const Frame& f, double sign, double a) {
     PieceItem it;
     it.pair = pair;
     it.pad = 0;
@@ -258,19 +265,30 @@ struct EmitSink {
     it.m10 = f.m10;
     it.m11 = f.m11;
     it.a = a;
-    it.b = b;
-    it.c = c;
     *dst++ = it;
   }
   __device__ void disc(double sign) { piece_disc(*K, acc, sign); }
   __device__ void half_disc(const Frame& f, double sign) { piece_half_disc(*K, acc, f, sign); }
-  __device__ void cone(const Frame& f, double gamma, double L, double sign) {
-    put(cone_items, f, sign, gamma, L, 0.0);
+  __device__ void sector(const Frame& f, double gamma, double, double sign) { put(sector_items, f, sign, gamma); }
+  __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
+                       bool window, double sign) {
+    StubItem it;
+    it.pair = pair;
+    it.window = window ? 1 : 0;
+    it.sign = sign;
+    it.m00 = f.m00;
+    it.m01 = f.m01;
+    it.m10 = f.m10;
+    it.m11 = f.m11;
+    it.gamma = gamma;
+    it.l = l;
+    it.D = D;
+    it.beta = beta;
+    it.lo = lo;
+    it.u = u;
+    *stub_items++ = it;
   }
-  __device__ void bound(const Frame& f, double x, double D, double beta, double sign) {
-    put(bound_items, f, sign, x, D, beta);
-  }
-  __device__ void segment(const Frame& f, double d, double sign) { put(seg_items, f, sign, d, 0.0, 0.0); }
+  __device__ void segment(const Frame& f, double d, double sign) { put(seg_items, f, sign, d); }
 };
 
 // pair sources
@@ -327,18 +345,28 @@ __global__ void __launch_bounds__(128) k_pipe_count(Src src, int64_t n, double h
   normalized_pair(qx, qy, h, t6, nv, perm);
   CountSink c{0u, 0u, 0u, 0u, counters};
   integrate_normalized(c, nv);
-  cnt[k] = c.n_cone;
-  cnt[n + 1 + k] = c.n_bound;
+  cnt[k] = c.n_sector;
+  cnt[n + 1 + k] = c.n_stub;
   cnt[2 * (n + 1) + k] = c.n_seg;
   if (c.status) atomicOr(status_or, c.status);
 }
 
+// Per-pair record written by the emit pass: the inline pieces (full / half
+// discs) and, for field mode, the field's barycentric plane tau in the
+// particle frame, so that combine needs no geometry.
+struct PairRec {
+  double acc[18];
+  double tau[6];
+  int nondeg;
+  int pad;
+};
+
 template <class Src>
 __global__ void __launch_bounds__(128)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
-                const unsigned long long* __restrict__ off, PieceItem* __restrict__ cone_items,
-                PieceItem* __restrict__ bound_items, PieceItem* __restrict__ seg_items,
-                AccOut* __restrict__ partial, unsigned* status_or) {
+                const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
+                StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
+                PairRec* __restrict__ rec, unsigned* status_or) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   double qx, qy, t6[6], a3[3];
@@ -351,35 +379,58 @@ __global__ void __launch_bounds__(128)
   acc_zero(e.acc);
   e.status = 0;
   e.pair = static_cast<int>(k);
-  e.cone_items = cone_items + off[k];
-  e.bound_items = bound_items + off[n + 1 + k];
+  e.sector_items = sector_items + off[k];
+  e.stub_items = stub_items + off[n + 1 + k];
   e.seg_items = seg_items + off[2 * (n + 1) + k];
-  integrate_normalized(e, nv);
-  acc_to_out(e.acc, partial[k]);
+  const bool nondeg_route = integrate_normalized(e, nv);
+  PairRec& r = rec[k];
+  AccOut o;
+  acc_to_out(e.acc, o);
+  for (int j = 0; j < 18; ++j) r.acc[j] = o.v[j];
+  HatPlanes H;
+  const bool nondeg = nondeg_route && hat_planes(nv, H);
+  r.nondeg = nondeg ? 1 : 0;
+  r.pad = 0;
+  dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
+  if (nondeg) {
+    const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
+    for (int i = 0; i < 3; ++i) {
+      tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
+      tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
+      tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
+    }
+  }
+  r.tau[0] = tau1.hi;
+  r.tau[1] = tau1.lo;
+  r.tau[2] = tau2.hi;
+  r.tau[3] = tau2.lo;
+  r.tau[4] = tau3.hi;
+  r.tau[5] = tau3.lo;
   if (e.status) atomicOr(status_or, e.status);
 }
 
 __global__ void __launch_bounds__(128)
-    k_pipe_cone(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
-                AccOut* __restrict__ out) {
+    k_pipe_sector(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                  AccOut* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const PieceItem it = items[k];
   PairAcc a;
   acc_zero(a);
-  piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.b, it.sign);
+  piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, 1.0, it.sign);
   acc_to_out(a, out[k]);
 }
 
 __global__ void __launch_bounds__(128)
-    k_pipe_bound(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
-                 AccOut* __restrict__ out) {
+    k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
+                AccOut* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const PieceItem it = items[k];
+  const StubItem it = items[k];
   PairAcc a;
   acc_zero(a);
-  piece_bound(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.b, it.c, it.sign);
+  piece_stub(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
+             it.window != 0, it.sign);
   acc_to_out(a, out[k]);
 }
 
@@ -395,15 +446,44 @@ __global__ void __launch_bounds__(128)
   acc_to_out(a, out[k]);
 }
 
-// combine: out3 = (value, gx, gy) per pair (mode 0; `stride` doubles per
-// pair, imag residual 0 written when stride == 4) or the three vertex bases
-// (mode 1, 12 doubles per pair, original vertex order).
+__device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t n, int64_t k,
+                                          const unsigned long long* __restrict__ off,
+                                          const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
+                                          const AccOut* __restrict__ seg_out) {
+  acc_zero(a);
+  acc_add_out(a, r.acc);
+  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, sec_out[j].v);
+  for (unsigned long long j = off[n + 1 + k]; j < off[n + 1 + k + 1]; ++j) acc_add_out(a, stub_out[j].v);
+  for (unsigned long long j = off[2 * (n + 1) + k]; j < off[2 * (n + 1) + k + 1]; ++j) acc_add_out(a, seg_out[j].v);
+}
+
+// combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0])
+__global__ void __launch_bounds__(128)
+    k_pipe_combine(const __grid_constant__ KernelConsts K, int64_t n, double h,
+                   const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
+                   const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
+                   const AccOut* __restrict__ seg_out, int stride, double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PairRec& r = rec[k];
+  double o[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r.nondeg) {
+    PairAcc a;
+    sum_items(a, r, n, k, off, sec_out, stub_out, seg_out);
+    double raw[3];
+    combine_plane(a, dd{r.tau[0], r.tau[1]}, dd{r.tau[2], r.tau[3]}, dd{r.tau[4], r.tau[5]}, raw);
+    finalize(raw, K.c2, h, o);
+  }
+  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
+}
+
+// combine, vertex-basis mode: 12 doubles per pair in the original vertex order
 template <class Src>
 __global__ void __launch_bounds__(128)
-    k_pipe_combine(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
-                   const AccOut* __restrict__ partial, const unsigned long long* __restrict__ off,
-                   const AccOut* __restrict__ cone_out, const AccOut* __restrict__ bound_out,
-                   const AccOut* __restrict__ seg_out, int mode, int stride, double* __restrict__ out) {
+    k_pipe_combine_bases(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
+                         const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
+                         const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
+                         const AccOut* __restrict__ seg_out, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   double qx, qy, t6[6], a3[3];
@@ -411,42 +491,20 @@ __global__ void __launch_bounds__(128)
   P2 nv[3];
   int perm[3];
   normalized_pair(qx, qy, h, t6, nv, perm);
-  PairAcc a;
-  acc_zero(a);
-  acc_add_out(a, partial[k].v);
-  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, cone_out[j].v);
-  for (unsigned long long j = off[n + 1 + k]; j < off[n + 1 + k + 1]; ++j) acc_add_out(a, bound_out[j].v);
-  for (unsigned long long j = off[2 * (n + 1) + k]; j < off[2 * (n + 1) + k + 1]; ++j)
-    acc_add_out(a, seg_out[j].v);
+  const PairRec& r = rec[k];
+  double o[12];
+  for (int j = 0; j < 12; ++j) o[j] = 0.0;
   HatPlanes H;
-  const bool nondeg = !(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes(nv, H);
-  if (mode == 0) {
-    double o[4] = {0.0, 0.0, 0.0, 0.0};
-    if (nondeg) {
-      const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
-      dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
-      for (int i = 0; i < 3; ++i) {
-        tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
-        tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
-        tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
-      }
+  if (r.nondeg && hat_planes(nv, H)) {
+    PairAcc a;
+    sum_items(a, r, n, k, off, sec_out, stub_out, seg_out);
+    for (int i = 0; i < 3; ++i) {
       double raw[3];
-      combine_plane(a, tau1, tau2, tau3, raw);
-      finalize(raw, K.c2, h, o);
+      combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
+      finalize(raw, K.c2, h, o + 4 * perm[i]);
     }
-    for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
-  } else {
-    double o[12];
-    for (int j = 0; j < 12; ++j) o[j] = 0.0;
-    if (nondeg) {
-      for (int i = 0; i < 3; ++i) {
-        double raw[3];
-        combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
-        finalize(raw, K.c2, h, o + 4 * perm[i]);
-      }
-    }
-    for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
   }
+  for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -722,39 +780,47 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
     if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
   }
-  unsigned long long tot[3];
+  unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->h_flags + 4);
   for (int j = 0; j < 3; ++j)
     SPHBI_CUDA_TRY(cudaMemcpyAsync(tot + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
-  PieceItem *ic, *ib, *is;
-  AccOut *oc, *ob, *os, *part;
-  if ((st = scratch_t(c, kBufItemsC, tot[0], &ic)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsB, tot[1], &ib)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsS, tot[2], &is)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutC, tot[0], &oc)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutB, tot[1], &ob)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutS, tot[2], &os)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPartial, n, &part)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, ic, ib, is, part, dflags);
+  const unsigned long long n_sec = tot[0], n_stub = tot[1], n_seg = tot[2];
+  PieceItem *isec, *iseg;
+  StubItem* istub;
+  AccOut *osec, *ostub, *oseg;
+  PairRec* rec;
+  if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
-  if (tot[1]) {
-    k_pipe_bound<<<grid_for(tot[1], 128), 128, 0, s>>>(K, (int64_t)tot[1], ib, ob);
-    if ((st = check_launch(c, "k_pipe_bound")) != SPHBI_OK) return st;
+  if (n_stub) {
+    k_pipe_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(K, (int64_t)n_stub, istub, ostub);
+    if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
   }
-  if (tot[0]) {
-    k_pipe_cone<<<grid_for(tot[0], 128), 128, 0, s>>>(K, (int64_t)tot[0], ic, oc);
-    if ((st = check_launch(c, "k_pipe_cone")) != SPHBI_OK) return st;
+  if (n_sec) {
+    k_pipe_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(K, (int64_t)n_sec, isec, osec);
+    if ((st = check_launch(c, "k_pipe_sector")) != SPHBI_OK) return st;
   }
-  if (tot[2]) {
-    k_pipe_segment<<<grid_for(tot[2], 128), 128, 0, s>>>(K, (int64_t)tot[2], is, os);
+  if (n_seg) {
+    k_pipe_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(K, (int64_t)n_seg, iseg, oseg);
     if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
   }
-  k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, part, off, oc, ob, os, mode, stride, dout);
-  if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
+  if (mode == 0) {
+    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, n, h, rec, off, osec, ostub, oseg, stride, dout);
+    if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
+  } else {
+    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, rec, off, osec, ostub, oseg, dout);
+    if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
+  }
   if (ps) {
-    ps->n_cone += tot[0];
-    ps->n_bound += tot[1];
-    ps->n_seg += tot[2];
+    ps->n_cone += n_sec;
+    ps->n_bound += n_stub;
+    ps->n_seg += n_seg;
   }
   return SPHBI_OK;
 }
@@ -814,7 +880,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   }
   c->stream = c->own_stream;
   for (auto& e : c->ev) cudaEventCreate(&e);
-  cudaMallocHost(&c->h_flags, 64);
+  cudaMallocHost(&c->h_flags, 256);
   if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
     cudaGetLastError();
     return fail(SPHBI_ERR_OUT_OF_MEMORY, "counter allocation failed");
@@ -891,7 +957,7 @@ sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel
   const int nout = mode == 0 ? 4 : 12;
   const double *dq = query_xy, *dt = tri_xy, *dv = values;
   double* dout = out;
-  uint32_t* dstat = nullptr;
+  uint32_t* dstat = nullptr;  // per-pair status is reported per call (status bits)
   unsigned* dflags = nullptr;
   if ((st = scratch_t(c, kBufFlags, 4, &dflags)) != SPHBI_OK) return st;
   if (mem == SPHBI_MEM_HOST) {
