@@ -59,6 +59,14 @@ struct KernelConsts {
   dd tg[kMaxKernelDegree + 1];
   dd rg[kMaxKernelDegree + 1];
   dd pv1, qv1, pg1, rg1;             // the polynomials at x = 1
+  // division-free chain weights (see radial_chains): U_m = m!! P_m,
+  // V_m = e_m I_m with e_m = (m+1) e_(m-2), e_0 = e_1 = 1
+  dd wpv[kMaxKernelDegree + 4];   // weight of U_m in sPv  (pv[m-1] / m!!)
+  dd wpg[kMaxKernelDegree + 4];   // weight of U_m in sPg  (pg[m-1] / m!!)
+  dd wiv[kMaxKernelDegree + 4];   // weight of V_m in sIv  (b[m-2] / e_m)
+  dd wig[kMaxKernelDegree + 4];   // weight of V_m in sIg  (wh[m] / e_m)
+  double dfac[kMaxKernelDegree + 4];  // m!!
+  double efac[kMaxKernelDegree + 4];  // e_m
 };
 
 // Exact quotient of a double by a small positive integer, as a dd.
@@ -98,13 +106,40 @@ inline bool build_kernel_consts(const double* coef, int ncoef, double c2, Kernel
   K->qv1 = s[1];
   K->pg1 = s[2];
   K->rg1 = s[3];
+  for (int m = 0; m < kMaxKernelDegree + 4; ++m) {
+    K->dfac[m] = m < 2 ? 1.0 : m * K->dfac[m - 2];
+    K->efac[m] = m < 2 ? 1.0 : (m + 1) * K->efac[m - 2];
+  }
+  const dd z{0.0, 0.0};
+  for (int m = 0; m < kMaxKernelDegree + 4; ++m) {
+    const dd inv_d = dd_div(dd_make(1.0), dd_make(K->dfac[m]));
+    const dd inv_e = dd_div(dd_make(1.0), dd_make(K->efac[m]));
+    const int kp = m - 1;  // P_m carries pv[m-1], pg[m-1]
+    K->wpv[m] = (kp >= 0 && kp <= deg) ? dd_mul(K->pv[kp], inv_d) : z;
+    K->wpg[m] = (kp >= 1 && kp <= deg) ? dd_mul(K->pg[kp], inv_d) : z;
+    const int ki = m - 2;  // I_m carries b[m-2] and wh[m]
+    K->wiv[m] = (ki >= 0 && ki <= deg) ? dd_mul(dd_make(K->b[ki]), inv_e) : z;
+    K->wig[m] = (m >= 1 && m <= deg) ? dd_mul(dd_make(K->wh[m]), inv_e) : z;
+  }
   return true;
 }
 
-// sum_{k=0}^{deg} c_k x^(k+off) by double-double Horner.
+// sum_{k=0}^{deg} c_k x^(k+off): compensated Horner (Graillat-Langlois-Louvet)
+// on dd coefficients -- as accurate as double-double Horner (error ~ eps^2 x
+// condition) at ~2/3 of the FP64 instructions.
 SPHBI_HD dd poly_dd(const dd* c, int deg, double x, int off) {
-  dd acc = c[deg];
-  for (int k = deg - 1; k >= 0; --k) acc = dd_add(dd_mul_d(acc, x), c[k]);
+  double r = c[deg].hi;
+  double e = c[deg].lo;
+  for (int k = deg - 1; k >= 0; --k) {
+    const double p = r * x;
+    const double pi = fma(r, x, -p);
+    const double s = p + c[k].hi;
+    const double bb = s - p;
+    const double sig = (p - (s - bb)) + (c[k].hi - bb);
+    e = fma(e, x, pi + sig + c[k].lo);
+    r = s;
+  }
+  dd acc = quick_two_sum(r, e);
   for (int j = 0; j < off; ++j) acc = dd_mul_d(acc, x);
   return acc;
 }
@@ -202,20 +237,20 @@ SPHBI_HD dd dd_scale(dd a, double s) { return s == 1.0 ? a : (s == -1.0 ? dd_neg
 // acc += sign * (M^T S M) (see header comment): tau' = M tau; g = M^T g'.
 SPHBI_HD void acc_add_region(PairAcc& a, const S9& S, const Frame& M, double sign) {
   // value covector
-  const dd v1 = dd_add(dd_mul_d(S.v1, M.m00), dd_mul_d(S.v2, M.m10));
-  const dd v2 = dd_add(dd_mul_d(S.v1, M.m01), dd_mul_d(S.v2, M.m11));
+  const dd v1 = dd_dot2_d(S.v1, M.m00, S.v2, M.m10);
+  const dd v2 = dd_dot2_d(S.v1, M.m01, S.v2, M.m11);
   // A = M^T G'
-  const dd a00 = dd_add(dd_mul_d(S.gx1, M.m00), dd_mul_d(S.gy1, M.m10));
-  const dd a01 = dd_add(dd_mul_d(S.gx2, M.m00), dd_mul_d(S.gy2, M.m10));
-  const dd a10 = dd_add(dd_mul_d(S.gx1, M.m01), dd_mul_d(S.gy1, M.m11));
-  const dd a11 = dd_add(dd_mul_d(S.gx2, M.m01), dd_mul_d(S.gy2, M.m11));
+  const dd a00 = dd_dot2_d(S.gx1, M.m00, S.gy1, M.m10);
+  const dd a01 = dd_dot2_d(S.gx2, M.m00, S.gy2, M.m10);
+  const dd a10 = dd_dot2_d(S.gx1, M.m01, S.gy1, M.m11);
+  const dd a11 = dd_dot2_d(S.gx2, M.m01, S.gy2, M.m11);
   // G = A M
-  const dd g00 = dd_add(dd_mul_d(a00, M.m00), dd_mul_d(a01, M.m10));
-  const dd g01 = dd_add(dd_mul_d(a00, M.m01), dd_mul_d(a01, M.m11));
-  const dd g10 = dd_add(dd_mul_d(a10, M.m00), dd_mul_d(a11, M.m10));
-  const dd g11 = dd_add(dd_mul_d(a10, M.m01), dd_mul_d(a11, M.m11));
-  const dd g3x = dd_add(dd_mul_d(S.gx3, M.m00), dd_mul_d(S.gy3, M.m10));
-  const dd g3y = dd_add(dd_mul_d(S.gx3, M.m01), dd_mul_d(S.gy3, M.m11));
+  const dd g00 = dd_dot2_d(a00, M.m00, a01, M.m10);
+  const dd g01 = dd_dot2_d(a00, M.m01, a01, M.m11);
+  const dd g10 = dd_dot2_d(a10, M.m00, a11, M.m10);
+  const dd g11 = dd_dot2_d(a10, M.m01, a11, M.m11);
+  const dd g3x = dd_dot2_d(S.gx3, M.m00, S.gy3, M.m10);
+  const dd g3y = dd_dot2_d(S.gx3, M.m01, S.gy3, M.m11);
   a.v1 = dd_add(a.v1, dd_scale(v1, sign));
   a.v2 = dd_add(a.v2, dd_scale(v2, sign));
   a.v3 = dd_add(a.v3, dd_scale(S.v3, sign));
@@ -314,39 +349,40 @@ SPHBI_HD void chain_seeds(double x, double D, ChainSeeds& S) {
 
 SPHBI_HD void radial_chains(const KernelConsts& K, double x, double D, ChainSums& C) {
   // The chain values feed sums whose monomial coefficients cancel heavily
-  // (the kernel polynomial in the power basis), so seeds and recurrences
-  // all run in double-double.
+  // (the kernel polynomial in the power basis), so seeds and recurrences run
+  // in double-double. The recurrences are scaled to be division-free:
+  //   U_m = m!! P~_m      U_m = (m-2)!! x^(m-1) R   + (m-1) D^2 U_(m-2)
+  //   V_m = e_m I_m       V_m = e_(m-2) x^(m-2) R^3 + (m-2) D^2 V_(m-2)
+  // with the 1/m!!, 1/e_m folded into the dd weights (KernelConsts::w*).
   const int N = K.deg;
   ChainSeeds sd;
   chain_seeds(x, D, sd);
   const dd D2 = two_prod(D, D);
   const dd R3 = dd_mul(dd_mul(sd.R, sd.R), sd.R);
-  dd aPv{0, 0}, aPg{0, 0}, aIv{0, 0}, aIg{0, 0};
-  dd pm2 = sd.p0, pm1 = sd.R;
-  dd im2{0.0, 0.0}, im1 = sd.i1;
-  aPv = dd_mul(K.pv[0], sd.R);
-  if (N >= 1) aIg = dd_mul_d(im1, K.wh[1]);
-  dd xpm2 = dd_make(1.0), xpm1 = dd_make(x);
+  acc2 aPv{0, 0}, aPg{0, 0}, aIv{0, 0}, aIg{0, 0};
+  dd um2 = sd.p0, um1 = sd.R;  // U_0 = P~_0, U_1 = R
+  dd vm2{0.0, 0.0}, vm1 = sd.i1;  // V_0 (unused), V_1 = I_1
+  acc_add_dddd(aPv, K.wpv[1], um1);
+  acc_add_dddd(aIg, K.wig[1], vm1);
+  dd xpm2 = dd_make(1.0), xpm1 = dd_make(x);  // x^(m-2), x^(m-1)
   for (int m = 2; m <= N + 2; ++m) {
-    const dd pm = dd_div_d_small(dd_add(dd_mul(xpm1, sd.R), dd_mul_d(dd_mul(D2, pm2), (double)(m - 1))), m);
-    const dd im = dd_div_d_small(dd_add(dd_mul(xpm2, R3), dd_mul_d(dd_mul(D2, im2), (double)(m - 2))), m + 1);
-    if (m <= N + 1) {
-      aPv = dd_add(aPv, dd_mul(K.pv[m - 1], pm));
-      aPg = dd_add(aPg, dd_mul(K.pg[m - 1], pm));
-    }
-    aIv = dd_add(aIv, dd_mul_d(im, K.b[m - 2]));
-    if (m <= N) aIg = dd_add(aIg, dd_mul_d(im, K.wh[m]));
-    pm2 = pm1;
-    pm1 = pm;
-    im2 = im1;
-    im1 = im;
+    const dd um = dd_add(dd_mul_d(dd_mul(xpm1, sd.R), K.dfac[m - 2]), dd_mul_d(dd_mul(D2, um2), (double)(m - 1)));
+    const dd vm = dd_add(dd_mul_d(dd_mul(xpm2, R3), K.efac[m - 2]), dd_mul_d(dd_mul(D2, vm2), (double)(m - 2)));
+    acc_add_dddd(aPv, K.wpv[m], um);
+    acc_add_dddd(aPg, K.wpg[m], um);
+    acc_add_dddd(aIv, K.wiv[m], vm);
+    acc_add_dddd(aIg, K.wig[m], vm);
+    um2 = um1;
+    um1 = um;
+    vm2 = vm1;
+    vm1 = vm;
     xpm2 = xpm1;
     xpm1 = dd_mul_d(xpm1, x);
   }
-  C.sPv = aPv;
-  C.sPg = aPg;
-  C.sIv = aIv;
-  C.sIg = aIg;
+  C.sPv = acc_dd(aPv);
+  C.sPg = acc_dd(aPg);
+  C.sIv = acc_dd(aIv);
+  C.sIg = acc_dd(aIg);
   C.R = sd.R.hi;
 }
 

@@ -177,6 +177,27 @@ SPHBI_HD void acc_add_ddprod(acc2& a, dd w, double y) {
   a.c += ep + es;
 }
 SPHBI_HD dd acc_dd(acc2 a) { return two_sum(a.s, a.c); }
+// w * y accumulated, w and y both dd (terms below eps^2 |w y| dropped).
+SPHBI_HD void acc_add_dddd(acc2& a, dd w, dd y) {
+  const double p = w.hi * y.hi;
+  const double ep = fma(w.hi, y.lo, fma(w.lo, y.hi, fma(w.hi, y.hi, -p)));
+  const double s = a.s + p;
+  const double bb = s - a.s;
+  const double es = (a.s - (s - bb)) + (p - bb);
+  a.s = s;
+  a.c += ep + es;
+}
+// a*m1 + b*m2 (a, b dd; m1, m2 double), one rounding-free pass.
+SPHBI_HD dd dd_dot2_d(dd a, double m1, dd b, double m2) {
+  const double p1 = a.hi * m1;
+  const double e1 = fma(a.lo, m1, fma(a.hi, m1, -p1));
+  const double p2 = b.hi * m2;
+  const double e2 = fma(b.lo, m2, fma(b.hi, m2, -p2));
+  const double s = p1 + p2;
+  const double bb = s - p1;
+  const double es = (p1 - (s - bb)) + (p2 - bb);
+  return quick_two_sum(s, es + e1 + e2);
+}
 
 // ---------------------------------------------------------------------------
 // libm wrappers (device intrinsics / host libm)
