@@ -698,96 +698,15 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
 }
 
 // ---------------------------------------------------------------------------
-// Flattened decomposition. The reference recurses (t3 -> wedge + t2 + wedge,
-// wedge -> stubs -> split stubs, wedge -> segments). Here each routine exists
-// ONCE in the generated code: decomposition queues wedge / segment / stub
-// tasks and three loops drain them. Branch decisions, signs and constants are
-// the reference's; only the order in which pieces reach the sink differs
-// (immaterial: pieces are summed in double-double).
+// Stackless decomposition. The reference recurses (t3 -> wedge + t2 + wedge,
+// wedge -> stubs -> split stubs, wedge -> segment). Here each routine exists
+// ONCE in the generated code and holds almost no local memory: the <= 4
+// wedges of a pair are produced on the fly from a register schedule, each
+// wedge's (<= 1) segment and (<= 2) stubs are handled before the next wedge,
+// and only stub splits use a 4-deep LIFO. Branch decisions, signs and
+// constants are the reference's; only the order in which pieces reach the
+// sink differs (immaterial: pieces are summed in double-double).
 // ---------------------------------------------------------------------------
-struct WedgeTask {
-  P2 n0, n1, n2;
-  double sign;
-};
-struct SegTask {
-  P2 t0, t1, keep;
-  double sign;
-};
-struct StubTask {
-  P2 v1, v2;
-  double sign;
-};
-constexpr int kMaxWedges = 4;   // t3 -> 4 wedges
-constexpr int kMaxSegs = 2;     // <= 1 per wedge (drained per wedge)
-constexpr int kMaxStubs = 8;    // <= 2 per wedge, + 1 per split (LIFO, drained per wedge)
-
-struct Tasks {
-  WedgeTask w[kMaxWedges];
-  SegTask sg[kMaxSegs];
-  StubTask st[kMaxStubs];
-  int nw, nsg, nst;
-};
-
-SPHBI_HD void tasks_init(Tasks& T) { T.nw = T.nsg = T.nst = 0; }
-
-template <class Sink>
-SPHBI_HD void push_wedge(Sink& c, Tasks& T, P2 n0, P2 n1, P2 n2, double sign) {
-  if (T.nw >= kMaxWedges) {
-    c.status |= kStatusStack;
-    return;
-  }
-  T.w[T.nw++] = WedgeTask{n0, n1, n2, sign};
-}
-template <class Sink>
-SPHBI_HD void push_seg(Sink& c, Tasks& T, P2 t0, P2 t1, P2 keep, double sign) {
-  if (T.nsg >= kMaxSegs) {
-    c.status |= kStatusStack;
-    return;
-  }
-  T.sg[T.nsg++] = SegTask{t0, t1, keep, sign};
-}
-template <class Sink>
-SPHBI_HD void push_stub(Sink& c, Tasks& T, P2 v1, P2 v2, double sign) {
-  if (T.nst >= kMaxStubs) {
-    c.status |= kStatusStack;
-    return;
-  }
-  T.st[T.nst++] = StubTask{v1, v2, sign};
-}
-
-// region_t2 (:607-616): two wedges about the auxiliary point at distance 3.
-template <class Sink>
-SPHBI_HD void tasks_t2(Sink& c, Tasks& T, P2 a, P2 b, P2 cc, double sign) {
-  if (signed_area(a, b, cc) < 0.0) {
-    const P2 t = a;
-    a = b;
-    b = t;
-  }
-  const P2 u = p_sub(b, a);
-  const double len = p_norm(u);
-  const P2 x{a.x + 3.0 * u.x / len, a.y + 3.0 * u.y / len};
-  push_wedge(c, T, a, x, cc, sign);
-  push_wedge(c, T, b, x, cc, -sign);
-}
-
-// region_t3 (:620-632): wedge - t2 - wedge.
-template <class Sink>
-SPHBI_HD void tasks_t3(Sink& c, Tasks& T, P2 a, P2 b, P2 cc, double sign) {
-  if (signed_area(a, b, cc) < 0.0) {
-    const P2 t = b;
-    b = cc;
-    cc = t;
-  }
-  const P2 d1 = p_sub(b, a);
-  const P2 d2 = p_sub(cc, a);
-  const double l1 = p_norm(d1), l2 = p_norm(d2);
-  const P2 x1{a.x + 3.0 * d1.x / l1, a.y + 3.0 * d1.y / l1};
-  const P2 x2{a.x + 3.0 * d2.x / l2, a.y + 3.0 * d2.y / l2};
-  push_wedge(c, T, a, x1, x2, sign);
-  tasks_t2(c, T, b, cc, x1, -sign);
-  push_wedge(c, T, cc, x1, x2, -sign);
-}
-
 // segment_circle_crossings (:494-509)
 struct Crossings {
   int count;
@@ -818,107 +737,6 @@ SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
   return out;
 }
 SPHBI_HD P2 last_crossing(const Crossings& x) { return x.count == 2 ? x.pts[1] : x.pts[0]; }
-
-// region_wedge body (:514-603): emits discs / the arc sector directly and
-// queues its stubs and segments.
-template <class Sink>
-SPHBI_HD void wedge_body(Sink& c, Tasks& T, P2 n0, P2 n1, P2 n2, double sign) {
-  if (signed_area(n0, n1, n2) < 0.0) {
-    const P2 t = n1;
-    n1 = n2;
-    n2 = t;
-  }
-  if (fabs(signed_area(n0, n1, n2)) < kGeomEps) return;
-  Crossings x01 = segment_circle_crossings(n0, n1);
-  Crossings x02 = segment_circle_crossings(n0, n2);
-  Crossings x12 = segment_circle_crossings(n1, n2);
-  const P2 origin{0.0, 0.0};
-  const bool origin_inside = point_in_triangle(origin, n0, n1, n2);
-  if (x01.count == 0 && x02.count == 0 && x12.count == 0) {
-    if (origin_inside) {
-      c.bump(kWedgeNoCrossingsDisc);
-      c.disc(sign);
-      return;
-    }
-    c.bump(kWedgeNoCrossingsZero);
-    return;
-  }
-  const int crossing_edges = (x01.count > 0 ? 1 : 0) + (x02.count > 0 ? 1 : 0) +
-                             (x12.count > 0 ? 1 : 0);
-  if (crossing_edges == 1) {
-    P2 e0 = n0, e1 = n1, opp = n2;
-    int count = x01.count;
-    if (x02.count > 0) {
-      e0 = n0;
-      e1 = n2;
-      opp = n1;
-      count = x02.count;
-    } else if (x12.count > 0) {
-      e0 = n1;
-      e1 = n2;
-      opp = n0;
-      count = x12.count;
-    }
-    if (count == 2) {
-      c.bump(kWedgeSingleEdgeSegment);
-      push_seg(c, T, e0, e1, opp, sign);
-      return;
-    }
-    c.bump(kWedgeLoneTouch);
-    if (origin_inside) c.disc(sign);
-    return;
-  }
-  if (x01.count == 0 || x02.count == 0) {
-    if (x01.count > 0 && x12.count > 0) {
-      const P2 t0 = n0;
-      n0 = n1;
-      n1 = n2;
-      n2 = t0;
-    } else if (x02.count > 0 && x12.count > 0) {
-      const P2 t2 = n2;
-      n2 = n1;
-      n1 = n0;
-      n0 = t2;
-    }
-    if (signed_area(n0, n1, n2) < 0.0) {
-      const P2 t = n1;
-      n1 = n2;
-      n2 = t;
-    }
-    x01 = segment_circle_crossings(n0, n1);
-    x02 = segment_circle_crossings(n0, n2);
-    x12 = segment_circle_crossings(n1, n2);
-  }
-  c.bump(kWedgeGeneral);
-  // x01 / x02 could in principle lose their crossings after relabeling; the
-  // reference would then read points[-1] (UB). Flag instead of reading.
-  if (x01.count == 0 || x02.count == 0) {
-    c.status |= kStatusLogic;
-    return;
-  }
-  const P2 s1 = last_crossing(x01);
-  const P2 s2 = last_crossing(x02);
-  const double arc_orient = signed_area(origin, s1, s2);
-  if (fabs(arc_orient) > kGeomEps) {
-    double sector_sign = sign;
-    if (!(arc_orient > 0.0)) {
-      // reflex arc: negated sector plus the full disc
-      c.bump(kWedgeReflexDisc);
-      sector_sign = -sign;
-      c.disc(sign);
-    }
-    region_sector(c, s1, s2, sector_sign);
-  }
-  const double stub_a = signed_area(origin, n0, s1);
-  if (fabs(stub_a) > kGeomEps) push_stub(c, T, n0, s1, stub_a > 0.0 ? sign : -sign);
-  const double stub_b = signed_area(origin, s2, n0);
-  if (fabs(stub_b) > kGeomEps) push_stub(c, T, s2, n0, stub_b > 0.0 ? sign : -sign);
-  if (x12.count == 2) {
-    c.bump(kWedgeCapSubtracted);
-    const P2 mirror{n1.x + n2.x - n0.x, n1.y + n2.y - n0.y};
-    push_seg(c, T, n1, n2, mirror, -sign);
-  }
-}
 
 // region_segment body (:369-423).
 template <class Sink>
@@ -956,57 +774,236 @@ SPHBI_HD void segment_body(Sink& c, P2 t0, P2 t1, P2 q_keep, double sign) {
   c.segment(Frame{n.x, n.y, -n.y, n.x}, d, sign);
 }
 
-// region_stub body (:426-484): a direct stub is emitted (cone + window
-// bounds); an acute one is split at the perpendicular foot (LIFO, in the
-// reference's order: stub(v1, foot) then stub(v2, foot)).
+// region_stub (:426-484): a direct stub is emitted (cone + window bounds);
+// an acute one is split at the perpendicular foot into stub(v1, foot) and
+// stub(v2, foot), processed in that order.
+struct StubTask {
+  P2 v1, v2;
+};
+constexpr int kMaxStubStack = 4;
+
 template <class Sink>
-SPHBI_HD void stub_body(Sink& c, Tasks& T, P2 v1, P2 v2, double sign) {
-  double r1 = p_norm(v1), r2 = p_norm(v2);
-  if (r1 < r2) {
-    const P2 tv = v1;
-    v1 = v2;
-    v2 = tv;
-    const double tr = r1;
-    r1 = r2;
-    r2 = tr;
+SPHBI_HD void stub_process(Sink& c, P2 v1_in, P2 v2_in, double sign) {
+  StubTask st[kMaxStubStack];
+  st[0] = StubTask{v1_in, v2_in};
+  int top = 1;
+  while (top > 0) {
+    --top;
+    P2 v1 = st[top].v1, v2 = st[top].v2;
+    double r1 = p_norm(v1), r2 = p_norm(v2);
+    if (r1 < r2) {
+      const P2 tv = v1;
+      v1 = v2;
+      v2 = tv;
+      const double tr = r1;
+      r1 = r2;
+      r2 = tr;
+    }
+    const double area2 = p_cross(v1, v2);
+    if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
+      c.bump(kStubDegenerate);
+      continue;
+    }
+    const P2 b = p_sub(v1, v2);
+    const double dot_a = -(v2.x * b.x + v2.y * b.y);
+    if (dot_a <= kGeomEps) {
+      c.bump(kStubDirect);
+      stub_direct(c, v1, v2, r1, r2, area2, b, sign);
+      continue;
+    }
+    c.bump(kStubSplit);
+    const double t = dot_a / p_norm2(b);
+    const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
+    if (top + 2 > kMaxStubStack) {
+      c.status |= kStatusStack;
+      continue;
+    }
+    st[top++] = StubTask{v2, foot};
+    st[top++] = StubTask{v1, foot};
   }
-  const double area2 = p_cross(v1, v2);
-  if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
-    c.bump(kStubDegenerate);
-    return;
-  }
-  const P2 b = p_sub(v1, v2);
-  const double dot_a = -(v2.x * b.x + v2.y * b.y);
-  if (dot_a <= kGeomEps) {
-    c.bump(kStubDirect);
-    stub_direct(c, v1, v2, r1, r2, area2, b, sign);
-    return;
-  }
-  c.bump(kStubSplit);
-  const double t = dot_a / p_norm2(b);
-  const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
-  push_stub(c, T, v2, foot, sign);
-  push_stub(c, T, v1, foot, sign);
 }
 
-// Drain the queues: wedges first (they queue segments and stubs), then
-// segments, then stubs (LIFO, splits push back).
+// region_wedge (:514-603)
 template <class Sink>
-SPHBI_HD void drain_pieces(Sink& c, Tasks& T) {
-  for (int i = 0; i < T.nsg; ++i) segment_body(c, T.sg[i].t0, T.sg[i].t1, T.sg[i].keep, T.sg[i].sign);
-  T.nsg = 0;
-  while (T.nst > 0) {
-    --T.nst;
-    const StubTask s = T.st[T.nst];
-    stub_body(c, T, s.v1, s.v2, s.sign);
+SPHBI_HD void wedge_body(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
+  if (signed_area(n0, n1, n2) < 0.0) {
+    const P2 t = n1;
+    n1 = n2;
+    n2 = t;
   }
+  if (fabs(signed_area(n0, n1, n2)) < kGeomEps) return;
+  Crossings x01 = segment_circle_crossings(n0, n1);
+  Crossings x02 = segment_circle_crossings(n0, n2);
+  Crossings x12 = segment_circle_crossings(n1, n2);
+  const P2 origin{0.0, 0.0};
+  const bool origin_inside = point_in_triangle(origin, n0, n1, n2);
+  if (x01.count == 0 && x02.count == 0 && x12.count == 0) {
+    if (origin_inside) {
+      c.bump(kWedgeNoCrossingsDisc);
+      c.disc(sign);
+      return;
+    }
+    c.bump(kWedgeNoCrossingsZero);
+    return;
+  }
+  const int crossing_edges = (x01.count > 0 ? 1 : 0) + (x02.count > 0 ? 1 : 0) +
+                             (x12.count > 0 ? 1 : 0);
+  bool have_seg = false;
+  P2 sg0{0.0, 0.0}, sg1{0.0, 0.0}, sgk{0.0, 0.0};
+  double sg_sign = sign;
+  int nstub = 0;
+  P2 s1{0.0, 0.0}, s2{0.0, 0.0};
+  double stub_a = 0.0, stub_b = 0.0;
+  if (crossing_edges == 1) {
+    P2 e0 = n0, e1 = n1, opp = n2;
+    int count = x01.count;
+    if (x02.count > 0) {
+      e0 = n0;
+      e1 = n2;
+      opp = n1;
+      count = x02.count;
+    } else if (x12.count > 0) {
+      e0 = n1;
+      e1 = n2;
+      opp = n0;
+      count = x12.count;
+    }
+    if (count == 2) {
+      c.bump(kWedgeSingleEdgeSegment);
+      have_seg = true;
+      sg0 = e0;
+      sg1 = e1;
+      sgk = opp;
+    } else {
+      c.bump(kWedgeLoneTouch);
+      if (origin_inside) c.disc(sign);
+      return;
+    }
+  } else {
+    if (x01.count == 0 || x02.count == 0) {
+      if (x01.count > 0 && x12.count > 0) {
+        const P2 t0 = n0;
+        n0 = n1;
+        n1 = n2;
+        n2 = t0;
+      } else if (x02.count > 0 && x12.count > 0) {
+        const P2 t2 = n2;
+        n2 = n1;
+        n1 = n0;
+        n0 = t2;
+      }
+      if (signed_area(n0, n1, n2) < 0.0) {
+        const P2 t = n1;
+        n1 = n2;
+        n2 = t;
+      }
+      x01 = segment_circle_crossings(n0, n1);
+      x02 = segment_circle_crossings(n0, n2);
+      x12 = segment_circle_crossings(n1, n2);
+    }
+    c.bump(kWedgeGeneral);
+    // x01 / x02 could in principle lose their crossings after relabeling; the
+    // reference would then read points[-1] (UB). Flag instead of reading.
+    if (x01.count == 0 || x02.count == 0) {
+      c.status |= kStatusLogic;
+      return;
+    }
+    s1 = last_crossing(x01);
+    s2 = last_crossing(x02);
+    const double arc_orient = signed_area(origin, s1, s2);
+    if (fabs(arc_orient) > kGeomEps) {
+      double sector_sign = sign;
+      if (!(arc_orient > 0.0)) {
+        // reflex arc: negated sector plus the full disc
+        c.bump(kWedgeReflexDisc);
+        sector_sign = -sign;
+        c.disc(sign);
+      }
+      region_sector(c, s1, s2, sector_sign);
+    }
+    stub_a = signed_area(origin, n0, s1);
+    stub_b = signed_area(origin, s2, n0);
+    nstub = 2;
+    if (x12.count == 2) {
+      c.bump(kWedgeCapSubtracted);
+      have_seg = true;
+      sg0 = n1;
+      sg1 = n2;
+      sgk = P2{n1.x + n2.x - n0.x, n1.y + n2.y - n0.y};
+      sg_sign = -sign;
+    }
+  }
+  // stubs (n0, s1) and (s2, n0), one call site
+  for (int j = 0; j < nstub; ++j) {
+    const double ar = j == 0 ? stub_a : stub_b;
+    if (fabs(ar) > kGeomEps)
+      stub_process(c, j == 0 ? n0 : s2, j == 0 ? s1 : n0, ar > 0.0 ? sign : -sign);
+  }
+  if (have_seg) segment_body(c, sg0, sg1, sgk, sg_sign);
 }
+
+// Wedge schedule of one dispatch (integrate_normalized :637-674 with
+// region_t2 :607-616 and region_t3 :620-632 unrolled): kind 1 = a single
+// wedge (p0, p1, p2); kind 2 = t2(p0, p1, p2); kind 3 = t3(p0, p1, p2).
 template <class Sink>
-SPHBI_HD void run_tasks(Sink& c, Tasks& T) {
-  drain_pieces(c, T);  // pieces queued directly (region-level entry points)
-  for (int i = 0; i < T.nw; ++i) {
-    wedge_body(c, T, T.w[i].n0, T.w[i].n1, T.w[i].n2, T.w[i].sign);
-    drain_pieces(c, T);
+SPHBI_HD void run_wedges(Sink& c, int kind, P2 a, P2 b, P2 cc, double sign) {
+  P2 x1{0.0, 0.0}, x2{0.0, 0.0}, b2{0.0, 0.0}, c2{0.0, 0.0}, x{0.0, 0.0};
+  int nw = 1;
+  if (kind == 2) {
+    // region_t2(a, b, cc): wedge(a, x, cc, +) - wedge(b, x, cc)
+    if (signed_area(a, b, cc) < 0.0) {
+      const P2 t = a;
+      a = b;
+      b = t;
+    }
+    const P2 u = p_sub(b, a);
+    const double len = p_norm(u);
+    x = P2{a.x + 3.0 * u.x / len, a.y + 3.0 * u.y / len};
+    nw = 2;
+  } else if (kind == 3) {
+    // region_t3(a, b, cc): wedge(a, x1, x2) - t2(b, cc, x1) - wedge(cc, x1, x2)
+    if (signed_area(a, b, cc) < 0.0) {
+      const P2 t = b;
+      b = cc;
+      cc = t;
+    }
+    const P2 d1 = p_sub(b, a);
+    const P2 d2 = p_sub(cc, a);
+    const double l1 = p_norm(d1), l2 = p_norm(d2);
+    x1 = P2{a.x + 3.0 * d1.x / l1, a.y + 3.0 * d1.y / l1};
+    x2 = P2{a.x + 3.0 * d2.x / l2, a.y + 3.0 * d2.y / l2};
+    b2 = b;
+    c2 = cc;
+    if (signed_area(b2, c2, x1) < 0.0) {
+      const P2 t = b2;
+      b2 = c2;
+      c2 = t;
+    }
+    const P2 u = p_sub(c2, b2);
+    const double len = p_norm(u);
+    x = P2{b2.x + 3.0 * u.x / len, b2.y + 3.0 * u.y / len};
+    nw = 4;
+  }
+  for (int i = 0; i < nw; ++i) {
+    P2 n0 = a, n1 = b, n2 = cc;
+    double sg = sign;
+    if (kind == 2) {
+      n0 = i == 0 ? a : b;
+      n1 = x;
+      n2 = cc;
+      sg = i == 0 ? sign : -sign;
+    } else if (kind == 3) {
+      if (i == 0) {
+        n0 = a; n1 = x1; n2 = x2; sg = sign;
+      } else if (i == 1) {
+        n0 = b2; n1 = x; n2 = x1; sg = -sign;
+      } else if (i == 2) {
+        n0 = c2; n1 = x; n2 = x1; sg = sign;
+      } else {
+        n0 = cc; n1 = x1; n2 = x2; sg = -sign;
+      }
+    }
+    wedge_body(c, n0, n1, n2, sg);
   }
 }
 
@@ -1017,71 +1014,62 @@ SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
     c.bump(kDispatchDegenerate);
     return false;
   }
-  Tasks T;
-  tasks_init(T);
-  const double r[3] = {p_norm(v[0]), p_norm(v[1]), p_norm(v[2])};
-  int inside_count = 0, in0 = 0, in1 = 0;
-  for (int i = 0; i < 3; ++i)
-    if (r[i] <= 1.0 + kOnCircleTol) {
-      if (inside_count == 0) in0 = i;
-      if (inside_count == 1) in1 = i;
-      ++inside_count;
-    }
+  const double r0 = p_norm(v[0]), r1 = p_norm(v[1]), r2 = p_norm(v[2]);
+  const bool i0 = r0 <= 1.0 + kOnCircleTol, i1 = r1 <= 1.0 + kOnCircleTol, i2 = r2 <= 1.0 + kOnCircleTol;
+  const int inside_count = (i0 ? 1 : 0) + (i1 ? 1 : 0) + (i2 ? 1 : 0);
   if (inside_count <= 1) {
-    int i0 = in0;
+    int k0;
     if (inside_count == 0) {
       c.bump(kDispatchWedgeOutside);
-      i0 = 0;
-      if (r[1] < r[i0]) i0 = 1;
-      if (r[2] < r[i0]) i0 = 2;
+      k0 = 0;
+      double rk = r0;
+      if (r1 < rk) {
+        k0 = 1;
+        rk = r1;
+      }
+      if (r2 < rk) k0 = 2;
     } else {
       c.bump(kDispatchWedgeSingle);
+      k0 = i0 ? 0 : (i1 ? 1 : 2);
     }
-    push_wedge(c, T, v[i0], v[(i0 + 1) % 3], v[(i0 + 2) % 3], 1.0);
+    const P2 a = k0 == 0 ? v[0] : (k0 == 1 ? v[1] : v[2]);
+    const P2 b = k0 == 0 ? v[1] : (k0 == 1 ? v[2] : v[0]);
+    const P2 cc = k0 == 0 ? v[2] : (k0 == 1 ? v[0] : v[1]);
+    run_wedges(c, 1, a, b, cc, 1.0);
   } else if (inside_count == 2) {
     c.bump(kDispatchTwoInside);
-    tasks_t2(c, T, v[in0], v[in1], v[3 - in0 - in1], 1.0);
+    // inside[0] < inside[1] in index order, then the outside vertex
+    const P2 a = i0 ? v[0] : v[1];
+    const P2 b = i0 ? (i1 ? v[1] : v[2]) : v[2];
+    const P2 cc = !i0 ? v[0] : (!i1 ? v[1] : v[2]);
+    run_wedges(c, 2, a, b, cc, 1.0);
   } else {
     c.bump(kDispatchThreeInside);
-    tasks_t3(c, T, v[0], v[1], v[2], 1.0);
+    run_wedges(c, 3, v[0], v[1], v[2], 1.0);
   }
-  run_tasks(c, T);
   return true;
 }
 
-// Region-level entry points (test surface): the reference's region_* with a
-// single task queued.
+// Region-level entry points (test surface, triangle_integrator.hpp:335-632).
 template <class Sink>
 SPHBI_HD void region_segment(Sink& c, P2 t0, P2 t1, P2 keep, double sign) {
   segment_body(c, t0, t1, keep, sign);
 }
 template <class Sink>
 SPHBI_HD void region_stub(Sink& c, P2 v1, P2 v2, double sign) {
-  Tasks T;
-  tasks_init(T);
-  push_stub(c, T, v1, v2, sign);
-  run_tasks(c, T);
+  stub_process(c, v1, v2, sign);
 }
 template <class Sink>
 SPHBI_HD void region_wedge(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
-  Tasks T;
-  tasks_init(T);
-  push_wedge(c, T, n0, n1, n2, sign);
-  run_tasks(c, T);
+  run_wedges(c, 1, n0, n1, n2, sign);
 }
 template <class Sink>
 SPHBI_HD void region_t2(Sink& c, P2 a, P2 b, P2 cc, double sign) {
-  Tasks T;
-  tasks_init(T);
-  tasks_t2(c, T, a, b, cc, sign);
-  run_tasks(c, T);
+  run_wedges(c, 2, a, b, cc, sign);
 }
 template <class Sink>
 SPHBI_HD void region_t3(Sink& c, P2 a, P2 b, P2 cc, double sign) {
-  Tasks T;
-  tasks_init(T);
-  tasks_t3(c, T, a, b, cc, sign);
-  run_tasks(c, T);
+  run_wedges(c, 3, a, b, cc, sign);
 }
 
 // ---------------------------------------------------------------------------
