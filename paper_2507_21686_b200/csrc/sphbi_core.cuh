@@ -934,6 +934,7 @@ SPHBI_HD void wedge_body(Sink& c, P2 n0, P2 n1, P2 n2, double sign) {
     }
   }
   // stubs (n0, s1) and (s2, n0), one call site
+#pragma unroll 1
   for (int j = 0; j < nstub; ++j) {
     const double ar = j == 0 ? stub_a : stub_b;
     if (fabs(ar) > kGeomEps)
@@ -984,6 +985,7 @@ SPHBI_HD void run_wedges(Sink& c, int kind, P2 a, P2 b, P2 cc, double sign) {
     x = P2{b2.x + 3.0 * u.x / len, b2.y + 3.0 * u.y / len};
     nw = 4;
   }
+#pragma unroll 1
   for (int i = 0; i < nw; ++i) {
     P2 n0 = a, n1 = b, n2 = cc;
     double sg = sign;
@@ -1017,6 +1019,8 @@ SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
   const double r0 = p_norm(v[0]), r1 = p_norm(v[1]), r2 = p_norm(v[2]);
   const bool i0 = r0 <= 1.0 + kOnCircleTol, i1 = r1 <= 1.0 + kOnCircleTol, i2 = r2 <= 1.0 + kOnCircleTol;
   const int inside_count = (i0 ? 1 : 0) + (i1 ? 1 : 0) + (i2 ? 1 : 0);
+  int kind;
+  P2 a, b, cc;
   if (inside_count <= 1) {
     int k0;
     if (inside_count == 0) {
@@ -1032,21 +1036,25 @@ SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
       c.bump(kDispatchWedgeSingle);
       k0 = i0 ? 0 : (i1 ? 1 : 2);
     }
-    const P2 a = k0 == 0 ? v[0] : (k0 == 1 ? v[1] : v[2]);
-    const P2 b = k0 == 0 ? v[1] : (k0 == 1 ? v[2] : v[0]);
-    const P2 cc = k0 == 0 ? v[2] : (k0 == 1 ? v[0] : v[1]);
-    run_wedges(c, 1, a, b, cc, 1.0);
+    kind = 1;
+    a = k0 == 0 ? v[0] : (k0 == 1 ? v[1] : v[2]);
+    b = k0 == 0 ? v[1] : (k0 == 1 ? v[2] : v[0]);
+    cc = k0 == 0 ? v[2] : (k0 == 1 ? v[0] : v[1]);
   } else if (inside_count == 2) {
     c.bump(kDispatchTwoInside);
     // inside[0] < inside[1] in index order, then the outside vertex
-    const P2 a = i0 ? v[0] : v[1];
-    const P2 b = i0 ? (i1 ? v[1] : v[2]) : v[2];
-    const P2 cc = !i0 ? v[0] : (!i1 ? v[1] : v[2]);
-    run_wedges(c, 2, a, b, cc, 1.0);
+    kind = 2;
+    a = i0 ? v[0] : v[1];
+    b = i0 ? (i1 ? v[1] : v[2]) : v[2];
+    cc = !i0 ? v[0] : (!i1 ? v[1] : v[2]);
   } else {
     c.bump(kDispatchThreeInside);
-    run_wedges(c, 3, v[0], v[1], v[2], 1.0);
+    kind = 3;
+    a = v[0];
+    b = v[1];
+    cc = v[2];
   }
+  run_wedges(c, kind, a, b, cc, 1.0);  // single call site: one inlined copy
   return true;
 }
 
