@@ -668,7 +668,7 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
     f.m11 = -f.m11;
     w2.y = -w2.y;
   }
-  const double gamma = atan2(w2.y, w2.x);
+  const double gamma = d_atan2(w2.y, w2.x);
   c.sector(f, gamma, fmin(l, 1.0), sign);
 }
 
@@ -683,12 +683,12 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
     f.m11 = -f.m11;
     w2.y = -w2.y;
   }
-  const double gamma = atan2(w2.y, w2.x);
+  const double gamma = d_atan2(w2.y, w2.x);
   const double D = fabs(area2) / p_norm(b);
   const double l = fmin(r2, 1.0);
   const double u = fmin(r1, 1.0);
   const P2 cc = p_sub(v2, v1);
-  const double beta = atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
+  const double beta = d_atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
   double lo = fmax(l, D);
   if (lo - D <= 256.0 * kDblEps * D) lo = D;
   const bool window = u > lo + kGeomEps;

@@ -91,7 +91,7 @@ SPHBI_HD dd dd_mul(dd a, dd b) {
   p.lo = fma(a.lo, b.hi, p.lo);
   return quick_two_sum(p.hi, p.lo);
 }
-SPHBI_HD dd dd_div(dd a, dd b) {
+SPHBI_HDNI dd dd_div(dd a, dd b) {
   const double q1 = a.hi / b.hi;
   dd r = dd_sub(a, dd_mul_d(b, q1));
   const double q2 = r.hi / b.hi;
@@ -211,6 +211,9 @@ SPHBI_HD void dsincos(double x, double* s, double* c) {
 #endif
 }
 
+// atan2, out of line on the device (3 call sites in the decomposition).
+SPHBI_HDNI double d_atan2(double y, double x) { return atan2(y, x); }
+
 // Bit-exact restatement of glibc's __hypot for finite inputs (non-FMA
 // kernel). Verified here against the host libm on 2e7 random pairs incl.
 // near-equal and widely scaled operands (0 mismatches).
@@ -230,7 +233,8 @@ SPHBI_HD double glibc_hypot_kernel(double ax, double ay) {
   return h;
 }
 
-SPHBI_HD double glibc_hypot(double x, double y) {
+// Out of line on the device: ~15 call sites per pair; scalar-only interface.
+SPHBI_HDNI double glibc_hypot(double x, double y) {
   x = fabs(x);
   y = fabs(y);
   const double ax = x < y ? y : x;
