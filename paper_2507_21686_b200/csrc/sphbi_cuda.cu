@@ -102,6 +102,9 @@ enum ScratchSlot {
   kBufOutB,
   kBufOutS,
   kBufPartial,
+  kBufClass,
+  kBufOrder,
+  kBufCubTemp2,
   kNumBufs
 };
 
@@ -332,6 +335,7 @@ __device__ __forceinline__ void normalized_pair(double qx, double qy, double h, 
 
 template <class Src>
 __global__ void __launch_bounds__(128) k_pipe_count(Src src, int64_t n, double h, unsigned* __restrict__ cnt,
+                                                    unsigned char* __restrict__ cls,
                                                     unsigned long long* counters, unsigned* status_or) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) {
@@ -348,6 +352,10 @@ __global__ void __launch_bounds__(128) k_pipe_count(Src src, int64_t n, double h
   cnt[k] = c.n_sector;
   cnt[n + 1 + k] = c.n_stub;
   cnt[2 * (n + 1) + k] = c.n_seg;
+  // decomposition signature: pairs with equal signatures follow the same
+  // control flow in the emit pass, which runs them in signature order
+  cls[k] = static_cast<unsigned char>((c.n_stub < 15 ? c.n_stub : 15) | ((c.n_sector < 3 ? c.n_sector : 3) << 4) |
+                                      ((c.n_seg < 3 ? c.n_seg : 3) << 6));
   if (c.status) atomicOr(status_or, c.status);
 }
 
@@ -366,9 +374,10 @@ __global__ void __launch_bounds__(128)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
                 StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
-                PairRec* __restrict__ rec, unsigned* status_or) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+                PairRec* __restrict__ rec, const int* __restrict__ order, unsigned* status_or) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t k = order ? order[j] : j;
   double qx, qy, t6[6], a3[3];
   src.load(k, qx, qy, t6, a3);
   P2 nv[3];
@@ -511,6 +520,11 @@ __global__ void __launch_bounds__(128)
 // K5: per-particle fixed-order reduction (pairs sorted by particle, then
 // triangle id), vectorised double2 gradient stores.
 // ---------------------------------------------------------------------------
+__global__ void k_iota(int n, int* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = i;
+}
+
 __global__ void k_row_ptr(int64_t npairs, const int* __restrict__ pp, int p_begin, int p_count,
                           int64_t* __restrict__ row_ptr) {
   // row_ptr[j] = first pair with particle >= p_begin + j, j in [0, p_count]
@@ -770,8 +784,25 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   const int64_t m = n + 1;
   if ((st = scratch_t(c, kBufPipeCnt, 3 * m, &cnt)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPipeOff, 3 * m, &off)) != SPHBI_OK) return st;
-  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(src, n, h, cnt, ctr, dflags);
+  unsigned char *cls, *cls_sorted;
+  int *iota, *order;
+  if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
+  cls_sorted = cls + m;
+  if ((st = scratch_t(c, kBufOrder, 2 * m, &iota)) != SPHBI_OK) return st;
+  order = iota + m;
+  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(src, n, h, cnt, cls, ctr, dflags);
   if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
+  // emit order: pairs grouped by decomposition signature (stable 8-bit radix sort)
+  k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, iota);
+  if ((st = check_launch(c, "k_iota")) != SPHBI_OK) return st;
+  {
+    size_t tmp_sort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, cls, cls_sorted, iota, order, (int)n, 0, 8, s);
+    void* dtmp_sort;
+    if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
+    cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, cls, cls_sorted, iota, order, (int)n, 0, 8, s);
+    if ((st = check_launch(c, "radix sort signatures")) != SPHBI_OK) return st;
+  }
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
   void* dtmp;
@@ -796,7 +827,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, dflags);
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
   if (n_stub) {
     k_pipe_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(K, (int64_t)n_stub, istub, ostub);
