@@ -78,6 +78,18 @@ def build_checkers(force: bool = False) -> None:
             raise RuntimeError(f"core_host build failed:\n{r.stderr[-4000:]}")
 
 
+def build_dropin_tests(force: bool = False) -> None:
+    """Compile the reference's own GTest files unchanged against include/sphbi
+    (tests/dropin/Makefile); only where /root/reference exists."""
+    if not Path("/root/reference/proj/tests/test_triangle_integrator.cpp").exists():
+        return
+    cmd = ["make", "-C", str(ROOT / "tests" / "dropin")] + (["-B"] if force else [])
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"drop-in test build failed:\n{r.stdout[-2000:]}\n{r.stderr[-4000:]}")
+
+
 if __name__ == "__main__":
     build_native(force=True, verbose=True)
     build_checkers(force=True)
+    build_dropin_tests(force=True)
