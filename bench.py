@@ -53,7 +53,8 @@ def env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the
+    timed region (one persistent `nvidia-smi -lms 100` process)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -62,43 +63,53 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self.proc is None:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows) if v is not None]
+        busy = [v for v in sm if v > 500] or sm  # samples under load
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
             for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                if r[5 + i].lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
@@ -145,6 +156,14 @@ def cpu_eval_pairs(scene, idx, nthreads):
     return dt, kind, st, out
 
 
+def bench_config(world, T=65536, n=4194304, npairs=4194304, h=0.05):
+    """The workload description shared by both arms (ours / --impl reference)."""
+    return {"workload": "cfg2 stress triangles, own-triangle pairs (mode A)", "pairs_per_gpu": npairs,
+            "triangles_per_gpu": T, "particles_per_gpu": n, "h": h, "kernel": "wendland_c4", "field": "1",
+            "l2": "flushed between timed steps (256 MB write) + inputs > L2",
+            "parallelism": f"weak x{world} (independent scenes, no collective)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference CPU path on the host cores."""
     if rank != 0:
@@ -167,9 +186,8 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+x87-f80",
-        "data": "synthetic", "config": {"workload": "cfg2 stress triangles, own-triangle pairs (mode A)",
-                                        "pairs_per_step": sample, "h": 0.05, "kernel": "wendland_c4"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (x87 f80 internal sums)",
+        "data": "synthetic", "config": bench_config(world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{sample} seeded random pairs of the 4,194,304-pair cfg2 workload per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -315,7 +333,8 @@ def main():
         achieved = f_pair * npairs / (k_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": f_info.get("traffic_bytes_per_launch"),
-                "kernel": "k_eval_scene_pairs", "kernel_ms": k_ms, "f_pair": f_pair,
+                "kernel": "K4 pair-integral pipeline (k_pipe_count/emit/stub/sector/segment/combine)",
+                "kernel_ms": k_ms, "f_pair": f_pair,
                 "peak_source": "measured live: DFMA loop (sphbi_measure_fp64_peak) in this run"}
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the same workload
@@ -334,10 +353,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 stress triangles, own-triangle pairs (mode A)", "pairs_per_gpu": npairs,
-                       "triangles_per_gpu": T, "particles_per_gpu": n, "h": sc.h, "kernel": "wendland_c4",
-                       "field": "1", "l2": "flushed between timed steps (256 MB write) + inputs > L2",
-                       "parallelism": f"weak x{world} (independent scenes, no collective)"},
+            "config": bench_config(world, T, n, npairs, sc.h),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roof,
