@@ -58,6 +58,18 @@ sphbi_status status_from_bits(unsigned bits) {
 }
 
 constexpr int kEvalBlock = 128;
+
+// minimum resident blocks per SM for the heavy pipeline kernels (register caps;
+// swept on the B200: 5/4/4 -> 96/128/128 registers was fastest)
+#ifndef SPHBI_MINB_COUNT
+#define SPHBI_MINB_COUNT 5
+#endif
+#ifndef SPHBI_MINB_EMIT
+#define SPHBI_MINB_EMIT 4
+#endif
+#ifndef SPHBI_MINB_STUB
+#define SPHBI_MINB_STUB 4
+#endif
 constexpr int kMaxChunkPairs = 1 << 23;  // 8 Mi pairs per evaluation chunk (pipeline scratch ~ a few GB)
 
 }  // namespace
@@ -334,7 +346,7 @@ __device__ __forceinline__ void normalized_pair(double qx, double qy, double h, 
 }
 
 template <class Src>
-__global__ void __launch_bounds__(128) k_pipe_count(Src src, int64_t n, double h, unsigned* __restrict__ cnt,
+__global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(Src src, int64_t n, double h, unsigned* __restrict__ cnt,
                                                     unsigned char* __restrict__ cls,
                                                     unsigned long long* counters, unsigned* status_or) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -370,7 +382,7 @@ struct PairRec {
 };
 
 template <class Src>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
                 StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
@@ -430,7 +442,7 @@ __global__ void __launch_bounds__(128)
   acc_to_out(a, out[k]);
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
                 AccOut* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
