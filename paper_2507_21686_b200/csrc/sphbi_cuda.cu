@@ -114,6 +114,8 @@ enum ScratchSlot {
   kBufOutB,
   kBufOutS,
   kBufPartial,
+  kBufUserPairs2,
+  kBufUserPairs3,
   kBufClass,
   kBufOrder,
   kBufCubTemp2,
@@ -131,6 +133,9 @@ struct sphbi_ctx {
   size_t cap[kNumBufs] = {};
   cudaEvent_t ev[8] = {};
   unsigned* h_flags = nullptr;  // pinned
+  // copy engines for the streamed host-buffer path (H2D / D2H overlap)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t sev[3][64] = {};  // per chunk: uploaded / computed / downloaded
 };
 
 namespace {
@@ -868,6 +873,117 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   return SPHBI_OK;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Streamed evaluation of an explicit, particle-sorted pair list held in PINNED
+// host memory: particle chunks are uploaded on c->h2d, evaluated on the compute
+// stream and downloaded on c->d2h, so the PCIe transfers overlap the K4
+// pipeline. Returns SPHBI_ERR_INTERNAL (without side effects on the outputs'
+// correctness) when the pair list turns out not to be sorted; the caller then
+// falls back to the general path.
+sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, int64_t n_particles,
+                               const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                               const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
+                               const int64_t* pair_triangle, double* out_value, double* out_grad,
+                               unsigned* dflags, unsigned long long* ctr) {
+  cudaStream_t s = c->stream;
+  sphbi_status st;
+  double *dp, *dt, *dv = nullptr, *dov, *dog;
+  if ((st = scratch_t(c, kBufPxy, 2 * n_particles, &dp)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufTri, 6 * n_triangles, &dt)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutV, n_particles, &dov)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutG, 2 * n_particles, &dog)) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(dt, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
+  if (tri_values) {
+    if ((st = scratch_t(c, kBufVals, 3 * n_triangles, &dv)) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(dv, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
+  }
+  // particle-aligned chunks (pairs sorted by particle: boundaries by binary search)
+  const int nchunks = (int)std::min<int64_t>(32, std::max<int64_t>(2, n_particles / (1 << 19)));
+  std::vector<int64_t> pb(nchunks + 1), qb(nchunks + 1);
+  for (int k = 0; k <= nchunks; ++k) {
+    pb[k] = n_particles * k / nchunks;
+    qb[k] = std::lower_bound(pair_particle, pair_particle + n_pairs, pb[k]) - pair_particle;
+  }
+  qb[nchunks] = n_pairs;
+  int64_t maxq = 0;
+  for (int k = 0; k < nchunks; ++k) maxq = std::max(maxq, qb[k + 1] - qb[k]);
+  int64_t *ip[2], *it[2];
+  if ((st = scratch_t(c, kBufUserPairs0, maxq, &ip[0])) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufUserPairs1, maxq, &it[0])) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufUserPairs2, maxq, &ip[1])) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufUserPairs3, maxq, &it[1])) != SPHBI_OK) return st;
+  unsigned long long* keys;
+  int *pp, *pt;
+  double* pout;
+  int64_t* row_ptr;
+  if ((st = scratch_t(c, kBufKeysA, maxq, &keys)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPairP, maxq, &pp)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPairT, maxq, &pt)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPairOut, 3 * maxq, &pout)) != SPHBI_OK) return st;
+  int64_t maxp = 0;
+  for (int k = 0; k < nchunks; ++k) maxp = std::max(maxp, pb[k + 1] - pb[k]);
+  if ((st = scratch_t(c, kBufRowPtr, maxp + 1, &row_ptr)) != SPHBI_OK) return st;
+  auto upload = [&](int k) -> sphbi_status {
+    const int b = k & 1;
+    if (k >= 2) SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->h2d, c->sev[1][(k - 2) % 64], 0));  // buffer b free
+    const int64_t np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(dp + 2 * pb[k], particle_xy + 2 * pb[k], 16 * np, cudaMemcpyHostToDevice, c->h2d));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(ip[b], pair_particle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(it[b], pair_triangle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
+    SPHBI_CUDA_TRY(cudaEventRecord(c->sev[0][k % 64], c->h2d));
+    return SPHBI_OK;
+  };
+  if ((st = upload(0)) != SPHBI_OK) return st;
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks && (st = upload(k + 1)) != SPHBI_OK) return st;
+    const int b = k & 1;
+    const int64_t p0 = pb[k], np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[0][k % 64], 0));
+    if (k >= 2) SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[2][(k - 2) % 64], 0));  // outputs of k-2 read
+    if (np > 0) {
+      SPHBI_CUDA_TRY(cudaMemsetAsync(dov + p0, 0, 8 * np, s));
+      SPHBI_CUDA_TRY(cudaMemsetAsync(dog + 2 * p0, 0, 16 * np, s));
+    }
+    if (nq > 0) {
+      // validate (range, sortedness) and convert to int32 pairs
+      k_pack_pairs<<<grid_for(nq, 256), 256, 0, s>>>(nq, ip[b], it[b], n_particles, n_triangles, keys, dflags + 1);
+      if ((st = check_launch(c, "k_pack_pairs")) != SPHBI_OK) return st;
+      k_unpack_keys<<<grid_for(nq, 256), 256, 0, s>>>(nq, keys, pp, pt);
+      if ((st = check_launch(c, "k_unpack_keys")) != SPHBI_OK) return st;
+      const SceneSrc src{pp, pt, dp, dt, dv};
+      if ((st = run_pipeline(c, K, h, src, nq, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
+      k_row_ptr<<<grid_for(nq + 1, 256), 256, 0, s>>>(nq, pp, (int)p0, (int)np, row_ptr);
+      if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
+      k_reduce_rows<<<grid_for(np, 256), 256, 0, s>>>((int)p0, (int)np, row_ptr, pout, dov, dog, 0);
+      if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
+    }
+    SPHBI_CUDA_TRY(cudaEventRecord(c->sev[1][k % 64], s));
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->sev[1][k % 64], 0));
+    if (np > 0) {
+      if (out_value)
+        SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value + p0, dov + p0, 8 * np, cudaMemcpyDeviceToHost, c->d2h));
+      if (out_grad)
+        SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad + 2 * p0, dog + 2 * p0, 16 * np, cudaMemcpyDeviceToHost, c->d2h));
+    }
+    SPHBI_CUDA_TRY(cudaEventRecord(c->sev[2][k % 64], c->d2h));
+  }
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->d2h));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->h2d));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (c->h_flags[1] & 1u) return fail(SPHBI_ERR_INVALID_ARGUMENT, "pair index out of range");
+  if (c->h_flags[1] & 2u) return SPHBI_ERR_INTERNAL;  // unsorted: caller falls back
+  return SPHBI_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -923,6 +1039,10 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   }
   c->stream = c->own_stream;
   for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
+  for (auto& row : c->sev)
+    for (auto& e : row) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaMallocHost(&c->h_flags, 256);
   if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
     cudaGetLastError();
@@ -940,6 +1060,10 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   for (int i = 0; i < kNumBufs; ++i)
     if (c->buf[i]) cudaFree(c->buf[i]);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& row : c->sev)
+    for (auto& e : row) cudaEventDestroy(e);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->h_flags) cudaFreeHost(c->h_flags);
   if (c->d_counters) cudaFree(c->d_counters);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -1103,6 +1227,24 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
   if (timing) {
     std::memset(stats, 0, sizeof(*stats));
     cudaEventRecord(c->ev[0], s);
+  }
+  // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
+  if (mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
+      !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
+      (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
+    unsigned* sflags;
+    if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemsetAsync(sflags, 0, 32, s));
+    unsigned long long* sctr = c->counters_on ? c->d_counters : nullptr;
+    st = evaluate_streamed(c, K, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
+                           pair_particle, pair_triangle, out_value, out_grad, sflags, sctr);
+    if (st == SPHBI_OK) {
+      if (pair_list_capacity) *pair_list_capacity = n_pairs;
+      if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "pair evaluation: reference-domain error on device");
+      return SPHBI_OK;
+    }
+    if (st != SPHBI_ERR_INTERNAL) return st;
+    // unsorted pair list: fall through to the general path (which sorts)
   }
   // ---- inputs on the device
   const double *dp = particle_xy, *dt = tri_xy, *dv = tri_values;

@@ -372,3 +372,35 @@ def test_branch_coverage_all_routes(S, ctx):
     counts = c.read_counters(reset=True)
     c.close()
     assert all(int(x) > 0 for x in counts), dict(zip(S.COUNTER_NAMES, counts))
+
+
+def test_streamed_pinned_host_path_is_bitwise_identical(S, ctx):
+    """Pinned host buffers take the chunked H2D / compute / D2H overlap path;
+    results must be bitwise identical to the device-resident path, and an
+    unsorted pair list must fall back to the general path."""
+    import ctypes
+    import torch
+    from paper_2507_21686_b200 import _native as N
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg2(T=32768, per_tri=64, linear_field=True)  # 2,097,152 pairs
+    k = sc.kernels[0]
+    desc = table_of(S, k).desc()
+    n, T = sc.particles.shape[0], sc.triangles.shape[0]
+    ref_v, ref_g, _ = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), tri_values=sc.values,
+                                 pairs=sc.pairs, ctx=ctx)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    P, Tr, V = pin(sc.particles), pin(sc.triangles), pin(sc.values)
+    for order in ("sorted", "shuffled"):
+        if order == "sorted":
+            ip, it = pin(sc.pairs[0]), pin(sc.pairs[1])
+        else:
+            perm = np.random.default_rng(3).permutation(sc.pairs[0].shape[0])
+            ip, it = pin(sc.pairs[0][perm]), pin(sc.pairs[1][perm])
+        ov = torch.empty(n, dtype=torch.float64).pin_memory()
+        og = torch.empty((n, 2), dtype=torch.float64).pin_memory()
+        vp = ctypes.c_void_p
+        rc = ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), sc.h, n, vp(P.data_ptr()), T, vp(Tr.data_ptr()),
+                                    vp(V.data_ptr()), ip.shape[0], vp(ip.data_ptr()), vp(it.data_ptr()),
+                                    vp(ov.data_ptr()), vp(og.data_ptr()), None, None, None, N.MEM_HOST)
+        assert rc == 0, N.last_error()
+        assert np.array_equal(ov.numpy(), ref_v) and np.array_equal(og.numpy(), ref_g), order
