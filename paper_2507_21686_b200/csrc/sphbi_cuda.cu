@@ -136,6 +136,8 @@ struct sphbi_ctx {
   // copy engines for the streamed host-buffer path (H2D / D2H overlap)
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t sev[3][64] = {};  // per chunk: uploaded / computed / downloaded
+  bool force_exact = false;     // host-sized work-item buffers (after a bounded overflow)
+  bool overflowed = false;      // the last bounded pipeline overflowed its buffers
 };
 
 namespace {
@@ -391,7 +393,8 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
                 StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
-                PairRec* __restrict__ rec, const int* __restrict__ order, unsigned* status_or) {
+                PairRec* __restrict__ rec, const int* __restrict__ order, ulonglong4 cap,
+                unsigned* status_or) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t k = order ? order[j] : j;
@@ -408,6 +411,10 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.sector_items = sector_items + off[k];
   e.stub_items = stub_items + off[n + 1 + k];
   e.seg_items = seg_items + off[2 * (n + 1) + k];
+  if (off[n] > cap.x || off[2 * n + 1] > cap.y || off[3 * n + 2] > cap.z) {
+    atomicOr(status_or + 1, 4u);  // bounded work-item buffers overflowed: redo exactly
+    return;
+  }
   const bool nondeg_route = integrate_normalized(e, nv);
   PairRec& r = rec[k];
   AccOut o;
@@ -436,40 +443,46 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
 }
 
 __global__ void __launch_bounds__(128)
-    k_pipe_sector(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
-                  AccOut* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[k];
-  PairAcc a;
-  acc_zero(a);
-  piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, 1.0, it.sign);
-  acc_to_out(a, out[k]);
+    k_pipe_sector(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
+                  const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const PieceItem it = items[k];
+    PairAcc a;
+    acc_zero(a);
+    piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, 1.0, it.sign);
+    acc_to_out(a, out[k]);
+  }
 }
 
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
-    k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
-                AccOut* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const StubItem it = items[k];
-  PairAcc a;
-  acc_zero(a);
-  piece_stub(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
-             it.window != 0, it.sign);
-  acc_to_out(a, out[k]);
+    k_pipe_stub(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
+                const StubItem* __restrict__ items, AccOut* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const StubItem it = items[k];
+    PairAcc a;
+    acc_zero(a);
+    piece_stub(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
+               it.window != 0, it.sign);
+    acc_to_out(a, out[k]);
+  }
 }
 
 __global__ void __launch_bounds__(128)
-    k_pipe_segment(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
-                   AccOut* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[k];
-  PairAcc a;
-  acc_zero(a);
-  piece_segment(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.sign);
-  acc_to_out(a, out[k]);
+    k_pipe_segment(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
+                   const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const PieceItem it = items[k];
+    PairAcc a;
+    acc_zero(a);
+    piece_segment(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.sign);
+    acc_to_out(a, out[k]);
+  }
 }
 
 __device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t n, int64_t k,
@@ -790,9 +803,19 @@ struct PipeStats {
   unsigned long long n_cone = 0, n_bound = 0, n_seg = 0;
 };
 
+// Work-item buffer capacities per pair (sector, stub, segment) for the
+// sync-free mode; the exact totals are only known on the device. Measured on
+// cfg2: 0.7 / 1.9 / 0.25 items per pair; worst single pairs reach ~16 stubs.
+constexpr unsigned long long kCapSectorPerPair = 4, kCapStubPerPair = 8, kCapSegPerPair = 2;
+
+// K4 pipeline over n pairs. bounded = true: no host synchronisation -- the work
+// item buffers are sized by per-pair capacities, piece kernels read their item
+// count on the device, and an overflow sets dflags[1] bit 4 (caller redoes the
+// call with bounded = false, exact host-sized buffers).
 template <class Src>
 sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
-                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps) {
+                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
+                          bool bounded = true) {
   if (n <= 0) return SPHBI_OK;
   cudaStream_t s = c->stream;
   sphbi_status st;
@@ -828,34 +851,50 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
     if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
   }
-  unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->h_flags + 4);
-  for (int j = 0; j < 3; ++j)
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(tot + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
-  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
-  const unsigned long long n_sec = tot[0], n_stub = tot[1], n_seg = tot[2];
+  unsigned long long cap[3];
+  if (c->force_exact) bounded = false;
+  if (bounded) {
+    cap[0] = kCapSectorPerPair * (unsigned long long)n;
+    cap[1] = kCapStubPerPair * (unsigned long long)n;
+    cap[2] = kCapSegPerPair * (unsigned long long)n;
+  } else {
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->h_flags + 4);
+    for (int j = 0; j < 3; ++j)
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(tot + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int j = 0; j < 3; ++j) cap[j] = tot[j];
+  }
+  const ulonglong4 dcap = make_ulonglong4(cap[0], cap[1], cap[2], 0ull);
   PieceItem *isec, *iseg;
   StubItem* istub;
   AccOut *osec, *ostub, *oseg;
   PairRec* rec;
-  if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsC, cap[0], &isec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, cap[1], &istub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, cap[2], &iseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutC, cap[0], &osec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutB, cap[1], &ostub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutS, cap[2], &oseg)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, dflags);
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, dcap, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
-  if (n_stub) {
-    k_pipe_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(K, (int64_t)n_stub, istub, ostub);
+  // piece kernels: grid-stride over the device-resident totals off[j*m + n]
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  auto blocks_for = [&](unsigned long long cap_items, int per_sm) {
+    const unsigned long long need = (cap_items + 127) / 128;
+    return (int)std::max<unsigned long long>(1, std::min<unsigned long long>(need, (unsigned long long)sms * per_sm));
+  };
+  if (cap[1]) {
+    k_pipe_stub<<<blocks_for(cap[1], 4 * 8), 128, 0, s>>>(K, off + m + n, istub, ostub);
     if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
   }
-  if (n_sec) {
-    k_pipe_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(K, (int64_t)n_sec, isec, osec);
+  if (cap[0]) {
+    k_pipe_sector<<<blocks_for(cap[0], 8 * 8), 128, 0, s>>>(K, off + n, isec, osec);
     if ((st = check_launch(c, "k_pipe_sector")) != SPHBI_OK) return st;
   }
-  if (n_seg) {
-    k_pipe_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(K, (int64_t)n_seg, iseg, oseg);
+  if (cap[2]) {
+    k_pipe_segment<<<blocks_for(cap[2], 8 * 8), 128, 0, s>>>(K, off + 2 * m + n, iseg, oseg);
     if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
   }
   if (mode == 0) {
@@ -865,11 +904,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, rec, off, osec, ostub, oseg, dout);
     if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
   }
-  if (ps) {
-    ps->n_cone += n_sec;
-    ps->n_bound += n_stub;
-    ps->n_seg += n_seg;
-  }
+  (void)ps;
   return SPHBI_OK;
 }
 
@@ -906,7 +941,11 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     SPHBI_CUDA_TRY(cudaMemcpyAsync(dv, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
   }
   // particle-aligned chunks (pairs sorted by particle: boundaries by binary search)
-  const int nchunks = (int)std::min<int64_t>(32, std::max<int64_t>(2, n_particles / (1 << 19)));
+#ifndef SPHBI_STREAM_CHUNK_LOG2
+#define SPHBI_STREAM_CHUNK_LOG2 20
+#endif
+  const int nchunks =
+      (int)std::min<int64_t>(32, std::max<int64_t>(2, n_particles >> SPHBI_STREAM_CHUNK_LOG2));
   std::vector<int64_t> pb(nchunks + 1), qb(nchunks + 1);
   for (int k = 0; k <= nchunks; ++k) {
     pb[k] = n_particles * k / nchunks;
@@ -947,7 +986,6 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     const int b = k & 1;
     const int64_t p0 = pb[k], np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
     SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[0][k % 64], 0));
-    if (k >= 2) SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[2][(k - 2) % 64], 0));  // outputs of k-2 read
     if (np > 0) {
       SPHBI_CUDA_TRY(cudaMemsetAsync(dov + p0, 0, 8 * np, s));
       SPHBI_CUDA_TRY(cudaMemsetAsync(dog + 2 * p0, 0, 16 * np, s));
@@ -980,6 +1018,10 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
   SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
   if (c->h_flags[1] & 1u) return fail(SPHBI_ERR_INVALID_ARGUMENT, "pair index out of range");
+  if (c->h_flags[1] & 4u) {
+    c->overflowed = true;
+    return SPHBI_ERR_INTERNAL;
+  }
   if (c->h_flags[1] & 2u) return SPHBI_ERR_INTERNAL;  // unsorted: caller falls back
   return SPHBI_OK;
 }
@@ -1043,7 +1085,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  cudaMallocHost(&c->h_flags, 256);
+  cudaMallocHost(&c->h_flags, 512);
   if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
     cudaGetLastError();
     return fail(SPHBI_ERR_OUT_OF_MEMORY, "counter allocation failed");
@@ -1107,9 +1149,9 @@ sphbi_status sphbi_kernel_validate(const sphbi_kernel_desc* k) {
   return make_consts(k, &K);
 }
 
-sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
-                                   const double* query_xy, const double* tri_xy, const double* values,
-                                   int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
+static sphbi_status integrate_pairs_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                        const double* query_xy, const double* tri_xy, const double* values,
+                                        int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (mode != 0 && mode != 1) return fail(SPHBI_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
@@ -1160,12 +1202,16 @@ sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel
                       nullptr);
     if (st != SPHBI_OK) return st;
   }
-  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 4, cudaMemcpyDeviceToHost, c->stream));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, c->stream));
   if (mem == SPHBI_MEM_HOST) {
     SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(double) * nout * n, cudaMemcpyDeviceToHost, c->stream));
     if (status_out) std::memset(status_out, 0, 4 * n);  // per-call status is reported as a whole
   }
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->h_flags[1] & 4u) {
+    c->overflowed = true;
+    return SPHBI_ERR_INTERNAL;
+  }
   const unsigned bits = c->h_flags[0];
   if (bits) return fail(status_from_bits(bits), "integrate_triangle: reference-domain error on device");
   return SPHBI_OK;
@@ -1207,7 +1253,7 @@ sphbi_status sphbi_integrate_regions(sphbi_ctx* c, const sphbi_kernel_desc* kern
   return SPHBI_OK;
 }
 
-sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
+static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
                             const double* particle_xy, int64_t n_triangles, const double* tri_xy,
                             const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
@@ -1243,7 +1289,7 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
       if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "pair evaluation: reference-domain error on device");
       return SPHBI_OK;
     }
-    if (st != SPHBI_ERR_INTERNAL) return st;
+    if (st != SPHBI_ERR_INTERNAL || c->overflowed) return st;
     // unsorted pair list: fall through to the general path (which sorts)
   }
   // ---- inputs on the device
@@ -1515,8 +1561,12 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
     if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, dov, 8 * n_particles, cudaMemcpyDeviceToHost, s));
     if (out_grad) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, dog, 16 * n_particles, cudaMemcpyDeviceToHost, s));
   }
-  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 4, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (c->h_flags[1] & 4u) {
+    c->overflowed = true;
+    return SPHBI_ERR_INTERNAL;
+  }
   if (timing) {
     float a = 0, b = 0, d = 0;
     cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
@@ -1531,6 +1581,43 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
   }
   if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "pair evaluation: reference-domain error on device");
   return SPHBI_OK;
+}
+
+// Public entry points: a bounded (sync-free) pipeline that overflowed its
+// work-item buffers is redone once with exact, host-sized buffers.
+sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                   const double* query_xy, const double* tri_xy, const double* values,
+                                   int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
+  if (c) c->overflowed = false;
+  sphbi_status st = integrate_pairs_impl(c, kernel, h, n, query_xy, tri_xy, values, mode, out, status_out, mem);
+  if (c && c->overflowed) {
+    c->overflowed = false;
+    c->force_exact = true;
+    st = integrate_pairs_impl(c, kernel, h, n, query_xy, tri_xy, values, mode, out, status_out, mem);
+    c->force_exact = false;
+  }
+  return st;
+}
+
+sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
+                            const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                            const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
+                            const int64_t* pair_triangle, double* out_value, double* out_grad,
+                            int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
+                            sphbi_memory mem) {
+  if (c) c->overflowed = false;
+  sphbi_status st = evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
+                                  pair_particle, pair_triangle, out_value, out_grad, pair_list_out,
+                                  pair_list_capacity, stats, mem);
+  if (c && c->overflowed) {
+    c->overflowed = false;
+    c->force_exact = true;
+    st = evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
+                       pair_particle, pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats,
+                       mem);
+    c->force_exact = false;
+  }
+  return st;
 }
 
 }  // extern "C"

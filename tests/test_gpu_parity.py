@@ -404,3 +404,20 @@ def test_streamed_pinned_host_path_is_bitwise_identical(S, ctx):
                                     vp(ov.data_ptr()), vp(og.data_ptr()), None, None, None, N.MEM_HOST)
         assert rc == 0, N.last_error()
         assert np.array_equal(ov.numpy(), ref_v) and np.array_equal(og.numpy(), ref_g), order
+
+
+def test_work_item_overflow_falls_back_to_exact_buffers(S, ctx, O):
+    """A t3 pair that decomposes into 16 stubs (> the 8-per-pair bounded
+    capacity) forces the sync-free pipeline to overflow; the call must redo
+    itself with exact buffers and still match the oracle."""
+    tri = [-0.53803811928132661, 0.27444965756174206, -0.7970968587426418, 0.08483556470540346,
+           -0.30603716636650558, 0.18140456437346095]
+    n = 1000
+    Q = np.zeros((n, 2))
+    T = np.tile(tri, (n, 1))
+    V = np.tile([0.3, -1.1, 0.7], (n, 1))
+    got = S.integrate_pairs(Q, 1.0, T, V, S.table1_terms(S.wendland4()), ctx=ctx)
+    st, want = OL.oracle_integrate(O, (0.0, 0.0), 1.0, tri, [0.3, -1.1, 0.7], OL.W4, OL.C4)
+    assert st == 0
+    assert OL.parity_ratio(got[:, :3], np.tile(want[:3], (n, 1)), OL.C4, 1.0) <= 1.0
+    assert np.all(got == got[0])
