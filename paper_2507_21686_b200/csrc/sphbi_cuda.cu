@@ -1166,9 +1166,8 @@ static sphbi_status integrate_pairs_impl(sphbi_ctx* c, const sphbi_kernel_desc* 
   const int nout = mode == 0 ? 4 : 12;
   const double *dq = query_xy, *dt = tri_xy, *dv = values;
   double* dout = out;
-  uint32_t* dstat = nullptr;  // per-pair status is reported per call (status bits)
-  unsigned* dflags = nullptr;
-  if ((st = scratch_t(c, kBufFlags, 4, &dflags)) != SPHBI_OK) return st;
+  unsigned* dflags = nullptr;  // [0] status bits, [1] pipeline flags (overflow, ...)
+  if ((st = scratch_t(c, kBufFlags, 8, &dflags)) != SPHBI_OK) return st;
   if (mem == SPHBI_MEM_HOST) {
     double *a, *b, *v, *o;
     if ((st = scratch_t(c, kBufPxy, 2 * n, &a)) != SPHBI_OK) return st;
@@ -1185,15 +1184,8 @@ static sphbi_status integrate_pairs_impl(sphbi_ctx* c, const sphbi_kernel_desc* 
       dv = v;
     }
     dout = o;
-    if (status_out) {
-      if ((st = scratch_t(c, kBufFlags + 0, 4 + n, &dflags)) != SPHBI_OK) return st;
-      dstat = dflags + 4;
-    }
-  } else {
-    dstat = status_out;
   }
-  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, c->stream));
-  (void)dstat;
+  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, c->stream));
   if (status_out && mem == SPHBI_MEM_DEVICE)
     SPHBI_CUDA_TRY(cudaMemsetAsync(status_out, 0, 4 * n, c->stream));
   {
@@ -1279,7 +1271,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
-    if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;  // 8 x u32
     SPHBI_CUDA_TRY(cudaMemsetAsync(sflags, 0, 32, s));
     unsigned long long* sctr = c->counters_on ? c->d_counters : nullptr;
     st = evaluate_streamed(c, K, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
