@@ -446,8 +446,9 @@ __global__ void __launch_bounds__(128)
     k_pipe_sector(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
                   const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
   const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  {
     const PieceItem it = items[k];
     PairAcc a;
     acc_zero(a);
@@ -460,8 +461,9 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     k_pipe_stub(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
                 const StubItem* __restrict__ items, AccOut* __restrict__ out) {
   const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  {
     const StubItem it = items[k];
     PairAcc a;
     acc_zero(a);
@@ -475,8 +477,9 @@ __global__ void __launch_bounds__(128)
     k_pipe_segment(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
                    const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
   const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  {
     const PieceItem it = items[k];
     PairAcc a;
     acc_zero(a);
@@ -808,14 +811,16 @@ struct PipeStats {
 // cfg2: 0.7 / 1.9 / 0.25 items per pair; worst single pairs reach ~16 stubs.
 constexpr unsigned long long kCapSectorPerPair = 4, kCapStubPerPair = 8, kCapSegPerPair = 2;
 
-// K4 pipeline over n pairs. bounded = true: no host synchronisation -- the work
-// item buffers are sized by per-pair capacities, piece kernels read their item
-// count on the device, and an overflow sets dflags[1] bit 4 (caller redoes the
-// call with bounded = false, exact host-sized buffers).
+// K4 pipeline over n pairs. Default (exact): the three item totals are read
+// back once (one host sync) and size the buffers and grids. bounded = true
+// skips that sync (buffers sized by per-pair capacities, piece kernels read
+// their counts on the device; an overflow sets dflags[1] bit 4 and the public
+// entry point redoes the call exactly). Measured on the B200: the sync costs
+// less than the over-sized grids, so the exact mode is the default.
 template <class Src>
 sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
                           int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
-                          bool bounded = true) {
+                          bool bounded = false) {
   if (n <= 0) return SPHBI_OK;
   cudaStream_t s = c->stream;
   sphbi_status st;
@@ -886,15 +891,15 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     return (int)std::max<unsigned long long>(1, std::min<unsigned long long>(need, (unsigned long long)sms * per_sm));
   };
   if (cap[1]) {
-    k_pipe_stub<<<blocks_for(cap[1], 4 * 8), 128, 0, s>>>(K, off + m + n, istub, ostub);
+    k_pipe_stub<<<blocks_for(cap[1], 1 << 20), 128, 0, s>>>(K, off + m + n, istub, ostub);
     if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
   }
   if (cap[0]) {
-    k_pipe_sector<<<blocks_for(cap[0], 8 * 8), 128, 0, s>>>(K, off + n, isec, osec);
+    k_pipe_sector<<<blocks_for(cap[0], 1 << 20), 128, 0, s>>>(K, off + n, isec, osec);
     if ((st = check_launch(c, "k_pipe_sector")) != SPHBI_OK) return st;
   }
   if (cap[2]) {
-    k_pipe_segment<<<blocks_for(cap[2], 8 * 8), 128, 0, s>>>(K, off + 2 * m + n, iseg, oseg);
+    k_pipe_segment<<<blocks_for(cap[2], 1 << 20), 128, 0, s>>>(K, off + 2 * m + n, iseg, oseg);
     if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
   }
   if (mode == 0) {

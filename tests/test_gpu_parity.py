@@ -406,10 +406,10 @@ def test_streamed_pinned_host_path_is_bitwise_identical(S, ctx):
         assert np.array_equal(ov.numpy(), ref_v) and np.array_equal(og.numpy(), ref_g), order
 
 
-def test_work_item_overflow_falls_back_to_exact_buffers(S, ctx, O):
-    """A t3 pair that decomposes into 16 stubs (> the 8-per-pair bounded
-    capacity) forces the sync-free pipeline to overflow; the call must redo
-    itself with exact buffers and still match the oracle."""
+def test_heaviest_decomposition_t3_with_16_stubs(S, ctx, O):
+    """A t3 pair that decomposes into 4 wedges, 4 sectors and 16 stubs (the
+    worst case found by a 2e6-sample search; > any per-pair capacity bound)
+    must match the oracle."""
     tri = [-0.53803811928132661, 0.27444965756174206, -0.7970968587426418, 0.08483556470540346,
            -0.30603716636650558, 0.18140456437346095]
     n = 1000
