@@ -1305,3 +1305,66 @@ int64_t oracle_find_pairs(int64_t p0, int64_t p1, const double* pxy, int64_t ntr
       }
   return n;
 }
+
+/* Grid-accelerated CPU pair finder (same exact predicate as oracle_find_pairs,
+ * same (particle, ascending triangle) order): triangles are binned by their
+ * h-expanded AABB into a uniform grid of cell size h; each particle tests the
+ * triangles of its cell. For the large scenes' CPU parity subsamples. */
+int64_t oracle_find_pairs_grid(int64_t n, const double* pxy, int64_t ntri, const double* tri6, double h,
+                               int64_t* out_pairs, int64_t cap) {
+  if (n <= 0 || ntri <= 0) return 0;
+  double x0 = pxy[0], y0 = pxy[1], x1 = pxy[0], y1 = pxy[1];
+  for (int64_t i = 0; i < n; ++i) {
+    x0 = fmin(x0, pxy[2 * i]); x1 = fmax(x1, pxy[2 * i]);
+    y0 = fmin(y0, pxy[2 * i + 1]); y1 = fmax(y1, pxy[2 * i + 1]);
+  }
+  const double pad = h * (1.0 + 1e-9);
+  x0 -= 2 * pad; y0 -= 2 * pad; x1 += 2 * pad; y1 += 2 * pad;
+  double cell = h;
+  while (((x1 - x0) / cell + 1) * ((y1 - y0) / cell + 1) > 4e7) cell *= 2;
+  const int64_t nx = (int64_t)((x1 - x0) / cell) + 1, ny = (int64_t)((y1 - y0) / cell) + 1;
+  int64_t* cnt = (int64_t*)calloc((size_t)(nx * ny + 1), sizeof(int64_t));
+  #define CELLC(v, o, nn) ({ double f_ = floor(((v) - (o)) / cell); int64_t c_ = f_ < 0 ? 0 : (int64_t)f_; c_ > (nn) - 1 ? (nn) - 1 : c_; })
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t* fillpos = NULL;
+    int64_t* list = NULL;
+    if (pass == 1) {
+      for (int64_t c = 1; c <= nx * ny; ++c) cnt[c] += cnt[c - 1];
+      list = (int64_t*)malloc((size_t)(cnt[nx * ny] + 1) * sizeof(int64_t));
+      fillpos = (int64_t*)malloc((size_t)(nx * ny) * sizeof(int64_t));
+      for (int64_t c = 0; c < nx * ny; ++c) fillpos[c] = cnt[c];
+    }
+    for (int64_t t = 0; t < ntri; ++t) {
+      const double* v = tri6 + 6 * t;
+      const double mnx = fmin(v[0], fmin(v[2], v[4])) - pad, mxx = fmax(v[0], fmax(v[2], v[4])) + pad;
+      const double mny = fmin(v[1], fmin(v[3], v[5])) - pad, mxy = fmax(v[1], fmax(v[3], v[5])) + pad;
+      if (mxx < x0 || mnx > x1 || mxy < y0 || mny > y1) continue;
+      const int64_t cx0 = CELLC(mnx, x0, nx), cx1 = CELLC(mxx, x0, nx);
+      const int64_t cy0 = CELLC(mny, y0, ny), cy1 = CELLC(mxy, y0, ny);
+      for (int64_t cy = cy0; cy <= cy1; ++cy)
+        for (int64_t cx = cx0; cx <= cx1; ++cx) {
+          if (pass == 0) cnt[cy * nx + cx + 1]++;
+          else list[fillpos[cy * nx + cx]++] = t;
+        }
+    }
+    if (pass == 1) {
+      const double h2 = h * h;
+      int64_t m = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t c = CELLC(pxy[2 * i + 1], y0, ny) * nx + CELLC(pxy[2 * i], x0, nx);
+        for (int64_t k = cnt[c]; k < cnt[c + 1]; ++k) {  /* ascending t within a cell */
+          const int64_t t = list[k];
+          if (oracle_pair_dist2(pxy[2 * i], pxy[2 * i + 1], tri6 + 6 * t) < h2) {
+            if (m < cap) { out_pairs[2 * m] = i; out_pairs[2 * m + 1] = t; }
+            ++m;
+          }
+        }
+      }
+      free(list); free(fillpos); free(cnt);
+      return m;
+    }
+  }
+  #undef CELLC
+  free(cnt);
+  return 0;
+}

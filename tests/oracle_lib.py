@@ -40,6 +40,8 @@ def oracle():
     L.oracle_eval_pairs.argtypes = [ctypes.c_int64, P, P, P, P, P, P, ctypes.c_int, D, D, ctypes.c_int, P, P]
     L.oracle_find_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int64, P, D, P, ctypes.c_int64]
     L.oracle_find_pairs.restype = ctypes.c_int64
+    L.oracle_find_pairs_grid.argtypes = [ctypes.c_int64, P, ctypes.c_int64, P, D, P, ctypes.c_int64]
+    L.oracle_find_pairs_grid.restype = ctypes.c_int64
     L.oracle_pair_dist2.argtypes = [D, D, P]
     L.oracle_pair_dist2.restype = D
     L.oracle_segment_integral.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, D, P]
@@ -153,3 +155,11 @@ def random_config(rng):
     q = rng.uniform(-0.4, 0.4, 2)
     h = rng.uniform(0.5, 2.0)
     return t, v, q, h
+
+
+def cpu_pairs_grid(L, P, T, h, cap=20_000_000):
+    """Exact-predicate pair list of particles P against triangles T (grid-accelerated)."""
+    buf = np.zeros((cap, 2), dtype=np.int64)
+    n = L.oracle_find_pairs_grid(P.shape[0], ptr(arr(P)), T.shape[0], ptr(arr(T)), h, ptr(buf), cap)
+    assert n <= cap
+    return buf[:n]

@@ -212,11 +212,7 @@ def test_explicit_pairs_unsorted_and_duplicated(S, ctx):
 
 
 def _cpu_pairs(O, P, T, h):
-    cap = 4_000_000
-    buf = np.zeros((cap, 2), dtype=np.int64)
-    n = O.oracle_find_pairs(0, P.shape[0], OL.ptr(OL.arr(P)), T.shape[0], OL.ptr(OL.arr(T)), h, OL.ptr(buf), cap)
-    assert n <= cap
-    return buf[:n]
+    return OL.cpu_pairs_grid(O, P, T, h)
 
 
 def test_cfg3_cell_list_pairs_bit_exact_and_parity(S, ctx, O):
@@ -421,3 +417,33 @@ def test_heaviest_decomposition_t3_with_16_stubs(S, ctx, O):
     assert st == 0
     assert OL.parity_ratio(got[:, :3], np.tile(want[:3], (n, 1)), OL.C4, 1.0) <= 1.0
     assert np.all(got == got[0])
+
+
+@pytest.mark.slow
+def test_cfg5_full_scene_16M_particles(S, ctx, O):
+    """BASELINE.json configs[4] at full size: 16,000,000 particles, ~2.0M
+    Delaunay obstacle triangles, h = 0.1, device cell list. Wendland C2 and the
+    2-piece cubic spline over the whole scene on the B200; a seeded
+    65,536-particle subsample checked against the CPU oracle (pair lists
+    bit-exact, per-particle sums within the parity tolerance)."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5()
+    idx = np.sort(np.random.default_rng(5).choice(sc.particles.shape[0], 65536, replace=False))
+    P = sc.particles[idx]
+    for name, ks in (("wendland_c2", [sc.kernels[0]]), ("cubic_spline", sc.kernels[1:])):
+        tv = np.zeros(P.shape[0]); tg = np.zeros((P.shape[0], 2)); wv = np.zeros_like(tv); wg = np.zeros_like(tg)
+        for k in ks:
+            h = sc.h * k.support_scale
+            v, g, st = S.evaluate(sc.particles, h, sc.triangles, table_of(S, k), ctx=ctx)
+            assert st.status_bits == 0 and st.n_pairs > 50_000_000
+            sub_pairs = OL.cpu_pairs_grid(O, P, sc.triangles, h)
+            v2, g2, st2, plist = S.evaluate(P, h, sc.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
+            assert np.array_equal(plist, sub_pairs)
+            assert np.array_equal(v2, v[idx]) and np.array_equal(g2, g[idx])  # subset == full-scene rows
+            st_o, vo, go = OL.oracle_scene_sums(O, P, sc.triangles, None, k.coefficients, k.normalization, h,
+                                                sub_pairs[:, 0], sub_pairs[:, 1], threads=16)
+            assert st_o == 0
+            tv += v2; tg += g2; wv += vo; wg += go
+        got = np.concatenate([tv[:, None], tg], axis=1)
+        want = np.concatenate([wv[:, None], wg], axis=1)
+        assert OL.parity_ratio(got, want, ks[0].normalization, sc.h) <= 1.0, name
