@@ -12,6 +12,8 @@
  *   sphbi_integrate_regions <- sphbi::detail::region_* / integrate_stub / _sector /
  *                              _segment / _wedge / _triangle2 / _triangle3 /
  *                              detail::integrate_normalized   triangle_integrator.hpp:335-674, 727-802
+ *   sphbi_integrate_pairs_p3, sphbi_evaluate_p3 <- (none: cubic P3 fields, configs[3];
+ *                              the reference is affine-only, triangle_integrator.hpp:104-118)
  *   sphbi_evaluate          <- SPEC.md:479 "evaluate(query points, h, mesh, field ...)"
  *                              (specified, never shipped) + the SPH-demo neighbour
  *                              search of SPEC.md:711 (uniform grid, AABB prefilter,
@@ -147,6 +149,30 @@ sphbi_status sphbi_evaluate(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, dou
                             const int64_t* pair_particle, const int64_t* pair_triangle,
                             double* out_value, double* out_grad, int64_t* pair_list_out,
                             int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
+
+/* ---- P3 (10-node cubic Lagrange) boundary fields -------------------------
+ * BASELINE.json configs[3]. No reference interface: the reference's term
+ * table is affine-only (triangle_integrator.hpp:104-118, harmonic cap 2), so
+ * these are new entry points in the same style as sphbi_integrate_pairs /
+ * sphbi_evaluate. Nodal values per triangle, 10 doubles in the order
+ *   v0, v1, v2, edge 01 at (2 v0 + v1)/3 and (v0 + 2 v1)/3, edge 12 at
+ *   (2 v1 + v2)/3 and (v1 + 2 v2)/3, edge 20 at (2 v2 + v0)/3 and
+ *   (v2 + 2 v0)/3, centroid
+ * (vertex order as given, NOT canonicalized). With nodal values sampled from
+ * an affine function the results equal sphbi_integrate_pairs mode 0. */
+/* out[4k..4k+3] = (value, grad_x, grad_y, 0) of the cubic field nodal10[10k..] */
+sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
+                                      int64_t n, const double* query_xy, const double* tri_xy,
+                                      const double* nodal10, double* out, uint32_t* status_out,
+                                      sphbi_memory mem);
+/* sphbi_evaluate with a P3 field (nodal10: 10 per triangle); same pairing,
+ * reduction order, outputs and statistics. */
+sphbi_status sphbi_evaluate_p3(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
+                               int64_t n_particles, const double* particle_xy, int64_t n_triangles,
+                               const double* tri_xy, const double* nodal10, int64_t n_pairs,
+                               const int64_t* pair_particle, const int64_t* pair_triangle,
+                               double* out_value, double* out_grad, int64_t* pair_list_out,
+                               int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
 
 /* ---- measurement utility ----------------------------------------------- */
 /* FP64 (DFMA-pipe) peak of the context's GPU at the current clocks: a

@@ -645,9 +645,165 @@ static LC fam_eval(const FamEval* f, Term t) {
   }
 }
 
+/* ---------------------------------------------------------------------------
+ * P3 (10-node cubic Lagrange) fields -- BASELINE.json configs[3]. NOT in the
+ * reference: its term table stops at harmonic 2 (triangle_integrator.hpp:
+ * 104-118), i.e. at affine fields. This extension keeps the reference's OWN
+ * decomposition and elementary integrals (cone/half-disc/segment/stub with
+ * the complex 2F1 machinery above, which accept any harmonic) and replaces
+ * only assemble_region's affine term table: in each region's frame the cubic
+ * field is rebuilt from the rotated vertices' barycentric planes (as
+ * assemble_region rebuilds the hat planes, :255-269), expanded in monomials
+ * x^i y^j, and every monomial moment is written as radial-power x harmonic
+ * integrals (cos^i sin^j expanded by hand below). The device path instead
+ * rotates harmonic sums (sphbi_p3.cuh); the two routes share no code.
+ * The per-region result travels in Basis slot 0 (value[0], grad_x[0],
+ * grad_y[0]) so the reference's signed add_scaled combination is unchanged.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const double* coef;
+  int ncoef;
+  P2 ref[3];           /* normalized vertices, ORIGINAL order */
+  const double* nodes; /* v0 v1 v2, e01 (near v0, near v1), e12, e20, centroid */
+} P3Ctx;
+static __thread const P3Ctx* g_p3;
+
+/* cos^p t sin^q t = sum_a C[a] cos(a t) + S[a] sin(a t), p + q <= 4 */
+static void trig_power(int p, int q, LD* C, LD* S) {
+  for (int a = 0; a < 5; ++a) C[a] = S[a] = 0;
+  switch (p * 10 + q) {
+    case 0: C[0] = 1; break;
+    case 1: S[1] = 1; break;
+    case 10: C[1] = 1; break;
+    case 2: C[0] = 0.5L; C[2] = -0.5L; break;
+    case 11: S[2] = 0.5L; break;
+    case 20: C[0] = 0.5L; C[2] = 0.5L; break;
+    case 3: S[1] = 0.75L; S[3] = -0.25L; break;
+    case 12: C[1] = 0.25L; C[3] = -0.25L; break;
+    case 21: S[1] = 0.25L; S[3] = 0.25L; break;
+    case 30: C[1] = 0.75L; C[3] = 0.25L; break;
+    case 4: C[0] = 0.375L; C[2] = -0.5L; C[4] = 0.125L; break;
+    case 13: S[2] = 0.25L; S[4] = -0.125L; break;
+    case 22: C[0] = 0.125L; C[4] = -0.125L; break;
+    case 31: S[2] = 0.25L; S[4] = 0.125L; break;
+    case 40: C[0] = 0.375L; C[2] = 0.5L; C[4] = 0.125L; break;
+    default: raise_status(ST_LOGIC);
+  }
+}
+
+/* bivariate polynomials of degree <= 3 as dense 4x4 arrays c[i][j] x^i y^j */
+typedef struct {
+  LD c[4][4];
+} BPoly;
+static BPoly bp_affine(LD a, LD b, LD c) {
+  BPoly r;
+  memset(&r, 0, sizeof(r));
+  r.c[0][0] = c;
+  r.c[1][0] = a;
+  r.c[0][1] = b;
+  return r;
+}
+static BPoly bp_mul(BPoly p, BPoly q) {
+  BPoly r;
+  memset(&r, 0, sizeof(r));
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; i + j < 4; ++j)
+      for (int k = 0; i + k < 4; ++k)
+        for (int l = 0; i + j + k + l < 4 && j + l < 4; ++l) r.c[i + k][j + l] += p.c[i][j] * q.c[k][l];
+  return r;
+}
+static void bp_axpy(BPoly* y, LD a, BPoly x) {
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) y->c[i][j] += a * x.c[i][j];
+}
+
+/* integral over the region of r^n {1, cos a t, sin a t} (the reference's Term) */
+static LC p3_moment(const FamEval* fam, int n, int harmonic, int sine) {
+  Term t;
+  t.n = n;
+  t.harmonic = harmonic;
+  t.family = harmonic == 0 ? FAM_P : (sine ? FAM_S : FAM_C);
+  return fam_eval(fam, t);
+}
+/* sum_k w_k int r^(k + shift) cos^p sin^q dr dt, w_k = b_k (value) or -k b_k */
+static LC p3_trig_moment(const FamEval* fam, const P3Ctx* P, int grad, int shift, int p, int q) {
+  LD C[5], S[5];
+  trig_power(p, q, C, S);
+  LC sum = cx(0, 0);
+  for (int k = 0; k < P->ncoef; ++k) {
+    const LD w = grad ? (LD)(-(double)k * P->coef[k]) : (LD)P->coef[k];
+    if (w == 0) continue;
+    for (int a = 0; a < 5; ++a) {
+      if (C[a] != 0) sum = cx_add(sum, cx_scale(p3_moment(fam, k + shift, a, 0), w * C[a]));
+      if (S[a] != 0) sum = cx_add(sum, cx_scale(p3_moment(fam, k + shift, a, 1), w * S[a]));
+    }
+  }
+  return sum;
+}
+
+static Basis p3_assemble(Mat2 frame, const FamEval* fam) {
+  const P3Ctx* P = g_p3;
+  LD tvx[3], tvy[3];
+  for (int i = 0; i < 3; ++i) {
+    tvx[i] = (LD)frame.m[0][0] * P->ref[i].x + (LD)frame.m[0][1] * P->ref[i].y;
+    tvy[i] = (LD)frame.m[1][0] * P->ref[i].x + (LD)frame.m[1][1] * P->ref[i].y;
+  }
+  const LD den = (tvy[1] - tvy[2]) * (tvx[0] - tvx[2]) + (tvx[2] - tvx[1]) * (tvy[0] - tvy[2]);
+  if (fabs((double)den) < 2.0 * kGeomEps) raise_status(ST_DOMAIN);
+  BPoly lam[3];
+  {
+    LD t1[3], t2[3];
+    t1[0] = (tvy[1] - tvy[2]) / den;
+    t2[0] = (tvx[2] - tvx[1]) / den;
+    t1[1] = (tvy[2] - tvy[0]) / den;
+    t2[1] = (tvx[0] - tvx[2]) / den;
+    t1[2] = -t1[0] - t1[1];
+    t2[2] = -t2[0] - t2[1];
+    for (int i = 0; i < 3; ++i)
+      lam[i] = bp_affine(t1[i], t2[i], (i == 2 ? 1.0L : 0.0L) - t1[i] * tvx[2] - t2[i] * tvy[2]);
+  }
+  BPoly three_m1[3], three_m2[3];
+  for (int i = 0; i < 3; ++i) {
+    three_m1[i] = lam[i];
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) three_m1[i].c[a][b] *= 3;
+    three_m2[i] = three_m1[i];
+    three_m1[i].c[0][0] -= 1;
+    three_m2[i].c[0][0] -= 2;
+  }
+  BPoly A;
+  memset(&A, 0, sizeof(A));
+  for (int i = 0; i < 3; ++i) bp_axpy(&A, 0.5L * P->nodes[i], bp_mul(bp_mul(lam[i], three_m1[i]), three_m2[i]));
+  static const int ea[3] = {0, 1, 2}, eb[3] = {1, 2, 0};
+  for (int e = 0; e < 3; ++e) {
+    const BPoly ll = bp_mul(lam[ea[e]], lam[eb[e]]);
+    bp_axpy(&A, 4.5L * P->nodes[3 + 2 * e], bp_mul(ll, three_m1[ea[e]]));
+    bp_axpy(&A, 4.5L * P->nodes[4 + 2 * e], bp_mul(ll, three_m1[eb[e]]));
+  }
+  bp_axpy(&A, 27.0L * P->nodes[9], bp_mul(bp_mul(lam[0], lam[1]), lam[2]));
+  LC v = cx(0, 0), gxp = cx(0, 0), gyp = cx(0, 0);
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; i + j < 4; ++j) {
+      const LD al = A.c[i][j];
+      if (al == 0) continue;
+      const int e = i + j;
+      v = cx_add(v, cx_scale(p3_trig_moment(fam, P, 0, e + 1, i, j), al));
+      gxp = cx_add(gxp, cx_scale(p3_trig_moment(fam, P, 1, e, i + 1, j), al));
+      gyp = cx_add(gyp, cx_scale(p3_trig_moment(fam, P, 1, e, i, j + 1), al));
+    }
+  const LC gx = cx_add(cx_scale(gxp, (LD)frame.m[0][0]), cx_scale(gyp, (LD)frame.m[1][0]));
+  const LC gy = cx_add(cx_scale(gxp, (LD)frame.m[0][1]), cx_scale(gyp, (LD)frame.m[1][1]));
+  Basis out = zero_basis();
+  out.value[0] = CMPLX((double)re_(v), (double)im_(v));
+  out.grad_x[0] = CMPLX((double)re_(gx), (double)im_(gx));
+  out.grad_y[0] = CMPLX((double)re_(gy), (double)im_(gy));
+  return out;
+}
+
 /* :244-319 */
 static Basis assemble_region(const Table* table, Mat2 frame, const P2* ref, const FamEval* fam) {
   ++g_assemblies;
+  if (g_p3) return p3_assemble(frame, fam);
   LD tvx[3], tvy[3];
   for (int i = 0; i < 3; ++i) {
     tvx[i] = (LD)frame.m[0][0] * ref[i].x + (LD)frame.m[0][1] * ref[i].y;
@@ -1149,6 +1305,39 @@ int oracle_integrate_bases(double qx, double qy, double h, const double* tri6, c
   return integrate_triangle_bases(qx, qy, h, tri6, &t, out12);
 }
 
+/* One pair with a P3 field (configs[3]); same decomposition as
+ * integrate_triangle (:808-822), field per region via p3_assemble. out4 =
+ * value, grad x, grad y, max |imag| (as finalize, :696-704). */
+int oracle_integrate_triangle_p3(double qx, double qy, double h, const double* tri6, const double* nodes10,
+                                 const double* coef, int ncoef, double c2, double* out4) {
+  g_status = ST_OK;
+  Table t;
+  const int s = table1_terms(coef, ncoef, c2, &t);
+  if (s) return s;
+  if (!(h > 0.0)) return ST_DOMAIN;
+  P3Ctx ctx;
+  ctx.coef = coef;
+  ctx.ncoef = ncoef;
+  ctx.nodes = nodes10;
+  for (int i = 0; i < 3; ++i) {
+    ctx.ref[i].x = (tri6[2 * i] - qx) / h;
+    ctx.ref[i].y = (tri6[2 * i + 1] - qy) / h;
+  }
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize_triangle(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) {
+    nv[i].x = (v[i].x - qx) / h;
+    nv[i].y = (v[i].y - qy) / h;
+  }
+  g_p3 = &ctx;
+  const Basis b = integrate_normalized(nv, &t);
+  g_p3 = NULL;
+  finalize(b.value[0], b.grad_x[0], b.grad_y[0], c2, h, out4);
+  return g_status;
+}
+
 /* Region-level raw basis triples (the detail::region_* surface): kind as in
  * sphbi_cuda.h sphbi_region_kind; out9 = (value_i, gx_i, gy_i) real parts. */
 int oracle_integrate_region(int kind, const double* a, const double* ref6, const double* coef, int ncoef,
@@ -1276,6 +1465,58 @@ int oracle_eval_pairs(int64_t npairs, const int64_t* pp, const int64_t* pt, cons
   job_run(&jobs[0]);
   for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
   s = ST_OK;
+  if (fail_index) *fail_index = -1;
+  for (int t = 0; t < nthreads; ++t)
+    if (jobs[t].status != ST_OK && s == ST_OK) {
+      s = jobs[t].status;
+      if (fail_index) *fail_index = jobs[t].fail_index;
+    }
+  free(jobs);
+  free(th);
+  return s;
+}
+
+/* oracle_integrate_triangle_p3 for each pair k (P3 fields, configs[3]):
+ * particle pp[k] vs triangle pt[k], nodal values nodes10[10 t ..]. */
+typedef struct {
+  int64_t npairs;
+  int stride, tid;
+  const int64_t *pp, *pt;
+  const double *pxy, *tri6, *nodes10, *coef;
+  int ncoef;
+  double c2, h;
+  double* out4;
+  int status;
+  int64_t fail_index;
+} JobP3;
+static void* job_run_p3(void* arg) {
+  JobP3* j = (JobP3*)arg;
+  for (int64_t k = j->tid; k < j->npairs; k += j->stride) {
+    const int64_t i = j->pp ? j->pp[k] : k;
+    const int64_t t = j->pt ? j->pt[k] : k;
+    const int s = oracle_integrate_triangle_p3(j->pxy[2 * i], j->pxy[2 * i + 1], j->h, j->tri6 + 6 * t,
+                                               j->nodes10 + 10 * t, j->coef, j->ncoef, j->c2, j->out4 + 4 * k);
+    if (s != ST_OK && j->status == ST_OK) {
+      j->status = s;
+      j->fail_index = k;
+    }
+  }
+  return NULL;
+}
+int oracle_eval_pairs_p3(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy, const double* tri6,
+                         const double* nodes10, const double* coef, int ncoef, double c2, double h, int nthreads,
+                         double* out4, int64_t* fail_index) {
+  if (nthreads < 1) nthreads = 1;
+  JobP3* jobs = (JobP3*)calloc((size_t)nthreads, sizeof(JobP3));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int t = 0; t < nthreads; ++t) {
+    JobP3 j = {npairs, nthreads, t, pp, pt, pxy, tri6, nodes10, coef, ncoef, c2, h, out4, ST_OK, -1};
+    jobs[t] = j;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, job_run_p3, &jobs[t]);
+  job_run_p3(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  int s = ST_OK;
   if (fail_index) *fail_index = -1;
   for (int t = 0; t < nthreads; ++t)
     if (jobs[t].status != ST_OK && s == ST_OK) {

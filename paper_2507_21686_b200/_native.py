@@ -71,6 +71,8 @@ EXPORTED_SYMBOLS = (
     "sphbi_integrate_pairs",
     "sphbi_integrate_regions",
     "sphbi_evaluate",
+    "sphbi_integrate_pairs_p3",
+    "sphbi_evaluate_p3",
     "sphbi_measure_fp64_peak",
 )
 
@@ -104,6 +106,9 @@ def load() -> ctypes.CDLL:
     lib.sphbi_evaluate.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64, P,
                                    ctypes.c_int64, P, P, ctypes.c_int64, P, P, P, P, P,
                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats), ctypes.c_int]
+    lib.sphbi_integrate_pairs_p3.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64,
+                                             P, P, P, P, P, ctypes.c_int]
+    lib.sphbi_evaluate_p3.argtypes = lib.sphbi_evaluate.argtypes
     lib.sphbi_measure_fp64_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib

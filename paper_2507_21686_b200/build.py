@@ -68,7 +68,7 @@ def build_checkers(force: bool = False) -> None:
         raise RuntimeError(f"oracle build failed:\n{r.stdout[-2000:]}\n{r.stderr[-4000:]}")
     native = ROOT / "tests" / "native"
     out = native / "_build" / "libcore_host.so"
-    deps = [native / "core_host_capi.cpp", CSRC / "sphbi_core.cuh", CSRC / "sphbi_math.cuh"]
+    deps = [native / "core_host_capi.cpp", CSRC / "sphbi_core.cuh", CSRC / "sphbi_math.cuh", CSRC / "sphbi_p3.cuh"]
     if force or _stale(out, deps):
         out.parent.mkdir(parents=True, exist_ok=True)
         cmd = ["g++", "-O2", "-mfma", "-ffp-contract=off", "-std=gnu++17", "-fPIC", "-shared", "-pthread",

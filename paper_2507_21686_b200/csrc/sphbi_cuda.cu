@@ -21,11 +21,13 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/sphbi_cuda.h"
 #include "sphbi_core.cuh"
+#include "sphbi_p3.cuh"
 
 using namespace sphbi_dev;
 
@@ -211,6 +213,53 @@ __global__ void __launch_bounds__(kEvalBlock)
   for (int j = 0; j < 6; ++j) r[j] = ref[6 * k + j];
   status[k] = eval_region(K, kind[k], a, r, o, counters);
   for (int j = 0; j < 9; ++j) out[9 * k + j] = o[j];
+}
+
+// ---------------------------------------------------------------------------
+// K4 for P3 (10-node cubic Lagrange) fields, BASELINE configs[3]
+// ---------------------------------------------------------------------------
+// Thread per pair, everything inlined through the shared decomposition with a
+// P3Sink (sphbi_p3.cuh). cfg4 has ~2.4e5 pairs per 4M particles, so the
+// affine path's divergence-aware work-item pipeline is not needed here.
+struct P3SceneSrc {
+  const int* pp;
+  const int* pt;
+  const double* pxy;
+  const double* tri;
+  const double* nodes;  // 10 per triangle
+  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* n10) const {
+    const int i = pp[k], t = pt[k];
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    qx = p.x;
+    qy = p.y;
+    for (int j = 0; j < 6; ++j) t6[j] = __ldg(tri + 6 * (int64_t)t + j);
+    for (int j = 0; j < 10; ++j) n10[j] = __ldg(nodes + 10 * (int64_t)t + j);
+  }
+};
+struct P3DirectSrc {
+  const double* q;
+  const double* tri;
+  const double* nodes;
+  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* n10) const {
+    qx = q[2 * k];
+    qy = q[2 * k + 1];
+    for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
+    for (int j = 0; j < 10; ++j) n10[j] = nodes[10 * k + j];
+  }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(128)
+    k_p3_pairs(const __grid_constant__ KernelConsts K, const __grid_constant__ P3Consts P, Src src, int64_t n,
+               double h, int stride, double* __restrict__ out, unsigned* __restrict__ status_or,
+               unsigned long long* counters) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6], n10[10], o[4];
+  src.load(k, qx, qy, t6, n10);
+  const unsigned st = eval_pair_p3(K, P, qx, qy, h, t6, n10, o, counters);
+  if (st) atomicOr(status_or, st);
+  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -1250,12 +1299,13 @@ sphbi_status sphbi_integrate_regions(sphbi_ctx* c, const sphbi_kernel_desc* kern
   return SPHBI_OK;
 }
 
+// nodal10 != NULL selects the P3 field (10 nodal values per triangle; tri_values ignored).
 static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
                             const double* particle_xy, int64_t n_triangles, const double* tri_xy,
                             const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
                             int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
-                            sphbi_memory mem) {
+                            sphbi_memory mem, const double* nodal10 = nullptr) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
@@ -1264,6 +1314,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   KernelConsts K;
   sphbi_status st = make_consts(kernel, &K);
   if (st != SPHBI_OK) return st;
+  std::unique_ptr<P3Consts> p3;
+  if (nodal10) {
+    p3.reset(new P3Consts);
+    build_p3_consts(kernel->coefficients, kernel->n_coefficients, p3.get());
+    tri_values = nullptr;
+  }
   cudaSetDevice(c->device);
   cudaStream_t s = c->stream;
   const bool timing = stats != nullptr;
@@ -1272,7 +1328,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     cudaEventRecord(c->ev[0], s);
   }
   // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
-  if (mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
+  if (!p3 && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
@@ -1305,7 +1361,25 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if (n_triangles) SPHBI_CUDA_TRY(cudaMemcpyAsync(v, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, s));
       dv = v;
     }
+    if (nodal10) {
+      if ((st = scratch_t(c, kBufVals, 10 * n_triangles, &v)) != SPHBI_OK) return st;
+      if (n_triangles) SPHBI_CUDA_TRY(cudaMemcpyAsync(v, nodal10, 80 * n_triangles, cudaMemcpyHostToDevice, s));
+      dv = v;
+    }
+  } else if (nodal10) {
+    dv = nodal10;
   }
+  // one chunk of particle-sorted scene pairs -> 3 doubles per pair
+  auto eval_chunk = [&](const int* cpp, const int* cpt, int64_t cnt, double* pout, unsigned* dflags,
+                        unsigned long long* ctr) -> sphbi_status {
+    if (p3) {
+      const P3SceneSrc src{cpp, cpt, dp, dt, dv};
+      k_p3_pairs<<<grid_for(cnt, 128), 128, 0, s>>>(K, *p3, src, cnt, h, 3, pout, dflags, ctr);
+      return check_launch(c, "k_p3_pairs");
+    }
+    const SceneSrc src{cpp, cpt, dp, dt, dv};
+    return run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr);
+  };
   if (mem == SPHBI_MEM_HOST || !out_value || !out_grad) {
     double *a, *b;
     if ((st = scratch_t(c, kBufOutV, n_particles, &a)) != SPHBI_OK) return st;
@@ -1372,10 +1446,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     while (done < n_pairs) {
       const int64_t cnt = std::min<int64_t>(n_pairs - done, kMaxChunkPairs);
       if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
-      {
-        const SceneSrc src{pp + done, pt + done, dp, dt, dv};
-        if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
-      }
+      if ((st = eval_chunk(pp + done, pt + done, cnt, pout, dflags, ctr)) != SPHBI_OK) return st;
       if (timing && done + cnt >= n_pairs) cudaEventRecord(c->ev[2], s);
       // rows: all particles, accumulate (a particle may straddle chunks)
       const int pc = static_cast<int>(n_particles);
@@ -1532,10 +1603,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           written += cnt;
         }
         if (timing && p0 == 0) cudaEventRecord(c->ev[1], s);
-        {
-          const SceneSrc src{pp, pt, dp, dt, dv};
-          if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
-        }
+        if ((st = eval_chunk(pp, pt, cnt, pout, dflags, ctr)) != SPHBI_OK) return st;
         if (timing && p1 >= np) cudaEventRecord(c->ev[2], s);
         if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
         k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp, p0, p1 - p0, row_ptr);
@@ -1615,6 +1683,67 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
     c->force_exact = false;
   }
   return st;
+}
+
+// P3 (10-node cubic Lagrange) fields -- BASELINE configs[3]; no reference
+// interface (the reference's term table is affine-only, triangle_integrator.hpp:104-118).
+sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                      const double* query_xy, const double* tri_xy, const double* nodal10,
+                                      double* out, uint32_t* status_out, sphbi_memory mem) {
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
+  if (n < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "n < 0");
+  KernelConsts K;
+  sphbi_status st = make_consts(kernel, &K);
+  if (st != SPHBI_OK) return st;
+  if (n == 0) return SPHBI_OK;
+  if (!query_xy || !tri_xy || !nodal10 || !out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL input/output array");
+  std::unique_ptr<P3Consts> P(new P3Consts);
+  build_p3_consts(kernel->coefficients, kernel->n_coefficients, P.get());
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  const double *dq = query_xy, *dt = tri_xy, *dn = nodal10;
+  double* dout = out;
+  unsigned* dflags = nullptr;
+  if ((st = scratch_t(c, kBufFlags, 8, &dflags)) != SPHBI_OK) return st;
+  if (mem == SPHBI_MEM_HOST) {
+    double *a, *b, *v, *o;
+    if ((st = scratch_t(c, kBufPxy, 2 * n, &a)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufTri, 6 * n, &b)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufVals, 10 * n, &v)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufPairOut, 4 * n, &o)) != SPHBI_OK) return st;
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(a, query_xy, 16 * n, cudaMemcpyHostToDevice, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n, cudaMemcpyHostToDevice, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(v, nodal10, 80 * n, cudaMemcpyHostToDevice, s));
+    dq = a;
+    dt = b;
+    dn = v;
+    dout = o;
+  }
+  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, s));
+  const P3DirectSrc src{dq, dt, dn};
+  k_p3_pairs<<<grid_for(n, 128), 128, 0, s>>>(K, *P, src, n, h, 4, dout, dflags,
+                                              c->counters_on ? c->d_counters : nullptr);
+  if ((st = check_launch(c, "k_p3_pairs")) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
+  if (mem == SPHBI_MEM_HOST) SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (status_out && mem == SPHBI_MEM_HOST) std::memset(status_out, 0, 4 * n);
+  if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "integrate_triangle_p3: reference-domain error on device");
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_evaluate_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
+                               const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                               const double* nodal10, int64_t n_pairs, const int64_t* pair_particle,
+                               const int64_t* pair_triangle, double* out_value, double* out_grad,
+                               int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
+                               sphbi_memory mem) {
+  if (!nodal10 && n_triangles > 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "nodal10 is NULL");
+  static const double kNoNodes = 0.0;
+  return evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs, pair_particle,
+                       pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats, mem,
+                       nodal10 ? nodal10 : &kNoNodes);
 }
 
 }  // extern "C"

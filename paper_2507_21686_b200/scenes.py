@@ -4,7 +4,8 @@ There is no public dataset for this path; every scene is generated from
 numpy's PCG64 with seed 2507216860 + k (config k), with the shapes, sizes and
 value distributions BASELINE.json names. Scenes are plain numpy arrays:
   particles (n, 2) float64, triangles (T, 6) float64 (x0,y0,x1,y1,x2,y2),
-  values (T, 3) float64 or None (field == 1), plus the kernel(s) and h.
+  values (T, 3) float64 (affine field), (T, 10) float64 (P3 field, cfg4) or
+  None (field == 1), plus the kernel(s) and h.
 """
 from __future__ import annotations
 
@@ -189,6 +190,76 @@ def cfg3(target_particles: int = 1_000_000) -> Scene:
     keep = r < radius(th)
     P = np.ascontiguousarray(P[keep])
     return Scene("cfg3", P, tris, None, [wendland_c6()], h, info={"r0": r0, "particles": int(P.shape[0])})
+
+
+def p3_node_points(tri: np.ndarray) -> np.ndarray:
+    """(T, 10, 2) P3 node positions in the node order of the P3 C-ABI
+    (include/sphbi_cuda.h): v0, v1, v2, edge 01 at 1/3 and 2/3 from v0, edge 12
+    from v1, edge 20 from v2, centroid."""
+    v = tri.reshape(-1, 3, 2)
+    out = np.empty((v.shape[0], 10, 2))
+    out[:, 0:3] = v
+    for e, (i, j) in enumerate(((0, 1), (1, 2), (2, 0))):
+        out[:, 3 + 2 * e] = (2.0 * v[:, i] + v[:, j]) / 3.0
+        out[:, 4 + 2 * e] = (v[:, i] + 2.0 * v[:, j]) / 3.0
+    out[:, 9] = v.mean(axis=1)
+    return out
+
+
+def p3_conforming_values(tri_vid: np.ndarray, n_vertices: int, rng: np.random.Generator) -> np.ndarray:
+    """Conforming P3 nodal values ~ N(0,1): one value per mesh vertex, two per
+    mesh edge (shared by both incident triangles, oriented), one per centroid.
+    tri_vid: (T, 3) vertex ids. Returns (T, 10)."""
+    T = tri_vid.shape[0]
+    vval = rng.standard_normal(n_vertices)
+    edges = {}
+    out = np.empty((T, 10))
+    out[:, 0:3] = vval[tri_vid]
+    for t in range(T):
+        for e, (i, j) in enumerate(((0, 1), (1, 2), (2, 0))):
+            a, b = int(tri_vid[t, i]), int(tri_vid[t, j])
+            key = (min(a, b), max(a, b))
+            if key not in edges:
+                edges[key] = rng.standard_normal(2)  # [near min id, near max id]
+            near_a = edges[key][0] if a < b else edges[key][1]
+            near_b = edges[key][1] if a < b else edges[key][0]
+            out[t, 3 + 2 * e] = near_a
+            out[t, 4 + 2 * e] = near_b
+    out[:, 9] = rng.standard_normal(T)
+    return out
+
+
+def cfg4(spacing_div: int = 4, max_particles: Optional[int] = None) -> Scene:
+    """cfg3's boundary mesh (same seed, 8,192 triangles) with a conforming P3
+    (10-node cubic Lagrange) field, nodal values N(0,1); generic degree-12
+    kernel c_k ~ N(0,1), normalised; h = 0.01; ~4M particles on cfg3's jittered
+    lattice at spacing h/4."""
+    rng = np.random.default_rng(SEED_BASE + 3)
+    h = 0.01
+    r0 = math.sqrt(1_000_000 * (h / 2) ** 2 / math.pi)
+    tris, radius, _, _ = star_mesh(rng, 4096, h, r0)
+    nv = 4096
+    j = np.arange(nv)
+    j1 = (j + 1) % nv
+    vid = np.empty((2 * nv, 3), dtype=np.int64)
+    vid[0::2] = np.stack([j, j1, nv + j1], axis=1)
+    vid[1::2] = np.stack([j, nv + j1, nv + j], axis=1)
+    rng4 = np.random.default_rng(SEED_BASE + 4)
+    kern = generic_deg12(rng4)
+    values = p3_conforming_values(vid, 2 * nv, rng4)
+    sp = h / spacing_div
+    rmax = r0 * 1.3
+    g = np.arange(-rmax, rmax + sp, sp)
+    X, Y = np.meshgrid(g, g)
+    P = np.stack([X.ravel(), Y.ravel()], axis=1)
+    P = P + rng4.uniform(-0.1 * sp, 0.1 * sp, P.shape)
+    r = np.hypot(P[:, 0], P[:, 1])
+    th = np.arctan2(P[:, 1], P[:, 0])
+    P = np.ascontiguousarray(P[r < radius(th)])
+    if max_particles is not None and P.shape[0] > max_particles:
+        P = np.ascontiguousarray(P[np.sort(rng4.choice(P.shape[0], max_particles, replace=False))])
+    return Scene("cfg4", P, tris, values, [kern], h, info={"r0": r0, "particles": int(P.shape[0]),
+                                                          "field": "p3", "vertex_ids": vid})
 
 
 def cfg5(n_particles: int = 16_000_000, n_discs: int = 500, target_tris: int = 2_000_000,

@@ -385,6 +385,28 @@ def integrate_triangle(query: Point2, h: float, tri: Triangle, values=None, tabl
     return IntegralResult(float(r[0]), (float(r[1]), float(r[2])), float(r[3]))
 
 
+def integrate_pairs_p3(query_xy, h: float, tri_xy, nodal10, table, ctx: Context | None = None):
+    """Batched pair integrals with a P3 (10-node cubic Lagrange) field; returns (n,4):
+    value, grad_x, grad_y, 0. Node order: include/sphbi_cuda.h (sphbi_integrate_pairs_p3)."""
+    ctx = ctx or default_context()
+    table = _as_table(table)
+    q = np.ascontiguousarray(query_xy, dtype=np.float64).reshape(-1, 2)
+    t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
+    v = np.ascontiguousarray(nodal10, dtype=np.float64)
+    n = q.shape[0]
+    if v.size != 10 * n:
+        raise InvalidArgument("nodal10 must hold 10 values per pair")
+    v = v.reshape(n, 10)
+    if t.shape[0] != n or v.shape[0] != n:
+        raise InvalidArgument("query / triangle / nodal value count mismatch")
+    out = np.zeros((n, 4), dtype=np.float64)
+    st = np.zeros(n, dtype=np.uint32)
+    desc = table.desc()
+    _raise(ctx.lib.sphbi_integrate_pairs_p3(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(q), _ptr(t),
+                                            _ptr(v), _ptr(out), _ptr(st), N.MEM_HOST), "integrate_triangle_p3")
+    return out
+
+
 def integrate_triangle_bases(query: Point2, h: float, tri: Triangle, table) -> list:
     """triangle_integrator.hpp:828-846."""
     if not (h > 0.0):
@@ -519,7 +541,8 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
              return_pairs: bool = False):
     """Per-particle sums of integrate_triangle over all triangles within h.
 
-    particles_xy (n,2); tri_xy (T,6); tri_values (T,3) or None (field == 1);
+    particles_xy (n,2); tri_xy (T,6); tri_values (T,3) barycentric, (T,10) P3
+    nodal values (cubic field, include/sphbi_cuda.h node order) or None (field == 1);
     pairs: None -> device cell list, or (pair_particle, pair_triangle) int64 arrays.
     Returns value (n,), grad (n,2), EvalStats [, pair list (m,2) int64].
     """
@@ -529,8 +552,15 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
         raise DomainError("integrate_triangle: support h must be > 0")
     p = np.ascontiguousarray(particles_xy, dtype=np.float64).reshape(-1, 2)
     t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
-    v = None if tri_values is None else np.ascontiguousarray(tri_values, dtype=np.float64).reshape(-1, 3)
     n, T = p.shape[0], t.shape[0]
+    fn = ctx.lib.sphbi_evaluate
+    v = None
+    if tri_values is not None:
+        v = np.ascontiguousarray(tri_values, dtype=np.float64)
+        if v.ndim == 2 and v.shape[1] == 10:  # P3 nodal values (configs[3])
+            fn = ctx.lib.sphbi_evaluate_p3
+        else:
+            v = v.reshape(-1, 3)
     out_v = np.zeros(n, dtype=np.float64)
     out_g = np.zeros((n, 2), dtype=np.float64)
     stats = N.Stats()
@@ -540,11 +570,11 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
         plist = None
         if return_pairs:
             # first pass sizes the list
-            _raise(ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t),
+            _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t),
                                           _ptr(v), -1, None, None, _ptr(out_v), _ptr(out_g), None,
                                           ctypes.byref(cap), ctypes.byref(stats), N.MEM_HOST), "evaluate")
             plist = np.zeros((max(cap.value, 1), 2), dtype=np.int64)
-        _raise(ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t),
+        _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t),
                                       _ptr(v), -1, None, None, _ptr(out_v), _ptr(out_g),
                                       _ptr(plist) if plist is not None else None, ctypes.byref(cap),
                                       ctypes.byref(stats), N.MEM_HOST), "evaluate")
@@ -554,7 +584,7 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
         return out_v, out_g, es
     ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
     it = np.ascontiguousarray(pairs[1], dtype=np.int64)
-    _raise(ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t), _ptr(v),
+    _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t), _ptr(v),
                                   ip.shape[0], _ptr(ip), _ptr(it), _ptr(out_v), _ptr(out_g), None, None,
                                   ctypes.byref(stats), N.MEM_HOST), "evaluate")
     return out_v, out_g, EvalStats(stats.n_pairs, stats.status_bits, stats.ms_pairs, stats.ms_eval, stats.ms_reduce)

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../paper_2507_21686_b200/csrc/sphbi_core.cuh"
+#include "../../paper_2507_21686_b200/csrc/sphbi_p3.cuh"
 
 using namespace sphbi_dev;
 
@@ -40,6 +41,78 @@ int core_host_eval_pairs(int64_t npairs, const int64_t* pp, const int64_t* pt, c
   work(0);
   for (auto& th : pool) th.join();
   return 0;
+}
+
+int core_host_eval_pair_p3(const double* coef, int ncoef, double c2, double qx, double qy, double h,
+                           const double* tri6, const double* nodes10, double* out4) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
+  static thread_local P3Consts P;
+  build_p3_consts(coef, ncoef, &P);
+  return (int)eval_pair_p3(K, P, qx, qy, h, tri6, nodes10, out4, nullptr);
+}
+
+// raw 24 harmonic sums of one elementary region (kind 0 cone(gamma, L), 1 segment(d),
+// 2 stub bound pair [lo, u] at (D, beta) without the cone part, 3 half disc)
+int core_host_h24(const double* coef, int ncoef, int kind, const double* a, double* out24) {
+  static thread_local P3Consts P;
+  build_p3_consts(coef, ncoef, &P);
+  H24 H;
+  h24_zero(H);
+  if (kind == 0) h24_cone(P, a[0], a[1], H);
+  else if (kind == 1) h24_segment(P, a[0], H);
+  else if (kind == 2) {
+    h24_stub_bound(P, a[3], a[0], a[1], 1.0, H);
+    h24_stub_bound(P, a[2], a[0], a[1], -1.0, H);
+  } else h24_half_disc(P, H);
+  for (int i = 0; i < kP3Sums; ++i) out24[i] = H.c[i].hi + H.c[i].lo;
+  return 0;
+}
+
+// piece log of one P3 pair: per piece 8 params (type, sign, f00, f01, f10, f11, p0..p6 ...) + 24 sums
+struct LogSink {
+  const P3Consts* P;
+  unsigned status;
+  unsigned long long* counters;
+  double* rec;
+  int n, cap;
+  SPHBI_HD void bump(int) {}
+  void put(int type, const Frame& f, double sign, const double* prm, int np, const H24& H) {
+    if (n >= cap) return;
+    double* r = rec + n * 40;
+    r[0] = type; r[1] = sign; r[2] = f.m00; r[3] = f.m01; r[4] = f.m10; r[5] = f.m11;
+    for (int i = 0; i < 10; ++i) r[6 + i] = i < np ? prm[i] : 0.0;
+    for (int i = 0; i < 24; ++i) r[16 + i] = H.c[i].hi + H.c[i].lo;
+    ++n;
+  }
+  void disc(double sign) { H24 H; h24_disc(*P, H); put(0, Frame{1, 0, 0, 1}, sign, nullptr, 0, H); }
+  void half_disc(const Frame& f, double sign) { H24 H; h24_half_disc(*P, H); put(1, f, sign, nullptr, 0, H); }
+  void sector(const Frame& f, double gamma, double L, double sign) {
+    H24 H; h24_cone(*P, gamma, L, H); const double prm[2] = {gamma, L}; put(2, f, sign, prm, 2, H);
+  }
+  void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u, bool window,
+            double sign) {
+    H24 H; h24_cone(*P, gamma, l, H);
+    if (window) { h24_stub_bound(*P, u, D, beta, 1.0, H); h24_stub_bound(*P, lo, D, beta, -1.0, H); }
+    const double prm[7] = {gamma, l, D, beta, lo, u, window ? 1.0 : 0.0};
+    put(3, f, sign, prm, 7, H);
+  }
+  void segment(const Frame& f, double d, double sign) {
+    H24 H; h24_segment(*P, d, H); const double prm[1] = {d}; put(4, f, sign, prm, 1, H);
+  }
+};
+int core_host_p3_pieces(const double* coef, int ncoef, double qx, double qy, double h, const double* tri6,
+                        double* rec, int cap) {
+  static thread_local P3Consts P;
+  build_p3_consts(coef, ncoef, &P);
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  LogSink s{&P, 0u, nullptr, rec, 0, cap};
+  integrate_normalized(s, nv);
+  return s.n;
 }
 
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }

@@ -38,6 +38,8 @@ def oracle():
     L.oracle_integrate_bases.argtypes = [D, D, D, P, P, ctypes.c_int, D, P]
     L.oracle_integrate_region.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, D, P]
     L.oracle_eval_pairs.argtypes = [ctypes.c_int64, P, P, P, P, P, P, ctypes.c_int, D, D, ctypes.c_int, P, P]
+    L.oracle_eval_pairs_p3.argtypes = L.oracle_eval_pairs.argtypes
+    L.oracle_integrate_triangle_p3.argtypes = [D, D, D, P, P, P, ctypes.c_int, D, P]
     L.oracle_find_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int64, P, D, P, ctypes.c_int64]
     L.oracle_find_pairs.restype = ctypes.c_int64
     L.oracle_find_pairs_grid.argtypes = [ctypes.c_int64, P, ctypes.c_int64, P, D, P, ctypes.c_int64]
@@ -77,6 +79,7 @@ def core():
     L = ctypes.CDLL(str(p))
     L.core_host_eval_pair.argtypes = [P, ctypes.c_int, D, D, D, D, P, P, ctypes.c_int, P, P, P]
     L.core_host_eval_pairs.argtypes = [ctypes.c_int64, P, P, P, P, P, P, ctypes.c_int, D, D, ctypes.c_int, P, P]
+    L.core_host_eval_pair_p3.argtypes = [P, ctypes.c_int, D, D, D, D, P, P, P]
     L.core_host_glibc_hypot.argtypes = [D, D]
     L.core_host_glibc_hypot.restype = D
     return L
@@ -106,13 +109,16 @@ def ref_integrate(L, q, h, tri, vals, coef, c2):
 
 
 def oracle_pairs(L, pp, pt, pxy, tri, vals, coef, c2, h, threads=8):
-    """integrate_triangle per pair (out (m,4)) with the C restatement."""
+    """integrate_triangle per pair (out (m,4)) with the C restatement; vals (T,10)
+    selects the P3 extension (oracle_integrate_triangle_p3)."""
     pp = arr(pp, np.int64)
     pt = arr(pt, np.int64)
     out = np.zeros((pp.shape[0], 4))
     c = arr(coef)
     fail = ctypes.c_int64(-1)
-    st = L.oracle_eval_pairs(pp.shape[0], ptr(pp), ptr(pt), ptr(arr(pxy)), ptr(arr(tri)),
+    p3 = vals is not None and np.ndim(vals) == 2 and np.shape(vals)[1] == 10  # P3 nodal values
+    fn = L.oracle_eval_pairs_p3 if p3 else L.oracle_eval_pairs
+    st = fn(pp.shape[0], ptr(pp), ptr(pt), ptr(arr(pxy)), ptr(arr(tri)),
                              ptr(arr(vals)) if vals is not None else None, ptr(c), c.shape[0], c2, h, threads,
                              ptr(out), ctypes.byref(fail))
     return st, out
@@ -138,7 +144,7 @@ def parity_ratio(got, want, c2, h):
     (BASELINE.json tolerance, literal floor; SURVEY.md §0 finding 3)."""
     got = np.asarray(got, dtype=np.float64)
     want = np.asarray(want, dtype=np.float64)
-    tol = np.maximum(1e-11 * np.maximum(abs(got), abs(want)), 1e-13 * c2 / h ** 2)
+    tol = np.maximum(1e-11 * np.maximum(abs(got), abs(want)), 1e-13 * abs(c2) / h ** 2)
     if got.size == 0:
         return 0.0
     return float((abs(got - want) / tol).max())
@@ -163,3 +169,59 @@ def cpu_pairs_grid(L, P, T, h, cap=20_000_000):
     n = L.oracle_find_pairs_grid(P.shape[0], ptr(arr(P)), T.shape[0], ptr(arr(T)), h, ptr(buf), cap)
     assert n <= cap
     return buf[:n]
+
+
+# ---------------------------------------------------------------------------
+# P3 (cubic) fields, configs[3]
+# ---------------------------------------------------------------------------
+P3_IJ = [(i, j) for i in range(4) for j in range(4 - i)]
+
+
+def p3_node_points(tri):
+    v = np.asarray(tri, dtype=np.float64).reshape(3, 2)
+    return np.array([v[0], v[1], v[2], (2 * v[0] + v[1]) / 3, (v[0] + 2 * v[1]) / 3, (2 * v[1] + v[2]) / 3,
+                     (v[1] + 2 * v[2]) / 3, (2 * v[2] + v[0]) / 3, (v[2] + 2 * v[0]) / 3, v.mean(axis=0)])
+
+
+def p3_nodes_from_poly(tri, f):
+    """Nodal values of the function f(x, y) (vectorised) at the P3 nodes."""
+    pts = p3_node_points(tri)
+    return np.ascontiguousarray(f(pts[:, 0], pts[:, 1]), dtype=np.float64)
+
+
+def p3_field_sup(q, h, tri, nodes):
+    """sup over the normalized support disc of the cubic interpolant (sampled)."""
+    pts = p3_node_points(tri)
+    xn, yn = (pts[:, 0] - q[0]) / h, (pts[:, 1] - q[1]) / h
+    M = np.array([[x ** i * y ** j for i, j in P3_IJ] for x, y in zip(xn, yn)])
+    al = np.linalg.solve(M, nodes)
+    r = np.sqrt(np.linspace(0, 1, 40))[:, None]
+    t = np.linspace(0, 2 * np.pi, 181)[None, :]
+    X, Y = r * np.cos(t), r * np.sin(t)
+    return float(np.abs(sum(a * X ** i * Y ** j for a, (i, j) in zip(al, P3_IJ))).max())
+
+
+def p3_ratio(got, want, c2, h, field_sup=1.0):
+    """parity_ratio with the absolute floor scaled by the field's magnitude on the
+    support disc (the north-star floor 1e-13 C/h^2 presumes |A| <= 1; a cubic
+    extrapolated from N(0,1) nodes over the disc reaches 1e2..1e4)."""
+    got = np.asarray(got, dtype=np.float64)[..., :3]
+    want = np.asarray(want, dtype=np.float64)[..., :3]
+    floor = 1e-13 * abs(c2) / h ** 2 * max(1.0, field_sup)
+    tol = np.maximum(1e-11 * np.maximum(np.abs(got), np.abs(want)), floor)
+    return float((np.abs(got - want) / tol).max())
+
+
+def core_p3(C, coef, c2, q, h, tri, nodes):
+    out = np.zeros(4)
+    c = arr(coef)
+    st = C.core_host_eval_pair_p3(ptr(c), c.shape[0], c2, q[0], q[1], h, ptr(arr(tri)), ptr(arr(nodes)), ptr(out))
+    return st, out
+
+
+def oracle_p3(L, coef, c2, q, h, tri, nodes):
+    out = np.zeros(4)
+    c = arr(coef)
+    st = L.oracle_integrate_triangle_p3(q[0], q[1], h, ptr(arr(tri)), ptr(arr(nodes)), ptr(c), c.shape[0], c2,
+                                        ptr(out))
+    return st, out
