@@ -425,11 +425,15 @@ SPHBI_HD void s9_put(dd& dst, dd v, double sgn) {
 //   c1_n = cb D X_(n-1) - sb I_n           s1_n = X_n - cb I_n - sb D X_(n-1)
 //   c2_n = c2b D I_(n-1) - s2b/2 E_n       s2_n = X_n/2 - c2b/2 E_n - s2b D I_(n-1)
 //   E_n = X_n - 2 D^2 X_(n-2)
-SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double beta, double cb,
-                              double sb, double c2b, double s2b, S9& S, double sgn = 0.0) {
+// XK: what is known about the bound at compile time -- 0 nothing, 1 x == 1
+// (far bound on the circle), 2 x == D (right-limit bound). The specialised
+// instantiations do exactly the operations the runtime tests select.
+template <int XK>
+SPHBI_HD void stub_bound_sums_k(const KernelConsts& K, double x, double D, double beta, double cb,
+                                double sb, double c2b, double s2b, S9& S, double sgn = 0.0) {
   // sgn == 0: S = sums at x; sgn = +-1: S += sgn * sums at x
   ChainSums C;
-  if (x == D) {
+  if (XK == 2 || (XK == 0 && x == D)) {
     // right-limit bound (the snapped lo = D of every right stub): R = 0, so
     // every chain term vanishes exactly and asin_ratio(D, D) = pi/2.
     const dd z{0.0, 0.0};
@@ -446,7 +450,7 @@ SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double 
     as = (kHalfPiHi - asin(C.R / x)) + kHalfPiLo;
   const double amb = as - beta;
   const int N = K.deg;
-  const bool one = x == 1.0;  // the far bound sits on the circle for most stubs
+  const bool one = XK == 1 || (XK == 0 && x == 1.0);  // the far bound sits on the circle for most stubs
   const dd Pv = one ? K.pv1 : poly_dd(K.pv, N, x, 2);
   const dd Qv = one ? K.qv1 : poly_dd(K.qv, N, x, 3);
   const dd Pg = one ? K.pg1 : poly_dd(K.pg, N, x, 2);
@@ -467,6 +471,11 @@ SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double 
   s9_put(S.gy1, gx2_val, sgn);
   s9_put(S.gx3, dd_sub(dd_mul_d(Tg, 2.0 * cbD), dd_mul_d(C.sIg, 2.0 * sb)), sgn);
   s9_put(S.gy3, dd_sub(dd_sub(Rg, dd_mul_d(C.sIg, 2.0 * cb)), dd_mul_d(Tg, 2.0 * sbD)), sgn);
+}
+
+SPHBI_HD void stub_bound_sums(const KernelConsts& K, double x, double D, double beta, double cb, double sb,
+                              double c2b, double s2b, S9& S, double sgn = 0.0) {
+  stub_bound_sums_k<0>(K, x, D, beta, cb, sb, c2b, s2b, S, sgn);
 }
 
 SPHBI_HD void s9_sub(S9& a, const S9& b) {
@@ -599,6 +608,38 @@ SPHBI_HD void piece_stub(const KernelConsts& K, PairAcc& acc, const Frame& f, do
     stub_bound_sums(K, u, D, beta, cb, sb, c2b, s2b, S, 1.0);
     stub_bound_sums(K, lo, D, beta, cb, sb, c2b, s2b, S, -1.0);
   }
+  acc_add_region(acc, S, f, sign);
+}
+
+// Stub classes (work-item buckets of the device pipeline): which window
+// bounds are known to be special. 0: lo == D, u == 1; 1: lo == D, u < 1;
+// 2: lo > D, u == 1; 3: anything else (incl. no window).
+SPHBI_HD int stub_class(double D, double lo, double u, bool window) {
+  if (!window) return 3;
+  return lo == D ? (u == 1.0 ? 0 : 1) : (u == 1.0 ? 2 : 3);
+}
+
+template <int CLS>
+SPHBI_HD void piece_stub_k(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double l, double D,
+                           double beta, double lo, double u, bool window, double sign) {
+  if (CLS == 3) {
+    piece_stub(K, acc, f, gamma, l, D, beta, lo, u, window, sign);
+    return;
+  }
+  S9 S;
+  if (l >= 1.0) {
+    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+  } else {
+    const int N = K.deg;
+    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+              poly_dd(K.rg, N, l, 1), S);
+  }
+  double sb, cb;
+  dsincos(beta, &sb, &cb);
+  const double s2b = 2.0 * sb * cb;
+  const double c2b = (cb - sb) * (cb + sb);
+  stub_bound_sums_k<(CLS == 0 || CLS == 2) ? 1 : 0>(K, u, D, beta, cb, sb, c2b, s2b, S, 1.0);
+  stub_bound_sums_k<(CLS == 0 || CLS == 1) ? 2 : 0>(K, lo, D, beta, cb, sb, c2b, s2b, S, -1.0);
   acc_add_region(acc, S, f, sign);
 }
 

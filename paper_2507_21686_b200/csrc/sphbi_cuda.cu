@@ -307,15 +307,21 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
   for (int i = 0; i < 9; ++i) *x[i] = dd_add(*x[i], dd{o[2 * i], o[2 * i + 1]});
 }
 
+// Work-item kinds: 0 sector, 1..4 stub classes (stub_class), 5 segment.
+constexpr int kKinds = 6;
+
 struct CountSink {
-  unsigned n_sector, n_stub, n_seg, status;
+  unsigned n[kKinds];
+  unsigned status;
   unsigned long long* counters;
   __device__ void bump(int w) { bump_counter(counters, w); }
   __device__ void disc(double) {}
   __device__ void half_disc(const Frame&, double) {}
-  __device__ void sector(const Frame&, double, double, double) { ++n_sector; }
-  __device__ void stub(const Frame&, double, double, double, double, double, double, bool, double) { ++n_stub; }
-  __device__ void segment(const Frame&, double, double) { ++n_seg; }
+  __device__ void sector(const Frame&, double, double, double) { ++n[0]; }
+  __device__ void stub(const Frame&, double, double, double D, double, double lo, double u, bool window, double) {
+    ++n[1 + stub_class(D, lo, u, window)];
+  }
+  __device__ void segment(const Frame&, double, double) { ++n[5]; }
 };
 
 struct EmitSink {
@@ -324,7 +330,7 @@ struct EmitSink {
   unsigned status;
   int pair;
   PieceItem *sector_items, *seg_items;
-  StubItem* stub_items;
+  StubItem* stub_items[4];  // per stub class
   __device__ void bump(int) {}
   __device__ void put(PieceItem*& dst, const Frame& f, double sign, double a) {
     PieceItem it;
@@ -357,7 +363,7 @@ struct EmitSink {
     it.beta = beta;
     it.lo = lo;
     it.u = u;
-    *stub_items++ = it;
+    *stub_items[stub_class(D, lo, u, window)]++ = it;
   }
   __device__ void segment(const Frame& f, double d, double sign) { put(seg_items, f, sign, d); }
 };
@@ -406,8 +412,10 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(Src src, i
                                                     unsigned char* __restrict__ cls,
                                                     unsigned long long* counters, unsigned* status_or) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t m = n + 1;
   if (k >= n) {
-    if (k == n) cnt[k] = cnt[n + 1 + k] = cnt[2 * (n + 1) + k] = 0;  // scan tails
+    if (k == n)
+      for (int j = 0; j < kKinds; ++j) cnt[j * m + k] = 0;  // scan tails
     return;
   }
   double qx, qy, t6[6], a3[3];
@@ -415,15 +423,17 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(Src src, i
   P2 nv[3];
   int perm[3];
   normalized_pair(qx, qy, h, t6, nv, perm);
-  CountSink c{0u, 0u, 0u, 0u, counters};
+  CountSink c;
+  for (int j = 0; j < kKinds; ++j) c.n[j] = 0u;
+  c.status = 0u;
+  c.counters = counters;
   integrate_normalized(c, nv);
-  cnt[k] = c.n_sector;
-  cnt[n + 1 + k] = c.n_stub;
-  cnt[2 * (n + 1) + k] = c.n_seg;
+  for (int j = 0; j < kKinds; ++j) cnt[j * m + k] = c.n[j];
   // decomposition signature: pairs with equal signatures follow the same
   // control flow in the emit pass, which runs them in signature order
-  cls[k] = static_cast<unsigned char>((c.n_stub < 15 ? c.n_stub : 15) | ((c.n_sector < 3 ? c.n_sector : 3) << 4) |
-                                      ((c.n_seg < 3 ? c.n_seg : 3) << 6));
+  const unsigned n_stub = c.n[1] + c.n[2] + c.n[3] + c.n[4];
+  cls[k] = static_cast<unsigned char>((n_stub < 15 ? n_stub : 15) | ((c.n[0] < 3 ? c.n[0] : 3) << 4) |
+                                      ((c.n[5] < 3 ? c.n[5] : 3) << 6));
   if (c.status) atomicOr(status_or, c.status);
 }
 
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
                 StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
-                PairRec* __restrict__ rec, const int* __restrict__ order, ulonglong4 cap,
+                PairRec* __restrict__ rec, const int* __restrict__ order, ulonglong4 stub_base,
                 unsigned* status_or) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -457,13 +467,13 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   acc_zero(e.acc);
   e.status = 0;
   e.pair = static_cast<int>(k);
+  const int64_t m = n + 1;
   e.sector_items = sector_items + off[k];
-  e.stub_items = stub_items + off[n + 1 + k];
-  e.seg_items = seg_items + off[2 * (n + 1) + k];
-  if (off[n] > cap.x || off[2 * n + 1] > cap.y || off[3 * n + 2] > cap.z) {
-    atomicOr(status_or + 1, 4u);  // bounded work-item buffers overflowed: redo exactly
-    return;
-  }
+  e.stub_items[0] = stub_items + stub_base.x + off[m + k];
+  e.stub_items[1] = stub_items + stub_base.y + off[2 * m + k];
+  e.stub_items[2] = stub_items + stub_base.z + off[3 * m + k];
+  e.stub_items[3] = stub_items + stub_base.w + off[4 * m + k];
+  e.seg_items = seg_items + off[5 * m + k];
   const bool nondeg_route = integrate_normalized(e, nv);
   PairRec& r = rec[k];
   AccOut o;
@@ -506,18 +516,19 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// one launch per stub class: warps run one specialised code path
+template <int CLS>
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
-    k_pipe_stub(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
-                const StubItem* __restrict__ items, AccOut* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+    k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
+                AccOut* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   {
     const StubItem it = items[k];
     PairAcc a;
     acc_zero(a);
-    piece_stub(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
-               it.window != 0, it.sign);
+    piece_stub_k<CLS>(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
+                      it.window != 0, it.sign);
     acc_to_out(a, out[k]);
   }
 }
@@ -537,30 +548,41 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// A pair's items: sectors, stub classes 0..3, segments, each in emission
+// order -- a fixed summation order (bitwise reproducible).
+struct ItemOuts {
+  const AccOut* sec;
+  const AccOut* stub;
+  const AccOut* seg;
+  ulonglong4 stub_base;
+};
 __device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t n, int64_t k,
-                                          const unsigned long long* __restrict__ off,
-                                          const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
-                                          const AccOut* __restrict__ seg_out) {
+                                          const unsigned long long* __restrict__ off, const ItemOuts& io) {
+  const int64_t m = n + 1;
   acc_zero(a);
   acc_add_out(a, r.acc);
-  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, sec_out[j].v);
-  for (unsigned long long j = off[n + 1 + k]; j < off[n + 1 + k + 1]; ++j) acc_add_out(a, stub_out[j].v);
-  for (unsigned long long j = off[2 * (n + 1) + k]; j < off[2 * (n + 1) + k + 1]; ++j) acc_add_out(a, seg_out[j].v);
+  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, io.sec[j].v);
+  const unsigned long long base[4] = {io.stub_base.x, io.stub_base.y, io.stub_base.z, io.stub_base.w};
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    const unsigned long long* o = off + (1 + c) * m;
+    for (unsigned long long j = o[k]; j < o[k + 1]; ++j) acc_add_out(a, io.stub[base[c] + j].v);
+  }
+  for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) acc_add_out(a, io.seg[j].v);
 }
 
 // combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0])
 __global__ void __launch_bounds__(128)
     k_pipe_combine(const __grid_constant__ KernelConsts K, int64_t n, double h,
-                   const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
-                   const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
-                   const AccOut* __restrict__ seg_out, int stride, double* __restrict__ out) {
+                   const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off, ItemOuts io,
+                   int stride, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const PairRec& r = rec[k];
   double o[4] = {0.0, 0.0, 0.0, 0.0};
   if (r.nondeg) {
     PairAcc a;
-    sum_items(a, r, n, k, off, sec_out, stub_out, seg_out);
+    sum_items(a, r, n, k, off, io);
     double raw[3];
     combine_plane(a, dd{r.tau[0], r.tau[1]}, dd{r.tau[2], r.tau[3]}, dd{r.tau[4], r.tau[5]}, raw);
     finalize(raw, K.c2, h, o);
@@ -573,8 +595,7 @@ template <class Src>
 __global__ void __launch_bounds__(128)
     k_pipe_combine_bases(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
                          const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
-                         const AccOut* __restrict__ sec_out, const AccOut* __restrict__ stub_out,
-                         const AccOut* __restrict__ seg_out, double* __restrict__ out) {
+                         ItemOuts io, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   double qx, qy, t6[6], a3[3];
@@ -588,7 +609,7 @@ __global__ void __launch_bounds__(128)
   HatPlanes H;
   if (r.nondeg && hat_planes(nv, H)) {
     PairAcc a;
-    sum_items(a, r, n, k, off, sec_out, stub_out, seg_out);
+    sum_items(a, r, n, k, off, io);
     for (int i = 0; i < 3; ++i) {
       double raw[3];
       combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
@@ -858,26 +879,23 @@ struct PipeStats {
 // Work-item buffer capacities per pair (sector, stub, segment) for the
 // sync-free mode; the exact totals are only known on the device. Measured on
 // cfg2: 0.7 / 1.9 / 0.25 items per pair; worst single pairs reach ~16 stubs.
-constexpr unsigned long long kCapSectorPerPair = 4, kCapStubPerPair = 8, kCapSegPerPair = 2;
 
-// K4 pipeline over n pairs. Default (exact): the three item totals are read
-// back once (one host sync) and size the buffers and grids. bounded = true
-// skips that sync (buffers sized by per-pair capacities, piece kernels read
-// their counts on the device; an overflow sets dflags[1] bit 4 and the public
-// entry point redoes the call exactly). Measured on the B200: the sync costs
-// less than the over-sized grids, so the exact mode is the default.
+// K4 pipeline over n pairs. The six item totals (sectors, four stub classes,
+// segments) are read back once (one host sync) and size the buffers and the
+// grids exactly. (A sync-free variant with per-pair capacity bounds and
+// device-resident counts was measured slower on the B200: over-sized grids
+// cost more than the sync.)
 template <class Src>
 sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
-                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
-                          bool bounded = false) {
+                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps) {
   if (n <= 0) return SPHBI_OK;
   cudaStream_t s = c->stream;
   sphbi_status st;
   unsigned* cnt;
   unsigned long long* off;
   const int64_t m = n + 1;
-  if ((st = scratch_t(c, kBufPipeCnt, 3 * m, &cnt)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPipeOff, 3 * m, &off)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPipeCnt, kKinds * m, &cnt)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPipeOff, kKinds * m, &off)) != SPHBI_OK) return st;
   unsigned char *cls, *cls_sorted;
   int *iota, *order;
   if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
@@ -901,61 +919,56 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
   void* dtmp;
   if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < kKinds; ++j) {
     cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
     if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
   }
-  unsigned long long cap[3];
-  if (c->force_exact) bounded = false;
-  if (bounded) {
-    cap[0] = kCapSectorPerPair * (unsigned long long)n;
-    cap[1] = kCapStubPerPair * (unsigned long long)n;
-    cap[2] = kCapSegPerPair * (unsigned long long)n;
-  } else {
-    unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->h_flags + 4);
-    for (int j = 0; j < 3; ++j)
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(tot + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
+  // exact item totals (one host sync): buffers and grids sized to fit
+  unsigned long long tot[kKinds];
+  {
+    unsigned long long* ht = reinterpret_cast<unsigned long long*>(c->h_flags + 8);
+    for (int j = 0; j < kKinds; ++j)
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(ht + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int j = 0; j < 3; ++j) cap[j] = tot[j];
+    for (int j = 0; j < kKinds; ++j) tot[j] = ht[j];
   }
-  const ulonglong4 dcap = make_ulonglong4(cap[0], cap[1], cap[2], 0ull);
+  unsigned long long sbase[5] = {0, 0, 0, 0, 0};
+  for (int cl = 0; cl < 4; ++cl) sbase[cl + 1] = sbase[cl] + tot[1 + cl];
+  const ulonglong4 stub_base = make_ulonglong4(sbase[0], sbase[1], sbase[2], sbase[3]);
+  const unsigned long long n_sec = tot[0], n_stub = sbase[4], n_seg = tot[5];
   PieceItem *isec, *iseg;
   StubItem* istub;
   AccOut *osec, *ostub, *oseg;
   PairRec* rec;
-  if ((st = scratch_t(c, kBufItemsC, cap[0], &isec)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsB, cap[1], &istub)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsS, cap[2], &iseg)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutC, cap[0], &osec)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutB, cap[1], &ostub)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOutS, cap[2], &oseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, dcap, dflags);
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, stub_base, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
-  // piece kernels: grid-stride over the device-resident totals off[j*m + n]
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  auto blocks_for = [&](unsigned long long cap_items, int per_sm) {
-    const unsigned long long need = (cap_items + 127) / 128;
-    return (int)std::max<unsigned long long>(1, std::min<unsigned long long>(need, (unsigned long long)sms * per_sm));
-  };
-  if (cap[1]) {
-    k_pipe_stub<<<blocks_for(cap[1], 1 << 20), 128, 0, s>>>(K, off + m + n, istub, ostub);
-    if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
-  }
-  if (cap[0]) {
-    k_pipe_sector<<<blocks_for(cap[0], 1 << 20), 128, 0, s>>>(K, off + n, isec, osec);
+  // piece kernels, thread per item; stubs one launch per class
+  if (tot[1]) k_pipe_stub<0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], istub + sbase[0], ostub + sbase[0]);
+  if (tot[2]) k_pipe_stub<1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], istub + sbase[1], ostub + sbase[1]);
+  if (tot[3]) k_pipe_stub<2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], istub + sbase[2], ostub + sbase[2]);
+  if (tot[4]) k_pipe_stub<3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], istub + sbase[3], ostub + sbase[3]);
+  if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
+  if (n_sec) {
+    k_pipe_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
     if ((st = check_launch(c, "k_pipe_sector")) != SPHBI_OK) return st;
   }
-  if (cap[2]) {
-    k_pipe_segment<<<blocks_for(cap[2], 1 << 20), 128, 0, s>>>(K, off + 2 * m + n, iseg, oseg);
+  if (n_seg) {
+    k_pipe_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
     if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
   }
+  const ItemOuts io{osec, ostub, oseg, stub_base};
   if (mode == 0) {
-    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, n, h, rec, off, osec, ostub, oseg, stride, dout);
+    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, n, h, rec, off, io, stride, dout);
     if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
   } else {
-    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, rec, off, osec, ostub, oseg, dout);
+    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, rec, off, io, dout);
     if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
   }
   (void)ps;

@@ -115,6 +115,38 @@ int core_host_p3_pieces(const double* coef, int ncoef, double qx, double qy, dou
   return s.n;
 }
 
+// stub-type histogram of a pair batch (analysis only):
+// [0] no window, [1] lo==D u==1, [2] lo==D u<1, [3] lo>D u==1, [4] lo>D u<1,
+// [5] cone l<1, [6] sectors, [7] segments, [8] discs/half discs
+struct StatSink {
+  unsigned status;
+  unsigned long long* h;
+  void bump(int) {}
+  void disc(double) { ++h[8]; }
+  void half_disc(const Frame&, double) { ++h[8]; }
+  void sector(const Frame&, double, double, double) { ++h[6]; }
+  void stub(const Frame&, double, double l, double D, double, double lo, double u, bool window, double) {
+    if (l < 1.0) ++h[5];
+    if (!window) { ++h[0]; return; }
+    const bool ld = lo == D, u1 = u == 1.0;
+    ++h[ld ? (u1 ? 1 : 2) : (u1 ? 3 : 4)];
+  }
+  void segment(const Frame&, double, double) { ++h[7]; }
+};
+void core_host_stub_stats(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
+                          const double* tri6, double h, unsigned long long* hist) {
+  for (int64_t k = 0; k < npairs; ++k) {
+    const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
+    P2 v[3] = {{tri6[6 * t], tri6[6 * t + 1]}, {tri6[6 * t + 2], tri6[6 * t + 3]}, {tri6[6 * t + 4], tri6[6 * t + 5]}};
+    int perm[3];
+    canonicalize(v, perm);
+    P2 nv[3];
+    for (int j = 0; j < 3; ++j) nv[j] = P2{(v[j].x - pxy[2 * i]) / h, (v[j].y - pxy[2 * i + 1]) / h};
+    StatSink s{0u, hist};
+    integrate_normalized(s, nv);
+  }
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 }  // extern "C"
