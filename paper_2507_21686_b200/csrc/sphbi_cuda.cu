@@ -121,6 +121,9 @@ enum ScratchSlot {
   kBufClass,
   kBufOrder,
   kBufCubTemp2,
+  kBufPreKey,
+  kBufPreOrder,
+  kBufNormRec,
   kNumBufs
 };
 
@@ -385,6 +388,15 @@ struct SceneSrc {  // particle pp[k] vs triangle pt[k]
 #pragma unroll
     for (int j = 0; j < 3; ++j) a3[j] = vals ? __ldg(vals + 3 * (int64_t)t + j) : 1.0;
   }
+  __device__ void load_vals(int64_t k, double* a3) const {
+    if (!vals) {
+      a3[0] = a3[1] = a3[2] = 1.0;
+      return;
+    }
+    const int t = pt[k];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = __ldg(vals + 3 * (int64_t)t + j);
+  }
 };
 struct DirectSrc {  // query, triangle, values per item
   const double* q;
@@ -398,6 +410,10 @@ struct DirectSrc {  // query, triangle, values per item
 #pragma unroll
     for (int j = 0; j < 3; ++j) a3[j] = vals ? vals[3 * k + j] : 1.0;
   }
+  __device__ void load_vals(int64_t k, double* a3) const {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a3[j] = vals ? vals[3 * k + j] : 1.0;
+  }
 };
 
 __device__ __forceinline__ void normalized_pair(double qx, double qy, double h, const double* t6, P2* nv,
@@ -407,22 +423,77 @@ __device__ __forceinline__ void normalized_pair(double qx, double qy, double h, 
   for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
 }
 
+// Cheap pre-classification (no decomposition): which vertices are inside the
+// support disc and how many times each edge crosses the circle. Pairs with
+// equal keys mostly take the same path through the decomposition, so the
+// count pass runs them in key order (converged warps).
+// The canonical normalized vertices of a pair (canonicalize + (v - q)/h),
+// computed once in pair order (coalesced) by k_pre_class; the count and emit
+// passes then gather ONE 64-byte record per pair instead of chasing
+// pair -> particle / triangle indices.
+struct __align__(16) NormRec {
+  double v[6];
+  int perm;  // perm[0] | perm[1] << 2 | perm[2] << 4
+  int pad;
+  double pad2;
+};
+__device__ __forceinline__ void load_norm(const NormRec* __restrict__ r, int64_t k, P2* nv, int* perm) {
+  const double2* p = reinterpret_cast<const double2*>(r + k);
+  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
+  nv[0] = P2{a.x, a.y};
+  nv[1] = P2{b.x, b.y};
+  nv[2] = P2{c.x, c.y};
+  const int pc = __double_as_longlong(d.x) & 0xffffffff;
+  perm[0] = pc & 3;
+  perm[1] = (pc >> 2) & 3;
+  perm[2] = (pc >> 4) & 3;
+}
+
 template <class Src>
-__global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(Src src, int64_t n, double h, unsigned* __restrict__ cnt,
-                                                    unsigned char* __restrict__ cls,
-                                                    unsigned long long* counters, unsigned* status_or) {
+__global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h, unsigned short* __restrict__ key,
+                                                   NormRec* __restrict__ nrec) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t m = n + 1;
-  if (k >= n) {
-    if (k == n)
-      for (int j = 0; j < kKinds; ++j) cnt[j * m + k] = 0;  // scan tails
-    return;
-  }
+  if (k >= n) return;
   double qx, qy, t6[6], a3[3];
   src.load(k, qx, qy, t6, a3);
   P2 nv[3];
   int perm[3];
   normalized_pair(qx, qy, h, t6, nv, perm);
+  {
+    NormRec r;
+    for (int i = 0; i < 3; ++i) {
+      r.v[2 * i] = nv[i].x;
+      r.v[2 * i + 1] = nv[i].y;
+    }
+    r.perm = perm[0] | (perm[1] << 2) | (perm[2] << 4);
+    r.pad = 0;
+    r.pad2 = 0.0;
+    nrec[k] = r;
+  }
+  unsigned kk = 0;
+  for (int i = 0; i < 3; ++i) {
+    if (p_norm2(nv[i]) <= 1.0) kk |= 1u << i;
+    const Crossings x = segment_circle_crossings(nv[i], nv[(i + 1) % 3]);
+    kk |= static_cast<unsigned>(x.count) << (3 + 2 * i);
+  }
+  key[k] = static_cast<unsigned short>(kk);
+}
+
+__global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const NormRec* __restrict__ nrec, int64_t n,
+                                                    unsigned* __restrict__ cnt, unsigned char* __restrict__ cls,
+                                                    unsigned long long* counters, unsigned* status_or,
+                                                    const int* __restrict__ order) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t m = n + 1;
+  if (j >= n) {
+    if (j == n)
+      for (int q = 0; q < kKinds; ++q) cnt[q * m + j] = 0;  // scan tails
+    return;
+  }
+  const int64_t k = order ? order[j] : j;
+  P2 nv[3];
+  int perm[3];
+  load_norm(nrec, k, nv, perm);
   CountSink c;
   for (int j = 0; j < kKinds; ++j) c.n[j] = 0u;
   c.status = 0u;
@@ -449,7 +520,7 @@ struct PairRec {
 
 template <class Src>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
-    k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
+    k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
                 StubItem* __restrict__ stub_items, PieceItem* __restrict__ seg_items,
                 PairRec* __restrict__ rec, const int* __restrict__ order, ulonglong4 stub_base,
@@ -457,11 +528,9 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t k = order ? order[j] : j;
-  double qx, qy, t6[6], a3[3];
-  src.load(k, qx, qy, t6, a3);
   P2 nv[3];
   int perm[3];
-  normalized_pair(qx, qy, h, t6, nv, perm);
+  load_norm(nrec, k, nv, perm);
   EmitSink e;
   e.K = &K;
   acc_zero(e.acc);
@@ -485,6 +554,8 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   r.pad = 0;
   dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
   if (nondeg) {
+    double a3[3];
+    src.load_vals(k, a3);
     const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
     for (int i = 0; i < 3; ++i) {
       tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
@@ -902,11 +973,28 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   cls_sorted = cls + m;
   if ((st = scratch_t(c, kBufOrder, 2 * m, &iota)) != SPHBI_OK) return st;
   order = iota + m;
-  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(src, n, h, cnt, cls, ctr, dflags);
-  if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
-  // emit order: pairs grouped by decomposition signature (stable 8-bit radix sort)
+  NormRec* nrec;
   k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, iota);
   if ((st = check_launch(c, "k_iota")) != SPHBI_OK) return st;
+  // count order: pairs grouped by the cheap pre-classification key
+  {
+    unsigned short* pk;
+    int* porder;
+    if ((st = scratch_t(c, kBufPreKey, 2 * m, &pk)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufPreOrder, m, &porder)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufNormRec, n, &nrec)) != SPHBI_OK) return st;
+    k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, nrec);
+    if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
+    size_t tmp_sort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, pk, pk + m, iota, porder, (int)n, 0, 9, s);
+    void* dtmp_sort;
+    if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
+    cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, pk, pk + m, iota, porder, (int)n, 0, 9, s);
+    if ((st = check_launch(c, "radix sort pre-class")) != SPHBI_OK) return st;
+    k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
+    if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
+  }
+  // emit order: pairs grouped by decomposition signature (stable 8-bit radix sort)
   {
     size_t tmp_sort = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, cls, cls_sorted, iota, order, (int)n, 0, 8, s);
@@ -947,7 +1035,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, off, isec, istub, iseg, rec, order, stub_base, dflags);
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, order, stub_base, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
   // piece kernels, thread per item; stubs one launch per class
   if (tot[1]) k_pipe_stub<0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], istub + sbase[0], ostub + sbase[0]);
