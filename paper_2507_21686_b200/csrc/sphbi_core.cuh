@@ -681,6 +681,7 @@ SPHBI_HD void bump_counter(unsigned long long* counters, int which) {
 }
 
 struct EvalSink {
+  static constexpr int kAngles = 2;
   const KernelConsts* K;
   PairAcc acc;
   unsigned status;
@@ -727,8 +728,16 @@ SPHBI_HD Frame rotation_taking_to_x(P2 v, Sink& c) {
 }
 
 // region_sector(v1, v2, l) (:349-366); the hot path always passes l = 1.
+// Sink::kAngles selects how much of a piece the geometry works out:
+//   2  frames and angles (gamma = atan2, beta = atan2)
+//   0  piece kinds and window bounds only (count pass: no frames, no angles;
+//      the emit pass repeats the geometry and reports every status)
 template <class Sink>
 SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) {
+  if constexpr (Sink::kAngles == 0) {
+    c.sector(Frame{1.0, 0.0, 0.0, 1.0}, 0.0, fmin(l, 1.0), sign);
+    return;
+  }
   Frame f = rotation_taking_to_x(v1, c);
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -740,10 +749,23 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
   c.sector(f, gamma, fmin(l, 1.0), sign);
 }
 
+// stub_integral validation (elementary_regions.hpp:179-183)
+SPHBI_HD bool stub_beta_ok(double beta) { return beta >= 0.0 && beta < kHalfPiHi; }
+
 // Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
 template <class Sink>
 SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double area2, P2 b,
                           double sign) {
+  const double D = fabs(area2) / p_norm(b);
+  const double l = fmin(r2, 1.0);
+  const double u = fmin(r1, 1.0);
+  double lo = fmax(l, D);
+  if (lo - D <= 256.0 * kDblEps * D) lo = D;
+  const bool window = u > lo + kGeomEps;
+  if constexpr (Sink::kAngles == 0) {
+    c.stub(Frame{1.0, 0.0, 0.0, 1.0}, 0.0, l, D, 0.0, lo, u, window, sign);
+    return;
+  }
   Frame f = rotation_taking_to_x(v1, c);
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -752,16 +774,9 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
     w2.y = -w2.y;
   }
   const double gamma = d_atan2(w2.y, w2.x);
-  const double D = fabs(area2) / p_norm(b);
-  const double l = fmin(r2, 1.0);
-  const double u = fmin(r1, 1.0);
   const P2 cc = p_sub(v2, v1);
   const double beta = d_atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
-  double lo = fmax(l, D);
-  if (lo - D <= 256.0 * kDblEps * D) lo = D;
-  const bool window = u > lo + kGeomEps;
-  // stub_integral validation (elementary_regions.hpp:179-183)
-  if (window && !(beta >= 0.0 && beta < kHalfPiHi)) c.status |= kStatusDomain;
+  if (window && !stub_beta_ok(beta)) c.status |= kStatusDomain;
   c.stub(f, gamma, l, D, beta, lo, u, window, sign);
 }
 
@@ -1177,6 +1192,16 @@ SPHBI_HD bool hat_planes(const P2* v, HatPlanes& H) {
     H.t3[i] = t3;
   }
   return true;
+}
+
+// hat_planes' degeneracy test alone (field == 1: the plane is (0, 0, 1)).
+SPHBI_HD bool hat_planes_nondeg(const P2* v) {
+  const dd dy12 = two_sum(v[1].y, -v[2].y);
+  const dd dx02 = two_sum(v[0].x, -v[2].x);
+  const dd dx21 = two_sum(v[2].x, -v[1].x);
+  const dd dy02 = two_sum(v[0].y, -v[2].y);
+  const dd den = dd_add(dd_mul(dy12, dx02), dd_mul(dx21, dy02));
+  return !(fabs(den.hi) < 2.0 * kGeomEps);
 }
 
 // Channel values for a field with plane coefficients (tau1, tau2, tau3):

@@ -314,6 +314,7 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
 constexpr int kKinds = 6;
 
 struct CountSink {
+  static constexpr int kAngles = 0;
   unsigned n[kKinds];
   unsigned status;
   unsigned long long* counters;
@@ -328,6 +329,7 @@ struct CountSink {
 };
 
 struct EmitSink {
+  static constexpr int kAngles = 2;
   const KernelConsts* K;
   PairAcc acc;
   unsigned status;
@@ -347,8 +349,15 @@ struct EmitSink {
     it.a = a;
     *dst++ = it;
   }
-  __device__ void disc(double sign) { piece_disc(*K, acc, sign); }
-  __device__ void half_disc(const Frame& f, double sign) { piece_half_disc(*K, acc, f, sign); }
+  bool has_acc;
+  __device__ void disc(double sign) {
+    piece_disc(*K, acc, sign);
+    has_acc = true;
+  }
+  __device__ void half_disc(const Frame& f, double sign) {
+    piece_half_disc(*K, acc, f, sign);
+    has_acc = true;
+  }
   __device__ void sector(const Frame& f, double gamma, double, double sign) { put(sector_items, f, sign, gamma); }
   __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
                        bool window, double sign) {
@@ -512,10 +521,9 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const Norm
 // discs) and, for field mode, the field's barycentric plane tau in the
 // particle frame, so that combine needs no geometry.
 struct PairRec {
+  int nondeg_route;  // integrate_normalized did not bail out (non-degenerate)
+  int has_acc;       // acc holds full / half disc contributions (else zero, not written)
   double acc[18];
-  double tau[6];
-  int nondeg;
-  int pad;
 };
 
 template <class Src>
@@ -543,32 +551,16 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.stub_items[2] = stub_items + stub_base.z + off[3 * m + k];
   e.stub_items[3] = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
+  e.has_acc = false;
   const bool nondeg_route = integrate_normalized(e, nv);
   PairRec& r = rec[k];
-  AccOut o;
-  acc_to_out(e.acc, o);
-  for (int j = 0; j < 18; ++j) r.acc[j] = o.v[j];
-  HatPlanes H;
-  const bool nondeg = nondeg_route && hat_planes(nv, H);
-  r.nondeg = nondeg ? 1 : 0;
-  r.pad = 0;
-  dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
-  if (nondeg) {
-    double a3[3];
-    src.load_vals(k, a3);
-    const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
-    for (int i = 0; i < 3; ++i) {
-      tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
-      tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
-      tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
-    }
+  r.nondeg_route = nondeg_route ? 1 : 0;
+  r.has_acc = e.has_acc ? 1 : 0;
+  if (e.has_acc) {
+    AccOut o;
+    acc_to_out(e.acc, o);
+    for (int q = 0; q < 18; ++q) r.acc[q] = o.v[q];
   }
-  r.tau[0] = tau1.hi;
-  r.tau[1] = tau1.lo;
-  r.tau[2] = tau2.hi;
-  r.tau[3] = tau2.lo;
-  r.tau[4] = tau3.hi;
-  r.tau[5] = tau3.lo;
   if (e.status) atomicOr(status_or, e.status);
 }
 
@@ -631,7 +623,7 @@ __device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t 
                                           const unsigned long long* __restrict__ off, const ItemOuts& io) {
   const int64_t m = n + 1;
   acc_zero(a);
-  acc_add_out(a, r.acc);
+  if (r.has_acc) acc_add_out(a, r.acc);
   for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, io.sec[j].v);
   const unsigned long long base[4] = {io.stub_base.x, io.stub_base.y, io.stub_base.z, io.stub_base.w};
 #pragma unroll 1
@@ -642,43 +634,68 @@ __device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t 
   for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) acc_add_out(a, io.seg[j].v);
 }
 
-// combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0])
+// combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0]).
+// The field's barycentric plane (assemble_region :255-269, solved once per
+// pair in the particle frame) is computed here, in pair order; for field == 1
+// the plane is exactly (0, 0, 1) and only the degeneracy test remains.
+template <class Src>
 __global__ void __launch_bounds__(128)
-    k_pipe_combine(const __grid_constant__ KernelConsts K, int64_t n, double h,
-                   const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off, ItemOuts io,
+    k_pipe_combine(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
+                   double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off, ItemOuts io,
                    int stride, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const PairRec& r = rec[k];
   double o[4] = {0.0, 0.0, 0.0, 0.0};
-  if (r.nondeg) {
-    PairAcc a;
-    sum_items(a, r, n, k, off, io);
-    double raw[3];
-    combine_plane(a, dd{r.tau[0], r.tau[1]}, dd{r.tau[2], r.tau[3]}, dd{r.tau[4], r.tau[5]}, raw);
-    finalize(raw, K.c2, h, o);
+  if (r.nondeg_route) {
+    P2 nv[3];
+    int perm[3];
+    load_norm(nrec, k, nv, perm);
+    dd tau1{0, 0}, tau2{0, 0}, tau3{1.0, 0};
+    bool nondeg;
+    if (src.vals) {
+      HatPlanes H;
+      nondeg = hat_planes(nv, H);
+      if (nondeg) {
+        double a3[3];
+        src.load_vals(k, a3);
+        const double av[3] = {a3[perm[0]], a3[perm[1]], a3[perm[2]]};
+        tau3 = dd{0, 0};
+        for (int i = 0; i < 3; ++i) {
+          tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
+          tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
+          tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
+        }
+      }
+    } else {
+      nondeg = hat_planes_nondeg(nv);
+    }
+    if (nondeg) {
+      PairAcc a;
+      sum_items(a, r, n, k, off, io);
+      double raw[3];
+      combine_plane(a, tau1, tau2, tau3, raw);
+      finalize(raw, K.c2, h, o);
+    }
   }
   for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
 }
 
 // combine, vertex-basis mode: 12 doubles per pair in the original vertex order
-template <class Src>
 __global__ void __launch_bounds__(128)
-    k_pipe_combine_bases(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h,
-                         const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
+    k_pipe_combine_bases(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
+                         double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
                          ItemOuts io, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  double qx, qy, t6[6], a3[3];
-  src.load(k, qx, qy, t6, a3);
   P2 nv[3];
   int perm[3];
-  normalized_pair(qx, qy, h, t6, nv, perm);
+  load_norm(nrec, k, nv, perm);
   const PairRec& r = rec[k];
   double o[12];
   for (int j = 0; j < 12; ++j) o[j] = 0.0;
   HatPlanes H;
-  if (r.nondeg && hat_planes(nv, H)) {
+  if (r.nondeg_route && hat_planes(nv, H)) {
     PairAcc a;
     sum_items(a, r, n, k, off, io);
     for (int i = 0; i < 3; ++i) {
@@ -1053,10 +1070,10 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   }
   const ItemOuts io{osec, ostub, oseg, stub_base};
   if (mode == 0) {
-    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, n, h, rec, off, io, stride, dout);
+    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
     if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
   } else {
-    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, src, n, h, rec, off, io, dout);
+    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, rec, off, io, dout);
     if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
   }
   (void)ps;

@@ -336,6 +336,7 @@ SPHBI_HD void h24_accumulate(H24& acc, const H24& H, const Frame& M, double sign
 }
 
 struct P3Sink {
+  static constexpr int kAngles = 2;
   const P3Consts* P;
   H24 acc;
   unsigned status;

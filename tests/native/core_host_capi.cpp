@@ -71,6 +71,7 @@ int core_host_h24(const double* coef, int ncoef, int kind, const double* a, doub
 
 // piece log of one P3 pair: per piece 8 params (type, sign, f00, f01, f10, f11, p0..p6 ...) + 24 sums
 struct LogSink {
+  static constexpr int kAngles = 2;
   const P3Consts* P;
   unsigned status;
   unsigned long long* counters;
@@ -119,6 +120,7 @@ int core_host_p3_pieces(const double* coef, int ncoef, double qx, double qy, dou
 // [0] no window, [1] lo==D u==1, [2] lo==D u<1, [3] lo>D u==1, [4] lo>D u<1,
 // [5] cone l<1, [6] sectors, [7] segments, [8] discs/half discs
 struct StatSink {
+  static constexpr int kAngles = 2;
   unsigned status;
   unsigned long long* h;
   void bump(int) {}
