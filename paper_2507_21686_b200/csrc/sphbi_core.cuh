@@ -670,6 +670,129 @@ SPHBI_HD void piece_disc_l(const KernelConsts& K, PairAcc& acc, double l, double
   acc.g22 = dd_add(acc.g22, dd_scale(g, sign));
 }
 
+// ---------------------------------------------------------------------------
+// constant field (A == 1; configs 1/2/3/5): the barycentric plane is exactly
+// (0, 0, 1), so only the tau3 channels v3, g13, g23 reach the result. These
+// functions perform, operation for operation, the tau3 part of the general
+// ones above (same results bit for bit) and skip the rest: 2 of 4 cone
+// polynomials, 3 of 5 bound polynomials, 2 of 4 chain accumulations, 2 of 12
+// rotation dot products, and a third of the work-item output traffic.
+// ---------------------------------------------------------------------------
+struct S3 {
+  dd v3, gx3, gy3;
+};
+struct PairAcc3 {
+  dd v3, g13, g23;
+};
+SPHBI_HD void acc3_zero(PairAcc3& a) { a.v3 = a.g13 = a.g23 = dd{0.0, 0.0}; }
+SPHBI_HD void acc3_add_region(PairAcc3& a, const S3& S, const Frame& M, double sign) {
+  const dd g3x = dd_dot2_d(S.gx3, M.m00, S.gy3, M.m10);
+  const dd g3y = dd_dot2_d(S.gx3, M.m01, S.gy3, M.m11);
+  a.v3 = dd_add(a.v3, dd_scale(S.v3, sign));
+  a.g13 = dd_add(a.g13, dd_scale(g3x, sign));
+  a.g23 = dd_add(a.g23, dd_scale(g3y, sign));
+}
+SPHBI_HD void cone_sums3(double gamma, dd Pv, dd Rg, S3& S) {
+  double sg, cg;
+  dsincos(gamma, &sg, &cg);
+  const double sh = sin(0.5 * gamma);
+  const double omc = 2.0 * sh * sh;
+  S.v3 = dd_mul_d(Pv, gamma);
+  S.gx3 = dd_mul_d(Rg, sg);
+  S.gy3 = dd_mul_d(Rg, omc);
+}
+SPHBI_HD void radial_chains3(const KernelConsts& K, double x, double D, dd& sPv, dd& sIg, double& R) {
+  const int N = K.deg;
+  ChainSeeds sd;
+  chain_seeds(x, D, sd);
+  const dd D2 = two_prod(D, D);
+  const dd R3 = dd_mul(dd_mul(sd.R, sd.R), sd.R);
+  acc2 aPv{0, 0}, aIg{0, 0};
+  dd um2 = sd.p0, um1 = sd.R;
+  dd vm2{0.0, 0.0}, vm1 = sd.i1;
+  acc_add_dddd(aPv, K.wpv[1], um1);
+  acc_add_dddd(aIg, K.wig[1], vm1);
+  dd xpm2 = dd_make(1.0), xpm1 = dd_make(x);
+  for (int m = 2; m <= N + 2; ++m) {
+    const dd um = cterm2(xpm1, sd.R, K.dfac[m - 2], D2, um2, (double)(m - 1));
+    const dd vm = cterm2(xpm2, R3, K.efac[m - 2], D2, vm2, (double)(m - 2));
+    acc_add_dddd(aPv, K.wpv[m], um);
+    acc_add_dddd(aIg, K.wig[m], vm);
+    um2 = um1;
+    um1 = um;
+    vm2 = vm1;
+    vm1 = vm;
+    xpm2 = xpm1;
+    xpm1 = cmul_d(xpm1, x);
+  }
+  sPv = acc_dd(aPv);
+  sIg = acc_dd(aIg);
+  R = sd.R.hi;
+}
+template <int XK>
+SPHBI_HD void stub_bound_sums3(const KernelConsts& K, double x, double D, double beta, double cb, double sb,
+                               S3& S, double sgn) {
+  dd sPv{0.0, 0.0}, sIg{0.0, 0.0};
+  double R = 0.0;
+  if (!(XK == 2 || (XK == 0 && x == D))) {
+    radial_chains3(K, x, D, sPv, sIg, R);
+  }
+  double as;
+  if (D <= 0.7 * x)
+    as = asin(D / x);
+  else
+    as = (kHalfPiHi - asin(R / x)) + kHalfPiLo;
+  const double amb = as - beta;
+  const int N = K.deg;
+  const bool one = XK == 1 || (XK == 0 && x == 1.0);
+  const dd Pv = one ? K.pv1 : poly_dd(K.pv, N, x, 2);
+  const dd Tg = one ? K.tg1 : poly_dd(K.tg, N, x, 0);
+  const dd Rg = one ? K.rg1 : poly_dd(K.rg, N, x, 1);
+  const double cbD = cb * D, sbD = sb * D;
+  const dd pcore_v = dd_add(dd_mul_d(Pv, amb), dd_mul_d(sPv, D));
+  s9_put(S.v3, pcore_v, sgn);
+  s9_put(S.gx3, dd_sub(dd_mul_d(Tg, 2.0 * cbD), dd_mul_d(sIg, 2.0 * sb)), sgn);
+  s9_put(S.gy3, dd_sub(dd_sub(Rg, dd_mul_d(sIg, 2.0 * cb)), dd_mul_d(Tg, 2.0 * sbD)), sgn);
+}
+template <int CLS>
+SPHBI_HD void piece_stub3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double gamma, double l, double D,
+                          double beta, double lo, double u, bool window, double sign) {
+  S3 S;
+  if (l >= 1.0) {
+    cone_sums3(gamma, K.pv1, K.rg1, S);
+  } else {
+    const int N = K.deg;
+    cone_sums3(gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.rg, N, l, 1), S);
+  }
+  if (CLS != 3 || window) {
+    double sb, cb;
+    dsincos(beta, &sb, &cb);
+    stub_bound_sums3<(CLS == 0 || CLS == 2) ? 1 : 0>(K, u, D, beta, cb, sb, S, 1.0);
+    stub_bound_sums3<(CLS == 0 || CLS == 1) ? 2 : 0>(K, lo, D, beta, cb, sb, S, -1.0);
+  }
+  acc3_add_region(acc, S, f, sign);
+}
+SPHBI_HD void piece_cone3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double gamma, double L,
+                          double sign) {
+  S3 S;
+  if (L >= 1.0)
+    cone_sums3(gamma, K.pv1, K.rg1, S);
+  else
+    cone_sums3(gamma, poly_dd(K.pv, K.deg, L, 2), poly_dd(K.rg, K.deg, L, 1), S);
+  acc3_add_region(acc, S, f, sign);
+}
+SPHBI_HD void piece_segment3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double d, double sign) {
+  dd sPv, sIg;
+  double R;
+  radial_chains3(K, 1.0, d, sPv, sIg, R);
+  const double acd = d <= 0.7 ? acos(d) : asin(R);
+  S3 S;
+  S.v3 = dd_sub(dd_mul_d(K.pv1, 2.0 * acd), dd_mul_d(sPv, 2.0 * d));
+  S.gx3 = dd_mul_d(sIg, 4.0);
+  S.gy3 = dd{0.0, 0.0};
+  acc3_add_region(acc, S, f, sign);
+}
+
 SPHBI_HD void bump_counter(unsigned long long* counters, int which) {
   if (counters) {
 #if defined(__CUDA_ARCH__)

@@ -296,6 +296,17 @@ struct StubItem {  // direct stub: cone (gamma, l) + radial window [lo, u] (D, b
 struct AccOut {  // one piece's rotated contribution (9 dd)
   double v[18];
 };
+struct AccOut3 {  // constant field: v3, g13, g23 only (3 dd)
+  double v[6];
+};
+SPHBI_HD void acc3_to_out(const PairAcc3& a, AccOut3& o) {
+  o.v[0] = a.v3.hi;
+  o.v[1] = a.v3.lo;
+  o.v[2] = a.g13.hi;
+  o.v[3] = a.g13.lo;
+  o.v[4] = a.g23.hi;
+  o.v[5] = a.g23.lo;
+}
 
 SPHBI_HD void acc_to_out(const PairAcc& a, AccOut& o) {
   const dd x[9] = {a.v1, a.v2, a.v3, a.g11, a.g12, a.g21, a.g22, a.g13, a.g23};
@@ -564,81 +575,112 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   if (e.status) atomicOr(status_or, e.status);
 }
 
+template <bool F1>
 __global__ void __launch_bounds__(128)
     k_pipe_sector(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
-                  const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+                  const PieceItem* __restrict__ items, void* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  {
-    const PieceItem it = items[k];
+  const PieceItem it = items[k];
+  const Frame f{it.m00, it.m01, it.m10, it.m11};
+  if constexpr (F1) {
+    PairAcc3 a;
+    acc3_zero(a);
+    piece_cone3(K, a, f, it.a, 1.0, it.sign);
+    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+  } else {
     PairAcc a;
     acc_zero(a);
-    piece_cone(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, 1.0, it.sign);
-    acc_to_out(a, out[k]);
+    piece_cone(K, a, f, it.a, 1.0, it.sign);
+    acc_to_out(a, static_cast<AccOut*>(out)[k]);
   }
 }
 
 // one launch per stub class: warps run one specialised code path
-template <int CLS>
+template <bool F1, int CLS>
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
-                AccOut* __restrict__ out) {
+                void* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  {
-    const StubItem it = items[k];
+  const StubItem it = items[k];
+  const Frame f{it.m00, it.m01, it.m10, it.m11};
+  if constexpr (F1) {
+    PairAcc3 a;
+    acc3_zero(a);
+    piece_stub3<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+  } else {
     PairAcc a;
     acc_zero(a);
-    piece_stub_k<CLS>(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.gamma, it.l, it.D, it.beta, it.lo, it.u,
-                      it.window != 0, it.sign);
-    acc_to_out(a, out[k]);
+    piece_stub_k<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+    acc_to_out(a, static_cast<AccOut*>(out)[k]);
   }
 }
 
+template <bool F1>
 __global__ void __launch_bounds__(128)
     k_pipe_segment(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
-                   const PieceItem* __restrict__ items, AccOut* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count (no host sync)
+                   const PieceItem* __restrict__ items, void* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  {
-    const PieceItem it = items[k];
+  const PieceItem it = items[k];
+  const Frame f{it.m00, it.m01, it.m10, it.m11};
+  if constexpr (F1) {
+    PairAcc3 a;
+    acc3_zero(a);
+    piece_segment3(K, a, f, it.a, it.sign);
+    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+  } else {
     PairAcc a;
     acc_zero(a);
-    piece_segment(K, a, Frame{it.m00, it.m01, it.m10, it.m11}, it.a, it.sign);
-    acc_to_out(a, out[k]);
+    piece_segment(K, a, f, it.a, it.sign);
+    acc_to_out(a, static_cast<AccOut*>(out)[k]);
   }
 }
 
 // A pair's items: sectors, stub classes 0..3, segments, each in emission
 // order -- a fixed summation order (bitwise reproducible).
 struct ItemOuts {
-  const AccOut* sec;
-  const AccOut* stub;
-  const AccOut* seg;
+  const void* sec;
+  const void* stub;
+  const void* seg;
   ulonglong4 stub_base;
 };
+template <bool F1>
+__device__ __forceinline__ void add_item(PairAcc& a, const void* base, unsigned long long j) {
+  if constexpr (F1) {
+    const double* o = static_cast<const AccOut3*>(base)[j].v;
+    a.v3 = dd_add(a.v3, dd{o[0], o[1]});
+    a.g13 = dd_add(a.g13, dd{o[2], o[3]});
+    a.g23 = dd_add(a.g23, dd{o[4], o[5]});
+  } else {
+    acc_add_out(a, static_cast<const AccOut*>(base)[j].v);
+  }
+}
+template <bool F1>
 __device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t n, int64_t k,
                                           const unsigned long long* __restrict__ off, const ItemOuts& io) {
   const int64_t m = n + 1;
   acc_zero(a);
   if (r.has_acc) acc_add_out(a, r.acc);
-  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) acc_add_out(a, io.sec[j].v);
+  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) add_item<F1>(a, io.sec, j);
   const unsigned long long base[4] = {io.stub_base.x, io.stub_base.y, io.stub_base.z, io.stub_base.w};
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {
     const unsigned long long* o = off + (1 + c) * m;
-    for (unsigned long long j = o[k]; j < o[k + 1]; ++j) acc_add_out(a, io.stub[base[c] + j].v);
+    for (unsigned long long j = o[k]; j < o[k + 1]; ++j) add_item<F1>(a, io.stub, base[c] + j);
   }
-  for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) acc_add_out(a, io.seg[j].v);
+  for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) add_item<F1>(a, io.seg, j);
 }
 
 // combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0]).
 // The field's barycentric plane (assemble_region :255-269, solved once per
 // pair in the particle frame) is computed here, in pair order; for field == 1
 // the plane is exactly (0, 0, 1) and only the degeneracy test remains.
-template <class Src>
+template <bool F1, class Src>
 __global__ void __launch_bounds__(128)
     k_pipe_combine(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
                    double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off, ItemOuts io,
@@ -672,7 +714,7 @@ __global__ void __launch_bounds__(128)
     }
     if (nondeg) {
       PairAcc a;
-      sum_items(a, r, n, k, off, io);
+      sum_items<F1>(a, r, n, k, off, io);
       double raw[3];
       combine_plane(a, tau1, tau2, tau3, raw);
       finalize(raw, K.c2, h, o);
@@ -697,7 +739,7 @@ __global__ void __launch_bounds__(128)
   HatPlanes H;
   if (r.nondeg_route && hat_planes(nv, H)) {
     PairAcc a;
-    sum_items(a, r, n, k, off, io);
+    sum_items<false>(a, r, n, k, off, io);
     for (int i = 0; i < 3; ++i) {
       double raw[3];
       combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
@@ -1054,23 +1096,33 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
   k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, order, stub_base, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
-  // piece kernels, thread per item; stubs one launch per class
-  if (tot[1]) k_pipe_stub<0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], istub + sbase[0], ostub + sbase[0]);
-  if (tot[2]) k_pipe_stub<1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], istub + sbase[1], ostub + sbase[1]);
-  if (tot[3]) k_pipe_stub<2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], istub + sbase[2], ostub + sbase[2]);
-  if (tot[4]) k_pipe_stub<3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], istub + sbase[3], ostub + sbase[3]);
-  if ((st = check_launch(c, "k_pipe_stub")) != SPHBI_OK) return st;
-  if (n_sec) {
-    k_pipe_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
-    if ((st = check_launch(c, "k_pipe_sector")) != SPHBI_OK) return st;
+  // piece kernels, thread per item; stubs one launch per class. A constant
+  // field (scene, tri_values == NULL) needs only the tau3 channels.
+  const bool f1 = mode == 0 && src.vals == nullptr;
+  AccOut3* ostub3 = reinterpret_cast<AccOut3*>(ostub);
+  const StubItem* is[4] = {istub + sbase[0], istub + sbase[1], istub + sbase[2], istub + sbase[3]};
+  if (f1) {
+    if (tot[1]) k_pipe_stub<true, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ostub3 + sbase[0]);
+    if (tot[2]) k_pipe_stub<true, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ostub3 + sbase[1]);
+    if (tot[3]) k_pipe_stub<true, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ostub3 + sbase[2]);
+    if (tot[4]) k_pipe_stub<true, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ostub3 + sbase[3]);
+    if (n_sec) k_pipe_sector<true><<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
+    if (n_seg) k_pipe_segment<true><<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
+  } else {
+    if (tot[1]) k_pipe_stub<false, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ostub + sbase[0]);
+    if (tot[2]) k_pipe_stub<false, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ostub + sbase[1]);
+    if (tot[3]) k_pipe_stub<false, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ostub + sbase[2]);
+    if (tot[4]) k_pipe_stub<false, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ostub + sbase[3]);
+    if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
+    if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
   }
-  if (n_seg) {
-    k_pipe_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
-    if ((st = check_launch(c, "k_pipe_segment")) != SPHBI_OK) return st;
-  }
+  if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
   const ItemOuts io{osec, ostub, oseg, stub_base};
   if (mode == 0) {
-    k_pipe_combine<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
+    if (f1)
+      k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
+    else
+      k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
     if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
   } else {
     k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, rec, off, io, dout);
