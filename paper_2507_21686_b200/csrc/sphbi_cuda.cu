@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -124,6 +125,7 @@ enum ScratchSlot {
   kBufPreKey,
   kBufPreOrder,
   kBufNormRec,
+  kBufIdx,
   kNumBufs
 };
 
@@ -141,7 +143,8 @@ struct sphbi_ctx {
   // copy engines for the streamed host-buffer path (H2D / D2H overlap)
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t sev[3][64] = {};  // per chunk: uploaded / computed / downloaded
-  bool force_exact = false;     // host-sized work-item buffers (after a bounded overflow)
+  bool force_exact = false;     // two-pass count/emit pipeline for this call (after a slot overflow)
+  bool two_pass = false;        // SPHBI_TWO_PASS=1: always the two-pass pipeline (testing)
   bool overflowed = false;      // the last bounded pipeline overflowed its buffers
 };
 
@@ -346,7 +349,9 @@ struct EmitSink {
   unsigned status;
   int pair;
   PieceItem *sector_items, *seg_items;
-  StubItem* stub_items[4];  // per stub class
+  // per stub class; four scalars, not an array: a dynamically indexed array
+  // would put the whole sink (and its accumulator) in local memory
+  StubItem *stub0, *stub1, *stub2, *stub3;
   __device__ void bump(int) {}
   __device__ void put(PieceItem*& dst, const Frame& f, double sign, double a) {
     PieceItem it;
@@ -386,7 +391,12 @@ struct EmitSink {
     it.beta = beta;
     it.lo = lo;
     it.u = u;
-    *stub_items[stub_class(D, lo, u, window)]++ = it;
+    switch (stub_class(D, lo, u, window)) {
+      case 0: *stub0++ = it; break;
+      case 1: *stub1++ = it; break;
+      case 2: *stub2++ = it; break;
+      default: *stub3++ = it; break;
+    }
   }
   __device__ void segment(const Frame& f, double d, double sign) { put(seg_items, f, sign, d); }
 };
@@ -557,10 +567,10 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.pair = static_cast<int>(k);
   const int64_t m = n + 1;
   e.sector_items = sector_items + off[k];
-  e.stub_items[0] = stub_items + stub_base.x + off[m + k];
-  e.stub_items[1] = stub_items + stub_base.y + off[2 * m + k];
-  e.stub_items[2] = stub_items + stub_base.z + off[3 * m + k];
-  e.stub_items[3] = stub_items + stub_base.w + off[4 * m + k];
+  e.stub0 = stub_items + stub_base.x + off[m + k];
+  e.stub1 = stub_items + stub_base.y + off[2 * m + k];
+  e.stub2 = stub_items + stub_base.z + off[3 * m + k];
+  e.stub3 = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
   e.has_acc = false;
   const bool nondeg_route = integrate_normalized(e, nv);
@@ -577,12 +587,11 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
 
 template <bool F1>
 __global__ void __launch_bounds__(128)
-    k_pipe_sector(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
-                  const PieceItem* __restrict__ items, void* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count
+    k_pipe_sector(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                  const int* __restrict__ idx, void* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const PieceItem it = items[k];
+  const PieceItem it = items[idx ? idx[k] : k];
   const Frame f{it.m00, it.m01, it.m10, it.m11};
   if constexpr (F1) {
     PairAcc3 a;
@@ -597,14 +606,179 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-pass emission into per-pair slots (the default): the geometry runs
+// once per pair; each pair owns kCapSec / kCapStub / kCapSeg item slots
+// (structural maxima of the decomposition: <= 4 wedges, each with <= 1
+// sector, <= 1 segment and <= 2 stub calls of <= 2 direct stubs), writes its
+// per-kind counts, and k_expand turns counts + class tags into dense,
+// pair-ordered index lists for the piece kernels and combine. A pair that
+// would exceed a cap (never seen; 4.5M-pair census in DESIGN.md) sets
+// dflags[1] bit 8 and the chunk is redone with the two-pass count/emit path.
+// ---------------------------------------------------------------------------
+constexpr int kCapSec = 4, kCapStub = 16, kCapSeg = 4;
+
+struct SlotSink {
+  static constexpr int kAngles = 2;
+  const KernelConsts* K;
+  PairAcc acc;
+  unsigned status;
+  int pair;
+  bool has_acc, overflow;
+  PieceItem *sec, *seg;
+  StubItem* stubs;
+  unsigned char* tag;
+  int nsec, nseg, nstub, c0, c1, c2, c3;
+  unsigned long long* counters;
+  __device__ void bump(int w) { bump_counter(counters, w); }
+  __device__ PieceItem piece(const Frame& f, double sign, double a) const {
+    PieceItem it;
+    it.pair = pair;
+    it.pad = 0;
+    it.sign = sign;
+    it.m00 = f.m00;
+    it.m01 = f.m01;
+    it.m10 = f.m10;
+    it.m11 = f.m11;
+    it.a = a;
+    return it;
+  }
+  __device__ void disc(double sign) {
+    piece_disc(*K, acc, sign);
+    has_acc = true;
+  }
+  __device__ void half_disc(const Frame& f, double sign) {
+    piece_half_disc(*K, acc, f, sign);
+    has_acc = true;
+  }
+  __device__ void sector(const Frame& f, double gamma, double, double sign) {
+    if (nsec < kCapSec)
+      sec[nsec] = piece(f, sign, gamma);
+    else
+      overflow = true;
+    ++nsec;
+  }
+  __device__ void segment(const Frame& f, double d, double sign) {
+    if (nseg < kCapSeg)
+      seg[nseg] = piece(f, sign, d);
+    else
+      overflow = true;
+    ++nseg;
+  }
+  __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
+                       bool window, double sign) {
+    const int cls = stub_class(D, lo, u, window);
+    if (nstub < kCapStub) {
+      StubItem it;
+      it.pair = pair;
+      it.window = window ? 1 : 0;
+      it.sign = sign;
+      it.m00 = f.m00;
+      it.m01 = f.m01;
+      it.m10 = f.m10;
+      it.m11 = f.m11;
+      it.gamma = gamma;
+      it.l = l;
+      it.D = D;
+      it.beta = beta;
+      it.lo = lo;
+      it.u = u;
+      stubs[nstub] = it;
+      tag[nstub] = static_cast<unsigned char>(cls);
+    } else {
+      overflow = true;
+    }
+    ++nstub;
+    c0 += cls == 0;
+    c1 += cls == 1;
+    c2 += cls == 2;
+    c3 += cls == 3;
+  }
+};
+
+__global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
+    k_pipe_emit_slots(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
+                      const int* __restrict__ order, PieceItem* __restrict__ sec_slots,
+                      StubItem* __restrict__ stub_slots, unsigned char* __restrict__ stub_tags,
+                      PieceItem* __restrict__ seg_slots, unsigned* __restrict__ cnt, PairRec* __restrict__ rec,
+                      unsigned long long* counters, unsigned* status_or) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t m = n + 1;
+  if (j >= n) {
+    if (j == n)
+      for (int q = 0; q < kKinds; ++q) cnt[q * m + j] = 0;  // scan tails
+    return;
+  }
+  const int64_t k = order ? order[j] : j;
+  P2 nv[3];
+  int perm[3];
+  load_norm(nrec, k, nv, perm);
+  SlotSink e;
+  e.K = &K;
+  acc_zero(e.acc);
+  e.status = 0;
+  e.pair = static_cast<int>(k);
+  e.has_acc = false;
+  e.overflow = false;
+  e.sec = sec_slots + kCapSec * k;
+  e.seg = seg_slots + kCapSeg * k;
+  e.stubs = stub_slots + kCapStub * k;
+  e.tag = stub_tags + kCapStub * k;
+  e.nsec = e.nseg = e.nstub = e.c0 = e.c1 = e.c2 = e.c3 = 0;
+  e.counters = counters;
+  const bool nondeg_route = integrate_normalized(e, nv);
+  cnt[k] = e.nsec;
+  cnt[m + k] = e.c0;
+  cnt[2 * m + k] = e.c1;
+  cnt[3 * m + k] = e.c2;
+  cnt[4 * m + k] = e.c3;
+  cnt[5 * m + k] = e.nseg;
+  PairRec& r = rec[k];
+  r.nondeg_route = nondeg_route ? 1 : 0;
+  r.has_acc = e.has_acc ? 1 : 0;
+  if (e.has_acc) {
+    AccOut o;
+    acc_to_out(e.acc, o);
+    for (int q = 0; q < 18; ++q) r.acc[q] = o.v[q];
+  }
+  if (e.status) atomicOr(status_or, e.status);
+  if (e.overflow) atomicOr(status_or + 1, 8u);
+}
+
+// dense, pair-ordered index lists (emission order within a pair and class)
+__global__ void __launch_bounds__(256)
+    k_expand(int64_t n, const unsigned long long* __restrict__ off, ulonglong4 stub_base,
+             const unsigned char* __restrict__ stub_tags, int* __restrict__ sec_idx, int* __restrict__ stub_idx,
+             int* __restrict__ seg_idx) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t m = n + 1;
+  {
+    const unsigned long long o = off[k], e = off[k + 1];
+    for (unsigned long long q = o; q < e; ++q) sec_idx[q] = static_cast<int>(kCapSec * k + (q - o));
+  }
+  {
+    const unsigned long long o = off[5 * m + k], e = off[5 * m + k + 1];
+    for (unsigned long long q = o; q < e; ++q) seg_idx[q] = static_cast<int>(kCapSeg * k + (q - o));
+  }
+  unsigned long long pos[4] = {stub_base.x + off[m + k], stub_base.y + off[2 * m + k], stub_base.z + off[3 * m + k],
+                               stub_base.w + off[4 * m + k]};
+  const int nst = static_cast<int>((off[m + k + 1] - off[m + k]) + (off[2 * m + k + 1] - off[2 * m + k]) +
+                                   (off[3 * m + k + 1] - off[3 * m + k]) + (off[4 * m + k + 1] - off[4 * m + k]));
+  for (int q = 0; q < nst; ++q) {
+    const int c = stub_tags[kCapStub * k + q];
+    stub_idx[pos[c]++] = static_cast<int>(kCapStub * k + q);
+  }
+}
+
 // one launch per stub class: warps run one specialised code path
 template <bool F1, int CLS>
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
-                void* __restrict__ out) {
+                const int* __restrict__ idx, void* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const StubItem it = items[k];
+  const StubItem it = items[idx ? idx[k] : k];
   const Frame f{it.m00, it.m01, it.m10, it.m11};
   if constexpr (F1) {
     PairAcc3 a;
@@ -621,12 +795,11 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
 
 template <bool F1>
 __global__ void __launch_bounds__(128)
-    k_pipe_segment(const __grid_constant__ KernelConsts K, const unsigned long long* __restrict__ count,
-                   const PieceItem* __restrict__ items, void* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(*count);  // device-resident item count
+    k_pipe_segment(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+                   const int* __restrict__ idx, void* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const PieceItem it = items[k];
+  const PieceItem it = items[idx ? idx[k] : k];
   const Frame f{it.m00, it.m01, it.m10, it.m11};
   if constexpr (F1) {
     PairAcc3 a;
@@ -1026,19 +1199,18 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   const int64_t m = n + 1;
   if ((st = scratch_t(c, kBufPipeCnt, kKinds * m, &cnt)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPipeOff, kKinds * m, &off)) != SPHBI_OK) return st;
-  unsigned char *cls, *cls_sorted;
   int *iota, *order;
-  if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
-  cls_sorted = cls + m;
   if ((st = scratch_t(c, kBufOrder, 2 * m, &iota)) != SPHBI_OK) return st;
   order = iota + m;
   NormRec* nrec;
+  int* porder;
+  PairRec* rec;
+  if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
   k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, iota);
   if ((st = check_launch(c, "k_iota")) != SPHBI_OK) return st;
-  // count order: pairs grouped by the cheap pre-classification key
+  // canonical normalized vertices + pre-classification key, pairs sorted by key
   {
     unsigned short* pk;
-    int* porder;
     if ((st = scratch_t(c, kBufPreKey, 2 * m, &pk)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufPreOrder, m, &porder)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufNormRec, n, &nrec)) != SPHBI_OK) return st;
@@ -1050,17 +1222,24 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
     cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, pk, pk + m, iota, porder, (int)n, 0, 9, s);
     if ((st = check_launch(c, "radix sort pre-class")) != SPHBI_OK) return st;
+  }
+  const bool two_pass = c->force_exact || c->two_pass;  // after a slot overflow: count + emit
+  PieceItem *isec = nullptr, *iseg = nullptr;
+  StubItem* istub = nullptr;
+  unsigned char* tags = nullptr;
+  if (!two_pass) {
+    if ((st = scratch_t(c, kBufItemsC, kCapSec * n, &isec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufItemsB, kCapStub * n, &istub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufItemsS, kCapSeg * n, &iseg)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufClass, kCapStub * n, &tags)) != SPHBI_OK) return st;
+    k_pipe_emit_slots<<<grid_for(m, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, tags, iseg, cnt, rec, ctr,
+                                                       dflags);
+    if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
+  } else {
+    unsigned char* cls;
+    if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
     k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
     if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
-  }
-  // emit order: pairs grouped by decomposition signature (stable 8-bit radix sort)
-  {
-    size_t tmp_sort = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, cls, cls_sorted, iota, order, (int)n, 0, 8, s);
-    void* dtmp_sort;
-    if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
-    cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, cls, cls_sorted, iota, order, (int)n, 0, 8, s);
-    if ((st = check_launch(c, "radix sort signatures")) != SPHBI_OK) return st;
   }
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
@@ -1070,51 +1249,75 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
     if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
   }
-  // exact item totals (one host sync): buffers and grids sized to fit
+  // exact item totals and the slot-overflow flag (one host sync)
   unsigned long long tot[kKinds];
   {
     unsigned long long* ht = reinterpret_cast<unsigned long long*>(c->h_flags + 8);
     for (int j = 0; j < kKinds; ++j)
       SPHBI_CUDA_TRY(cudaMemcpyAsync(ht + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 24, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     for (int j = 0; j < kKinds; ++j) tot[j] = ht[j];
+    if (!two_pass && (c->h_flags[24] & 8u)) {
+      // a pair exceeded its item slots: redo this chunk with count + emit
+      SPHBI_CUDA_TRY(cudaMemsetAsync(dflags + 1, 0, 4, s));
+      c->force_exact = true;
+      const sphbi_status r = run_pipeline(c, K, h, src, n, mode, stride, dout, dflags, nullptr, ps);
+      c->force_exact = false;
+      return r;
+    }
   }
   unsigned long long sbase[5] = {0, 0, 0, 0, 0};
   for (int cl = 0; cl < 4; ++cl) sbase[cl + 1] = sbase[cl] + tot[1 + cl];
   const ulonglong4 stub_base = make_ulonglong4(sbase[0], sbase[1], sbase[2], sbase[3]);
   const unsigned long long n_sec = tot[0], n_stub = sbase[4], n_seg = tot[5];
-  PieceItem *isec, *iseg;
-  StubItem* istub;
+  int *xsec = nullptr, *xstub = nullptr, *xseg = nullptr;
+  if (!two_pass) {
+    int* xall;
+    if ((st = scratch_t(c, kBufIdx, n_sec + n_stub + n_seg + 1, &xall)) != SPHBI_OK) return st;
+    xsec = xall;
+    xstub = xall + n_sec;
+    xseg = xall + n_sec + n_stub;
+    k_expand<<<grid_for(n, 256), 256, 0, s>>>(n, off, stub_base, tags, xsec, xstub, xseg);
+    if ((st = check_launch(c, "k_expand")) != SPHBI_OK) return st;
+  } else {
+    if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
+    k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder, stub_base,
+                                                 dflags);
+    if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
+  }
   AccOut *osec, *ostub, *oseg;
-  PairRec* rec;
-  if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, order, stub_base, dflags);
-  if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
   // piece kernels, thread per item; stubs one launch per class. A constant
   // field (scene, tri_values == NULL) needs only the tau3 channels.
   const bool f1 = mode == 0 && src.vals == nullptr;
   AccOut3* ostub3 = reinterpret_cast<AccOut3*>(ostub);
-  const StubItem* is[4] = {istub + sbase[0], istub + sbase[1], istub + sbase[2], istub + sbase[3]};
+  // slot path: items stay in their pair slots, the index lists select them;
+  // two-pass path: items are dense per class
+  const StubItem* is[4];
+  const int* ix[4];
+  for (int cl = 0; cl < 4; ++cl) {
+    is[cl] = two_pass ? istub + sbase[cl] : istub;
+    ix[cl] = two_pass ? nullptr : xstub + sbase[cl];
+  }
   if (f1) {
-    if (tot[1]) k_pipe_stub<true, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ostub3 + sbase[0]);
-    if (tot[2]) k_pipe_stub<true, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ostub3 + sbase[1]);
-    if (tot[3]) k_pipe_stub<true, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ostub3 + sbase[2]);
-    if (tot[4]) k_pipe_stub<true, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ostub3 + sbase[3]);
-    if (n_sec) k_pipe_sector<true><<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
-    if (n_seg) k_pipe_segment<true><<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
+    if (tot[1]) k_pipe_stub<true, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ix[0], ostub3 + sbase[0]);
+    if (tot[2]) k_pipe_stub<true, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ix[1], ostub3 + sbase[1]);
+    if (tot[3]) k_pipe_stub<true, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ix[2], ostub3 + sbase[2]);
+    if (tot[4]) k_pipe_stub<true, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ix[3], ostub3 + sbase[3]);
+    if (n_sec) k_pipe_sector<true><<<grid_for(n_sec, 128), 128, 0, s>>>(K, n_sec, isec, xsec, osec);
+    if (n_seg) k_pipe_segment<true><<<grid_for(n_seg, 128), 128, 0, s>>>(K, n_seg, iseg, xseg, oseg);
   } else {
-    if (tot[1]) k_pipe_stub<false, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ostub + sbase[0]);
-    if (tot[2]) k_pipe_stub<false, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ostub + sbase[1]);
-    if (tot[3]) k_pipe_stub<false, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ostub + sbase[2]);
-    if (tot[4]) k_pipe_stub<false, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ostub + sbase[3]);
-    if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, off + n, isec, osec);
-    if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, off + 5 * m + n, iseg, oseg);
+    if (tot[1]) k_pipe_stub<false, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ix[0], ostub + sbase[0]);
+    if (tot[2]) k_pipe_stub<false, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ix[1], ostub + sbase[1]);
+    if (tot[3]) k_pipe_stub<false, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ix[2], ostub + sbase[2]);
+    if (tot[4]) k_pipe_stub<false, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ix[3], ostub + sbase[3]);
+    if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, n_sec, isec, xsec, osec);
+    if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, n_seg, iseg, xseg, oseg);
   }
   if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
   const ItemOuts io{osec, ostub, oseg, stub_base};
@@ -1299,6 +1502,10 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   SPHBI_CUDA_TRY(cudaSetDevice(device));
   sphbi_ctx* c = new sphbi_ctx();
   c->device = device;
+  {
+    const char* tp = std::getenv("SPHBI_TWO_PASS");
+    c->two_pass = tp && tp[0] == '1';
+  }
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return fail(SPHBI_ERR_CUDA, "cudaStreamCreate failed");

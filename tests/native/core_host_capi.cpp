@@ -149,6 +149,42 @@ void core_host_stub_stats(int64_t npairs, const int64_t* pp, const int64_t* pt, 
   }
 }
 
+// per-pair maxima of piece counts by kind (sector, stub classes 0..3, segment)
+struct KindCountSink {
+  static constexpr int kAngles = 2;
+  unsigned status;
+  unsigned n[6];
+  void bump(int) {}
+  void disc(double) {}
+  void half_disc(const Frame&, double) {}
+  void sector(const Frame&, double, double, double) { ++n[0]; }
+  void stub(const Frame&, double, double, double D, double, double lo, double u, bool window, double) {
+    ++n[1 + stub_class(D, lo, u, window)];
+  }
+  void segment(const Frame&, double, double) { ++n[5]; }
+};
+void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
+                        const double* tri6, double h, unsigned* mx) {
+  for (int64_t k = 0; k < npairs; ++k) {
+    const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
+    P2 v[3] = {{tri6[6 * t], tri6[6 * t + 1]}, {tri6[6 * t + 2], tri6[6 * t + 3]}, {tri6[6 * t + 4], tri6[6 * t + 5]}};
+    int perm[3];
+    canonicalize(v, perm);
+    P2 nv[3];
+    for (int j = 0; j < 3; ++j) nv[j] = P2{(v[j].x - pxy[2 * i]) / h, (v[j].y - pxy[2 * i + 1]) / h};
+    KindCountSink s{0u, {0, 0, 0, 0, 0, 0}};
+    integrate_normalized(s, nv);
+    unsigned tot = 0;
+    for (int j = 0; j < 6; ++j) {
+      if (s.n[j] > mx[j]) mx[j] = s.n[j];
+      tot += s.n[j];
+    }
+    if (tot > mx[6]) mx[6] = tot;
+    const unsigned st = s.n[1] + s.n[2] + s.n[3] + s.n[4];
+    if (st > mx[7]) mx[7] = st;
+  }
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 }  // extern "C"

@@ -447,3 +447,38 @@ def test_cfg5_full_scene_16M_particles(S, ctx, O):
         got = np.concatenate([tv[:, None], tg], axis=1)
         want = np.concatenate([wv[:, None], wg], axis=1)
         assert OL.parity_ratio(got, want, ks[0].normalization, sc.h) <= 1.0, name
+
+
+def test_two_pass_pipeline_is_bitwise_identical(S, ctx):
+    """The slot-overflow fallback (count + emit two-pass pipeline, forced with
+    SPHBI_TWO_PASS=1 in a fresh process) gives bit-identical per-particle sums
+    to the default single-pass slot pipeline -- field == 1 and linear field."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2507_21686_b200 import sphbi as S, scenes
+out = {}
+for lin in (False, True):
+    sc = scenes.cfg2(T=4096, per_tri=16, linear_field=lin)
+    k = sc.kernels[0]
+    t = S.table1_terms(S.PolyKernel(k.coefficients, k.normalization))
+    v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, t, tri_values=sc.values, pairs=sc.pairs)
+    out["v%d" % lin] = v
+    out["g%d" % lin] = g
+np.savez(sys.argv[1], **out)
+'''
+    import os
+    import tempfile
+    root = Path(__file__).resolve().parents[1]
+    with tempfile.TemporaryDirectory() as d:
+        res = []
+        for flag in ("0", "1"):
+            f = os.path.join(d, f"r{flag}.npz")
+            env = dict(os.environ, SPHBI_TWO_PASS=flag)
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res.append(np.load(f))
+        for key in res[0].files:
+            assert np.array_equal(res[0][key], res[1][key]), key
