@@ -73,7 +73,7 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 4
 #endif
-constexpr int kMaxChunkPairs = 1 << 23;  // 8 Mi pairs per evaluation chunk (pipeline scratch ~ a few GB)
+constexpr int kMaxChunkPairs = 1 << 22;  // 4 Mi pairs per evaluation chunk (item slots ~2 KB per pair: ~8 GB scratch)
 
 }  // namespace
 
