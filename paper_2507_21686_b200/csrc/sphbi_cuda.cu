@@ -126,6 +126,7 @@ enum ScratchSlot {
   kBufPreOrder,
   kBufNormRec,
   kBufIdx,
+  kBufPartOrder,
   kNumBufs
 };
 
@@ -1119,37 +1120,81 @@ __global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid 
   cell[i] = static_cast<unsigned>(cy * g.nx + cx);
 }
 
-// count (fill == 0) or emit (fill == 1) the pairs of particles [p0, p1)
-__global__ void k_find_pairs(int p0, int p1, const double* __restrict__ pxy,
-                             const unsigned* __restrict__ pcell,
-                             const unsigned long long* __restrict__ cell_start,
-                             const int* __restrict__ cell_tris, const double* __restrict__ tri,
-                             double h2, int fill, unsigned long long* __restrict__ count_or_offset,
-                             long long base, int* __restrict__ pp, int* __restrict__ pt) {
-  const int i = p0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p1) return;
-  const double px = pxy[2 * (int64_t)i], py = pxy[2 * (int64_t)i + 1];
-  const unsigned c = pcell[i];
-  const unsigned long long b = cell_start[c], e = cell_start[c + 1];
-  unsigned long long n = 0;
-  unsigned long long o = fill ? count_or_offset[i] - base : 0;
-  for (unsigned long long k = b; k < e; ++k) {
-    const int t = cell_tris[k];
-    double tv[6];
+// Count (fill == 0) or emit (fill == 1) the pairs of a set of particles.
+// A warp takes 32 particles -- 32 consecutive entries of `order` (particles
+// sorted by cell: neighbouring warps read the same cell lists and triangles
+// from L1/L2) or, with order == NULL, the index range p0 + [32w, 32w + 32).
+// Particles with an empty cell list are done at once; the warp then walks
+// each remaining particle's list with all 32 lanes, 32 candidates at a time
+// (cfg2 mode B: ~15k candidates per particle; cfg3/cfg5: tens). Hits are
+// compacted with a ballot in lane order, so a particle's pairs come out in
+// ascending triangle id (stably sorted cell lists) -- the CPU finder's list.
+constexpr int kFindBlock = 256;
+__global__ void __launch_bounds__(kFindBlock)
+    k_find_pairs(int64_t count, const int* __restrict__ order, int p0, const double* __restrict__ pxy,
+                 const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
+                 const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
+                 unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
+                 int* __restrict__ pt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if ((pos & ~31ll) >= count) return;  // whole warps
+  const bool valid = pos < count;
+  int i = 0;
+  double px = 0.0, py = 0.0;
+  unsigned long long b = 0, e = 0, o = 0;
+  if (valid) {
+    i = order ? order[pos] : p0 + static_cast<int>(pos);
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    px = p.x;
+    py = p.y;
+    const unsigned c = pcell[i];
+    b = cell_start[c];
+    e = cell_start[c + 1];
+    if (fill) o = count_or_offset[i] - base;
+    else if (e == b) count_or_offset[i] = 0;
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, valid && e > b);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const double qx = __shfl_sync(0xffffffffu, px, src), qy = __shfl_sync(0xffffffffu, py, src);
+    const unsigned long long qb = __shfl_sync(0xffffffffu, b, src), qe = __shfl_sync(0xffffffffu, e, src);
+    unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
+    const int qi = __shfl_sync(0xffffffffu, i, src);
+    unsigned long long n = 0;
+    for (unsigned long long k0 = qb; k0 < qe; k0 += 32) {
+      const unsigned long long k = k0 + lane;
+      bool hit = false;
+      int t = 0;
+      if (k < qe) {
+        t = __ldg(cell_tris + k);
+        double tv[6];
 #pragma unroll
-    for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * (int64_t)t + j);
-    if (pair_dist2(px, py, tv) < h2) {
+        for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * (int64_t)t + j);
+        hit = pair_dist2(qx, qy, tv) < h2;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (fill) {
-        pp[o] = i;
-        pt[o] = t;
-        ++o;
+        if (hit) {
+          const unsigned long long q = qo + __popc(m & ((1u << lane) - 1u));
+          pp[q] = qi;
+          pt[q] = t;
+        }
+        qo += __popc(m);
       } else {
-        ++n;
+        n += __popc(m);
       }
     }
+    if (!fill && lane == src) count_or_offset[qi] = n;
   }
-  if (!fill) count_or_offset[i] = n;
 }
+static int find_grid(int64_t count) {
+  return static_cast<int>(((count + 31) / 32 * 32 + kFindBlock - 1) / kFindBlock);
+}
+// pairs held on the device at once by the cell-list path (pp, pt: 8 B each);
+// above this the pairs are found chunk by chunk (particle index ranges)
+constexpr int64_t kMaxResidentPairs = 1ll << 29;
 
 // ---------------------------------------------------------------------------
 // FP64 peak probe: 8 independent DFMA chains per thread
@@ -1919,11 +1964,29 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if ((st = scratch_t(c, kBufPartOffset, n_particles + 1, &poff)) != SPHBI_OK) return st;
     k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
     if ((st = check_launch(c, "k_particle_cell")) != SPHBI_OK) return st;
+    // particles in cell order (the finder walks them so)
+    int* sorder;
+    {
+      unsigned* pcell_sorted;
+      int* piota;
+      if ((st = scratch_t(c, kBufKeysA, n_particles, &pcell_sorted)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufValsA, n_particles, &piota)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPartOrder, n_particles, &sorder)) != SPHBI_OK) return st;
+      k_iota<<<grid_for(n_particles, 256), 256, 0, s>>>((int)n_particles, piota);
+      int bits = 1;
+      while ((1ll << bits) < ncells) ++bits;
+      size_t tmp = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp2, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceRadixSort::SortPairs(dtmp, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
+      if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
+    }
     // K3: count, scan
     const double h2 = h * h;
     const int np = static_cast<int>(n_particles);
-    k_find_pairs<<<grid_for(np, 128), 128, 0, s>>>(0, np, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
-                                                    nullptr, nullptr);
+    k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount,
+                                                      0, nullptr, nullptr);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
@@ -1934,31 +1997,59 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       cub::DeviceScan::ExclusiveSum(dtmp, tmp, pcount, poff, (int)(n_particles + 1), s);
       if ((st = check_launch(c, "scan pair counts")) != SPHBI_OK) return st;
     }
-    std::vector<unsigned long long> hoff(static_cast<size_t>(n_particles) + 1);
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(hoff.data(), poff, 8 * (n_particles + 1), cudaMemcpyDeviceToHost, s));
+    // the total first; the per-particle offsets come to the host only when
+    // the pairs need more than one evaluation chunk (chunk boundaries)
+    unsigned long long* htot = reinterpret_cast<unsigned long long*>(c->h_flags + 32);
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
-    total_pairs = static_cast<int64_t>(hoff[static_cast<size_t>(n_particles)]);
+    total_pairs = static_cast<int64_t>(*htot);
+    std::vector<unsigned long long> hoff;
+    if (total_pairs > kMaxChunkPairs) {
+      hoff.resize(static_cast<size_t>(n_particles) + 1);
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(hoff.data(), poff, 8 * (n_particles + 1), cudaMemcpyDeviceToHost, s));
+      SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    }
     if (timing && total_pairs == 0) {
       cudaEventRecord(c->ev[1], s);
       cudaEventRecord(c->ev[2], s);
+    }
+    // all pairs at once when they fit (one fill pass in cell order), else per chunk
+    const bool resident = total_pairs <= kMaxResidentPairs;
+    int *gpp = nullptr, *gpt = nullptr;
+    if (resident && total_pairs > 0) {
+      if ((st = scratch_t(c, kBufPairP, total_pairs, &gpp)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPairT, total_pairs, &gpt)) != SPHBI_OK) return st;
+      k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff,
+                                                        0, gpp, gpt);
+      if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
     }
     // K4 + K5 in chunks of whole particles
     int p0 = 0;
     int64_t written = 0;
     while (p0 < np) {
       // largest p1 with off[p1] - off[p0] <= budget (at least one particle)
-      const unsigned long long base = hoff[p0];
-      int p1 = static_cast<int>(std::upper_bound(hoff.begin() + p0 + 1, hoff.end(), base + kMaxChunkPairs) -
-                                hoff.begin()) - 1;
-      if (p1 <= p0) p1 = p0 + 1;
-      const int64_t cnt = static_cast<int64_t>(hoff[p1] - base);
+      unsigned long long base = 0;
+      int p1 = np;
+      int64_t cnt = total_pairs;
+      if (!hoff.empty()) {
+        base = hoff[p0];
+        p1 = static_cast<int>(std::upper_bound(hoff.begin() + p0 + 1, hoff.end(), base + kMaxChunkPairs) -
+                              hoff.begin()) - 1;
+        if (p1 <= p0) p1 = p0 + 1;
+        cnt = static_cast<int64_t>(hoff[p1] - base);
+      }
       if (cnt > 0) {
-        if ((st = scratch_t(c, kBufPairP, cnt, &pp)) != SPHBI_OK) return st;
-        if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
         if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
-        k_find_pairs<<<grid_for(p1 - p0, 128), 128, 0, s>>>(p0, p1, dp, pcell, cell_start, vb, dt, h2, 1, poff,
-                                                            (long long)base, pp, pt);
-        if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
+        if (resident) {
+          pp = gpp + base;
+          pt = gpt + base;
+        } else {
+          if ((st = scratch_t(c, kBufPairP, cnt, &pp)) != SPHBI_OK) return st;
+          if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
+          k_find_pairs<<<find_grid(p1 - p0), kFindBlock, 0, s>>>(p1 - p0, nullptr, p0, dp, pcell, cell_start, vb,
+                                                                 dt, h2, 1, poff, (long long)base, pp, pt);
+          if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
+        }
         if (pair_list_out && pair_list_capacity && *pair_list_capacity >= total_pairs) {
           std::vector<int> a(static_cast<size_t>(cnt)), b(static_cast<size_t>(cnt));
           SPHBI_CUDA_TRY(cudaMemcpyAsync(a.data(), pp, 4 * cnt, cudaMemcpyDeviceToHost, s));

@@ -164,7 +164,7 @@ struct KindCountSink {
   void segment(const Frame&, double, double) { ++n[5]; }
 };
 void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
-                        const double* tri6, double h, unsigned* mx) {
+                        const double* tri6, double h, unsigned* mx, unsigned long long* sum) {
   for (int64_t k = 0; k < npairs; ++k) {
     const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
     P2 v[3] = {{tri6[6 * t], tri6[6 * t + 1]}, {tri6[6 * t + 2], tri6[6 * t + 3]}, {tri6[6 * t + 4], tri6[6 * t + 5]}};
@@ -178,6 +178,7 @@ void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, co
     for (int j = 0; j < 6; ++j) {
       if (s.n[j] > mx[j]) mx[j] = s.n[j];
       tot += s.n[j];
+      if (sum) sum[j] += s.n[j];
     }
     if (tot > mx[6]) mx[6] = tot;
     const unsigned st = s.n[1] + s.n[2] + s.n[3] + s.n[4];
