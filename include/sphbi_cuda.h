@@ -20,6 +20,8 @@
  *                              exact distance test)
  *   sphbi_read_counters     <- sphbi::branch_counters / reset_branch_counters
  *                              triangle_integrator.hpp:158-185
+ *   sphbi_bases_create / _apply <- integrate_triangle_bases :828-846 over a scene +
+ *                              gradient_variant_weights :860-894 + combine_basis :706-717
  *
  * Error convention: every call returns a sphbi_status; nothing throws across
  * the ABI. The C++ wrappers map statuses back onto the reference's exception
@@ -173,6 +175,48 @@ sphbi_status sphbi_evaluate_p3(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, 
                                const int64_t* pair_particle, const int64_t* pair_triangle,
                                double* out_value, double* out_grad, int64_t* pair_list_out,
                                int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
+
+/* ---- vertex-basis cache and field sweeps --------------------------------
+ * integrate_triangle_bases (triangle_integrator.hpp:828-846)
+ * over a whole scene, kept on the device, then re-combined for many fields
+ * with the three SPH gradient forms of gradient_variant_weights (:860-894):
+ *   basic:      w_i = A_i
+ *   difference: w_i = rho_i (A_i - a0)
+ *   symmetric:  w_i = rho_i (A_i / rho_i^2 + a0 / rho0^2)
+ * where (A_i, rho_i) are the field / density at vertex i of the triangle and
+ * (a0, rho0) those of the particle. sphbi_bases_apply returns, per particle,
+ *   out_value[p] = sum_t integrate_triangle(p, h, T_t, w(p, t)).value   (t ascending)
+ * and the gradient likewise, without re-running any geometry. */
+typedef enum sphbi_gradient_variant {
+  SPHBI_VARIANT_BASIC = 0,      /* GradientVariant::basic      */
+  SPHBI_VARIANT_DIFFERENCE = 1, /* GradientVariant::difference */
+  SPHBI_VARIANT_SYMMETRIC = 2   /* GradientVariant::symmetric  */
+} sphbi_gradient_variant;
+
+typedef struct sphbi_basis_cache sphbi_basis_cache;
+
+/* Pairing exactly as sphbi_evaluate (n_pairs < 0: device cell list). The cache
+ * holds 72 B per pair on the device and belongs to ctx (destroy it first). */
+sphbi_status sphbi_bases_create(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
+                                int64_t n_particles, const double* particle_xy, int64_t n_triangles,
+                                const double* tri_xy, int64_t n_pairs, const int64_t* pair_particle,
+                                const int64_t* pair_triangle, sphbi_stats* stats, sphbi_memory mem,
+                                sphbi_basis_cache** out);
+sphbi_status sphbi_bases_info(const sphbi_basis_cache* cache, int64_t* n_particles, int64_t* n_triangles,
+                              int64_t* n_pairs);
+/* pair_list: 2 per pair (particle, triangle), sorted; bases: 9 per pair =
+ * (value, grad_x, grad_y) of vertex 0, 1, 2 (original order). Either may be NULL. */
+sphbi_status sphbi_bases_read(const sphbi_basis_cache* cache, int64_t* pair_list, double* bases,
+                              sphbi_memory mem);
+/* tri_values / tri_densities: 3 per triangle; particle_a0 / particle_rho0: 1 per
+ * particle (densities, a0, rho0 may be NULL for the basic variant). A
+ * nonpositive density -> SPHBI_ERR_DOMAIN (std::domain_error). ms_apply
+ * (optional): device time of the re-combination kernel. */
+sphbi_status sphbi_bases_apply(sphbi_basis_cache* cache, int32_t variant, const double* tri_values,
+                               const double* tri_densities, const double* particle_a0,
+                               const double* particle_rho0, double* out_value, double* out_grad,
+                               double* ms_apply, sphbi_memory mem);
+sphbi_status sphbi_bases_destroy(sphbi_basis_cache* cache);
 
 /* ---- measurement utility ----------------------------------------------- */
 /* FP64 (DFMA-pipe) peak of the context's GPU at the current clocks: a

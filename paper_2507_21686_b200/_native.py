@@ -74,6 +74,11 @@ EXPORTED_SYMBOLS = (
     "sphbi_integrate_pairs_p3",
     "sphbi_evaluate_p3",
     "sphbi_measure_fp64_peak",
+    "sphbi_bases_create",
+    "sphbi_bases_info",
+    "sphbi_bases_read",
+    "sphbi_bases_apply",
+    "sphbi_bases_destroy",
 )
 
 _lib = None
@@ -110,6 +115,15 @@ def load() -> ctypes.CDLL:
                                              P, P, P, P, P, ctypes.c_int]
     lib.sphbi_evaluate_p3.argtypes = lib.sphbi_evaluate.argtypes
     lib.sphbi_measure_fp64_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.sphbi_bases_create.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64, P,
+                                       ctypes.c_int64, P, ctypes.c_int64, P, P, ctypes.POINTER(Stats), ctypes.c_int,
+                                       ctypes.POINTER(P)]
+    I64 = ctypes.POINTER(ctypes.c_int64)
+    lib.sphbi_bases_info.argtypes = [P, I64, I64, I64]
+    lib.sphbi_bases_read.argtypes = [P, P, P, ctypes.c_int]
+    lib.sphbi_bases_apply.argtypes = [P, ctypes.c_int32, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.c_int]
+    lib.sphbi_bases_destroy.argtypes = [P]
     _lib = lib
     return lib
 

@@ -692,6 +692,15 @@ SPHBI_HD void acc3_add_region(PairAcc3& a, const S3& S, const Frame& M, double s
   a.g13 = dd_add(a.g13, dd_scale(g3x, sign));
   a.g23 = dd_add(a.g23, dd_scale(g3y, sign));
 }
+// half disc, tau3 channels only (piece_half_disc's S9 restricted to v3, gx3, gy3)
+SPHBI_HD void piece_half_disc3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double sign) {
+  const dd pi{kPiHi, kPiLo};
+  S3 S;
+  S.v3 = dd_mul(K.pv1, pi);
+  S.gx3 = dd_mul_d(K.rg1, 2.0);
+  S.gy3 = dd{0.0, 0.0};
+  acc3_add_region(acc, S, f, sign);
+}
 SPHBI_HD void cone_sums3(double gamma, dd Pv, dd Rg, S3& S) {
   double sg, cg;
   dsincos(gamma, &sg, &cg);

@@ -335,7 +335,7 @@ struct CountSink {
   unsigned long long* counters;
   __device__ void bump(int w) { bump_counter(counters, w); }
   __device__ void disc(double) {}
-  __device__ void half_disc(const Frame&, double) {}
+  __device__ void half_disc(const Frame&, double) { ++n[0]; }  // a tagged sector item
   __device__ void sector(const Frame&, double, double, double) { ++n[0]; }
   __device__ void stub(const Frame&, double, double, double D, double, double lo, double u, bool window, double) {
     ++n[1 + stub_class(D, lo, u, window)];
@@ -346,7 +346,6 @@ struct CountSink {
 struct EmitSink {
   static constexpr int kAngles = 2;
   const KernelConsts* K;
-  PairAcc acc;
   unsigned status;
   int pair;
   PieceItem *sector_items, *seg_items;
@@ -366,14 +365,14 @@ struct EmitSink {
     it.a = a;
     *dst++ = it;
   }
-  bool has_acc;
-  __device__ void disc(double sign) {
-    piece_disc(*K, acc, sign);
-    has_acc = true;
-  }
+  int disc_n;
+  // full discs: only their signed count is kept (kernel constants, combine);
+  // half discs: sector items tagged 1 (evaluated by k_pipe_sector)
+  __device__ void disc(double sign) { disc_n += sign > 0.0 ? 1 : -1; }
   __device__ void half_disc(const Frame& f, double sign) {
-    piece_half_disc(*K, acc, f, sign);
-    has_acc = true;
+    PieceItem* d = sector_items;
+    put(sector_items, f, sign, 0.0);
+    d->pad = 1;
   }
   __device__ void sector(const Frame& f, double gamma, double, double sign) { put(sector_items, f, sign, gamma); }
   __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
@@ -544,8 +543,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const Norm
 // particle frame, so that combine needs no geometry.
 struct PairRec {
   int nondeg_route;  // integrate_normalized did not bail out (non-degenerate)
-  int has_acc;       // acc holds full / half disc contributions (else zero, not written)
-  double acc[18];
+  int disc_n;        // signed count of full unit discs (a kernel constant each)
 };
 
 template <class Src>
@@ -563,7 +561,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   load_norm(nrec, k, nv, perm);
   EmitSink e;
   e.K = &K;
-  acc_zero(e.acc);
+  e.disc_n = 0;
   e.status = 0;
   e.pair = static_cast<int>(k);
   const int64_t m = n + 1;
@@ -573,16 +571,8 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.stub2 = stub_items + stub_base.z + off[3 * m + k];
   e.stub3 = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
-  e.has_acc = false;
   const bool nondeg_route = integrate_normalized(e, nv);
-  PairRec& r = rec[k];
-  r.nondeg_route = nondeg_route ? 1 : 0;
-  r.has_acc = e.has_acc ? 1 : 0;
-  if (e.has_acc) {
-    AccOut o;
-    acc_to_out(e.acc, o);
-    for (int q = 0; q < 18; ++q) r.acc[q] = o.v[q];
-  }
+  rec[k] = PairRec{nondeg_route ? 1 : 0, e.disc_n};
   if (e.status) atomicOr(status_or, e.status);
 }
 
@@ -594,15 +584,22 @@ __global__ void __launch_bounds__(128)
   if (k >= n) return;
   const PieceItem it = items[idx ? idx[k] : k];
   const Frame f{it.m00, it.m01, it.m10, it.m11};
+  // pad == 1: a half disc in frame f (segment_body's |d| < 1e-9 route)
   if constexpr (F1) {
     PairAcc3 a;
     acc3_zero(a);
-    piece_cone3(K, a, f, it.a, 1.0, it.sign);
+    if (it.pad)
+      piece_half_disc3(K, a, f, it.sign);
+    else
+      piece_cone3(K, a, f, it.a, 1.0, it.sign);
     acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
   } else {
     PairAcc a;
     acc_zero(a);
-    piece_cone(K, a, f, it.a, 1.0, it.sign);
+    if (it.pad)
+      piece_half_disc(K, a, f, it.sign);
+    else
+      piece_cone(K, a, f, it.a, 1.0, it.sign);
     acc_to_out(a, static_cast<AccOut*>(out)[k]);
   }
 }
@@ -611,21 +608,21 @@ __global__ void __launch_bounds__(128)
 // Single-pass emission into per-pair slots (the default): the geometry runs
 // once per pair; each pair owns kCapSec / kCapStub / kCapSeg item slots
 // (structural maxima of the decomposition: <= 4 wedges, each with <= 1
-// sector, <= 1 segment and <= 2 stub calls of <= 2 direct stubs), writes its
+// sector and <= 1 half disc, <= 1 segment and <= 2 stub calls of <= 2 direct stubs), writes its
 // per-kind counts, and k_expand turns counts + class tags into dense,
 // pair-ordered index lists for the piece kernels and combine. A pair that
 // would exceed a cap (never seen; 4.5M-pair census in DESIGN.md) sets
 // dflags[1] bit 8 and the chunk is redone with the two-pass count/emit path.
 // ---------------------------------------------------------------------------
-constexpr int kCapSec = 4, kCapStub = 16, kCapSeg = 4;
+constexpr int kCapSec = 8, kCapStub = 16, kCapSeg = 4;  // sector slots also hold half discs
 
 struct SlotSink {
   static constexpr int kAngles = 2;
   const KernelConsts* K;
-  PairAcc acc;
   unsigned status;
   int pair;
-  bool has_acc, overflow;
+  int disc_n;  // signed count of full discs
+  bool overflow;
   PieceItem *sec, *seg;
   StubItem* stubs;
   unsigned char* tag;
@@ -644,13 +641,16 @@ struct SlotSink {
     it.a = a;
     return it;
   }
-  __device__ void disc(double sign) {
-    piece_disc(*K, acc, sign);
-    has_acc = true;
-  }
+  __device__ void disc(double sign) { disc_n += sign > 0.0 ? 1 : -1; }
   __device__ void half_disc(const Frame& f, double sign) {
-    piece_half_disc(*K, acc, f, sign);
-    has_acc = true;
+    if (nsec < kCapSec) {
+      PieceItem it = piece(f, sign, 0.0);
+      it.pad = 1;  // tagged: evaluated as a half disc by k_pipe_sector
+      sec[nsec] = it;
+    } else {
+      overflow = true;
+    }
+    ++nsec;
   }
   __device__ void sector(const Frame& f, double gamma, double, double sign) {
     if (nsec < kCapSec)
@@ -716,10 +716,9 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   load_norm(nrec, k, nv, perm);
   SlotSink e;
   e.K = &K;
-  acc_zero(e.acc);
   e.status = 0;
   e.pair = static_cast<int>(k);
-  e.has_acc = false;
+  e.disc_n = 0;
   e.overflow = false;
   e.sec = sec_slots + kCapSec * k;
   e.seg = seg_slots + kCapSeg * k;
@@ -734,14 +733,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   cnt[3 * m + k] = e.c2;
   cnt[4 * m + k] = e.c3;
   cnt[5 * m + k] = e.nseg;
-  PairRec& r = rec[k];
-  r.nondeg_route = nondeg_route ? 1 : 0;
-  r.has_acc = e.has_acc ? 1 : 0;
-  if (e.has_acc) {
-    AccOut o;
-    acc_to_out(e.acc, o);
-    for (int q = 0; q < 18; ++q) r.acc[q] = o.v[q];
-  }
+  rec[k] = PairRec{nondeg_route ? 1 : 0, e.disc_n};
   if (e.status) atomicOr(status_or, e.status);
   if (e.overflow) atomicOr(status_or + 1, 8u);
 }
@@ -835,11 +827,11 @@ __device__ __forceinline__ void add_item(PairAcc& a, const void* base, unsigned 
   }
 }
 template <bool F1>
-__device__ __forceinline__ void sum_items(PairAcc& a, const PairRec& r, int64_t n, int64_t k,
+__device__ __forceinline__ void sum_items(const KernelConsts& K, PairAcc& a, const PairRec& r, int64_t n, int64_t k,
                                           const unsigned long long* __restrict__ off, const ItemOuts& io) {
   const int64_t m = n + 1;
   acc_zero(a);
-  if (r.has_acc) acc_add_out(a, r.acc);
+  if (r.disc_n) piece_disc(K, a, static_cast<double>(r.disc_n));
   for (unsigned long long j = off[k]; j < off[k + 1]; ++j) add_item<F1>(a, io.sec, j);
   const unsigned long long base[4] = {io.stub_base.x, io.stub_base.y, io.stub_base.z, io.stub_base.w};
 #pragma unroll 1
@@ -888,7 +880,7 @@ __global__ void __launch_bounds__(128)
     }
     if (nondeg) {
       PairAcc a;
-      sum_items<F1>(a, r, n, k, off, io);
+      sum_items<F1>(K, a, r, n, k, off, io);
       double raw[3];
       combine_plane(a, tau1, tau2, tau3, raw);
       finalize(raw, K.c2, h, o);
@@ -897,11 +889,13 @@ __global__ void __launch_bounds__(128)
   for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
 }
 
-// combine, vertex-basis mode: 12 doubles per pair in the original vertex order
+// combine, vertex-basis mode: per pair and vertex i (original order) the
+// finalized (value, grad_x, grad_y[, imag = 0]) of the hat field of vertex i;
+// stride 12 (integrate_triangle_bases' layout) or 9 (basis cache, no imag).
 __global__ void __launch_bounds__(128)
     k_pipe_combine_bases(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
                          double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
-                         ItemOuts io, double* __restrict__ out) {
+                         ItemOuts io, int stride, double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   P2 nv[3];
@@ -913,14 +907,19 @@ __global__ void __launch_bounds__(128)
   HatPlanes H;
   if (r.nondeg_route && hat_planes(nv, H)) {
     PairAcc a;
-    sum_items<false>(a, r, n, k, off, io);
+    sum_items<false>(K, a, r, n, k, off, io);
     for (int i = 0; i < 3; ++i) {
       double raw[3];
       combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
       finalize(raw, K.c2, h, o + 4 * perm[i]);
     }
   }
-  for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
+  if (stride == 12) {
+    for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
+  } else {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) out[9 * k + 3 * i + j] = o[4 * i + j];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -964,6 +963,62 @@ __global__ void k_reduce_rows(int p_begin, int p_count, const int64_t* __restric
   }
   out_v[p_begin + j] = v;
   reinterpret_cast<double2*>(out_g)[p_begin + j] = make_double2(gx, gy);
+}
+
+// ---------------------------------------------------------------------------
+// Basis-cache re-combination (field sweeps): per particle,
+// sum over its cached pairs (ascending triangle id) of
+//   sum_i w_i * basis_i,  w = gradient_variant_weights(variant, a0, rho0, A_t, rho_t)
+// (triangle_integrator.hpp:860-894 weights, :706-717 combine_basis). Thread per
+// particle row; HBM-bound (72 B of cached bases + 4 B triangle id per pair).
+// ---------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(256)
+    k_bases_apply(int np, const int64_t* __restrict__ row_ptr, const int* __restrict__ pt,
+                  const double* __restrict__ B, const double* __restrict__ vals, const double* __restrict__ dens,
+                  const double* __restrict__ a0, const double* __restrict__ rho0, double* __restrict__ ov,
+                  double* __restrict__ og, unsigned* __restrict__ flags) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= np) return;
+  double A0 = 0.0, R0 = 1.0;
+  bool bad = false;
+  if (V != 0) {
+    A0 = a0[j];
+    R0 = rho0[j];
+  } else if (rho0) {
+    R0 = rho0[j];
+  }
+  if (V != 0 || rho0) bad = !(R0 > 0.0);
+  const double r0sq = R0 * R0;
+  double v = 0.0, gx = 0.0, gy = 0.0;
+  const int64_t e = row_ptr[j + 1];
+  for (int64_t k = row_ptr[j]; k < e; ++k) {
+    const int64_t t = pt[k];
+    double w[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double A = __ldg(vals + 3 * t + i);
+      if (dens) {
+        const double rho = __ldg(dens + 3 * t + i);
+        bad |= !(rho > 0.0);
+        if (V == 1)
+          w[i] = rho * (A - A0);
+        else if (V == 2)
+          w[i] = rho * (A / (rho * rho) + A0 / r0sq);
+        else
+          w[i] = A;
+      } else {
+        w[i] = A;
+      }
+    }
+    const double* b = B + 9 * k;
+    v += fma(w[2], b[6], fma(w[1], b[3], w[0] * b[0]));
+    gx += fma(w[2], b[7], fma(w[1], b[4], w[0] * b[1]));
+    gy += fma(w[2], b[8], fma(w[1], b[5], w[0] * b[2]));
+  }
+  if (bad) atomicOr(flags, kStatusDomain);
+  ov[j] = v;
+  reinterpret_cast<double2*>(og)[j] = make_double2(gx, gy);
 }
 
 // ---------------------------------------------------------------------------
@@ -1373,7 +1428,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
       k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
     if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
   } else {
-    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, rec, off, io, dout);
+    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, rec, off, io, stride, dout);
     if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
   }
   (void)ps;
@@ -1721,13 +1776,51 @@ sphbi_status sphbi_integrate_regions(sphbi_ctx* c, const sphbi_kernel_desc* kern
   return SPHBI_OK;
 }
 
+// Device-resident vertex-basis cache of a scene: the
+// pipeline runs once in integrate_triangle_bases mode and keeps, per pair
+// (sorted by particle, then triangle), the three finalized hat-field results;
+// sphbi_bases_apply re-combines them for any field / gradient variant.
+struct sphbi_basis_cache {
+  sphbi_ctx* ctx = nullptr;
+  int64_t n_particles = 0, n_triangles = 0, n_pairs = 0;
+  double h = 0.0;
+  int* pp = nullptr;            // pair particle (int32, sorted)
+  int* pt = nullptr;            // pair triangle
+  int64_t* row_ptr = nullptr;   // n_particles + 1
+  double* bases = nullptr;      // 9 per pair: (value, gx, gy) x vertex 0..2 (original order)
+  double* stage = nullptr;      // host-memory apply staging
+  size_t stage_cap = 0;
+  unsigned* flags = nullptr;
+  sphbi_status reserve(int64_t total) {
+    n_pairs = total;
+    const size_t np = static_cast<size_t>(total > 0 ? total : 1);
+    if (cudaMalloc(&pp, 4 * np) != cudaSuccess || cudaMalloc(&pt, 4 * np) != cudaSuccess ||
+        cudaMalloc(&bases, 72 * np) != cudaSuccess ||
+        cudaMalloc(&row_ptr, 8 * static_cast<size_t>(n_particles + 1)) != cudaSuccess ||
+        cudaMalloc(&flags, 32) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPHBI_ERR_OUT_OF_MEMORY, "basis cache: cudaMalloc failed");
+    }
+    return SPHBI_OK;
+  }
+  void release() {
+    for (void* q : {(void*)pp, (void*)pt, (void*)bases, (void*)row_ptr, (void*)stage, (void*)flags})
+      if (q) cudaFree(q);
+    pp = pt = nullptr;
+    bases = stage = nullptr;
+    row_ptr = nullptr;
+    flags = nullptr;
+  }
+};
+
 // nodal10 != NULL selects the P3 field (10 nodal values per triangle; tri_values ignored).
 static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
                             const double* particle_xy, int64_t n_triangles, const double* tri_xy,
                             const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
                             int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
-                            sphbi_memory mem, const double* nodal10 = nullptr) {
+                            sphbi_memory mem, const double* nodal10 = nullptr,
+                            sphbi_basis_cache* bc = nullptr) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
@@ -1750,7 +1843,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     cudaEventRecord(c->ev[0], s);
   }
   // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
-  if (!p3 && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
+  if (!p3 && !bc && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
@@ -1791,9 +1884,16 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   } else if (nodal10) {
     dv = nodal10;
   }
-  // one chunk of particle-sorted scene pairs -> 3 doubles per pair
+  // one chunk of particle-sorted scene pairs -> 3 doubles per pair (or, for a
+  // basis cache, 9 per pair into the cache at pair offset `at`)
   auto eval_chunk = [&](const int* cpp, const int* cpt, int64_t cnt, double* pout, unsigned* dflags,
-                        unsigned long long* ctr) -> sphbi_status {
+                        unsigned long long* ctr, int64_t at) -> sphbi_status {
+    if (bc) {
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pp + at, cpp, 4 * cnt, cudaMemcpyDeviceToDevice, s));
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pt + at, cpt, 4 * cnt, cudaMemcpyDeviceToDevice, s));
+      const SceneSrc src{cpp, cpt, dp, dt, nullptr};
+      return run_pipeline(c, K, h, src, cnt, 1, 9, bc->bases + 9 * at, dflags, ctr, nullptr);
+    }
     if (p3) {
       const P3SceneSrc src{cpp, cpt, dp, dt, dv};
       k_p3_pairs<<<grid_for(cnt, 128), 128, 0, s>>>(K, *p3, src, cnt, h, 3, pout, dflags, ctr);
@@ -1862,14 +1962,19 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = check_launch(c, "k_unpack_keys")) != SPHBI_OK) return st;
     }
     if (timing) cudaEventRecord(c->ev[1], s);
+    if (bc && (st = bc->reserve(n_pairs)) != SPHBI_OK) return st;
     // evaluate in chunks (ms_eval = first eval launch .. last eval launch; with a
     // single chunk -- every bench workload -- exactly the K4 kernel)
     int64_t done = 0;
     while (done < n_pairs) {
       const int64_t cnt = std::min<int64_t>(n_pairs - done, kMaxChunkPairs);
       if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
-      if ((st = eval_chunk(pp + done, pt + done, cnt, pout, dflags, ctr)) != SPHBI_OK) return st;
+      if ((st = eval_chunk(pp + done, pt + done, cnt, pout, dflags, ctr, done)) != SPHBI_OK) return st;
       if (timing && done + cnt >= n_pairs) cudaEventRecord(c->ev[2], s);
+      if (bc) {
+        done += cnt;
+        continue;
+      }
       // rows: all particles, accumulate (a particle may straddle chunks)
       const int pc = static_cast<int>(n_particles);
       if ((st = scratch_t(c, kBufRowPtr, pc + 1, &row_ptr)) != SPHBI_OK) return st;
@@ -2013,6 +2118,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       cudaEventRecord(c->ev[1], s);
       cudaEventRecord(c->ev[2], s);
     }
+    if (bc && (st = bc->reserve(total_pairs)) != SPHBI_OK) return st;
     // all pairs at once when they fit (one fill pass in cell order), else per chunk
     const bool resident = total_pairs <= kMaxResidentPairs;
     int *gpp = nullptr, *gpt = nullptr;
@@ -2071,8 +2177,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           written += cnt;
         }
         if (timing && p0 == 0) cudaEventRecord(c->ev[1], s);
-        if ((st = eval_chunk(pp, pt, cnt, pout, dflags, ctr)) != SPHBI_OK) return st;
+        if ((st = eval_chunk(pp, pt, cnt, pout, dflags, ctr, static_cast<int64_t>(base))) != SPHBI_OK) return st;
         if (timing && p1 >= np) cudaEventRecord(c->ev[2], s);
+        if (bc) {
+          p0 = p1;
+          continue;
+        }
         if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
         k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp, p0, p1 - p0, row_ptr);
         if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
@@ -2089,6 +2199,11 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     cudaEventRecord(c->ev[3], s);
   }
   if (pair_list_capacity) *pair_list_capacity = total_pairs;
+  if (bc) {
+    if (!bc->pp && (st = bc->reserve(total_pairs)) != SPHBI_OK) return st;
+    k_row_ptr<<<grid_for(total_pairs + 1, 256), 256, 0, s>>>(total_pairs, bc->pp, 0, (int)n_particles, bc->row_ptr);
+    if ((st = check_launch(c, "k_row_ptr(bases)")) != SPHBI_OK) return st;
+  }
   // ---- outputs
   if (mem == SPHBI_MEM_HOST && n_particles) {
     if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, dov, 8 * n_particles, cudaMemcpyDeviceToHost, s));
@@ -2212,6 +2327,155 @@ sphbi_status sphbi_evaluate_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, do
   return evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs, pair_particle,
                        pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats, mem,
                        nodal10 ? nodal10 : &kNoNodes);
+}
+
+// ---- vertex-basis cache + field sweeps -------------
+sphbi_status sphbi_bases_create(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
+                                const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                                int64_t n_pairs, const int64_t* pair_particle, const int64_t* pair_triangle,
+                                sphbi_stats* stats, sphbi_memory mem, sphbi_basis_cache** out) {
+  if (!out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  std::unique_ptr<sphbi_basis_cache> bc(new sphbi_basis_cache);
+  bc->ctx = c;
+  bc->n_particles = n_particles;
+  bc->n_triangles = n_triangles;
+  bc->h = h;
+  const sphbi_status st =
+      evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs, pair_particle,
+                    pair_triangle, nullptr, nullptr, nullptr, nullptr, stats, mem, nullptr, bc.get());
+  if (st != SPHBI_OK) {
+    bc->release();
+    return st;
+  }
+  *out = bc.release();
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_bases_info(const sphbi_basis_cache* bc, int64_t* n_particles, int64_t* n_triangles,
+                              int64_t* n_pairs) {
+  if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
+  if (n_particles) *n_particles = bc->n_particles;
+  if (n_triangles) *n_triangles = bc->n_triangles;
+  if (n_pairs) *n_pairs = bc->n_pairs;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_bases_read(const sphbi_basis_cache* bc, int64_t* pair_list, double* bases, sphbi_memory mem) {
+  if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
+  sphbi_ctx* c = bc->ctx;
+  cudaSetDevice(c->device);
+  const int64_t n = bc->n_pairs;
+  if (n == 0) return SPHBI_OK;
+  const cudaMemcpyKind kind = mem == SPHBI_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (bases) SPHBI_CUDA_TRY(cudaMemcpyAsync(bases, bc->bases, 72 * n, kind, c->stream));
+  if (pair_list) {
+    std::vector<int> a(static_cast<size_t>(n)), b(static_cast<size_t>(n));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(a.data(), bc->pp, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(b.data(), bc->pt, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> il(static_cast<size_t>(2 * n));
+    for (int64_t k = 0; k < n; ++k) {
+      il[static_cast<size_t>(2 * k)] = a[static_cast<size_t>(k)];
+      il[static_cast<size_t>(2 * k + 1)] = b[static_cast<size_t>(k)];
+    }
+    SPHBI_CUDA_TRY(cudaMemcpy(pair_list, il.data(), 16 * n,
+                              mem == SPHBI_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
+  }
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_bases_apply(sphbi_basis_cache* bc, int32_t variant, const double* tri_values,
+                               const double* tri_densities, const double* particle_a0,
+                               const double* particle_rho0, double* out_value, double* out_grad, double* ms_apply,
+                               sphbi_memory mem) {
+  if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
+  if (variant < 0 || variant > 2) return fail(SPHBI_ERR_INVALID_ARGUMENT, "unknown gradient variant");
+  if (bc->n_triangles > 0 && !tri_values) return fail(SPHBI_ERR_INVALID_ARGUMENT, "tri_values is NULL");
+  if (variant != 0 && (!tri_densities || !particle_a0 || !particle_rho0))
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "difference / symmetric variants need densities, a0 and rho0");
+  sphbi_ctx* c = bc->ctx;
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  const int64_t n = bc->n_particles, T = bc->n_triangles;
+  const double *dv = tri_values, *dd_ = tri_densities, *da = particle_a0, *dr = particle_rho0;
+  double *ov = out_value, *og = out_grad;
+  if (mem == SPHBI_MEM_HOST || !out_value || !out_grad) {
+    // staging: [out g 2n (16-B aligned for double2) | values 3T | densities 3T | a0 n | rho0 n | out v n]
+    const size_t need = static_cast<size_t>(6 * T + 5 * n + 1);
+    if (bc->stage_cap < need) {
+      if (bc->stage) cudaFree(bc->stage);
+      bc->stage = nullptr;
+      bc->stage_cap = 0;
+      if (cudaMalloc(&bc->stage, 8 * need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPHBI_ERR_OUT_OF_MEMORY, "basis cache: staging cudaMalloc failed");
+      }
+      bc->stage_cap = need;
+    }
+    double* sg = bc->stage;
+    double* sv = sg + 2 * n;
+    double* sd = sv + 3 * T;
+    double* sa = sd + 3 * T;
+    double* sr = sa + n;
+    double* so = sr + n;
+    if (mem == SPHBI_MEM_HOST) {
+      if (T && tri_values) SPHBI_CUDA_TRY(cudaMemcpyAsync(sv, tri_values, 24 * T, cudaMemcpyHostToDevice, s));
+      if (T && tri_densities) SPHBI_CUDA_TRY(cudaMemcpyAsync(sd, tri_densities, 24 * T, cudaMemcpyHostToDevice, s));
+      if (n && particle_a0) SPHBI_CUDA_TRY(cudaMemcpyAsync(sa, particle_a0, 8 * n, cudaMemcpyHostToDevice, s));
+      if (n && particle_rho0) SPHBI_CUDA_TRY(cudaMemcpyAsync(sr, particle_rho0, 8 * n, cudaMemcpyHostToDevice, s));
+      dv = tri_values ? sv : nullptr;
+      dd_ = tri_densities ? sd : nullptr;
+      da = particle_a0 ? sa : nullptr;
+      dr = particle_rho0 ? sr : nullptr;
+      ov = so;
+      og = sg;
+    } else {
+      if (!out_value) ov = so;
+      if (!out_grad) og = sg;
+    }
+  }
+  SPHBI_CUDA_TRY(cudaMemsetAsync(bc->flags, 0, 8, s));
+  if (ms_apply) cudaEventRecord(c->ev[4], s);
+  if (n > 0) {
+    const int np = static_cast<int>(n);
+    if (variant == 0)
+      k_bases_apply<0><<<grid_for(np, 256), 256, 0, s>>>(np, bc->row_ptr, bc->pt, bc->bases, dv, dd_, da, dr, ov,
+                                                        og, bc->flags);
+    else if (variant == 1)
+      k_bases_apply<1><<<grid_for(np, 256), 256, 0, s>>>(np, bc->row_ptr, bc->pt, bc->bases, dv, dd_, da, dr, ov,
+                                                        og, bc->flags);
+    else
+      k_bases_apply<2><<<grid_for(np, 256), 256, 0, s>>>(np, bc->row_ptr, bc->pt, bc->bases, dv, dd_, da, dr, ov,
+                                                        og, bc->flags);
+    sphbi_status st;
+    if ((st = check_launch(c, "k_bases_apply")) != SPHBI_OK) return st;
+  }
+  if (ms_apply) cudaEventRecord(c->ev[5], s);
+  if (mem == SPHBI_MEM_HOST && n) {
+    if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, ov, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (out_grad) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, og, 16 * n, cudaMemcpyDeviceToHost, s));
+  }
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, bc->flags, 4, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (ms_apply) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+    *ms_apply = ms;
+  }
+  if (c->h_flags[0]) return fail(SPHBI_ERR_DOMAIN, "gradient_variant_weights: nonpositive density");
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_bases_destroy(sphbi_basis_cache* bc) {
+  if (!bc) return SPHBI_OK;
+  cudaSetDevice(bc->ctx->device);
+  cudaStreamSynchronize(bc->ctx->stream);
+  bc->release();
+  delete bc;
+  return SPHBI_OK;
 }
 
 }  // extern "C"

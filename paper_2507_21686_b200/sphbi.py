@@ -588,3 +588,85 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
                                   ip.shape[0], _ptr(ip), _ptr(it), _ptr(out_v), _ptr(out_g), None, None,
                                   ctypes.byref(stats), N.MEM_HOST), "evaluate")
     return out_v, out_g, EvalStats(stats.n_pairs, stats.status_bits, stats.ms_pairs, stats.ms_eval, stats.ms_reduce)
+
+
+# ---------------------------------------------------------------------------
+# vertex-basis cache + field sweeps
+# ---------------------------------------------------------------------------
+_VARIANT_CODE = {"basic": 0, "difference": 1, "symmetric": 2}  # GradientVariant order, :859
+
+
+class BasisCache:
+    """integrate_triangle_bases (triangle_integrator.hpp:828-846) over a whole
+    scene, kept on the device (72 B per pair), re-combined per field with the
+    gradient forms of gradient_variant_weights (:860-894) -- no geometry reruns.
+
+    cache = BasisCache(particles, h, triangles, table[, pairs])
+    v, g = cache.apply("difference", tri_values, tri_densities, a0, rho0)
+    """
+
+    def __init__(self, particles_xy, h: float, tri_xy, table, pairs=None, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        table = _as_table(table)
+        if not (h > 0.0):
+            raise DomainError("integrate_triangle_bases: support h must be > 0")
+        p = np.ascontiguousarray(particles_xy, dtype=np.float64).reshape(-1, 2)
+        t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
+        self.n, self.T = p.shape[0], t.shape[0]
+        stats = N.Stats()
+        desc = table.desc()
+        h_out = ctypes.c_void_p()
+        lib = self.ctx.lib
+        if pairs is None:
+            st = lib.sphbi_bases_create(self.ctx.handle, ctypes.byref(desc), float(h), self.n, _ptr(p), self.T,
+                                        _ptr(t), -1, None, None, ctypes.byref(stats), N.MEM_HOST,
+                                        ctypes.byref(h_out))
+        else:
+            ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
+            it = np.ascontiguousarray(pairs[1], dtype=np.int64)
+            st = lib.sphbi_bases_create(self.ctx.handle, ctypes.byref(desc), float(h), self.n, _ptr(p), self.T,
+                                        _ptr(t), ip.shape[0], _ptr(ip), _ptr(it), ctypes.byref(stats),
+                                        N.MEM_HOST, ctypes.byref(h_out))
+        _raise(st, "bases_create")
+        self.handle = h_out
+        self.stats = EvalStats(stats.n_pairs, stats.status_bits, stats.ms_pairs, stats.ms_eval, stats.ms_reduce)
+        npairs = ctypes.c_int64(0)
+        _raise(lib.sphbi_bases_info(self.handle, None, None, ctypes.byref(npairs)), "bases_info")
+        self.n_pairs = int(npairs.value)
+        self.last_ms = 0.0
+
+    def read(self):
+        """(pair list (m,2) int64, bases (m,3,3): [pair, vertex, (value, gx, gy)])"""
+        pl = np.zeros((max(self.n_pairs, 1), 2), dtype=np.int64)
+        b = np.zeros((max(self.n_pairs, 1), 3, 3), dtype=np.float64)
+        _raise(self.ctx.lib.sphbi_bases_read(self.handle, _ptr(pl), _ptr(b), N.MEM_HOST), "bases_read")
+        return pl[: self.n_pairs], b[: self.n_pairs]
+
+    def apply(self, variant="basic", tri_values=None, tri_densities=None, a0=None, rho0=None):
+        """Per-particle sums of integrate_triangle with the vertex weights
+        gradient_variant_weights(variant, a0[p], rho0[p], tri_values[t], tri_densities[t])."""
+        var = _VARIANT_CODE[variant] if isinstance(variant, str) else int(variant)
+        f64 = lambda a, shape: None if a is None else np.ascontiguousarray(a, dtype=np.float64).reshape(shape)
+        vals = f64(tri_values, (-1, 3))
+        dens = f64(tri_densities, (-1, 3))
+        pa = f64(a0, (-1,))
+        pr = f64(rho0, (-1,))
+        out_v = np.zeros(self.n, dtype=np.float64)
+        out_g = np.zeros((self.n, 2), dtype=np.float64)
+        ms = ctypes.c_double(0.0)
+        _raise(self.ctx.lib.sphbi_bases_apply(self.handle, var, _ptr(vals), _ptr(dens), _ptr(pa), _ptr(pr),
+                                              _ptr(out_v), _ptr(out_g), ctypes.byref(ms), N.MEM_HOST),
+               "bases_apply")
+        self.last_ms = ms.value
+        return out_v, out_g
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.ctx.lib.sphbi_bases_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
