@@ -176,6 +176,25 @@ sphbi_status sphbi_evaluate_p3(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, 
                                double* out_value, double* out_grad, int64_t* pair_list_out,
                                int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
 
+/* ---- piecewise kernels in one pass --------------------------------------
+ * SURVEY.md §8(f) #3 ("extended to piecewise kernel functions ...
+ * through careful evaluation of the integral bounds for each piece"):
+ *   W(r) = sum_j C_j / h_j^2 k_j(r / h_j) [r < h_j],  h_j = scales[j] * h,
+ * scales[0] == 1 >= scales[j] > 0 (e.g. the cubic spline: outer (1-q)^3 at h,
+ * inner -4 (1/2 - q)^3 at h/2). One pair search at h; each inner piece's pairs
+ * are the found pairs passing the exact predicate at h_j (bit-identical to a
+ * separate search at h_j); per-particle sums of all pieces in one reduction:
+ *   out_value[i] = sum_t sum_j integrate_triangle(p_i, h_j, T_t, A_t, table_j).value
+ * Arguments after `h` as sphbi_evaluate; stats->n_pairs counts pair
+ * evaluations over all pieces; pair_list_out receives piece 0's pairs. */
+sphbi_status sphbi_evaluate_piecewise(sphbi_ctx* ctx, int32_t n_pieces, const sphbi_kernel_desc* pieces,
+                                      const double* scales, double h, int64_t n_particles,
+                                      const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                                      const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
+                                      const int64_t* pair_triangle, double* out_value, double* out_grad,
+                                      int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
+                                      sphbi_memory mem);
+
 /* ---- vertex-basis cache and field sweeps --------------------------------
  * integrate_triangle_bases (triangle_integrator.hpp:828-846)
  * over a whole scene, kept on the device, then re-combined for many fields

@@ -74,6 +74,7 @@ EXPORTED_SYMBOLS = (
     "sphbi_integrate_pairs_p3",
     "sphbi_evaluate_p3",
     "sphbi_measure_fp64_peak",
+    "sphbi_evaluate_piecewise",
     "sphbi_bases_create",
     "sphbi_bases_info",
     "sphbi_bases_read",
@@ -115,6 +116,9 @@ def load() -> ctypes.CDLL:
                                              P, P, P, P, P, ctypes.c_int]
     lib.sphbi_evaluate_p3.argtypes = lib.sphbi_evaluate.argtypes
     lib.sphbi_measure_fp64_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.sphbi_evaluate_piecewise.argtypes = [P, ctypes.c_int32, ctypes.POINTER(KernelDesc), P, ctypes.c_double,
+                                             ctypes.c_int64, P, ctypes.c_int64, P, P, ctypes.c_int64, P, P, P, P, P,
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats), ctypes.c_int]
     lib.sphbi_bases_create.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64, P,
                                        ctypes.c_int64, P, ctypes.c_int64, P, P, ctypes.POINTER(Stats), ctypes.c_int,
                                        ctypes.POINTER(P)]

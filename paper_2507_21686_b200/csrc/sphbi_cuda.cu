@@ -127,6 +127,11 @@ enum ScratchSlot {
   kBufNormRec,
   kBufIdx,
   kBufPartOrder,
+  kBufPieceIdx,
+  kBufPiecePP,
+  kBufPiecePT,
+  kBufPieceOut,
+  kBufPieceFlag,
   kNumBufs
 };
 
@@ -1244,6 +1249,68 @@ __global__ void __launch_bounds__(kFindBlock)
     if (!fill && lane == src) count_or_offset[qi] = n;
   }
 }
+// Piecewise kernels: the pairs of an inner piece with
+// support h_j <= h are the chunk's pairs that pass the same exact predicate at
+// h_j (so its pair list is bit-identical to a separate pass at h_j).
+__global__ void k_piece_flags(int64_t n, const int* __restrict__ pp, const int* __restrict__ pt,
+                              const double* __restrict__ pxy, const double* __restrict__ tri, double hj2,
+                              unsigned char* __restrict__ flag) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + pp[k]);
+  double tv[6];
+  const int64_t t = pt[k];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * t + j);
+  flag[k] = pair_dist2(p.x, p.y, tv) < hj2 ? 1 : 0;
+}
+__global__ void k_piece_gather(int64_t m, const int* __restrict__ idx, const int* __restrict__ pp,
+                               const int* __restrict__ pt, int* __restrict__ qp, int* __restrict__ qt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int j = idx[k];
+  qp[k] = pp[j];
+  qt[k] = pt[j];
+}
+// pout[idx[k]] += piece_out[k] (one piece at a time: no write conflicts)
+__global__ void k_piece_add(int64_t m, const int* __restrict__ idx, const double* __restrict__ po,
+                            double* __restrict__ pout) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t j = idx[k];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) pout[3 * j + c] += po[3 * k + c];
+}
+
+// Chunk boundaries of a particle-sorted pair list on the device (greedy:
+// p_{k+1} = largest p with off[p] - off[p_k] <= budget, at least one particle
+// further), so that only the boundaries -- not n_particles offsets -- travel
+// to the host. out[2k] = p_k, out[2k + 1] = off[p_k]; *nchunks = K.
+__global__ void k_chunk_bounds(int np, const unsigned long long* __restrict__ off, unsigned long long budget,
+                               int max_chunks, long long* __restrict__ out, int* __restrict__ nchunks) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int p0 = 0, k = 0;
+  out[0] = 0;
+  out[1] = static_cast<long long>(off[0]);
+  while (p0 < np && k < max_chunks) {
+    const unsigned long long lim = off[p0] + budget;
+    int lo = p0 + 1, hi = np;  // largest p in [p0 + 1, np] with off[p] <= lim (else p0 + 1)
+    if (off[lo] > lim) {
+      hi = lo;
+    } else {
+      while (lo < hi) {
+        const int mid = lo + (hi - lo + 1) / 2;
+        if (off[mid] <= lim) lo = mid; else hi = mid - 1;
+      }
+      hi = lo;
+    }
+    p0 = hi;
+    ++k;
+    out[2 * k] = p0;
+    out[2 * k + 1] = static_cast<long long>(off[p0]);
+  }
+  *nchunks = p0 < np ? -1 : k;
+}
 static int find_grid(int64_t count) {
   return static_cast<int>(((count + 31) / 32 * 32 + kFindBlock - 1) / kFindBlock);
 }
@@ -1813,6 +1880,14 @@ struct sphbi_basis_cache {
   }
 };
 
+// Piecewise kernel: W = sum_j C_j / h_j^2 k_j(r / h_j) [r < h_j], h_j = scale_j h.
+constexpr int kMaxPieces = 4;
+struct PieceSet {
+  int n = 0;
+  KernelConsts K[kMaxPieces];
+  double h[kMaxPieces];
+};
+
 // nodal10 != NULL selects the P3 field (10 nodal values per triangle; tri_values ignored).
 static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
                             const double* particle_xy, int64_t n_triangles, const double* tri_xy,
@@ -1820,15 +1895,19 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
                             int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
                             sphbi_memory mem, const double* nodal10 = nullptr,
-                            sphbi_basis_cache* bc = nullptr) {
+                            sphbi_basis_cache* bc = nullptr, const PieceSet* pieces = nullptr) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
   if (n_particles >= (1ll << 31) || n_triangles >= (1ll << 31))
     return fail(SPHBI_ERR_INVALID_ARGUMENT, "particle / triangle counts must be < 2^31");
   KernelConsts K;
-  sphbi_status st = make_consts(kernel, &K);
-  if (st != SPHBI_OK) return st;
+  sphbi_status st = SPHBI_OK;
+  if (pieces) {
+    K = pieces->K[0];  // piece 0 carries the full support h
+  } else if ((st = make_consts(kernel, &K)) != SPHBI_OK) {
+    return st;
+  }
   std::unique_ptr<P3Consts> p3;
   if (nodal10) {
     p3.reset(new P3Consts);
@@ -1843,7 +1922,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     cudaEventRecord(c->ev[0], s);
   }
   // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
-  if (!p3 && !bc && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
+  if (!p3 && !bc && !pieces && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
@@ -1884,6 +1963,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   } else if (nodal10) {
     dv = nodal10;
   }
+  int64_t piece_pairs = 0;  // inner-piece pair evaluations (piecewise kernels)
   // one chunk of particle-sorted scene pairs -> 3 doubles per pair (or, for a
   // basis cache, 9 per pair into the cache at pair offset `at`)
   auto eval_chunk = [&](const int* cpp, const int* cpt, int64_t cnt, double* pout, unsigned* dflags,
@@ -1900,7 +1980,42 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       return check_launch(c, "k_p3_pairs");
     }
     const SceneSrc src{cpp, cpt, dp, dt, dv};
-    return run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr);
+    if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
+    // inner pieces: the subset of the chunk's pairs within h_j, one pipeline
+    // run each, added per pair (outer + inner) before the per-particle sums
+    for (int j = 1; pieces && j < pieces->n; ++j) {
+      unsigned char* flag;
+      int *idx, *qp, *qt, *dnum;
+      double* po;
+      if ((st = scratch_t(c, kBufPieceFlag, cnt + 16, &flag)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPieceIdx, cnt + 1, &idx)) != SPHBI_OK) return st;
+      dnum = reinterpret_cast<int*>(flag + ((cnt + 3) & ~3ll));
+      k_piece_flags<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, cpp, cpt, dp, dt, pieces->h[j] * pieces->h[j], flag);
+      if ((st = check_launch(c, "k_piece_flags")) != SPHBI_OK) return st;
+      size_t tmp = 0;
+      cub::CountingInputIterator<int> ci(0);
+      cub::DeviceSelect::Flagged(nullptr, tmp, ci, flag, idx, dnum, (int)cnt, s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceSelect::Flagged(dtmp, tmp, ci, flag, idx, dnum, (int)cnt, s);
+      if ((st = check_launch(c, "select piece pairs")) != SPHBI_OK) return st;
+      int m = 0;
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(&m, dnum, 4, cudaMemcpyDeviceToHost, s));
+      SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+      piece_pairs += m;
+      if (m == 0) continue;
+      if ((st = scratch_t(c, kBufPiecePP, m, &qp)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPiecePT, m, &qt)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPieceOut, 3 * (size_t)m, &po)) != SPHBI_OK) return st;
+      k_piece_gather<<<grid_for(m, 256), 256, 0, s>>>(m, idx, cpp, cpt, qp, qt);
+      if ((st = check_launch(c, "k_piece_gather")) != SPHBI_OK) return st;
+      const SceneSrc sj{qp, qt, dp, dt, dv};
+      if ((st = run_pipeline(c, pieces->K[j], pieces->h[j], sj, m, 0, 3, po, dflags, ctr, nullptr)) != SPHBI_OK)
+        return st;
+      k_piece_add<<<grid_for(m, 256), 256, 0, s>>>(m, idx, po, pout);
+      if ((st = check_launch(c, "k_piece_add")) != SPHBI_OK) return st;
+    }
+    return SPHBI_OK;
   };
   if (mem == SPHBI_MEM_HOST || !out_value || !out_grad) {
     double *a, *b;
@@ -2108,11 +2223,22 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     total_pairs = static_cast<int64_t>(*htot);
-    std::vector<unsigned long long> hoff;
+    // chunk boundaries (particle index, pair offset), computed on the device
+    std::vector<long long> cb;
     if (total_pairs > kMaxChunkPairs) {
-      hoff.resize(static_cast<size_t>(n_particles) + 1);
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(hoff.data(), poff, 8 * (n_particles + 1), cudaMemcpyDeviceToHost, s));
+      const int max_chunks = static_cast<int>(std::min<int64_t>(n_particles, 2 * (total_pairs / kMaxChunkPairs) + 8));
+      long long* dbounds;
+      if ((st = scratch_t(c, kBufGeneric0, 2 * (size_t)max_chunks + 4, &dbounds)) != SPHBI_OK) return st;
+      int* dn = reinterpret_cast<int*>(dbounds + 2 * max_chunks + 2);
+      k_chunk_bounds<<<1, 1, 0, s>>>(static_cast<int>(n_particles), poff, kMaxChunkPairs, max_chunks, dbounds, dn);
+      if ((st = check_launch(c, "k_chunk_bounds")) != SPHBI_OK) return st;
+      int nch = 0;
+      cb.resize(2 * (size_t)max_chunks + 2);
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(&nch, dn, 4, cudaMemcpyDeviceToHost, s));
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(cb.data(), dbounds, 8 * cb.size(), cudaMemcpyDeviceToHost, s));
       SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+      if (nch <= 0) return fail(SPHBI_ERR_INTERNAL, "chunk bound computation overflowed");
+      cb.resize(2 * (size_t)nch + 2);
     }
     if (timing && total_pairs == 0) {
       cudaEventRecord(c->ev[1], s);
@@ -2132,17 +2258,17 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // K4 + K5 in chunks of whole particles
     int p0 = 0;
     int64_t written = 0;
+    size_t chunk = 0;
     while (p0 < np) {
-      // largest p1 with off[p1] - off[p0] <= budget (at least one particle)
+      // chunk [p0, p1): off[p1] - off[p0] <= budget (at least one particle)
       unsigned long long base = 0;
       int p1 = np;
       int64_t cnt = total_pairs;
-      if (!hoff.empty()) {
-        base = hoff[p0];
-        p1 = static_cast<int>(std::upper_bound(hoff.begin() + p0 + 1, hoff.end(), base + kMaxChunkPairs) -
-                              hoff.begin()) - 1;
-        if (p1 <= p0) p1 = p0 + 1;
-        cnt = static_cast<int64_t>(hoff[p1] - base);
+      if (!cb.empty()) {
+        base = static_cast<unsigned long long>(cb[2 * chunk + 1]);
+        p1 = static_cast<int>(cb[2 * chunk + 2]);
+        cnt = static_cast<int64_t>(static_cast<unsigned long long>(cb[2 * chunk + 3]) - base);
+        ++chunk;
       }
       if (cnt > 0) {
         if ((st = scratch_t(c, kBufPairOut, 3 * cnt, &pout)) != SPHBI_OK) return st;
@@ -2223,7 +2349,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     stats->ms_pairs = a;
     stats->ms_eval = b;
     stats->ms_reduce = d;
-    stats->n_pairs = total_pairs;
+    stats->n_pairs = total_pairs + piece_pairs;  // pair evaluations over all pieces
     stats->n_candidates = candidates;
     stats->status_bits = c->h_flags[0];
   }
@@ -2476,6 +2602,32 @@ sphbi_status sphbi_bases_destroy(sphbi_basis_cache* bc) {
   bc->release();
   delete bc;
   return SPHBI_OK;
+}
+
+// ---- piecewise kernels in one pass ------------------
+sphbi_status sphbi_evaluate_piecewise(sphbi_ctx* c, int32_t n_pieces, const sphbi_kernel_desc* pieces,
+                                      const double* scales, double h, int64_t n_particles,
+                                      const double* particle_xy, int64_t n_triangles, const double* tri_xy,
+                                      const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
+                                      const int64_t* pair_triangle, double* out_value, double* out_grad,
+                                      int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
+                                      sphbi_memory mem) {
+  if (n_pieces < 1 || n_pieces > kMaxPieces || !pieces || !scales)
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "piecewise kernel: 1..4 pieces with scales");
+  if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
+  if (scales[0] != 1.0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "piecewise kernel: piece 0 must have scale 1");
+  std::unique_ptr<PieceSet> ps(new PieceSet);
+  ps->n = n_pieces;
+  for (int j = 0; j < n_pieces; ++j) {
+    if (!(scales[j] > 0.0 && scales[j] <= 1.0))
+      return fail(SPHBI_ERR_DOMAIN, "piecewise kernel: piece scales must lie in (0, 1]");
+    sphbi_status st = make_consts(pieces + j, &ps->K[j]);
+    if (st != SPHBI_OK) return st;
+    ps->h[j] = scales[j] * h;
+  }
+  return evaluate_impl(c, pieces, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
+                       pair_particle, pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats,
+                       mem, nullptr, nullptr, ps.get());
 }
 
 }  // extern "C"

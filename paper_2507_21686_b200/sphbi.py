@@ -590,6 +590,54 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
     return out_v, out_g, EvalStats(stats.n_pairs, stats.status_bits, stats.ms_pairs, stats.ms_eval, stats.ms_reduce)
 
 
+
+def evaluate_piecewise(particles_xy, h: float, tri_xy, pieces, tri_values=None, pairs=None,
+                       ctx: Context | None = None, return_pairs: bool = False):
+    """One-pass evaluation of a piecewise kernel:
+    pieces = [(table_j, scale_j), ...], scale_0 = 1 >= scale_j > 0; piece j is
+    integrate_triangle(p, scale_j h, T, A, table_j) over the pairs within scale_j h.
+    One pair search at h, per-particle sums of all pieces in one reduction.
+    Returns value (n,), grad (n,2), EvalStats [, piece-0 pair list (m,2) int64]."""
+    ctx = ctx or default_context()
+    if not (h > 0.0):
+        raise DomainError("integrate_triangle: support h must be > 0")
+    npc = len(pieces)
+    descs = (N.KernelDesc * npc)()
+    scales = np.zeros(npc, dtype=np.float64)
+    for j, (tab, sc_) in enumerate(pieces):
+        descs[j] = _as_table(tab).desc()
+        scales[j] = float(sc_)
+    p = np.ascontiguousarray(particles_xy, dtype=np.float64).reshape(-1, 2)
+    t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
+    n, T = p.shape[0], t.shape[0]
+    v = None if tri_values is None else np.ascontiguousarray(tri_values, dtype=np.float64).reshape(-1, 3)
+    out_v = np.zeros(n, dtype=np.float64)
+    out_g = np.zeros((n, 2), dtype=np.float64)
+    stats = N.Stats()
+    cap = ctypes.c_int64(0)
+    fn = ctx.lib.sphbi_evaluate_piecewise
+    if pairs is None:
+        ip = it = None
+        npairs = -1
+    else:
+        ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
+        it = np.ascontiguousarray(pairs[1], dtype=np.int64)
+        npairs = ip.shape[0]
+    plist = None
+    if return_pairs:
+        _raise(fn(ctx.handle, npc, descs, _ptr(scales), float(h), n, _ptr(p), T, _ptr(t), _ptr(v), npairs,
+                  _ptr(ip), _ptr(it), _ptr(out_v), _ptr(out_g), None, ctypes.byref(cap), ctypes.byref(stats),
+                  N.MEM_HOST), "evaluate_piecewise")
+        plist = np.zeros((max(cap.value, 1), 2), dtype=np.int64)
+    _raise(fn(ctx.handle, npc, descs, _ptr(scales), float(h), n, _ptr(p), T, _ptr(t), _ptr(v), npairs,
+              _ptr(ip), _ptr(it), _ptr(out_v), _ptr(out_g), _ptr(plist) if plist is not None else None,
+              ctypes.byref(cap), ctypes.byref(stats), N.MEM_HOST), "evaluate_piecewise")
+    es = EvalStats(stats.n_pairs, stats.status_bits, stats.ms_pairs, stats.ms_eval, stats.ms_reduce)
+    if return_pairs:
+        return out_v, out_g, es, plist[: cap.value]
+    return out_v, out_g, es
+
+
 # ---------------------------------------------------------------------------
 # vertex-basis cache + field sweeps (SURVEY.md §8(f) #1)
 # ---------------------------------------------------------------------------

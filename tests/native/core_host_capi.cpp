@@ -188,4 +188,12 @@ void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, co
 
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
+// region-level evaluation with the device core (sphbi_integrate_regions' math, host build)
+int core_host_eval_region(const double* coef, int ncoef, double c2, int kind, const double* a8,
+                          const double* ref6, double* out9) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
+  return (int)eval_region(K, kind, a8, ref6, out9, nullptr);
+}
+
 }  // extern "C"

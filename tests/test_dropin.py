@@ -33,3 +33,11 @@ def test_reference_kernels_suite():
 def test_reference_triangle_integrator_suite_on_b200():
     out = _run("test_triangle_integrator")
     assert "30/30" in out
+
+
+@pytest.mark.gpu
+def test_batched_cpp_api_on_b200():
+    """sphbi::evaluate / sphbi::BasisSweep (include/sphbi/evaluate.hpp) against
+    per-pair sphbi::integrate_triangle calls of the same headers."""
+    out = _run("test_evaluate_api")
+    assert "2/2" in out

@@ -36,9 +36,15 @@ from paper_2507_21686_b200.sphbi import Context, PolyKernel, _raise, table1_term
 dev = torch.device("cuda", 0)
 
 
-def run_device(ctx, sc, kernel, h, reps, pairs=None, repeat=1):
-    """Device-resident evaluation; returns dict of best-of-reps timings."""
+def run_device(ctx, sc, kernel, h, reps, pairs=None, repeat=1, pieces=None):
+    """Device-resident evaluation; returns dict of best-of-reps timings.
+    pieces: list of KernelSpec -> one-pass piecewise evaluation (sphbi_evaluate_piecewise)."""
     desc = table1_terms(PolyKernel(list(kernel.coefficients), kernel.normalization)).desc()
+    if pieces is not None:
+        descs = (N.KernelDesc * len(pieces))()
+        for j, kk in enumerate(pieces):
+            descs[j] = table1_terms(PolyKernel(list(kk.coefficients), kk.normalization)).desc()
+        scales = np.array([kk.support_scale for kk in pieces], dtype=np.float64)
     p = torch.from_numpy(np.ascontiguousarray(sc.particles)).to(dev)
     t = torch.from_numpy(np.ascontiguousarray(sc.triangles)).to(dev)
     vals = None
@@ -63,10 +69,18 @@ def run_device(ctx, sc, kernel, h, reps, pairs=None, repeat=1):
         t0 = time.perf_counter()
         tot = [0.0, 0.0, 0.0]
         for _ in range(repeat):
-            _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, vp(p.data_ptr()), T, vp(t.data_ptr()),
-                      vp(vals.data_ptr()) if vals is not None else None, npairs,
-                      vp(ip.data_ptr()) if ip is not None else None, vp(it.data_ptr()) if it is not None else None,
-                      vp(ov.data_ptr()), vp(og.data_ptr()), None, None, ctypes.byref(st), N.MEM_DEVICE))
+            if pieces is not None:
+                _raise(ctx.lib.sphbi_evaluate_piecewise(
+                    ctx.handle, len(pieces), descs, vp(scales.ctypes.data), float(h), n, vp(p.data_ptr()), T,
+                    vp(t.data_ptr()), vp(vals.data_ptr()) if vals is not None else None, npairs,
+                    vp(ip.data_ptr()) if ip is not None else None, vp(it.data_ptr()) if it is not None else None,
+                    vp(ov.data_ptr()), vp(og.data_ptr()), None, None, ctypes.byref(st), N.MEM_DEVICE))
+            else:
+                _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, vp(p.data_ptr()), T, vp(t.data_ptr()),
+                          vp(vals.data_ptr()) if vals is not None else None, npairs,
+                          vp(ip.data_ptr()) if ip is not None else None,
+                          vp(it.data_ptr()) if it is not None else None,
+                          vp(ov.data_ptr()), vp(og.data_ptr()), None, None, ctypes.byref(st), N.MEM_DEVICE))
             tot[0] += st.ms_pairs
             tot[1] += st.ms_eval
             tot[2] += st.ms_reduce
@@ -80,6 +94,59 @@ def run_device(ctx, sc, kernel, h, reps, pairs=None, repeat=1):
                 best["ms_pairs"] + best["ms_eval"] + best["ms_reduce"]:
             best = rec
     return best
+
+
+def run_sweep(ctx, sc, kernel, h, reps, pairs=None, variant=1):
+    """Vertex-basis cache (sphbi_bases_create) + field sweeps (sphbi_bases_apply,
+    difference variant) with device-resident inputs; the apply kernel is
+    HBM-bound: algorithmic bytes = 76 per pair (9 cached doubles + triangle id)
+    + 40 per particle (row pointer, a0, rho0, value, gradient) + 48 per triangle."""
+    desc = table1_terms(PolyKernel(list(kernel.coefficients), kernel.normalization)).desc()
+    vp = ctypes.c_void_p
+    p = torch.from_numpy(np.ascontiguousarray(sc.particles)).to(dev)
+    t = torch.from_numpy(np.ascontiguousarray(sc.triangles)).to(dev)
+    n, T = p.shape[0], t.shape[0]
+    ip = it = None
+    npairs = -1
+    if pairs is not None:
+        ip = torch.from_numpy(np.ascontiguousarray(pairs[0], dtype=np.int64)).to(dev)
+        it = torch.from_numpy(np.ascontiguousarray(pairs[1], dtype=np.int64)).to(dev)
+        npairs = ip.shape[0]
+    st = N.Stats()
+    cache = vp()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _raise(ctx.lib.sphbi_bases_create(ctx.handle, ctypes.byref(desc), float(h), n, vp(p.data_ptr()), T,
+                                      vp(t.data_ptr()), npairs, vp(ip.data_ptr()) if ip is not None else None,
+                                      vp(it.data_ptr()) if it is not None else None, ctypes.byref(st),
+                                      N.MEM_DEVICE, ctypes.byref(cache)), "bases_create")
+    torch.cuda.synchronize()
+    create_ms = (time.perf_counter() - t0) * 1e3
+    m = ctypes.c_int64(0)
+    ctx.lib.sphbi_bases_info(cache, None, None, ctypes.byref(m))
+    g = torch.Generator(device="cpu").manual_seed(5)
+    A = torch.randn((T, 3), generator=g, dtype=torch.float64).to(dev)
+    rho = (0.5 + 1.5 * torch.rand((T, 3), generator=g, dtype=torch.float64)).to(dev)
+    a0 = torch.randn(n, generator=g, dtype=torch.float64).to(dev)
+    rho0 = (0.5 + 1.5 * torch.rand(n, generator=g, dtype=torch.float64)).to(dev)
+    ov = torch.empty(n, dtype=torch.float64, device=dev)
+    og = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    best = None
+    for r in range(reps + 2):
+        flush.fill_(float(r))  # L2 flush between sweeps
+        ms = ctypes.c_double(0.0)
+        _raise(ctx.lib.sphbi_bases_apply(cache, variant, vp(A.data_ptr()), vp(rho.data_ptr()), vp(a0.data_ptr()),
+                                         vp(rho0.data_ptr()), vp(ov.data_ptr()), vp(og.data_ptr()),
+                                         ctypes.byref(ms), N.MEM_DEVICE), "bases_apply")
+        if r >= 1 and (best is None or ms.value < best):
+            best = ms.value
+    ctx.lib.sphbi_bases_destroy(cache)
+    mp = int(m.value)
+    algo = 76.0 * mp + 40.0 * n + 48.0 * T
+    return {"pairs": mp, "ms_create_wall": create_ms, "ms_create_eval": st.ms_eval, "ms_apply": best,
+            "sweep_pair_evals_per_s": mp / (best * 1e-3), "apply_GBps_algorithmic": algo / (best * 1e-3) / 1e9,
+            "apply_bytes_algorithmic": algo}
 
 
 def cpu_rate(sc, kernel, h, pairs, sample):
@@ -119,7 +186,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--cpu", action="store_true")
-    ap.add_argument("--configs", default="cfg1,cfg2A,cfg2B,cfg3,cfg4,cfg5_c2,cfg5_cubic")
+    ap.add_argument("--configs", default="cfg1,cfg2A,cfg2B,cfg3,cfg4,cfg5_c2,cfg5_cubic,cfg5_cubic_1pass,cfg2A_sweep,cfg5_sweep")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     ctx = Context(0)
@@ -153,17 +220,43 @@ def main():
             k = sc.kernels[0]
             r = run_device(ctx, sc, k, sc.h, a.reps)
             note = "device cell list over all particles; P3 field" if name == "cfg4" else "device cell list"
-        elif name.startswith("cfg5"):
+        elif name.startswith("cfg5") and not name.endswith("_sweep"):
             if cfg5 is None:
                 cfg5 = scenes.cfg5()
             sc = cfg5
             ks = [sc.kernels[0]] if name == "cfg5_c2" else sc.kernels[1:]
-            rs = [run_device(ctx, sc, kk, sc.h * kk.support_scale, a.reps) for kk in ks]
-            r = {key: sum(x[key] for x in rs) for key in rs[0]}
-            r["pairs"] = sum(x["pairs"] for x in rs)
+            if name == "cfg5_cubic_1pass":
+                r = run_device(ctx, sc, ks[0], sc.h, a.reps, pieces=ks)
+                note = ("cubic spline in one pass (sphbi_evaluate_piecewise): one pair search at h, "
+                        "inner piece on the pairs within h/2, one reduction; pairs = evaluations of both pieces")
+            else:
+                rs = [run_device(ctx, sc, kk, sc.h * kk.support_scale, a.reps) for kk in ks]
+                r = {key: sum(x[key] for x in rs) for key in rs[0]}
+                r["pairs"] = sum(x["pairs"] for x in rs)
+                note = ("Wendland C2, h = 0.1" if name == "cfg5_c2" else
+                        "cubic spline as outer (h) + inner (h/2) passes; pairs summed over both passes")
             k = ks[0]
-            note = ("Wendland C2, h = 0.1" if name == "cfg5_c2" else
-                    "cubic spline as outer (h) + inner (h/2) passes; pairs summed over both passes")
+        elif name.endswith("_sweep"):
+            base = name[: -len("_sweep")]
+            if base == "cfg2A":
+                sc = scenes.cfg2()
+                pr = sc.pairs
+            elif base == "cfg5":
+                if cfg5 is None:
+                    cfg5 = scenes.cfg5()
+                sc, pr = cfg5, None
+            else:
+                raise SystemExit(f"unknown sweep config {name}")
+            k = sc.kernels[0]
+            r = run_sweep(ctx, sc, k, sc.h, a.reps, pairs=pr)
+            row = {"config": name, "particles": int(sc.particles.shape[0]), "triangles": int(sc.triangles.shape[0]),
+                   "kernel": k.name, "h": sc.h, **r,
+                   "note": "basis cache built once (integrate_triangle_bases per pair), then field sweeps "
+                           "(difference variant) re-combining cached bases; best of reps, L2 flushed"}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+            print(f"  [{name} took {time.time() - t0:.1f} s]", file=sys.stderr, flush=True)
+            continue
         else:
             raise SystemExit(f"unknown config {name}")
         dev_ms = r["ms_pairs"] + r["ms_eval"] + r["ms_reduce"]
