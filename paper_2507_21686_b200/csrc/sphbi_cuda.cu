@@ -228,53 +228,6 @@ __global__ void __launch_bounds__(kEvalBlock)
 }
 
 // ---------------------------------------------------------------------------
-// K4 for P3 (10-node cubic Lagrange) fields, BASELINE configs[3]
-// ---------------------------------------------------------------------------
-// Thread per pair, everything inlined through the shared decomposition with a
-// P3Sink (sphbi_p3.cuh). cfg4 has ~2.4e5 pairs per 4M particles, so the
-// affine path's divergence-aware work-item pipeline is not needed here.
-struct P3SceneSrc {
-  const int* pp;
-  const int* pt;
-  const double* pxy;
-  const double* tri;
-  const double* nodes;  // 10 per triangle
-  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* n10) const {
-    const int i = pp[k], t = pt[k];
-    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
-    qx = p.x;
-    qy = p.y;
-    for (int j = 0; j < 6; ++j) t6[j] = __ldg(tri + 6 * (int64_t)t + j);
-    for (int j = 0; j < 10; ++j) n10[j] = __ldg(nodes + 10 * (int64_t)t + j);
-  }
-};
-struct P3DirectSrc {
-  const double* q;
-  const double* tri;
-  const double* nodes;
-  __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* n10) const {
-    qx = q[2 * k];
-    qy = q[2 * k + 1];
-    for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
-    for (int j = 0; j < 10; ++j) n10[j] = nodes[10 * k + j];
-  }
-};
-
-template <class Src>
-__global__ void __launch_bounds__(128)
-    k_p3_pairs(const __grid_constant__ KernelConsts K, const __grid_constant__ P3Consts P, Src src, int64_t n,
-               double h, int stride, double* __restrict__ out, unsigned* __restrict__ status_or,
-               unsigned long long* counters) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double qx, qy, t6[6], n10[10], o[4];
-  src.load(k, qx, qy, t6, n10);
-  const unsigned st = eval_pair_p3(K, P, qx, qy, h, t6, n10, o, counters);
-  if (st) atomicOr(status_or, st);
-  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
-}
-
-// ---------------------------------------------------------------------------
 // K4 as a work-item pipeline (divergence-aware evaluation)
 // ---------------------------------------------------------------------------
 // A thread-per-pair kernel diverges badly (a pair decomposes into 1..~20
@@ -928,6 +881,125 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---------------------------------------------------------------------------
+// K4 for P3 (10-node cubic) fields on the same work-item pipeline: the
+// geometry passes (pre-class, emit) are field-agnostic; the piece kernels
+// evaluate the 24 harmonic sums of sphbi_p3.cuh per item (rotated to the
+// particle frame), and the P3 combine adds a pair's items, builds the cubic
+// field polynomial from its 10 nodal values and contracts.
+// ---------------------------------------------------------------------------
+struct H24Out {
+  double v[2 * kP3Sums];
+};
+__device__ __forceinline__ void h24_store(const H24& H, H24Out& o) {
+#pragma unroll
+  for (int i = 0; i < kP3Sums; ++i) {
+    o.v[2 * i] = H.c[i].hi;
+    o.v[2 * i + 1] = H.c[i].lo;
+  }
+}
+__global__ void __launch_bounds__(128)
+    k_p3_sector(const __grid_constant__ P3Consts P, int64_t n, const PieceItem* __restrict__ items,
+                const int* __restrict__ idx, H24Out* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PieceItem it = items[idx ? idx[k] : k];
+  H24 H, acc;
+  if (it.pad)
+    h24_half_disc(P, H);
+  else
+    h24_cone(P, it.a, 1.0, H);
+  h24_zero(acc);
+  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+  h24_store(acc, out[k]);
+}
+__global__ void __launch_bounds__(128)
+    k_p3_stub(const __grid_constant__ P3Consts P, int64_t n, const StubItem* __restrict__ items,
+              const int* __restrict__ idx, H24Out* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const StubItem it = items[idx ? idx[k] : k];
+  H24 H, acc;
+  h24_cone(P, it.gamma, it.l, H);
+  if (it.window) {
+    h24_stub_bound(P, it.u, it.D, it.beta, 1.0, H);
+    h24_stub_bound(P, it.lo, it.D, it.beta, -1.0, H);
+  }
+  h24_zero(acc);
+  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+  h24_store(acc, out[k]);
+}
+__global__ void __launch_bounds__(128)
+    k_p3_segment(const __grid_constant__ P3Consts P, int64_t n, const PieceItem* __restrict__ items,
+                 const int* __restrict__ idx, H24Out* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PieceItem it = items[idx ? idx[k] : k];
+  H24 H, acc;
+  h24_segment(P, it.a, H);
+  h24_zero(acc);
+  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+  h24_store(acc, out[k]);
+}
+__device__ __forceinline__ void h24_add_out(H24& a, const H24Out& o) {
+#pragma unroll
+  for (int i = 0; i < kP3Sums; ++i) a.c[i] = dd_add(a.c[i], dd{o.v[2 * i], o.v[2 * i + 1]});
+}
+// nodes: 10 per triangle; pt (scene) maps pair -> triangle, NULL: 10 per pair
+__global__ void __launch_bounds__(128)
+    k_p3_combine(const __grid_constant__ KernelConsts K, const __grid_constant__ P3Consts P,
+                 const NormRec* __restrict__ nrec, int64_t n, double h, const PairRec* __restrict__ rec,
+                 const unsigned long long* __restrict__ off, const H24Out* __restrict__ osec,
+                 const H24Out* __restrict__ ostub, const H24Out* __restrict__ oseg, ulonglong4 stub_base,
+                 const double* __restrict__ nodes, const int* __restrict__ pt, int stride,
+                 double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PairRec r = rec[k];
+  double o[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r.nondeg_route) {
+    P2 nv[3], nvo[3];
+    int perm[3];
+    load_norm(nrec, k, nv, perm);
+    for (int i = 0; i < 3; ++i) nvo[perm[i]] = nv[i];  // eval_pair_p3's original-order vertices, bitwise
+    H24 acc;
+    h24_zero(acc);
+    if (r.disc_n) {
+      H24 Hd;
+      h24_disc(P, Hd);
+      h24_accumulate(acc, Hd, Frame{1.0, 0.0, 0.0, 1.0}, static_cast<double>(r.disc_n));
+    }
+    const int64_t m = n + 1;
+    for (unsigned long long j = off[k]; j < off[k + 1]; ++j) h24_add_out(acc, osec[j]);
+    const unsigned long long base[4] = {stub_base.x, stub_base.y, stub_base.z, stub_base.w};
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      const unsigned long long* oc = off + (1 + c) * m;
+      for (unsigned long long j = oc[k]; j < oc[k + 1]; ++j) h24_add_out(acc, ostub[base[c] + j]);
+    }
+    for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) h24_add_out(acc, oseg[j]);
+    // nodal values straight from global memory (a local copy passed by pointer
+    // was clobbered by the callee's frame with nvcc 12.9)
+    const double* n10 = nodes + 10 * (pt ? static_cast<int64_t>(pt[k]) : k);
+    Poly3 A;
+    if (p3_field_poly(nvo, n10, A)) {
+      double raw[3];
+      p3_combine(P, acc, A, raw);
+      finalize(raw, K.c2, h, o);
+#ifdef SPHBI_DEBUG_P3
+      printf("k=%lld disc_n=%d deg=%d pc1=%g acc0=%g A0=%g raw=%g %g %g c2=%g nsec=%llu\n", (long long)k, r.disc_n,
+             P.deg, P.pc1[0][1].hi, acc.c[0].hi, A.c[0].hi, raw[0], raw[1], raw[2], K.c2, off[k + 1] - off[k]);
+      printf("nvo %g %g %g %g %g %g perm %d %d %d n10 %g %g %g %g %g %g %g %g %g %g\n", nvo[0].x, nvo[0].y, nvo[1].x,
+             nvo[1].y, nvo[2].x, nvo[2].y, perm[0], perm[1], perm[2], n10[0], n10[1], n10[2], n10[3], n10[4], n10[5],
+             n10[6], n10[7], n10[8], n10[9]);
+      for (int q = 0; q < 10; ++q) printf("A[%d]=%g ", q, A.c[q].hi);
+      printf("\n");
+#endif
+    }
+  }
+  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
+}
+
+// ---------------------------------------------------------------------------
 // K5: per-particle fixed-order reduction (pairs sorted by particle, then
 // triangle id), vectorised double2 gradient stores.
 // ---------------------------------------------------------------------------
@@ -1355,9 +1427,16 @@ struct PipeStats {
 // grids exactly. (A sync-free variant with per-pair capacity bounds and
 // device-resident counts was measured slower on the B200: over-sized grids
 // cost more than the sync.)
+// mode 0: field / field == 1; 1: vertex bases; 3: P3 field (p3 != NULL)
+struct P3Job {
+  const P3Consts* P;
+  const double* nodes;  // 10 per triangle (scene: indexed by pt) or per pair
+  const int* pt;        // scene pair -> triangle; NULL: nodes are per pair
+};
 template <class Src>
 sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
-                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps) {
+                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
+                          const P3Job* p3 = nullptr) {
   if (n <= 0) return SPHBI_OK;
   cudaStream_t s = c->stream;
   sphbi_status st;
@@ -1429,7 +1508,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
       // a pair exceeded its item slots: redo this chunk with count + emit
       SPHBI_CUDA_TRY(cudaMemsetAsync(dflags + 1, 0, 4, s));
       c->force_exact = true;
-      const sphbi_status r = run_pipeline(c, K, h, src, n, mode, stride, dout, dflags, nullptr, ps);
+      const sphbi_status r = run_pipeline(c, K, h, src, n, mode, stride, dout, dflags, nullptr, ps, p3);
       c->force_exact = false;
       return r;
     }
@@ -1454,6 +1533,22 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder, stub_base,
                                                  dflags);
     if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
+  }
+  if (mode == 3) {
+    // P3 field: one launch per piece kind (stub classes share one code path)
+    H24Out *qsec, *qstub, *qseg;
+    if ((st = scratch_t(c, kBufOutC, n_sec, &qsec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutB, n_stub, &qstub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutS, n_seg, &qseg)) != SPHBI_OK) return st;
+    const P3Consts& P = *p3->P;
+    if (n_stub) k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, n_stub, istub, two_pass ? nullptr : xstub, qstub);
+    if (n_sec) k_p3_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(P, n_sec, isec, xsec, qsec);
+    if (n_seg) k_p3_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(P, n_seg, iseg, xseg, qseg);
+    if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
+    k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, rec, off, qsec, qstub, qseg, stub_base, p3->nodes,
+                                                  p3->pt, stride, dout);
+    (void)ps;
+    return check_launch(c, "k_p3_combine");
   }
   AccOut *osec, *ostub, *oseg;
   if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
@@ -1975,9 +2070,9 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       return run_pipeline(c, K, h, src, cnt, 1, 9, bc->bases + 9 * at, dflags, ctr, nullptr);
     }
     if (p3) {
-      const P3SceneSrc src{cpp, cpt, dp, dt, dv};
-      k_p3_pairs<<<grid_for(cnt, 128), 128, 0, s>>>(K, *p3, src, cnt, h, 3, pout, dflags, ctr);
-      return check_launch(c, "k_p3_pairs");
+      const SceneSrc src{cpp, cpt, dp, dt, nullptr};  // geometry only; the field enters in k_p3_combine
+      const P3Job job{p3.get(), dv, cpt};
+      return run_pipeline(c, K, h, src, cnt, 3, 3, pout, dflags, ctr, nullptr, &job);
     }
     const SceneSrc src{cpp, cpt, dp, dt, dv};
     if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
@@ -2430,10 +2525,13 @@ sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* ker
     dout = o;
   }
   SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, s));
-  const P3DirectSrc src{dq, dt, dn};
-  k_p3_pairs<<<grid_for(n, 128), 128, 0, s>>>(K, *P, src, n, h, 4, dout, dflags,
-                                              c->counters_on ? c->d_counters : nullptr);
-  if ((st = check_launch(c, "k_p3_pairs")) != SPHBI_OK) return st;
+  {
+    const DirectSrc src{dq, dt, nullptr};  // geometry only; the field enters in k_p3_combine
+    const P3Job job{P.get(), dn, nullptr};
+    if ((st = run_pipeline(c, K, h, src, n, 3, 4, dout, dflags, c->counters_on ? c->d_counters : nullptr, nullptr,
+                           &job)) != SPHBI_OK)
+      return st;
+  }
   SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
   if (mem == SPHBI_MEM_HOST) SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
