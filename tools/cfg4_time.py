@@ -8,7 +8,8 @@ sc = scenes.cfg4()
 k = sc.kernels[0]
 table = S.table1_terms(S.PolyKernel(list(k.coefficients), k.normalization))
 ctx = S.Context(0)
-for it in range(4):
+import os
+for it in range(int(os.environ.get("REPS", "4"))):
     t0 = time.time()
     v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, table, tri_values=sc.values, ctx=ctx)
     t1 = time.time()
