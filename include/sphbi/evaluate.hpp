@@ -157,6 +157,32 @@ class BasisSweep {
     return out;
   }
 
+  // SPH coupling (PAPER.md Appendix): per-pair constant
+  // fields w (cache pair order; empty = 1) summed per particle.
+  std::vector<IntegralResult> apply_pairs(const std::vector<double>& pair_weights = {}) {
+    if (!pair_weights.empty() && static_cast<std::int64_t>(pair_weights.size()) != pair_count())
+      throw std::invalid_argument("BasisSweep::apply_pairs: one weight per cached pair");
+    std::vector<double> value(n_), grad(2 * n_);
+    detail::check(sphbi_bases_apply_pairs(cache_, pair_weights.empty() ? nullptr : pair_weights.data(), value.data(),
+                                          grad.data(), SPHBI_MEM_HOST));
+    std::vector<IntegralResult> out(n_);
+    for (std::size_t i = 0; i < n_; ++i) {
+      out[i].value = value[i];
+      out[i].gradient = {grad[2 * i], grad[2 * i + 1]};
+    }
+    return out;
+  }
+
+  // boundary_normal: -n/|n|, n = sum_T int grad W (field 1), pointing into
+  // the fluid; the zero vector when |n| <= 1e-12.
+  std::vector<Point2> boundary_normals() {
+    std::vector<double> nrm(2 * n_);
+    detail::check(sphbi_boundary_normals(cache_, nrm.data(), SPHBI_MEM_HOST));
+    std::vector<Point2> out(n_);
+    for (std::size_t i = 0; i < n_; ++i) out[i] = Point2{nrm[2 * i], nrm[2 * i + 1]};
+    return out;
+  }
+
  private:
   std::size_t n_, T_;
   sphbi_basis_cache* cache_ = nullptr;

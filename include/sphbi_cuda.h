@@ -237,6 +237,21 @@ sphbi_status sphbi_bases_apply(sphbi_basis_cache* cache, int32_t variant, const 
                                double* ms_apply, sphbi_memory mem);
 sphbi_status sphbi_bases_destroy(sphbi_basis_cache* cache);
 
+/* ---- SPH coupling consumers (PAPER.md Appendix,
+ * SPEC.md:669-685). No reference interface: the reference ships no SPH
+ * coupling; SPEC.md specifies boundary_normal and
+ * boundary_pressure_acceleration on top of integrate_triangle.
+ * sphbi_bases_apply_pairs: per-pair constant fields w_k (cache pair order, as
+ * sphbi_bases_read lists them; NULL = 1):
+ *   out_value[p] = sum_k w_k integrate_triangle(p, h, T_k).value, grad likewise
+ * (the contact-point pressure model's gradient channel, w_k = f_iT).
+ * sphbi_boundary_normals: out_normal[2p..] = -n/|n| with n = sum_k
+ * integrate_triangle(p, h, T_k).gradient (the boundary-normal integral, field
+ * 1), pointing from the boundary into the fluid; (0, 0) when |n| <= 1e-12. */
+sphbi_status sphbi_bases_apply_pairs(sphbi_basis_cache* cache, const double* pair_weights, double* out_value,
+                                     double* out_grad, sphbi_memory mem);
+sphbi_status sphbi_boundary_normals(sphbi_basis_cache* cache, double* out_normal, sphbi_memory mem);
+
 /* ---- measurement utility ----------------------------------------------- */
 /* FP64 (DFMA-pipe) peak of the context's GPU at the current clocks: a
  * dependent-chain-free DFMA loop over all SMs, timed with CUDA events.

@@ -80,6 +80,8 @@ EXPORTED_SYMBOLS = (
     "sphbi_bases_read",
     "sphbi_bases_apply",
     "sphbi_bases_destroy",
+    "sphbi_bases_apply_pairs",
+    "sphbi_boundary_normals",
 )
 
 _lib = None
@@ -128,6 +130,8 @@ def load() -> ctypes.CDLL:
     lib.sphbi_bases_apply.argtypes = [P, ctypes.c_int32, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_double),
                                       ctypes.c_int]
     lib.sphbi_bases_destroy.argtypes = [P]
+    lib.sphbi_bases_apply_pairs.argtypes = [P, P, P, P, ctypes.c_int]
+    lib.sphbi_boundary_normals.argtypes = [P, P, ctypes.c_int]
     _lib = lib
     return lib
 

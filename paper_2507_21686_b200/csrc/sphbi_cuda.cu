@@ -152,6 +152,15 @@ struct sphbi_ctx {
   bool force_exact = false;     // two-pass count/emit pipeline for this call (after a slot overflow)
   bool two_pass = false;        // SPHBI_TWO_PASS=1: always the two-pass pipeline (testing)
   bool overflowed = false;      // the last bounded pipeline overflowed its buffers
+  int sms = 148;                // multiprocessors (persistent item-kernel grids)
+  int item_grid = 0;            // SPHBI_ITEM_GRID: 0 adaptive, 1 sync (exact grids), 2 persistent
+  // items per pair of an earlier slot-path call (adaptive piece-kernel grids)
+  double item_ratio[6] = {2.0, 2.0, 2.0, 2.0, 2.0, 2.0};
+  unsigned* h_counts = nullptr;   // pinned, written asynchronously
+  cudaEvent_t count_ev = nullptr;
+  int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
+  bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  int stream_chunk_log2 = 20;   // SPHBI_STREAM_CHUNK_LOG2: particles per chunk of the streamed host path
 };
 
 namespace {
@@ -366,6 +375,7 @@ struct SceneSrc {  // particle pp[k] vs triangle pt[k]
   const double* pxy;
   const double* tri;
   const double* vals;  // nullable: field == 1
+  SceneSrc shifted(int64_t o) const { return SceneSrc{pp + o, pt + o, pxy, tri, vals}; }
   __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* a3) const {
     const int i = pp[k], t = pt[k];
     const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
@@ -390,6 +400,7 @@ struct DirectSrc {  // query, triangle, values per item
   const double* q;
   const double* tri;
   const double* vals;  // nullable
+  DirectSrc shifted(int64_t o) const { return DirectSrc{q + 2 * o, tri + 6 * o, vals ? vals + 3 * o : nullptr}; }
   __device__ void load(int64_t k, double& qx, double& qy, double* t6, double* a3) const {
     qx = q[2 * k];
     qy = q[2 * k + 1];
@@ -499,9 +510,24 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const Norm
 // Per-pair record written by the emit pass: the inline pieces (full / half
 // discs) and, for field mode, the field's barycentric plane tau in the
 // particle frame, so that combine needs no geometry.
-struct PairRec {
-  int nondeg_route;  // integrate_normalized did not bail out (non-degenerate)
-  int disc_n;        // signed count of full unit discs (a kernel constant each)
+struct PairRec {  // two-pass path, per pair
+  int flags;        // bit 0: integrate_normalized did not bail out (non-degenerate route)
+  int disc_n;       // signed count of full unit discs (a kernel constant each)
+};
+constexpr int kRecRoute = 1, kRecPlane = 2;
+// Slot path, per EMISSION position j (signature order): the pair, its flags
+// (bit 1: non-degenerate barycentric plane, hat_planes_nondeg), its item
+// counts, and the list position of its first item of each kind. A pair's items
+// of one kind sit at consecutive list positions (the emitting warp appended
+// them together), and the piece kernels write each output at its list
+// position, so combine reads them coalesced, in emission order.
+struct JRec {
+  int k;
+  int flags;   // kRecRoute | kRecPlane | nsec << 8 | nseg << 12
+  int disc_n;
+  int cnts;    // stub counts per class: 5 bits each
+  unsigned pos[6];  // sector, stub classes 0..3, segment
+  int pad[2];
 };
 
 template <class Src>
@@ -530,35 +556,52 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.stub3 = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
   const bool nondeg_route = integrate_normalized(e, nv);
-  rec[k] = PairRec{nondeg_route ? 1 : 0, e.disc_n};
+  rec[k] = PairRec{nondeg_route ? kRecRoute : 0, e.disc_n};
   if (e.status) atomicOr(status_or, e.status);
 }
 
+// Item count of a piece launch: host-known (two-pass path) or the device
+// counter the emit pass appended to (slot path: a persistent grid of
+// SMs x resident blocks, no host round trip between emit and the piece kernels).
+struct WorkN {
+  int64_t n;
+  const unsigned* dn;
+  int64_t back;  // > 0: the list fills from the back of a buffer of this capacity
+  __device__ __forceinline__ int64_t get() const { return dn ? static_cast<int64_t>(*dn) : n; }
+  __device__ __forceinline__ int64_t pos(int64_t k) const { return back > 0 ? back - 1 - k : k; }
+};
+#define SPHBI_ITEM_LOOP(k)                                                                       \
+  const int64_t n_items_ = wn.get();                                                              \
+  for (int64_t k_ = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k_ < n_items_;    \
+       k_ += static_cast<int64_t>(gridDim.x) * blockDim.x)                                        \
+    if (const int64_t k = wn.pos(k_); true)
+
 template <bool F1>
 __global__ void __launch_bounds__(128)
-    k_pipe_sector(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+    k_pipe_sector(const __grid_constant__ KernelConsts K, WorkN wn, const PieceItem* __restrict__ items,
                   const int* __restrict__ idx, void* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[idx ? idx[k] : k];
-  const Frame f{it.m00, it.m01, it.m10, it.m11};
-  // pad == 1: a half disc in frame f (segment_body's |d| < 1e-9 route)
-  if constexpr (F1) {
-    PairAcc3 a;
-    acc3_zero(a);
-    if (it.pad)
-      piece_half_disc3(K, a, f, it.sign);
-    else
-      piece_cone3(K, a, f, it.a, 1.0, it.sign);
-    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
-  } else {
-    PairAcc a;
-    acc_zero(a);
-    if (it.pad)
-      piece_half_disc(K, a, f, it.sign);
-    else
-      piece_cone(K, a, f, it.a, 1.0, it.sign);
-    acc_to_out(a, static_cast<AccOut*>(out)[k]);
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    const Frame f{it.m00, it.m01, it.m10, it.m11};
+    // pad == 1: a half disc in frame f (segment_body's |d| < 1e-9 route)
+    if constexpr (F1) {
+      PairAcc3 a;
+      acc3_zero(a);
+      if (it.pad)
+        piece_half_disc3(K, a, f, it.sign);
+      else
+        piece_cone3(K, a, f, it.a, 1.0, it.sign);
+      acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+    } else {
+      PairAcc a;
+      acc_zero(a);
+      if (it.pad)
+        piece_half_disc(K, a, f, it.sign);
+      else
+        piece_cone(K, a, f, it.a, 1.0, it.sign);
+      acc_to_out(a, static_cast<AccOut*>(out)[k]);
+    }
   }
 }
 
@@ -566,11 +609,13 @@ __global__ void __launch_bounds__(128)
 // Single-pass emission into per-pair slots (the default): the geometry runs
 // once per pair; each pair owns kCapSec / kCapStub / kCapSeg item slots
 // (structural maxima of the decomposition: <= 4 wedges, each with <= 1
-// sector and <= 1 half disc, <= 1 segment and <= 2 stub calls of <= 2 direct stubs), writes its
-// per-kind counts, and k_expand turns counts + class tags into dense,
-// pair-ordered index lists for the piece kernels and combine. A pair that
-// would exceed a cap (never seen; 4.5M-pair census in DESIGN.md) sets
-// dflags[1] bit 8 and the chunk is redone with the two-pass count/emit path.
+// sector and <= 1 half disc, <= 1 segment and <= 2 stub calls of <= 2 direct
+// stubs), records its slot counts in its PairRec and appends its slot indices
+// to per-kind work lists (SlotLists). The piece kernels write each item's
+// output into the item's slot, so combine reads a pair's outputs as three
+// contiguous runs, with no scans, index expansion or host round trip. A pair
+// that would exceed a cap (never seen; 4.5M-pair census in DESIGN.md) sets
+// dflags[1] bit 2 and the call is redone with the two-pass count/emit path.
 // ---------------------------------------------------------------------------
 constexpr int kCapSec = 8, kCapStub = 16, kCapSeg = 4;  // sector slots also hold half discs
 
@@ -583,7 +628,7 @@ struct SlotSink {
   bool overflow;
   PieceItem *sec, *seg;
   StubItem* stubs;
-  unsigned char* tag;
+  unsigned cls_bits;  // 2 bits per stub slot: its class (stub_class)
   int nsec, nseg, nstub, c0, c1, c2, c3;
   unsigned long long* counters;
   __device__ void bump(int w) { bump_counter(counters, w); }
@@ -643,7 +688,7 @@ struct SlotSink {
       it.lo = lo;
       it.u = u;
       stubs[nstub] = it;
-      tag[nstub] = static_cast<unsigned char>(cls);
+      cls_bits |= static_cast<unsigned>(cls) << (2 * nstub);
     } else {
       overflow = true;
     }
@@ -655,171 +700,276 @@ struct SlotSink {
   }
 };
 
+// Slot-path work lists: per kind a list of item slot indices, appended per
+// warp (one global atomic per kind and warp). Sector and segment lists fill
+// from the front of their buffers; the four stub classes share two buffers of
+// kCapStub * n entries, class 0 / 2 from the front and class 1 / 3 from the
+// back (the per-class totals are unknown until the emit pass has run).
+struct SlotLists {
+  int* sec;            // kCapSec * n
+  int* stub[2];        // kCapStub * n each: classes (0 | 1), (2 | 3)
+  int* seg;            // kCapSeg * n
+  unsigned* count;     // [kKinds] device counters (zeroed per chunk)
+  long long stub_cap;  // kCapStub * n
+};
+
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit_slots(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
                       const int* __restrict__ order, PieceItem* __restrict__ sec_slots,
-                      StubItem* __restrict__ stub_slots, unsigned char* __restrict__ stub_tags,
-                      PieceItem* __restrict__ seg_slots, unsigned* __restrict__ cnt, PairRec* __restrict__ rec,
-                      unsigned long long* counters, unsigned* status_or) {
+                      StubItem* __restrict__ stub_slots, PieceItem* __restrict__ seg_slots,
+                      JRec* __restrict__ jrec, SlotLists L, unsigned long long* counters, unsigned* status_or) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t m = n + 1;
-  if (j >= n) {
-    if (j == n)
-      for (int q = 0; q < kKinds; ++q) cnt[q * m + j] = 0;  // scan tails
-    return;
+  int64_t k = 0;
+  int my[kKinds] = {0, 0, 0, 0, 0, 0};
+  unsigned cls_bits = 0u;
+  int flags = 0, disc_n = 0;
+  if (j < n) {
+    k = order ? order[j] : j;
+    P2 nv[3];
+    int perm[3];
+    load_norm(nrec, k, nv, perm);
+    flags = hat_planes_nondeg(nv) ? kRecPlane : 0;
+    SlotSink e;
+    e.K = &K;
+    e.status = 0;
+    e.pair = static_cast<int>(k);
+    e.disc_n = 0;
+    e.overflow = false;
+    // slots by emission position: a warp writes one contiguous region
+    e.sec = sec_slots + kCapSec * j;
+    e.seg = seg_slots + kCapSeg * j;
+    e.stubs = stub_slots + kCapStub * j;
+    e.cls_bits = 0u;
+    e.nsec = e.nseg = e.nstub = e.c0 = e.c1 = e.c2 = e.c3 = 0;
+    e.counters = counters;
+    const bool nondeg_route = integrate_normalized(e, nv);
+    if (e.overflow) {
+      // the call is redone with the two-pass pipeline (dflags[1] bit 2); keep
+      // this pass in bounds
+      atomicOr(status_or + 1, 4u);
+      e.nsec = min(e.nsec, kCapSec);
+      e.nseg = min(e.nseg, kCapSeg);
+      e.nstub = min(e.nstub, kCapStub);
+      e.c0 = e.c1 = e.c2 = e.c3 = 0;
+      for (int q = 0; q < e.nstub; ++q) {
+        const int c = (e.cls_bits >> (2 * q)) & 3;
+        e.c0 += c == 0;
+        e.c1 += c == 1;
+        e.c2 += c == 2;
+        e.c3 += c == 3;
+      }
+    }
+    if (nondeg_route) flags |= kRecRoute;
+    flags |= (e.nsec << 8) | (e.nseg << 12);
+    disc_n = e.disc_n;
+    if (e.status) atomicOr(status_or, e.status);
+    my[0] = e.nsec;
+    my[1] = e.c0;
+    my[2] = e.c1;
+    my[3] = e.c2;
+    my[4] = e.c3;
+    my[5] = e.nseg;
+    cls_bits = e.cls_bits;
   }
-  const int64_t k = order ? order[j] : j;
-  P2 nv[3];
-  int perm[3];
-  load_norm(nrec, k, nv, perm);
-  SlotSink e;
-  e.K = &K;
-  e.status = 0;
-  e.pair = static_cast<int>(k);
-  e.disc_n = 0;
-  e.overflow = false;
-  e.sec = sec_slots + kCapSec * k;
-  e.seg = seg_slots + kCapSeg * k;
-  e.stubs = stub_slots + kCapStub * k;
-  e.tag = stub_tags + kCapStub * k;
-  e.nsec = e.nseg = e.nstub = e.c0 = e.c1 = e.c2 = e.c3 = 0;
-  e.counters = counters;
-  const bool nondeg_route = integrate_normalized(e, nv);
-  cnt[k] = e.nsec;
-  cnt[m + k] = e.c0;
-  cnt[2 * m + k] = e.c1;
-  cnt[3 * m + k] = e.c2;
-  cnt[4 * m + k] = e.c3;
-  cnt[5 * m + k] = e.nseg;
-  rec[k] = PairRec{nondeg_route ? 1 : 0, e.disc_n};
-  if (e.status) atomicOr(status_or, e.status);
-  if (e.overflow) atomicOr(status_or + 1, 8u);
-}
-
-// dense, pair-ordered index lists (emission order within a pair and class)
-__global__ void __launch_bounds__(256)
-    k_expand(int64_t n, const unsigned long long* __restrict__ off, ulonglong4 stub_base,
-             const unsigned char* __restrict__ stub_tags, int* __restrict__ sec_idx, int* __restrict__ stub_idx,
-             int* __restrict__ seg_idx) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int64_t m = n + 1;
+  // warp-aggregated appends: an inclusive scan of each kind's count over the
+  // warp, one global atomic per kind and warp (no block barrier: warps of a
+  // block finish the divergent geometry at different times)
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned pos[kKinds];
+#pragma unroll
+  for (int q = 0; q < kKinds; ++q) {
+    const unsigned v = static_cast<unsigned>(my[q]);
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    unsigned base = 0u;
+    if (lane == 31u && x) base = atomicAdd(L.count + q, x);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    const unsigned total = __shfl_sync(0xffffffffu, x, 31);
+    // classes 1 and 3 (kinds 2, 4) fill their buffers from the back
+    pos[q] = (q == 2 || q == 4) ? static_cast<unsigned>(L.stub_cap) - base - total + (x - v) : base + x - v;
+  }
+  if (j >= n) return;
   {
-    const unsigned long long o = off[k], e = off[k + 1];
-    for (unsigned long long q = o; q < e; ++q) sec_idx[q] = static_cast<int>(kCapSec * k + (q - o));
+    JRec r;
+    r.k = static_cast<int>(k);
+    r.flags = flags;
+    r.disc_n = disc_n;
+    r.cnts = my[1] | (my[2] << 5) | (my[3] << 10) | (my[4] << 15);
+#pragma unroll
+    for (int q = 0; q < kKinds; ++q) r.pos[q] = pos[q];
+    r.pad[0] = r.pad[1] = 0;
+    jrec[j] = r;
   }
-  {
-    const unsigned long long o = off[5 * m + k], e = off[5 * m + k + 1];
-    for (unsigned long long q = o; q < e; ++q) seg_idx[q] = static_cast<int>(kCapSeg * k + (q - o));
-  }
-  unsigned long long pos[4] = {stub_base.x + off[m + k], stub_base.y + off[2 * m + k], stub_base.z + off[3 * m + k],
-                               stub_base.w + off[4 * m + k]};
-  const int nst = static_cast<int>((off[m + k + 1] - off[m + k]) + (off[2 * m + k + 1] - off[2 * m + k]) +
-                                   (off[3 * m + k + 1] - off[3 * m + k]) + (off[4 * m + k + 1] - off[4 * m + k]));
-  for (int q = 0; q < nst; ++q) {
-    const int c = stub_tags[kCapStub * k + q];
-    stub_idx[pos[c]++] = static_cast<int>(kCapStub * k + q);
+  for (int q = 0; q < my[0]; ++q) L.sec[pos[0] + q] = static_cast<int>(kCapSec * j + q);
+  for (int q = 0; q < my[5]; ++q) L.seg[pos[5] + q] = static_cast<int>(kCapSeg * j + q);
+  const int nst = my[1] + my[2] + my[3] + my[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (!my[1 + c]) continue;
+    int* d = L.stub[c >> 1] + pos[1 + c];
+    for (int q = 0; q < nst; ++q)
+      if (((cls_bits >> (2 * q)) & 3) == static_cast<unsigned>(c)) *d++ = static_cast<int>(kCapStub * j + q);
   }
 }
 
 // one launch per stub class: warps run one specialised code path
 template <bool F1, int CLS>
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
-    k_pipe_stub(const __grid_constant__ KernelConsts K, int64_t n, const StubItem* __restrict__ items,
+    k_pipe_stub(const __grid_constant__ KernelConsts K, WorkN wn, const StubItem* __restrict__ items,
                 const int* __restrict__ idx, void* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const StubItem it = items[idx ? idx[k] : k];
-  const Frame f{it.m00, it.m01, it.m10, it.m11};
-  if constexpr (F1) {
-    PairAcc3 a;
-    acc3_zero(a);
-    piece_stub3<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
-    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
-  } else {
-    PairAcc a;
-    acc_zero(a);
-    piece_stub_k<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
-    acc_to_out(a, static_cast<AccOut*>(out)[k]);
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const StubItem it = items[slot];
+    const Frame f{it.m00, it.m01, it.m10, it.m11};
+    if constexpr (F1) {
+      PairAcc3 a;
+      acc3_zero(a);
+      piece_stub3<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+      acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+    } else {
+      PairAcc a;
+      acc_zero(a);
+      piece_stub_k<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+      acc_to_out(a, static_cast<AccOut*>(out)[k]);
+    }
   }
 }
 
 template <bool F1>
 __global__ void __launch_bounds__(128)
-    k_pipe_segment(const __grid_constant__ KernelConsts K, int64_t n, const PieceItem* __restrict__ items,
+    k_pipe_segment(const __grid_constant__ KernelConsts K, WorkN wn, const PieceItem* __restrict__ items,
                    const int* __restrict__ idx, void* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[idx ? idx[k] : k];
-  const Frame f{it.m00, it.m01, it.m10, it.m11};
-  if constexpr (F1) {
-    PairAcc3 a;
-    acc3_zero(a);
-    piece_segment3(K, a, f, it.a, it.sign);
-    acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
-  } else {
-    PairAcc a;
-    acc_zero(a);
-    piece_segment(K, a, f, it.a, it.sign);
-    acc_to_out(a, static_cast<AccOut*>(out)[k]);
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    const Frame f{it.m00, it.m01, it.m10, it.m11};
+    if constexpr (F1) {
+      PairAcc3 a;
+      acc3_zero(a);
+      piece_segment3(K, a, f, it.a, it.sign);
+      acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
+    } else {
+      PairAcc a;
+      acc_zero(a);
+      piece_segment(K, a, f, it.a, it.sign);
+      acc_to_out(a, static_cast<AccOut*>(out)[k]);
+    }
   }
 }
 
-// A pair's items: sectors, stub classes 0..3, segments, each in emission
-// order -- a fixed summation order (bitwise reproducible).
+// A pair's items in a fixed summation order: sectors, stub classes 0..3,
+// segments, each in emission order -- identical on both pipelines, so their
+// results agree bit for bit.
 struct ItemOuts {
   const void* sec;
-  const void* stub;
+  const void* stub[2];  // two-pass path: both point at the one dense stub array
   const void* seg;
+};
+__device__ __forceinline__ const void* item_base(const ItemOuts& io, int kind) {
+  return kind == 0 ? io.sec : (kind == 3 ? io.seg : io.stub[kind - 1]);
+}
+// two-pass path: per pair k, item ranges from the scanned counts
+struct DenseItems {
+  static constexpr bool kPlaneInRec = false;
+  using Rec = PairRec;
+  const PairRec* rec;
+  const unsigned long long* off;
+  int64_t m;  // n + 1
   ulonglong4 stub_base;
+  __device__ __forceinline__ Rec get(int64_t j) const { return rec[j]; }
+  __device__ __forceinline__ int64_t pair(int64_t j, const Rec&) const { return j; }
+  template <class F>
+  __device__ __forceinline__ void each(int64_t k, const Rec&, F&& f) const {
+    for (unsigned long long q = off[k]; q < off[k + 1]; ++q) f(0, q);
+    const unsigned long long base[4] = {stub_base.x, stub_base.y, stub_base.z, stub_base.w};
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      const unsigned long long* o = off + (1 + c) * m;
+      for (unsigned long long q = o[k]; q < o[k + 1]; ++q) f(1, base[c] + q);
+    }
+    for (unsigned long long q = off[5 * m + k]; q < off[5 * m + k + 1]; ++q) f(3, q);
+  }
+};
+// slot path: per emission position j (JRec)
+struct SlotItems {
+  static constexpr bool kPlaneInRec = true;
+  using Rec = JRec;
+  const JRec* rec;
+  __device__ __forceinline__ Rec get(int64_t j) const {
+    const int4* p = reinterpret_cast<const int4*>(rec + j);
+    const int4 a = p[0], b = p[1], c = p[2];
+    Rec r;
+    r.k = a.x;
+    r.flags = a.y;
+    r.disc_n = a.z;
+    r.cnts = a.w;
+    r.pos[0] = b.x;
+    r.pos[1] = b.y;
+    r.pos[2] = b.z;
+    r.pos[3] = b.w;
+    r.pos[4] = c.x;
+    r.pos[5] = c.y;
+    return r;
+  }
+  __device__ __forceinline__ int64_t pair(int64_t, const Rec& r) const { return r.k; }
+  template <class F>
+  __device__ __forceinline__ void each(int64_t, const Rec& r, F&& f) const {
+    const int ns = (r.flags >> 8) & 15, ng = (r.flags >> 12) & 7;
+    for (int q = 0; q < ns; ++q) f(0, static_cast<unsigned long long>(r.pos[0] + q));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int nc = (r.cnts >> (5 * c)) & 31;
+      for (int q = 0; q < nc; ++q) f(1 + (c >> 1), static_cast<unsigned long long>(r.pos[1 + c] + q));
+    }
+    for (int q = 0; q < ng; ++q) f(3, static_cast<unsigned long long>(r.pos[5] + q));
+  }
 };
 template <bool F1>
 __device__ __forceinline__ void add_item(PairAcc& a, const void* base, unsigned long long j) {
   if constexpr (F1) {
-    const double* o = static_cast<const AccOut3*>(base)[j].v;
-    a.v3 = dd_add(a.v3, dd{o[0], o[1]});
-    a.g13 = dd_add(a.g13, dd{o[2], o[3]});
-    a.g23 = dd_add(a.g23, dd{o[4], o[5]});
+    const double2* o = reinterpret_cast<const double2*>(static_cast<const AccOut3*>(base)[j].v);
+    const double2 x = o[0], y = o[1], z = o[2];
+    a.v3 = dd_add(a.v3, dd{x.x, x.y});
+    a.g13 = dd_add(a.g13, dd{y.x, y.y});
+    a.g23 = dd_add(a.g23, dd{z.x, z.y});
   } else {
     acc_add_out(a, static_cast<const AccOut*>(base)[j].v);
   }
 }
-template <bool F1>
-__device__ __forceinline__ void sum_items(const KernelConsts& K, PairAcc& a, const PairRec& r, int64_t n, int64_t k,
-                                          const unsigned long long* __restrict__ off, const ItemOuts& io) {
-  const int64_t m = n + 1;
+template <bool F1, class Items>
+__device__ __forceinline__ void sum_items(const KernelConsts& K, PairAcc& a, int disc_n, int64_t k,
+                                          const typename Items::Rec& r, const Items& items, const ItemOuts& io) {
   acc_zero(a);
-  if (r.disc_n) piece_disc(K, a, static_cast<double>(r.disc_n));
-  for (unsigned long long j = off[k]; j < off[k + 1]; ++j) add_item<F1>(a, io.sec, j);
-  const unsigned long long base[4] = {io.stub_base.x, io.stub_base.y, io.stub_base.z, io.stub_base.w};
-#pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    const unsigned long long* o = off + (1 + c) * m;
-    for (unsigned long long j = o[k]; j < o[k + 1]; ++j) add_item<F1>(a, io.stub, base[c] + j);
-  }
-  for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) add_item<F1>(a, io.seg, j);
+  if (disc_n) piece_disc(K, a, static_cast<double>(disc_n));
+  items.each(k, r, [&](int kind, unsigned long long q) { add_item<F1>(a, item_base(io, kind), q); });
 }
 
 // combine, field mode: out[stride*k ..] = (value, gx, gy[, imag = 0]).
 // The field's barycentric plane (assemble_region :255-269, solved once per
 // pair in the particle frame) is computed here, in pair order; for field == 1
-// the plane is exactly (0, 0, 1) and only the degeneracy test remains.
-template <bool F1, class Src>
+// the plane is exactly (0, 0, 1) and only the degeneracy test remains (on the
+// slot path the emit pass recorded it in the JRec: no NormRec read). The slot
+// path runs in emission order j (coalesced records and item outputs).
+template <bool F1, class Src, class Items>
 __global__ void __launch_bounds__(128)
     k_pipe_combine(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
-                   double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off, ItemOuts io,
-                   int stride, double* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PairRec& r = rec[k];
+                   double h, Items items, ItemOuts io, int stride, double* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const typename Items::Rec r = items.get(j);
+  const int64_t k = items.pair(j, r);
   double o[4] = {0.0, 0.0, 0.0, 0.0};
-  if (r.nondeg_route) {
-    P2 nv[3];
-    int perm[3];
-    load_norm(nrec, k, nv, perm);
+  if (r.flags & kRecRoute) {
     dd tau1{0, 0}, tau2{0, 0}, tau3{1.0, 0};
     bool nondeg;
     if (src.vals) {
+      P2 nv[3];
+      int perm[3];
+      load_norm(nrec, k, nv, perm);
       HatPlanes H;
       nondeg = hat_planes(nv, H);
       if (nondeg) {
@@ -833,39 +983,45 @@ __global__ void __launch_bounds__(128)
           tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
         }
       }
+    } else if constexpr (Items::kPlaneInRec) {
+      nondeg = (r.flags & kRecPlane) != 0;
     } else {
+      P2 nv[3];
+      int perm[3];
+      load_norm(nrec, k, nv, perm);
       nondeg = hat_planes_nondeg(nv);
     }
     if (nondeg) {
       PairAcc a;
-      sum_items<F1>(K, a, r, n, k, off, io);
+      sum_items<F1>(K, a, r.disc_n, k, r, items, io);
       double raw[3];
       combine_plane(a, tau1, tau2, tau3, raw);
       finalize(raw, K.c2, h, o);
     }
   }
-  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
+  for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
 }
 
 // combine, vertex-basis mode: per pair and vertex i (original order) the
 // finalized (value, grad_x, grad_y[, imag = 0]) of the hat field of vertex i;
 // stride 12 (integrate_triangle_bases' layout) or 9 (basis cache, no imag).
+template <class Items>
 __global__ void __launch_bounds__(128)
     k_pipe_combine_bases(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
-                         double h, const PairRec* __restrict__ rec, const unsigned long long* __restrict__ off,
-                         ItemOuts io, int stride, double* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+                         double h, Items items, ItemOuts io, int stride, double* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const typename Items::Rec r = items.get(j);
+  const int64_t k = items.pair(j, r);
   P2 nv[3];
   int perm[3];
   load_norm(nrec, k, nv, perm);
-  const PairRec& r = rec[k];
   double o[12];
   for (int j = 0; j < 12; ++j) o[j] = 0.0;
   HatPlanes H;
-  if (r.nondeg_route && hat_planes(nv, H)) {
+  if ((r.flags & kRecRoute) && hat_planes(nv, H)) {
     PairAcc a;
-    sum_items<false>(K, a, r, n, k, off, io);
+    sum_items<false>(K, a, r.disc_n, k, r, items, io);
     for (int i = 0; i < 3; ++i) {
       double raw[3];
       combine_plane(a, H.t1[i], H.t2[i], H.t3[i], raw);
@@ -873,10 +1029,10 @@ __global__ void __launch_bounds__(128)
     }
   }
   if (stride == 12) {
-    for (int j = 0; j < 12; ++j) out[12 * k + j] = o[j];
+    for (int q = 0; q < 12; ++q) out[12 * k + q] = o[q];
   } else {
     for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) out[9 * k + 3 * i + j] = o[4 * i + j];
+      for (int q = 0; q < 3; ++q) out[9 * k + 3 * i + q] = o[4 * i + q];
   }
 }
 
@@ -898,65 +1054,67 @@ __device__ __forceinline__ void h24_store(const H24& H, H24Out& o) {
   }
 }
 __global__ void __launch_bounds__(128)
-    k_p3_sector(const __grid_constant__ P3Consts P, int64_t n, const PieceItem* __restrict__ items,
+    k_p3_sector(const __grid_constant__ P3Consts P, WorkN wn, const PieceItem* __restrict__ items,
                 const int* __restrict__ idx, H24Out* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[idx ? idx[k] : k];
-  H24 H, acc;
-  if (it.pad)
-    h24_half_disc(P, H);
-  else
-    h24_cone(P, it.a, 1.0, H);
-  h24_zero(acc);
-  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
-  h24_store(acc, out[k]);
-}
-__global__ void __launch_bounds__(128)
-    k_p3_stub(const __grid_constant__ P3Consts P, int64_t n, const StubItem* __restrict__ items,
-              const int* __restrict__ idx, H24Out* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const StubItem it = items[idx ? idx[k] : k];
-  H24 H, acc;
-  h24_cone(P, it.gamma, it.l, H);
-  if (it.window) {
-    h24_stub_bound(P, it.u, it.D, it.beta, 1.0, H);
-    h24_stub_bound(P, it.lo, it.D, it.beta, -1.0, H);
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    H24 H, acc;
+    if (it.pad)
+      h24_half_disc(P, H);
+    else
+      h24_cone(P, it.a, 1.0, H);
+    h24_zero(acc);
+    h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+    h24_store(acc, out[k]);
   }
-  h24_zero(acc);
-  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
-  h24_store(acc, out[k]);
 }
 __global__ void __launch_bounds__(128)
-    k_p3_segment(const __grid_constant__ P3Consts P, int64_t n, const PieceItem* __restrict__ items,
+    k_p3_stub(const __grid_constant__ P3Consts P, WorkN wn, const StubItem* __restrict__ items,
+              const int* __restrict__ idx, H24Out* __restrict__ out) {
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const StubItem it = items[slot];
+    H24 H, acc;
+    h24_cone(P, it.gamma, it.l, H);
+    if (it.window) {
+      h24_stub_bound(P, it.u, it.D, it.beta, 1.0, H);
+      h24_stub_bound(P, it.lo, it.D, it.beta, -1.0, H);
+    }
+    h24_zero(acc);
+    h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+    h24_store(acc, out[k]);
+  }
+}
+__global__ void __launch_bounds__(128)
+    k_p3_segment(const __grid_constant__ P3Consts P, WorkN wn, const PieceItem* __restrict__ items,
                  const int* __restrict__ idx, H24Out* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PieceItem it = items[idx ? idx[k] : k];
-  H24 H, acc;
-  h24_segment(P, it.a, H);
-  h24_zero(acc);
-  h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
-  h24_store(acc, out[k]);
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    H24 H, acc;
+    h24_segment(P, it.a, H);
+    h24_zero(acc);
+    h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+    h24_store(acc, out[k]);
+  }
 }
 __device__ __forceinline__ void h24_add_out(H24& a, const H24Out& o) {
 #pragma unroll
   for (int i = 0; i < kP3Sums; ++i) a.c[i] = dd_add(a.c[i], dd{o.v[2 * i], o.v[2 * i + 1]});
 }
 // nodes: 10 per triangle; pt (scene) maps pair -> triangle, NULL: 10 per pair
+template <class Items>
 __global__ void __launch_bounds__(128)
     k_p3_combine(const __grid_constant__ KernelConsts K, const __grid_constant__ P3Consts P,
-                 const NormRec* __restrict__ nrec, int64_t n, double h, const PairRec* __restrict__ rec,
-                 const unsigned long long* __restrict__ off, const H24Out* __restrict__ osec,
-                 const H24Out* __restrict__ ostub, const H24Out* __restrict__ oseg, ulonglong4 stub_base,
-                 const double* __restrict__ nodes, const int* __restrict__ pt, int stride,
-                 double* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const PairRec r = rec[k];
+                 const NormRec* __restrict__ nrec, int64_t n, double h, Items items, ItemOuts io,
+                 const double* __restrict__ nodes, const int* __restrict__ pt, int stride, double* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const typename Items::Rec r = items.get(j);
+  const int64_t k = items.pair(j, r);
   double o[4] = {0.0, 0.0, 0.0, 0.0};
-  if (r.nondeg_route) {
+  if (r.flags & kRecRoute) {
     P2 nv[3], nvo[3];
     int perm[3];
     load_norm(nrec, k, nv, perm);
@@ -968,15 +1126,9 @@ __global__ void __launch_bounds__(128)
       h24_disc(P, Hd);
       h24_accumulate(acc, Hd, Frame{1.0, 0.0, 0.0, 1.0}, static_cast<double>(r.disc_n));
     }
-    const int64_t m = n + 1;
-    for (unsigned long long j = off[k]; j < off[k + 1]; ++j) h24_add_out(acc, osec[j]);
-    const unsigned long long base[4] = {stub_base.x, stub_base.y, stub_base.z, stub_base.w};
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      const unsigned long long* oc = off + (1 + c) * m;
-      for (unsigned long long j = oc[k]; j < oc[k + 1]; ++j) h24_add_out(acc, ostub[base[c] + j]);
-    }
-    for (unsigned long long j = off[5 * m + k]; j < off[5 * m + k + 1]; ++j) h24_add_out(acc, oseg[j]);
+    items.each(k, r, [&](int kind, unsigned long long q) {
+      h24_add_out(acc, static_cast<const H24Out*>(item_base(io, kind))[q]);
+    });
     // nodal values straight from global memory (a local copy passed by pointer
     // was clobbered by the callee's frame with nvcc 12.9)
     const double* n10 = nodes + 10 * (pt ? static_cast<int64_t>(pt[k]) : k);
@@ -996,7 +1148,7 @@ __global__ void __launch_bounds__(128)
 #endif
     }
   }
-  for (int j = 0; j < stride; ++j) out[stride * k + j] = o[j];
+  for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -1095,6 +1247,43 @@ __global__ void __launch_bounds__(256)
   }
   if (bad) atomicOr(flags, kStatusDomain);
   ov[j] = v;
+  reinterpret_cast<double2*>(og)[j] = make_double2(gx, gy);
+}
+
+// SPH coupling consumers of the basis cache (PAPER.md
+// Appendix): per-pair constant fields. A pair's field-1 integral is the sum of
+// its three vertex bases; with per-pair weights w_k (NULL: 1) the row sums are
+//   value[j] = sum_k w_k (B_k0 + B_k1 + B_k2),  grad likewise,
+// the contact-point pressure model's gradient channel (w_k = f_iT) and, with
+// w = 1, the boundary-normal integral n_i = int grad W. With `normal` set the
+// gradient is returned as the boundary normal -n/|n| (pointing from the wall
+// into the fluid; zero when |n| <= 1e-12).
+__global__ void __launch_bounds__(256)
+    k_bases_apply_pairs(int np, const int64_t* __restrict__ row_ptr, const double* __restrict__ B,
+                        const double* __restrict__ w, int normal, double* __restrict__ ov,
+                        double* __restrict__ og) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= np) return;
+  double v = 0.0, gx = 0.0, gy = 0.0;
+  const int64_t e = row_ptr[j + 1];
+  for (int64_t k = row_ptr[j]; k < e; ++k) {
+    const double* b = B + 9 * k;
+    const double wk = w ? __ldg(w + k) : 1.0;
+    // the bitwise order of k_bases_apply<0> with unit vertex weights
+    v += wk * ((b[0] + b[3]) + b[6]);
+    gx += wk * ((b[1] + b[4]) + b[7]);
+    gy += wk * ((b[2] + b[5]) + b[8]);
+  }
+  if (normal) {
+    const double m = sqrt(gx * gx + gy * gy);
+    if (m > 1e-12) {
+      gx = -gx / m;
+      gy = -gy / m;
+    } else {
+      gx = gy = 0.0;
+    }
+  }
+  if (ov) ov[j] = v;
   reinterpret_cast<double2*>(og)[j] = make_double2(gx, gy);
 }
 
@@ -1418,75 +1607,81 @@ struct PipeStats {
   unsigned long long n_cone = 0, n_bound = 0, n_seg = 0;
 };
 
-// Work-item buffer capacities per pair (sector, stub, segment) for the
-// sync-free mode; the exact totals are only known on the device. Measured on
-// cfg2: 0.7 / 1.9 / 0.25 items per pair; worst single pairs reach ~16 stubs.
-
-// K4 pipeline over n pairs. The six item totals (sectors, four stub classes,
-// segments) are read back once (one host sync) and size the buffers and the
-// grids exactly. (A sync-free variant with per-pair capacity bounds and
-// device-resident counts was measured slower on the B200: over-sized grids
-// cost more than the sync.)
 // mode 0: field / field == 1; 1: vertex bases; 3: P3 field (p3 != NULL)
 struct P3Job {
   const P3Consts* P;
   const double* nodes;  // 10 per triangle (scene: indexed by pt) or per pair
   const int* pt;        // scene pair -> triangle; NULL: nodes are per pair
+  P3Job shifted(int64_t o) const { return pt ? P3Job{P, nodes, pt + o} : P3Job{P, nodes + 10 * o, nullptr}; }
 };
+
+// Persistent grid for an item kernel: SMs x resident blocks of `block` threads.
+int resident_grid(sphbi_ctx* c, const void* fn, int block) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, block, 0) != cudaSuccess) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  return c->sms * (nb > 0 ? nb : 1);
+}
+template <class F>
+int rgrid(sphbi_ctx* c, F* fn) {
+  return resident_grid(c, reinterpret_cast<const void*>(fn), 128);
+}
+
+// Canonical normalized vertices (NormRec) + pre-classification key, pairs
+// sorted by key (shared by both pipelines).
 template <class Src>
-sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
-                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
-                          const P3Job* p3 = nullptr) {
-  if (n <= 0) return SPHBI_OK;
+sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, NormRec** nrec_out,
+                          int** porder_out) {
   cudaStream_t s = c->stream;
   sphbi_status st;
-  unsigned* cnt;
-  unsigned long long* off;
   const int64_t m = n + 1;
-  if ((st = scratch_t(c, kBufPipeCnt, kKinds * m, &cnt)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPipeOff, kKinds * m, &off)) != SPHBI_OK) return st;
-  int *iota, *order;
+  int* iota;
   if ((st = scratch_t(c, kBufOrder, 2 * m, &iota)) != SPHBI_OK) return st;
-  order = iota + m;
-  NormRec* nrec;
-  int* porder;
-  PairRec* rec;
-  if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
   k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, iota);
   if ((st = check_launch(c, "k_iota")) != SPHBI_OK) return st;
-  // canonical normalized vertices + pre-classification key, pairs sorted by key
-  {
-    unsigned short* pk;
-    if ((st = scratch_t(c, kBufPreKey, 2 * m, &pk)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufPreOrder, m, &porder)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufNormRec, n, &nrec)) != SPHBI_OK) return st;
-    k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, nrec);
-    if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
-    size_t tmp_sort = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, pk, pk + m, iota, porder, (int)n, 0, 9, s);
-    void* dtmp_sort;
-    if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
-    cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, pk, pk + m, iota, porder, (int)n, 0, 9, s);
-    if ((st = check_launch(c, "radix sort pre-class")) != SPHBI_OK) return st;
+  unsigned short* pk;
+  if ((st = scratch_t(c, kBufPreKey, 2 * m, &pk)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPreOrder, m, porder_out)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufNormRec, n, nrec_out)) != SPHBI_OK) return st;
+  k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, *nrec_out);
+  if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
+  if (c->no_sig_sort) {  // experiment: emit in pair order
+    *porder_out = nullptr;
+    return SPHBI_OK;
   }
-  const bool two_pass = c->force_exact || c->two_pass;  // after a slot overflow: count + emit
-  PieceItem *isec = nullptr, *iseg = nullptr;
-  StubItem* istub = nullptr;
-  unsigned char* tags = nullptr;
-  if (!two_pass) {
-    if ((st = scratch_t(c, kBufItemsC, kCapSec * n, &isec)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufItemsB, kCapStub * n, &istub)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufItemsS, kCapSeg * n, &iseg)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufClass, kCapStub * n, &tags)) != SPHBI_OK) return st;
-    k_pipe_emit_slots<<<grid_for(m, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, tags, iseg, cnt, rec, ctr,
-                                                       dflags);
-    if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
-  } else {
-    unsigned char* cls;
-    if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
-    k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
-    if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
-  }
+  size_t tmp_sort = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, pk, pk + m, iota, *porder_out, (int)n, 0, 9, s);
+  void* dtmp_sort;
+  if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
+  cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, pk, pk + m, iota, *porder_out, (int)n, 0, 9, s);
+  return check_launch(c, "radix sort pre-class");
+}
+
+// Two-pass K4 pipeline (after a slot overflow, or SPHBI_TWO_PASS=1): count
+// pass, CUB scans, one host sync for the exact item totals, dense emission,
+// dense piece kernels, combine over the scanned ranges.
+template <class Src>
+sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
+                                int stride, double* dout, unsigned* dflags, unsigned long long* ctr,
+                                const P3Job* p3) {
+  cudaStream_t s = c->stream;
+  sphbi_status st;
+  const int64_t m = n + 1;
+  NormRec* nrec;
+  int* porder;
+  if ((st = pre_classify(c, h, src, n, &nrec, &porder)) != SPHBI_OK) return st;
+  unsigned* cnt;
+  unsigned long long* off;
+  PairRec* rec;
+  if ((st = scratch_t(c, kBufPipeCnt, kKinds * m, &cnt)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPipeOff, kKinds * m, &off)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
+  unsigned char* cls;
+  if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
+  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
+  if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
   void* dtmp;
@@ -1495,106 +1690,235 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt + j * m, off + j * m, (int)m, s);
     if ((st = check_launch(c, "scan piece counts")) != SPHBI_OK) return st;
   }
-  // exact item totals and the slot-overflow flag (one host sync)
   unsigned long long tot[kKinds];
   {
     unsigned long long* ht = reinterpret_cast<unsigned long long*>(c->h_flags + 8);
     for (int j = 0; j < kKinds; ++j)
       SPHBI_CUDA_TRY(cudaMemcpyAsync(ht + j, off + j * m + n, 8, cudaMemcpyDeviceToHost, s));
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 24, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     for (int j = 0; j < kKinds; ++j) tot[j] = ht[j];
-    if (!two_pass && (c->h_flags[24] & 8u)) {
-      // a pair exceeded its item slots: redo this chunk with count + emit
-      SPHBI_CUDA_TRY(cudaMemsetAsync(dflags + 1, 0, 4, s));
-      c->force_exact = true;
-      const sphbi_status r = run_pipeline(c, K, h, src, n, mode, stride, dout, dflags, nullptr, ps, p3);
-      c->force_exact = false;
-      return r;
-    }
   }
   unsigned long long sbase[5] = {0, 0, 0, 0, 0};
   for (int cl = 0; cl < 4; ++cl) sbase[cl + 1] = sbase[cl] + tot[1 + cl];
   const ulonglong4 stub_base = make_ulonglong4(sbase[0], sbase[1], sbase[2], sbase[3]);
   const unsigned long long n_sec = tot[0], n_stub = sbase[4], n_seg = tot[5];
-  int *xsec = nullptr, *xstub = nullptr, *xseg = nullptr;
-  if (!two_pass) {
-    int* xall;
-    if ((st = scratch_t(c, kBufIdx, n_sec + n_stub + n_seg + 1, &xall)) != SPHBI_OK) return st;
-    xsec = xall;
-    xstub = xall + n_sec;
-    xseg = xall + n_sec + n_stub;
-    k_expand<<<grid_for(n, 256), 256, 0, s>>>(n, off, stub_base, tags, xsec, xstub, xseg);
-    if ((st = check_launch(c, "k_expand")) != SPHBI_OK) return st;
-  } else {
-    if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
-    if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
-    k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder, stub_base,
-                                                 dflags);
-    if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
-  }
+  PieceItem *isec, *iseg;
+  StubItem* istub;
+  if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
+  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder, stub_base,
+                                               dflags);
+  if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
+  const DenseItems items{rec, off, m, stub_base};
+  const WorkN wsec{(int64_t)n_sec, nullptr, 0}, wseg{(int64_t)n_seg, nullptr, 0};
   if (mode == 3) {
-    // P3 field: one launch per piece kind (stub classes share one code path)
     H24Out *qsec, *qstub, *qseg;
     if ((st = scratch_t(c, kBufOutC, n_sec, &qsec)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufOutB, n_stub, &qstub)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufOutS, n_seg, &qseg)) != SPHBI_OK) return st;
     const P3Consts& P = *p3->P;
-    if (n_stub) k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, n_stub, istub, two_pass ? nullptr : xstub, qstub);
-    if (n_sec) k_p3_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(P, n_sec, isec, xsec, qsec);
-    if (n_seg) k_p3_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(P, n_seg, iseg, xseg, qseg);
+    if (n_stub)
+      k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, WorkN{(int64_t)n_stub, nullptr, 0}, istub, nullptr, qstub);
+    if (n_sec) k_p3_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(P, wsec, isec, nullptr, qsec);
+    if (n_seg) k_p3_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(P, wseg, iseg, nullptr, qseg);
     if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
-    k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, rec, off, qsec, qstub, qseg, stub_base, p3->nodes,
-                                                  p3->pt, stride, dout);
-    (void)ps;
+    k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, items, ItemOuts{qsec, {qstub, qstub}, qseg},
+                                                  p3->nodes, p3->pt, stride, dout);
     return check_launch(c, "k_p3_combine");
   }
   AccOut *osec, *ostub, *oseg;
   if ((st = scratch_t(c, kBufOutC, n_sec, &osec)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutB, n_stub, &ostub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutS, n_seg, &oseg)) != SPHBI_OK) return st;
-  // piece kernels, thread per item; stubs one launch per class. A constant
-  // field (scene, tri_values == NULL) needs only the tau3 channels.
   const bool f1 = mode == 0 && src.vals == nullptr;
   AccOut3* ostub3 = reinterpret_cast<AccOut3*>(ostub);
-  // slot path: items stay in their pair slots, the index lists select them;
-  // two-pass path: items are dense per class
-  const StubItem* is[4];
-  const int* ix[4];
   for (int cl = 0; cl < 4; ++cl) {
-    is[cl] = two_pass ? istub + sbase[cl] : istub;
-    ix[cl] = two_pass ? nullptr : xstub + sbase[cl];
+    const unsigned long long nt = tot[1 + cl];
+    if (!nt) continue;
+    const WorkN w{(int64_t)nt, nullptr, 0};
+    const StubItem* is = istub + sbase[cl];
+    const int g = grid_for(nt, 128);
+    if (f1) {
+      AccOut3* o = ostub3 + sbase[cl];
+      switch (cl) {
+        case 0: k_pipe_stub<true, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 1: k_pipe_stub<true, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 2: k_pipe_stub<true, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        default: k_pipe_stub<true, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+      }
+    } else {
+      AccOut* o = ostub + sbase[cl];
+      switch (cl) {
+        case 0: k_pipe_stub<false, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 1: k_pipe_stub<false, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 2: k_pipe_stub<false, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        default: k_pipe_stub<false, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+      }
+    }
   }
   if (f1) {
-    if (tot[1]) k_pipe_stub<true, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ix[0], ostub3 + sbase[0]);
-    if (tot[2]) k_pipe_stub<true, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ix[1], ostub3 + sbase[1]);
-    if (tot[3]) k_pipe_stub<true, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ix[2], ostub3 + sbase[2]);
-    if (tot[4]) k_pipe_stub<true, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ix[3], ostub3 + sbase[3]);
-    if (n_sec) k_pipe_sector<true><<<grid_for(n_sec, 128), 128, 0, s>>>(K, n_sec, isec, xsec, osec);
-    if (n_seg) k_pipe_segment<true><<<grid_for(n_seg, 128), 128, 0, s>>>(K, n_seg, iseg, xseg, oseg);
+    if (n_sec) k_pipe_sector<true><<<grid_for(n_sec, 128), 128, 0, s>>>(K, wsec, isec, nullptr, osec);
+    if (n_seg) k_pipe_segment<true><<<grid_for(n_seg, 128), 128, 0, s>>>(K, wseg, iseg, nullptr, oseg);
   } else {
-    if (tot[1]) k_pipe_stub<false, 0><<<grid_for(tot[1], 128), 128, 0, s>>>(K, tot[1], is[0], ix[0], ostub + sbase[0]);
-    if (tot[2]) k_pipe_stub<false, 1><<<grid_for(tot[2], 128), 128, 0, s>>>(K, tot[2], is[1], ix[1], ostub + sbase[1]);
-    if (tot[3]) k_pipe_stub<false, 2><<<grid_for(tot[3], 128), 128, 0, s>>>(K, tot[3], is[2], ix[2], ostub + sbase[2]);
-    if (tot[4]) k_pipe_stub<false, 3><<<grid_for(tot[4], 128), 128, 0, s>>>(K, tot[4], is[3], ix[3], ostub + sbase[3]);
-    if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, n_sec, isec, xsec, osec);
-    if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, n_seg, iseg, xseg, oseg);
+    if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, wsec, isec, nullptr, osec);
+    if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, wseg, iseg, nullptr, oseg);
   }
   if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
-  const ItemOuts io{osec, ostub, oseg, stub_base};
+  const void* so = f1 ? (const void*)ostub3 : (const void*)ostub;
+  const ItemOuts io{osec, {so, so}, oseg};
   if (mode == 0) {
     if (f1)
-      k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
+      k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items, io, stride, dout);
     else
-      k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, rec, off, io, stride, dout);
-    if ((st = check_launch(c, "k_pipe_combine")) != SPHBI_OK) return st;
-  } else {
-    k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, rec, off, io, stride, dout);
-    if ((st = check_launch(c, "k_pipe_combine_bases")) != SPHBI_OK) return st;
+      k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items, io, stride, dout);
+    return check_launch(c, "k_pipe_combine");
   }
+  k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, items, io, stride, dout);
+  return check_launch(c, "k_pipe_combine_bases");
+}
+
+// Largest pair count one slot-path pass takes (item slots ~2.2 KB per pair,
+// output slots 28 x 48 / 144 / 384 B per pair for field == 1 / affine or
+// bases / P3); larger calls run in consecutive sub-chunks.
+int64_t slot_chunk(int mode, bool f1) {
+  if (mode == 3) return int64_t(1) << 19;
+  return f1 ? int64_t(kMaxChunkPairs) : int64_t(kMaxChunkPairs) / 2;
+}
+
+// K4 pipeline over n pairs (default: slot path, no host synchronisation).
+template <class Src>
+sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const Src& src, int64_t n, int mode,
+                          int stride, double* dout, unsigned* dflags, unsigned long long* ctr, PipeStats* ps,
+                          const P3Job* p3 = nullptr) {
   (void)ps;
-  return SPHBI_OK;
+  if (n <= 0) return SPHBI_OK;
+  if (c->force_exact || c->two_pass) return run_pipeline_dense(c, K, h, src, n, mode, stride, dout, dflags, ctr, p3);
+  const bool f1 = mode == 0 && src.vals == nullptr;
+  const int64_t cap = slot_chunk(mode, f1);
+  if (n > cap) {
+    for (int64_t o = 0; o < n; o += cap) {
+      const P3Job pj = p3 ? p3->shifted(o) : P3Job{nullptr, nullptr, nullptr};
+      const sphbi_status st = run_pipeline(c, K, h, src.shifted(o), std::min(cap, n - o), mode, stride,
+                                           dout + stride * o, dflags, ctr, nullptr, p3 ? &pj : nullptr);
+      if (st != SPHBI_OK) return st;
+    }
+    return SPHBI_OK;
+  }
+  cudaStream_t s = c->stream;
+  sphbi_status st;
+  NormRec* nrec;
+  int* porder;
+  if ((st = pre_classify(c, h, src, n, &nrec, &porder)) != SPHBI_OK) return st;
+  JRec* jrec;
+  if ((st = scratch_t(c, kBufPartial, n, &jrec)) != SPHBI_OK) return st;
+  PieceItem *isec, *iseg;
+  StubItem* istub;
+  if ((st = scratch_t(c, kBufItemsC, kCapSec * n, &isec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsB, kCapStub * n, &istub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufItemsS, kCapSeg * n, &iseg)) != SPHBI_OK) return st;
+  int* lists;
+  unsigned* lcount;
+  if ((st = scratch_t(c, kBufIdx, (kCapSec + 2 * kCapStub + kCapSeg) * n, &lists)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufPipeCnt, kKinds, &lcount)) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned) * kKinds, s));
+  const long long scap = static_cast<long long>(kCapStub) * n;
+  const SlotLists L{lists, {lists + kCapSec * n, lists + kCapSec * n + scap}, lists + kCapSec * n + 2 * scap, lcount,
+                    scap};
+  k_pipe_emit_slots<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr, dflags);
+  if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
+  const SlotItems items{jrec};
+  // Piece-kernel grids without a host round trip: the kernels read their item
+  // counts on the device and loop grid-stride, so any grid is correct; the
+  // grid is sized from the items-per-pair ratios of an earlier call (read back
+  // asynchronously, never waited for; 2 per pair before the first). Exact
+  // grids beat persistent ones here: fresh blocks keep the latency-bound
+  // piece kernels fed. SPHBI_ITEM_GRID=sync: read the counts back and wait;
+  // =persist: SMs x resident blocks.
+  if (cudaEventQuery(c->count_ev) == cudaSuccess && c->count_n > 0) {
+    for (int q = 0; q < kKinds; ++q) c->item_ratio[q] = static_cast<double>(c->h_counts[q]) / c->count_n;
+    c->count_n = 0;
+  } else {
+    cudaGetLastError();  // cudaErrorNotReady
+  }
+  unsigned hc[kKinds] = {0, 0, 0, 0, 0, 0};
+  const unsigned* dcount = lcount;
+  if (c->item_grid == 1) {
+    unsigned* hp = c->h_flags + 32;
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(hp, lcount, sizeof(unsigned) * kKinds, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int q = 0; q < kKinds; ++q) hc[q] = hp[q];
+    dcount = nullptr;
+  } else if (c->count_n == 0 && cudaEventQuery(c->count_ev) == cudaSuccess) {
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_counts, lcount, sizeof(unsigned) * kKinds, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaEventRecord(c->count_ev, s));
+    c->count_n = n;
+  } else {
+    cudaGetLastError();
+  }
+  auto wn = [&](int q, int64_t back) { return WorkN{hc[q], dcount ? dcount + q : nullptr, back}; };
+  const WorkN wsec = wn(0, 0), wseg = wn(5, 0);
+  // stub classes 0 / 2 fill their buffer from the front, 1 / 3 from the back
+  const WorkN wst[4] = {wn(1, 0), wn(2, scap), wn(3, 0), wn(4, scap)};
+  auto igrid = [&](auto* fn, int q) {
+    if (c->item_grid == 1) return grid_for(hc[q], 128);
+    if (c->item_grid == 2) return rgrid(c, fn);
+    const double est = 1.1 * c->item_ratio[q] * static_cast<double>(n) + 256.0;
+    return std::max(grid_for(static_cast<int64_t>(est), 128), c->sms);
+  };
+  const int* xst[4] = {L.stub[0], L.stub[0], L.stub[1], L.stub[1]};
+  if (mode == 3) {
+    H24Out *qsec, *qstub, *qseg;
+    if ((st = scratch_t(c, kBufOutC, kCapSec * n, &qsec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutB, 2 * scap, &qstub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &qseg)) != SPHBI_OK) return st;
+    H24Out* qst[4] = {qstub, qstub, qstub + scap, qstub + scap};
+    const P3Consts& P = *p3->P;
+    for (int cl = 0; cl < 4; ++cl) k_p3_stub<<<igrid(k_p3_stub, 1 + cl), 128, 0, s>>>(P, wst[cl], istub, xst[cl], qst[cl]);
+    k_p3_sector<<<igrid(k_p3_sector, 0), 128, 0, s>>>(P, wsec, isec, L.sec, qsec);
+    k_p3_segment<<<igrid(k_p3_segment, 5), 128, 0, s>>>(P, wseg, iseg, L.seg, qseg);
+    if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
+    k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, items,
+                                                  ItemOuts{qsec, {qstub, qstub + scap}, qseg}, p3->nodes, p3->pt,
+                                                  stride, dout);
+    return check_launch(c, "k_p3_combine");
+  }
+  if (f1) {
+    AccOut3 *osec, *ostub, *oseg;
+    if ((st = scratch_t(c, kBufOutC, kCapSec * n, &osec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutB, 2 * scap, &ostub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &oseg)) != SPHBI_OK) return st;
+    AccOut3* ost[4] = {ostub, ostub, ostub + scap, ostub + scap};
+    k_pipe_stub<true, 0><<<igrid(k_pipe_stub<true, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0]);
+    k_pipe_stub<true, 1><<<igrid(k_pipe_stub<true, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1]);
+    k_pipe_stub<true, 2><<<igrid(k_pipe_stub<true, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2]);
+    k_pipe_stub<true, 3><<<igrid(k_pipe_stub<true, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3]);
+    k_pipe_sector<true><<<igrid(k_pipe_sector<true>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
+    k_pipe_segment<true><<<igrid(k_pipe_segment<true>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
+    if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+    k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items,
+                                                          ItemOuts{osec, {ostub, ostub + scap}, oseg}, stride, dout);
+    return check_launch(c, "k_pipe_combine");
+  }
+  AccOut *osec, *ostub, *oseg;
+  if ((st = scratch_t(c, kBufOutC, kCapSec * n, &osec)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutB, 2 * scap, &ostub)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &oseg)) != SPHBI_OK) return st;
+  AccOut* ost[4] = {ostub, ostub, ostub + scap, ostub + scap};
+  k_pipe_stub<false, 0><<<igrid(k_pipe_stub<false, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0]);
+  k_pipe_stub<false, 1><<<igrid(k_pipe_stub<false, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1]);
+  k_pipe_stub<false, 2><<<igrid(k_pipe_stub<false, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2]);
+  k_pipe_stub<false, 3><<<igrid(k_pipe_stub<false, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3]);
+  k_pipe_sector<false><<<igrid(k_pipe_sector<false>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
+  k_pipe_segment<false><<<igrid(k_pipe_segment<false>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
+  if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+  const ItemOuts io{osec, {ostub, ostub + scap}, oseg};
+  if (mode == 0) {
+    k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items, io, stride, dout);
+    return check_launch(c, "k_pipe_combine");
+  }
+  k_pipe_combine_bases<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, h, items, io, stride, dout);
+  return check_launch(c, "k_pipe_combine_bases");
 }
 
 bool is_pinned(const void* p) {
@@ -1630,11 +1954,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     SPHBI_CUDA_TRY(cudaMemcpyAsync(dv, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
   }
   // particle-aligned chunks (pairs sorted by particle: boundaries by binary search)
-#ifndef SPHBI_STREAM_CHUNK_LOG2
-#define SPHBI_STREAM_CHUNK_LOG2 20
-#endif
-  const int nchunks =
-      (int)std::min<int64_t>(32, std::max<int64_t>(2, n_particles >> SPHBI_STREAM_CHUNK_LOG2));
+  const int nchunks = (int)std::min<int64_t>(64, std::max<int64_t>(2, n_particles >> c->stream_chunk_log2));
   std::vector<int64_t> pb(nchunks + 1), qb(nchunks + 1);
   for (int k = 0; k <= nchunks; ++k) {
     pb[k] = n_particles * k / nchunks;
@@ -1764,9 +2084,16 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   SPHBI_CUDA_TRY(cudaSetDevice(device));
   sphbi_ctx* c = new sphbi_ctx();
   c->device = device;
+  c->sms = prop.multiProcessorCount;
   {
     const char* tp = std::getenv("SPHBI_TWO_PASS");
     c->two_pass = tp && tp[0] == '1';
+    const char* ig = std::getenv("SPHBI_ITEM_GRID");
+    c->item_grid = !ig ? 0 : (std::strcmp(ig, "sync") == 0 ? 1 : (std::strcmp(ig, "persist") == 0 ? 2 : 0));
+    const char* ns = std::getenv("SPHBI_NO_SIG_SORT");
+    c->no_sig_sort = ns && ns[0] == '1';
+    const char* cl = std::getenv("SPHBI_STREAM_CHUNK_LOG2");
+    if (cl) c->stream_chunk_log2 = std::max(12, std::min(26, std::atoi(cl)));
   }
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -1779,6 +2106,8 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaMallocHost(&c->h_flags, 512);
+  cudaMallocHost(&c->h_counts, 64);
+  cudaEventCreateWithFlags(&c->count_ev, cudaEventDisableTiming);
   if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
     cudaGetLastError();
     return fail(SPHBI_ERR_OUT_OF_MEMORY, "counter allocation failed");
@@ -1800,6 +2129,8 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->h_flags) cudaFreeHost(c->h_flags);
+  if (c->h_counts) cudaFreeHost(c->h_counts);
+  if (c->count_ev) cudaEventDestroy(c->count_ev);
   if (c->d_counters) cudaFree(c->d_counters);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
@@ -2452,8 +2783,24 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   return SPHBI_OK;
 }
 
-// Public entry points: a bounded (sync-free) pipeline that overflowed its
-// work-item buffers is redone once with exact, host-sized buffers.
+// Public entry points: a slot-path pipeline in which a pair overflowed its
+// item slots (dflags[1] bit 2 -> c->overflowed) is redone once with the
+// exact two-pass pipeline.
+}  // extern "C"
+template <class F>
+static sphbi_status retry_exact(sphbi_ctx* c, F&& f) {
+  if (c) c->overflowed = false;
+  sphbi_status st = f();
+  if (c && c->overflowed) {
+    c->overflowed = false;
+    c->force_exact = true;
+    st = f();
+    c->force_exact = false;
+  }
+  return st;
+}
+extern "C" {
+
 sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
                                    const double* query_xy, const double* tri_xy, const double* values,
                                    int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
@@ -2491,9 +2838,9 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
 
 // P3 (10-node cubic Lagrange) fields -- BASELINE configs[3]; no reference
 // interface (the reference's term table is affine-only, triangle_integrator.hpp:104-118).
-sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
-                                      const double* query_xy, const double* tri_xy, const double* nodal10,
-                                      double* out, uint32_t* status_out, sphbi_memory mem) {
+static sphbi_status integrate_pairs_p3_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                           const double* query_xy, const double* tri_xy, const double* nodal10,
+                                           double* out, uint32_t* status_out, sphbi_memory mem) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (n < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "n < 0");
@@ -2536,8 +2883,19 @@ sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* ker
   if (mem == SPHBI_MEM_HOST) SPHBI_CUDA_TRY(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
   if (status_out && mem == SPHBI_MEM_HOST) std::memset(status_out, 0, 4 * n);
+  if (c->h_flags[1] & 4u) {
+    c->overflowed = true;
+    return SPHBI_ERR_INTERNAL;
+  }
   if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "integrate_triangle_p3: reference-domain error on device");
   return SPHBI_OK;
+}
+sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
+                                      const double* query_xy, const double* tri_xy, const double* nodal10,
+                                      double* out, uint32_t* status_out, sphbi_memory mem) {
+  return retry_exact(c, [&] {
+    return integrate_pairs_p3_impl(c, kernel, h, n, query_xy, tri_xy, nodal10, out, status_out, mem);
+  });
 }
 
 sphbi_status sphbi_evaluate_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n_particles,
@@ -2548,9 +2906,11 @@ sphbi_status sphbi_evaluate_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, do
                                sphbi_memory mem) {
   if (!nodal10 && n_triangles > 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "nodal10 is NULL");
   static const double kNoNodes = 0.0;
-  return evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs, pair_particle,
-                       pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats, mem,
-                       nodal10 ? nodal10 : &kNoNodes);
+  return retry_exact(c, [&] {
+    return evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs,
+                         pair_particle, pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats,
+                         mem, nodal10 ? nodal10 : &kNoNodes);
+  });
 }
 
 // ---- vertex-basis cache + field sweeps -------------
@@ -2566,9 +2926,11 @@ sphbi_status sphbi_bases_create(sphbi_ctx* c, const sphbi_kernel_desc* kernel, d
   bc->n_particles = n_particles;
   bc->n_triangles = n_triangles;
   bc->h = h;
-  const sphbi_status st =
-      evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs, pair_particle,
-                    pair_triangle, nullptr, nullptr, nullptr, nullptr, stats, mem, nullptr, bc.get());
+  const sphbi_status st = retry_exact(c, [&] {
+    return evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, n_pairs,
+                         pair_particle, pair_triangle, nullptr, nullptr, nullptr, nullptr, stats, mem, nullptr,
+                         bc.get());
+  });
   if (st != SPHBI_OK) {
     bc->release();
     return st;
@@ -2693,6 +3055,59 @@ sphbi_status sphbi_bases_apply(sphbi_basis_cache* bc, int32_t variant, const dou
   return SPHBI_OK;
 }
 
+static sphbi_status bases_pairs_impl(sphbi_basis_cache* bc, const double* pair_weights, int normal,
+                                    double* out_value, double* out_grad, sphbi_memory mem) {
+  if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
+  if (!out_grad) return fail(SPHBI_ERR_INVALID_ARGUMENT, "out_grad is NULL");
+  sphbi_ctx* c = bc->ctx;
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  const int64_t n = bc->n_particles, P = bc->n_pairs;
+  if (n <= 0) return SPHBI_OK;
+  const double* dw = pair_weights;
+  double *ov = out_value, *og = out_grad;
+  if (mem == SPHBI_MEM_HOST) {
+    // staging: [grad 2n | value n | weights P]
+    const size_t need = static_cast<size_t>(3 * n + (pair_weights ? P : 0) + 1);
+    if (bc->stage_cap < need) {
+      if (bc->stage) cudaFree(bc->stage);
+      bc->stage = nullptr;
+      bc->stage_cap = 0;
+      if (cudaMalloc(&bc->stage, 8 * need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPHBI_ERR_OUT_OF_MEMORY, "basis cache: staging cudaMalloc failed");
+      }
+      bc->stage_cap = need;
+    }
+    og = bc->stage;
+    ov = out_value ? og + 2 * n : nullptr;
+    if (pair_weights) {
+      double* sw = og + 3 * n;
+      if (P) SPHBI_CUDA_TRY(cudaMemcpyAsync(sw, pair_weights, 8 * P, cudaMemcpyHostToDevice, s));
+      dw = sw;
+    }
+  }
+  const int np = static_cast<int>(n);
+  k_bases_apply_pairs<<<grid_for(np, 256), 256, 0, s>>>(np, bc->row_ptr, bc->bases, dw, normal, ov, og);
+  sphbi_status st;
+  if ((st = check_launch(c, "k_bases_apply_pairs")) != SPHBI_OK) return st;
+  if (mem == SPHBI_MEM_HOST) {
+    if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, ov, 8 * n, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, og, 16 * n, cudaMemcpyDeviceToHost, s));
+  }
+  SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_bases_apply_pairs(sphbi_basis_cache* bc, const double* pair_weights, double* out_value,
+                                     double* out_grad, sphbi_memory mem) {
+  return bases_pairs_impl(bc, pair_weights, 0, out_value, out_grad, mem);
+}
+
+sphbi_status sphbi_boundary_normals(sphbi_basis_cache* bc, double* out_normal, sphbi_memory mem) {
+  return bases_pairs_impl(bc, nullptr, 1, nullptr, out_normal, mem);
+}
+
 sphbi_status sphbi_bases_destroy(sphbi_basis_cache* bc) {
   if (!bc) return SPHBI_OK;
   cudaSetDevice(bc->ctx->device);
@@ -2723,9 +3138,11 @@ sphbi_status sphbi_evaluate_piecewise(sphbi_ctx* c, int32_t n_pieces, const sphb
     if (st != SPHBI_OK) return st;
     ps->h[j] = scales[j] * h;
   }
-  return evaluate_impl(c, pieces, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
-                       pair_particle, pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats,
-                       mem, nullptr, nullptr, ps.get());
+  return retry_exact(c, [&] {
+    return evaluate_impl(c, pieces, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
+                         pair_particle, pair_triangle, out_value, out_grad, pair_list_out, pair_list_capacity, stats,
+                         mem, nullptr, nullptr, ps.get());
+  });
 }
 
 }  // extern "C"

@@ -708,6 +708,24 @@ class BasisCache:
         self.last_ms = ms.value
         return out_v, out_g
 
+    def apply_pairs(self, pair_weights=None):
+        """Per-particle sums over the cached pairs of w_k * integrate_triangle(p, h, T_k)
+        (field 1 per pair); pair_weights in cache pair order (read()), None = 1."""
+        w = None if pair_weights is None else np.ascontiguousarray(pair_weights, dtype=np.float64).reshape(-1)
+        if w is not None and w.shape[0] != self.n_pairs:
+            raise InvalidArgument("apply_pairs: one weight per cached pair")
+        out_v = np.zeros(self.n, dtype=np.float64)
+        out_g = np.zeros((self.n, 2), dtype=np.float64)
+        _raise(self.ctx.lib.sphbi_bases_apply_pairs(self.handle, _ptr(w), _ptr(out_v), _ptr(out_g), N.MEM_HOST),
+               "bases_apply_pairs")
+        return out_v, out_g
+
+    def boundary_normals(self):
+        """-n/|n| per particle, n = sum_T int grad W (field 1); zero if |n| <= 1e-12."""
+        out = np.zeros((self.n, 2), dtype=np.float64)
+        _raise(self.ctx.lib.sphbi_boundary_normals(self.handle, _ptr(out), N.MEM_HOST), "boundary_normals")
+        return out
+
     def close(self):
         if getattr(self, "handle", None):
             self.ctx.lib.sphbi_bases_destroy(self.handle)

@@ -102,3 +102,43 @@ TEST(EvaluateApi, BasisSweepVariantsMatchWeightedIntegrals) {
   rho[3][1] = -1.0;
   EXPECT_THROW(sweep.apply(sphbi::GradientVariant::difference, A, rho, a0, rho0), std::domain_error);
 }
+
+// SPH coupling: contact-point channel and boundary normals
+// against per-pair sphbi::integrate_triangle with a constant field.
+TEST(EvaluateApi, CouplingPairWeightsAndNormals) {
+  const Scene s = make_scene(17);
+  const double h = 0.3;
+  const auto table = sphbi::table1_terms(sphbi::wendland4());
+  sphbi::BasisSweep sweep(s.particles, h, s.mesh, table, &s.pairs);
+  const std::int64_t m = sweep.pair_count();
+  ASSERT_EQ(m, static_cast<std::int64_t>(s.pairs.size()));  // explicit pairs, kept in (particle, triangle) order
+  std::vector<double> w(m);
+  for (std::int64_t k = 0; k < m; ++k) w[k] = 0.5 + 0.25 * static_cast<double>(k % 7);
+  const auto res = sweep.apply_pairs(w);
+  const auto nrm = sweep.boundary_normals();
+  const std::array<double, 3> one{1.0, 1.0, 1.0};
+  for (std::size_t i = 0; i < s.particles.size(); ++i) {
+    double v = 0, gx = 0, gy = 0, nx = 0, ny = 0;
+    for (std::size_t t = 0; t < s.mesh.size(); ++t) {
+      const std::size_t k = i * s.mesh.size() + t;
+      const auto r = sphbi::integrate_triangle(s.particles[i], h, s.mesh[t], one, table);
+      v += w[k] * r.value;
+      gx += w[k] * r.gradient[0];
+      gy += w[k] * r.gradient[1];
+      nx += r.gradient[0];
+      ny += r.gradient[1];
+    }
+    const double sc = 2.0;  // max |w|
+    EXPECT_LE(std::abs(res[i].value - v), sc * tol(res[i].value, v, table.normalization, h));
+    EXPECT_LE(std::abs(res[i].gradient[0] - gx), sc * tol(res[i].gradient[0], gx, table.normalization, h));
+    EXPECT_LE(std::abs(res[i].gradient[1] - gy), sc * tol(res[i].gradient[1], gy, table.normalization, h));
+    const double mag = std::hypot(nx, ny);
+    if (mag > 1e-6) {
+      EXPECT_NEAR(nrm[i].x, -nx / mag, 1e-10);
+      EXPECT_NEAR(nrm[i].y, -ny / mag, 1e-10);
+    } else if (mag <= 1e-12) {
+      EXPECT_EQ(nrm[i].x, 0.0);
+      EXPECT_EQ(nrm[i].y, 0.0);
+    }
+  }
+}
