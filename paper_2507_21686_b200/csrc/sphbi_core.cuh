@@ -859,9 +859,50 @@ SPHBI_HD Frame rotation_taking_to_x(P2 v, Sink& c) {
   return Frame{v.x / n, v.y / n, -v.y / n, v.x / n};
 }
 
+// Frame and opening angle of a sector (:352-360), given the rotation f taking
+// v1 onto +x: mirror so that v2 lies in the upper half plane, gamma = its angle.
+SPHBI_HD void sector_frame_angle(P2 v1, P2 v2, Frame& f, double& gamma) {
+  (void)v1;
+  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
+  if (w2.y < 0.0) {
+    f.m10 = -f.m10;
+    f.m11 = -f.m11;
+    w2.y = -w2.y;
+  }
+  gamma = d_atan2(w2.y, w2.x);
+}
+// Deferred sector (work-item pipeline): the same operations from the raw
+// chord points, in the (converged) piece kernel. v1 is a crossing point, so
+// its norm is ~1 and rotation_taking_to_x's degeneracy test cannot fire.
+SPHBI_HD void sector_from_raw(P2 v1, P2 v2, Frame& f, double& gamma) {
+  const double n = p_norm(v1);
+  f = Frame{v1.x / n, v1.y / n, -v1.y / n, v1.x / n};
+  sector_frame_angle(v1, v2, f, gamma);
+}
+
+// Frame and angles of a direct stub (:440-462): rotation taking v1 onto +x
+// (r1 == p_norm(v1), computed by the caller), mirrored so v2 lies above;
+// gamma = opening angle, beta = angle at v1 between the chord and the origin.
+// Identical operations whether called by the geometry pass or, deferred, by
+// the stub piece kernels.
+SPHBI_HD void stub_frame_angles(P2 v1, P2 v2, double r1, Frame& f, double& gamma, double& beta) {
+  f = Frame{v1.x / r1, v1.y / r1, -v1.y / r1, v1.x / r1};
+  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
+  if (w2.y < 0.0) {
+    f.m10 = -f.m10;
+    f.m11 = -f.m11;
+    w2.y = -w2.y;
+  }
+  gamma = d_atan2(w2.y, w2.x);
+  const P2 cc = p_sub(v2, v1);
+  beta = d_atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
+}
+
 // region_sector(v1, v2, l) (:349-366); the hot path always passes l = 1.
 // Sink::kAngles selects how much of a piece the geometry works out:
 //   2  frames and angles (gamma = atan2, beta = atan2)
+//   1  raw piece geometry (chord points, r1); the piece kernels derive frames
+//      and angles (sector_from_raw / stub_frame_angles) where warps converge
 //   0  piece kinds and window bounds only (count pass: no frames, no angles;
 //      the emit pass repeats the geometry and reports every status)
 template <class Sink>
@@ -870,15 +911,14 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
     c.sector(Frame{1.0, 0.0, 0.0, 1.0}, 0.0, fmin(l, 1.0), sign);
     return;
   }
-  Frame f = rotation_taking_to_x(v1, c);
-  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
-  if (w2.y < 0.0) {
-    f.m10 = -f.m10;
-    f.m11 = -f.m11;
-    w2.y = -w2.y;
+  if constexpr (Sink::kAngles == 1) {
+    c.sector_raw(v1, v2, fmin(l, 1.0), sign);
+  } else {
+    Frame f = rotation_taking_to_x(v1, c);
+    double gamma;
+    sector_frame_angle(v1, v2, f, gamma);
+    c.sector(f, gamma, fmin(l, 1.0), sign);
   }
-  const double gamma = d_atan2(w2.y, w2.x);
-  c.sector(f, gamma, fmin(l, 1.0), sign);
 }
 
 // stub_integral validation (elementary_regions.hpp:179-183)
@@ -898,18 +938,17 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
     c.stub(Frame{1.0, 0.0, 0.0, 1.0}, 0.0, l, D, 0.0, lo, u, window, sign);
     return;
   }
-  Frame f = rotation_taking_to_x(v1, c);
-  P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
-  if (w2.y < 0.0) {
-    f.m10 = -f.m10;
-    f.m11 = -f.m11;
-    w2.y = -w2.y;
+  if constexpr (Sink::kAngles == 1) {
+    c.stub_raw(v1, v2, r1, l, D, lo, u, window, sign);
+  } else {
+    // r1 = p_norm(v1) > 0 (stub_process rejected r2 < kGeomEps <= r1), so
+    // rotation_taking_to_x's degeneracy test cannot fire here
+    Frame f;
+    double gamma, beta;
+    stub_frame_angles(v1, v2, r1, f, gamma, beta);
+    if (window && !stub_beta_ok(beta)) c.status |= kStatusDomain;
+    c.stub(f, gamma, l, D, beta, lo, u, window, sign);
   }
-  const double gamma = d_atan2(w2.y, w2.x);
-  const P2 cc = p_sub(v2, v1);
-  const double beta = d_atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
-  if (window && !stub_beta_ok(beta)) c.status |= kStatusDomain;
-  c.stub(f, gamma, l, D, beta, lo, u, window, sign);
 }
 
 // ---------------------------------------------------------------------------

@@ -251,18 +251,33 @@ __global__ void __launch_bounds__(kEvalBlock)
 //           same straight-line FP64 / double-double code (converged)
 //   combine: thread per pair sums its items in the particle frame (fixed
 //           order, double-double) and applies the barycentric field.
-struct PieceItem {  // sector (a = gamma) / segment (a = d)
+// Sector items carry their raw chord points (pad == 0: m00, m01 = v1 and
+// m10, m11 = v2; the sector kernel derives frame and angle, sector_from_raw);
+// half discs (pad == 1) and segments (a = d) carry their frame.
+struct PieceItem {
   int pair;
   int pad;
   double sign, m00, m01, m10, m11;
   double a;
 };
-struct StubItem {  // direct stub: cone (gamma, l) + radial window [lo, u] (D, beta)
+// Direct stub: cone (gamma, l) + radial window [lo, u] at distance D. The
+// geometry pass stores the raw stub (v1, v2, r1 = |v1|); the stub kernels
+// derive frame, gamma and beta (stub_frame_angles), in converged warps.
+struct StubItem {
   int pair;
   int window;
-  double sign, m00, m01, m10, m11;
-  double gamma, l, D, beta, lo, u;
+  double sign, v1x, v1y, v2x, v2y, r1;
+  double l, D, lo, u;
 };
+__device__ __forceinline__ void stub_item_geometry(const StubItem& it, Frame& f, double& gamma, double& beta,
+                                                   unsigned* status_or) {
+  stub_frame_angles(P2{it.v1x, it.v1y}, P2{it.v2x, it.v2y}, it.r1, f, gamma, beta);
+  // stub_integral's beta validation (elementary_regions.hpp:179-183)
+  if (it.window && !stub_beta_ok(beta)) atomicOr(status_or, kStatusDomain);
+}
+__device__ __forceinline__ void sector_item_geometry(const PieceItem& it, Frame& f, double& gamma) {
+  sector_from_raw(P2{it.m00, it.m01}, P2{it.m10, it.m11}, f, gamma);
+}
 
 struct AccOut {  // one piece's rotated contribution (9 dd)
   double v[18];
@@ -310,8 +325,39 @@ struct CountSink {
   __device__ void segment(const Frame&, double, double) { ++n[5]; }
 };
 
+// Raw stub / sector items (Sink::kAngles == 1)
+__device__ __forceinline__ StubItem make_stub_item(int pair, P2 v1, P2 v2, double r1, double l, double D, double lo,
+                                                   double u, bool window, double sign) {
+  StubItem it;
+  it.pair = pair;
+  it.window = window ? 1 : 0;
+  it.sign = sign;
+  it.v1x = v1.x;
+  it.v1y = v1.y;
+  it.v2x = v2.x;
+  it.v2y = v2.y;
+  it.r1 = r1;
+  it.l = l;
+  it.D = D;
+  it.lo = lo;
+  it.u = u;
+  return it;
+}
+__device__ __forceinline__ PieceItem make_sector_item(int pair, P2 v1, P2 v2, double sign) {
+  PieceItem it;
+  it.pair = pair;
+  it.pad = 0;
+  it.sign = sign;
+  it.m00 = v1.x;
+  it.m01 = v1.y;
+  it.m10 = v2.x;
+  it.m11 = v2.y;
+  it.a = 0.0;
+  return it;
+}
+
 struct EmitSink {
-  static constexpr int kAngles = 2;
+  static constexpr int kAngles = 1;
   const KernelConsts* K;
   unsigned status;
   int pair;
@@ -341,23 +387,10 @@ struct EmitSink {
     put(sector_items, f, sign, 0.0);
     d->pad = 1;
   }
-  __device__ void sector(const Frame& f, double gamma, double, double sign) { put(sector_items, f, sign, gamma); }
-  __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
-                       bool window, double sign) {
-    StubItem it;
-    it.pair = pair;
-    it.window = window ? 1 : 0;
-    it.sign = sign;
-    it.m00 = f.m00;
-    it.m01 = f.m01;
-    it.m10 = f.m10;
-    it.m11 = f.m11;
-    it.gamma = gamma;
-    it.l = l;
-    it.D = D;
-    it.beta = beta;
-    it.lo = lo;
-    it.u = u;
+  __device__ void sector_raw(P2 v1, P2 v2, double, double sign) { *sector_items++ = make_sector_item(pair, v1, v2, sign); }
+  __device__ void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window,
+                           double sign) {
+    const StubItem it = make_stub_item(pair, v1, v2, r1, l, D, lo, u, window, sign);
     switch (stub_class(D, lo, u, window)) {
       case 0: *stub0++ = it; break;
       case 1: *stub1++ = it; break;
@@ -583,15 +616,18 @@ __global__ void __launch_bounds__(128)
   SPHBI_ITEM_LOOP(k) {
     const int64_t slot = idx ? idx[k] : k;
     const PieceItem it = items[slot];
-    const Frame f{it.m00, it.m01, it.m10, it.m11};
-    // pad == 1: a half disc in frame f (segment_body's |d| < 1e-9 route)
+    // pad == 1: a half disc in frame f (segment_body's |d| < 1e-9 route);
+    // pad == 0: a sector from its raw chord points
+    Frame f{it.m00, it.m01, it.m10, it.m11};
+    double gamma = 0.0;
+    if (!it.pad) sector_item_geometry(it, f, gamma);
     if constexpr (F1) {
       PairAcc3 a;
       acc3_zero(a);
       if (it.pad)
         piece_half_disc3(K, a, f, it.sign);
       else
-        piece_cone3(K, a, f, it.a, 1.0, it.sign);
+        piece_cone3(K, a, f, gamma, 1.0, it.sign);
       acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
     } else {
       PairAcc a;
@@ -599,7 +635,7 @@ __global__ void __launch_bounds__(128)
       if (it.pad)
         piece_half_disc(K, a, f, it.sign);
       else
-        piece_cone(K, a, f, it.a, 1.0, it.sign);
+        piece_cone(K, a, f, gamma, 1.0, it.sign);
       acc_to_out(a, static_cast<AccOut*>(out)[k]);
     }
   }
@@ -620,7 +656,7 @@ __global__ void __launch_bounds__(128)
 constexpr int kCapSec = 8, kCapStub = 16, kCapSeg = 4;  // sector slots also hold half discs
 
 struct SlotSink {
-  static constexpr int kAngles = 2;
+  static constexpr int kAngles = 1;
   const KernelConsts* K;
   unsigned status;
   int pair;
@@ -655,9 +691,9 @@ struct SlotSink {
     }
     ++nsec;
   }
-  __device__ void sector(const Frame& f, double gamma, double, double sign) {
+  __device__ void sector_raw(P2 v1, P2 v2, double, double sign) {
     if (nsec < kCapSec)
-      sec[nsec] = piece(f, sign, gamma);
+      sec[nsec] = make_sector_item(pair, v1, v2, sign);
     else
       overflow = true;
     ++nsec;
@@ -669,25 +705,11 @@ struct SlotSink {
       overflow = true;
     ++nseg;
   }
-  __device__ void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u,
-                       bool window, double sign) {
+  __device__ void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window,
+                           double sign) {
     const int cls = stub_class(D, lo, u, window);
     if (nstub < kCapStub) {
-      StubItem it;
-      it.pair = pair;
-      it.window = window ? 1 : 0;
-      it.sign = sign;
-      it.m00 = f.m00;
-      it.m01 = f.m01;
-      it.m10 = f.m10;
-      it.m11 = f.m11;
-      it.gamma = gamma;
-      it.l = l;
-      it.D = D;
-      it.beta = beta;
-      it.lo = lo;
-      it.u = u;
-      stubs[nstub] = it;
+      stubs[nstub] = make_stub_item(pair, v1, v2, r1, l, D, lo, u, window, sign);
       cls_bits |= static_cast<unsigned>(cls) << (2 * nstub);
     } else {
       overflow = true;
@@ -820,20 +842,22 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
 template <bool F1, int CLS>
 __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     k_pipe_stub(const __grid_constant__ KernelConsts K, WorkN wn, const StubItem* __restrict__ items,
-                const int* __restrict__ idx, void* __restrict__ out) {
+                const int* __restrict__ idx, void* __restrict__ out, unsigned* status_or) {
   SPHBI_ITEM_LOOP(k) {
     const int64_t slot = idx ? idx[k] : k;
     const StubItem it = items[slot];
-    const Frame f{it.m00, it.m01, it.m10, it.m11};
+    Frame f;
+    double gamma, beta;
+    stub_item_geometry(it, f, gamma, beta, status_or);
     if constexpr (F1) {
       PairAcc3 a;
       acc3_zero(a);
-      piece_stub3<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+      piece_stub3<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign);
       acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
     } else {
       PairAcc a;
       acc_zero(a);
-      piece_stub_k<CLS>(K, a, f, it.gamma, it.l, it.D, it.beta, it.lo, it.u, it.window != 0, it.sign);
+      piece_stub_k<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign);
       acc_to_out(a, static_cast<AccOut*>(out)[k]);
     }
   }
@@ -1060,29 +1084,36 @@ __global__ void __launch_bounds__(128)
     const int64_t slot = idx ? idx[k] : k;
     const PieceItem it = items[slot];
     H24 H, acc;
-    if (it.pad)
+    Frame f{it.m00, it.m01, it.m10, it.m11};
+    if (it.pad) {
       h24_half_disc(P, H);
-    else
-      h24_cone(P, it.a, 1.0, H);
+    } else {
+      double gamma;
+      sector_item_geometry(it, f, gamma);
+      h24_cone(P, gamma, 1.0, H);
+    }
     h24_zero(acc);
-    h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+    h24_accumulate(acc, H, f, it.sign);
     h24_store(acc, out[k]);
   }
 }
 __global__ void __launch_bounds__(128)
     k_p3_stub(const __grid_constant__ P3Consts P, WorkN wn, const StubItem* __restrict__ items,
-              const int* __restrict__ idx, H24Out* __restrict__ out) {
+              const int* __restrict__ idx, H24Out* __restrict__ out, unsigned* status_or) {
   SPHBI_ITEM_LOOP(k) {
     const int64_t slot = idx ? idx[k] : k;
     const StubItem it = items[slot];
+    Frame f;
+    double gamma, beta;
+    stub_item_geometry(it, f, gamma, beta, status_or);
     H24 H, acc;
-    h24_cone(P, it.gamma, it.l, H);
+    h24_cone(P, gamma, it.l, H);
     if (it.window) {
-      h24_stub_bound(P, it.u, it.D, it.beta, 1.0, H);
-      h24_stub_bound(P, it.lo, it.D, it.beta, -1.0, H);
+      h24_stub_bound(P, it.u, it.D, beta, 1.0, H);
+      h24_stub_bound(P, it.lo, it.D, beta, -1.0, H);
     }
     h24_zero(acc);
-    h24_accumulate(acc, H, Frame{it.m00, it.m01, it.m10, it.m11}, it.sign);
+    h24_accumulate(acc, H, f, it.sign);
     h24_store(acc, out[k]);
   }
 }
@@ -1719,7 +1750,7 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
     if ((st = scratch_t(c, kBufOutS, n_seg, &qseg)) != SPHBI_OK) return st;
     const P3Consts& P = *p3->P;
     if (n_stub)
-      k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, WorkN{(int64_t)n_stub, nullptr, 0}, istub, nullptr, qstub);
+      k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, WorkN{(int64_t)n_stub, nullptr, 0}, istub, nullptr, qstub, dflags);
     if (n_sec) k_p3_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(P, wsec, isec, nullptr, qsec);
     if (n_seg) k_p3_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(P, wseg, iseg, nullptr, qseg);
     if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
@@ -1742,18 +1773,18 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
     if (f1) {
       AccOut3* o = ostub3 + sbase[cl];
       switch (cl) {
-        case 0: k_pipe_stub<true, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        case 1: k_pipe_stub<true, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        case 2: k_pipe_stub<true, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        default: k_pipe_stub<true, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 0: k_pipe_stub<true, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        case 1: k_pipe_stub<true, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        case 2: k_pipe_stub<true, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        default: k_pipe_stub<true, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
       }
     } else {
       AccOut* o = ostub + sbase[cl];
       switch (cl) {
-        case 0: k_pipe_stub<false, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        case 1: k_pipe_stub<false, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        case 2: k_pipe_stub<false, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
-        default: k_pipe_stub<false, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o); break;
+        case 0: k_pipe_stub<false, 0><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        case 1: k_pipe_stub<false, 1><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        case 2: k_pipe_stub<false, 2><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
+        default: k_pipe_stub<false, 3><<<g, 128, 0, s>>>(K, w, is, nullptr, o, dflags); break;
       }
     }
   }
@@ -1874,7 +1905,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &qseg)) != SPHBI_OK) return st;
     H24Out* qst[4] = {qstub, qstub, qstub + scap, qstub + scap};
     const P3Consts& P = *p3->P;
-    for (int cl = 0; cl < 4; ++cl) k_p3_stub<<<igrid(k_p3_stub, 1 + cl), 128, 0, s>>>(P, wst[cl], istub, xst[cl], qst[cl]);
+    for (int cl = 0; cl < 4; ++cl) k_p3_stub<<<igrid(k_p3_stub, 1 + cl), 128, 0, s>>>(P, wst[cl], istub, xst[cl], qst[cl], dflags);
     k_p3_sector<<<igrid(k_p3_sector, 0), 128, 0, s>>>(P, wsec, isec, L.sec, qsec);
     k_p3_segment<<<igrid(k_p3_segment, 5), 128, 0, s>>>(P, wseg, iseg, L.seg, qseg);
     if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
@@ -1889,10 +1920,10 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if ((st = scratch_t(c, kBufOutB, 2 * scap, &ostub)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &oseg)) != SPHBI_OK) return st;
     AccOut3* ost[4] = {ostub, ostub, ostub + scap, ostub + scap};
-    k_pipe_stub<true, 0><<<igrid(k_pipe_stub<true, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0]);
-    k_pipe_stub<true, 1><<<igrid(k_pipe_stub<true, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1]);
-    k_pipe_stub<true, 2><<<igrid(k_pipe_stub<true, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2]);
-    k_pipe_stub<true, 3><<<igrid(k_pipe_stub<true, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3]);
+    k_pipe_stub<true, 0><<<igrid(k_pipe_stub<true, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0], dflags);
+    k_pipe_stub<true, 1><<<igrid(k_pipe_stub<true, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1], dflags);
+    k_pipe_stub<true, 2><<<igrid(k_pipe_stub<true, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2], dflags);
+    k_pipe_stub<true, 3><<<igrid(k_pipe_stub<true, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3], dflags);
     k_pipe_sector<true><<<igrid(k_pipe_sector<true>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
     k_pipe_segment<true><<<igrid(k_pipe_segment<true>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
     if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
@@ -1905,10 +1936,10 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   if ((st = scratch_t(c, kBufOutB, 2 * scap, &ostub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &oseg)) != SPHBI_OK) return st;
   AccOut* ost[4] = {ostub, ostub, ostub + scap, ostub + scap};
-  k_pipe_stub<false, 0><<<igrid(k_pipe_stub<false, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0]);
-  k_pipe_stub<false, 1><<<igrid(k_pipe_stub<false, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1]);
-  k_pipe_stub<false, 2><<<igrid(k_pipe_stub<false, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2]);
-  k_pipe_stub<false, 3><<<igrid(k_pipe_stub<false, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3]);
+  k_pipe_stub<false, 0><<<igrid(k_pipe_stub<false, 0>, 1), 128, 0, s>>>(K, wst[0], istub, xst[0], ost[0], dflags);
+  k_pipe_stub<false, 1><<<igrid(k_pipe_stub<false, 1>, 2), 128, 0, s>>>(K, wst[1], istub, xst[1], ost[1], dflags);
+  k_pipe_stub<false, 2><<<igrid(k_pipe_stub<false, 2>, 3), 128, 0, s>>>(K, wst[2], istub, xst[2], ost[2], dflags);
+  k_pipe_stub<false, 3><<<igrid(k_pipe_stub<false, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3], dflags);
   k_pipe_sector<false><<<igrid(k_pipe_sector<false>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
   k_pipe_segment<false><<<igrid(k_pipe_segment<false>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
   if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
