@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -142,8 +143,15 @@ struct sphbi_ctx {
   unsigned long long* d_counters = nullptr;
   bool counters_on = false;
   int64_t launches = 0;
-  void* buf[kNumBufs] = {};
-  size_t cap[kNumBufs] = {};
+  // scratch banks: the streamed host path runs consecutive particle chunks on
+  // two compute streams (own scratch each), so one chunk's pipeline tail
+  // overlaps the next chunk's work; everything else uses bank 0
+  static constexpr int kBanks = 2;
+  int bank = 0;
+  cudaStream_t aux = nullptr;  // second compute stream (bank 1)
+  bool one_bank = false;       // SPHBI_STREAM_BANKS=1: chunks on one stream (experiment)
+  void* buf[kBanks * kNumBufs] = {};
+  size_t cap[kBanks * kNumBufs] = {};
   cudaEvent_t ev[8] = {};
   unsigned* h_flags = nullptr;  // pinned
   // copy engines for the streamed host-buffer path (H2D / D2H overlap)
@@ -158,15 +166,25 @@ struct sphbi_ctx {
   double item_ratio[6] = {2.0, 2.0, 2.0, 2.0, 2.0, 2.0};
   unsigned* h_counts = nullptr;   // pinned, written asynchronously
   cudaEvent_t count_ev = nullptr;
+  cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
-  int stream_chunk_log2 = 20;   // SPHBI_STREAM_CHUNK_LOG2: particles per chunk of the streamed host path
+  int stream_chunk_log2 = 0;    // SPHBI_STREAM_CHUNK_LOG2: equal chunks of 2^L particles (0: the ramp)
+  std::vector<double> stream_ramp{1, 2, 3, 4, 3, 2, 1};  // SPHBI_STREAM_RAMP: relative chunk sizes
+  // SPHBI_TIMELINE=1: the streamed path records timing events per chunk and
+  // prints the (upload, compute, download) completion times to stderr
+  bool timeline = false;
+  cudaEvent_t tl[4 * 64 + 1] = {};
+  double tl_host[64] = {};
+  cudaEvent_t tl2[64][4] = {};  // per chunk: pre-classified / emitted / pieces done / combined
+  int tl_chunk = -1;
 };
 
 namespace {
 
 sphbi_status scratch(sphbi_ctx* c, int slot, size_t bytes, void** out) {
   if (bytes == 0) bytes = 16;
+  slot += c->bank * kNumBufs;
   if (c->cap[slot] < bytes) {
     if (c->buf[slot]) cudaFree(c->buf[slot]);
     c->buf[slot] = nullptr;
@@ -215,6 +233,21 @@ sphbi_status make_consts(const sphbi_kernel_desc* k, KernelConsts* K) {
 int grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return static_cast<int>(g < 1 ? 1 : g);
+}
+
+__global__ void k_zero_words(int64_t n, unsigned* __restrict__ p) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[k] = 0u;
+}
+// Zeroing as a kernel, not cudaMemsetAsync: on the streamed host path a memset
+// can be queued behind the bulk H2D / D2H transfers on a copy engine and stall
+// the compute stream until they drain (measured: +0.2-0.3 ms per chunk).
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(bytes / 4);
+  if (n <= 0) return cudaSuccess;
+  k_zero_words<<<static_cast<int>(std::min<int64_t>(grid_for(n, 256), 4096)), 256, 0, s>>>(n, static_cast<unsigned*>(p));
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -481,34 +514,95 @@ __device__ __forceinline__ void load_norm(const NormRec* __restrict__ r, int64_t
   perm[2] = (pc >> 4) & 3;
 }
 
+// Signature bins: 3 inside bits + 3 x 2 crossing-count bits.
+constexpr int kSigBins = 512;
+
+// Block-level signature histogram, added to the global one (one atomic per
+// non-empty bin and block).
+__device__ __forceinline__ void sig_hist_add(unsigned* sh, unsigned kk, bool valid, unsigned* __restrict__ hist) {
+  for (int b = threadIdx.x; b < kSigBins; b += blockDim.x) sh[b] = 0u;
+  __syncthreads();
+  if (valid) atomicAdd(sh + kk, 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kSigBins; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
 template <class Src>
 __global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h, unsigned short* __restrict__ key,
-                                                   NormRec* __restrict__ nrec) {
+                                                   NormRec* __restrict__ nrec, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[kSigBins];
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double qx, qy, t6[6], a3[3];
-  src.load(k, qx, qy, t6, a3);
-  P2 nv[3];
-  int perm[3];
-  normalized_pair(qx, qy, h, t6, nv, perm);
-  {
-    NormRec r;
-    for (int i = 0; i < 3; ++i) {
-      r.v[2 * i] = nv[i].x;
-      r.v[2 * i + 1] = nv[i].y;
-    }
-    r.perm = perm[0] | (perm[1] << 2) | (perm[2] << 4);
-    r.pad = 0;
-    r.pad2 = 0.0;
-    nrec[k] = r;
-  }
   unsigned kk = 0;
-  for (int i = 0; i < 3; ++i) {
-    if (p_norm2(nv[i]) <= 1.0) kk |= 1u << i;
-    const Crossings x = segment_circle_crossings(nv[i], nv[(i + 1) % 3]);
-    kk |= static_cast<unsigned>(x.count) << (3 + 2 * i);
+  if (k < n) {
+    double qx, qy, t6[6], a3[3];
+    src.load(k, qx, qy, t6, a3);
+    P2 nv[3];
+    int perm[3];
+    normalized_pair(qx, qy, h, t6, nv, perm);
+    {
+      NormRec r;
+      for (int i = 0; i < 3; ++i) {
+        r.v[2 * i] = nv[i].x;
+        r.v[2 * i + 1] = nv[i].y;
+      }
+      r.perm = perm[0] | (perm[1] << 2) | (perm[2] << 4);
+      r.pad = 0;
+      r.pad2 = 0.0;
+      nrec[k] = r;
+    }
+    for (int i = 0; i < 3; ++i) {
+      if (p_norm2(nv[i]) <= 1.0) kk |= 1u << i;
+      const Crossings x = segment_circle_crossings(nv[i], nv[(i + 1) % 3]);
+      kk |= static_cast<unsigned>(x.count) << (3 + 2 * i);
+    }
+    key[k] = static_cast<unsigned short>(kk);
   }
-  key[k] = static_cast<unsigned short>(kk);
+  sig_hist_add(sh, kk, k < n, hist);  // the whole block reaches its barriers
+}
+
+// Exclusive scan of the signature histogram -> per-bin cursors (one block).
+__global__ void __launch_bounds__(kSigBins) k_sig_offsets(const unsigned* __restrict__ hist,
+                                                          unsigned* __restrict__ cursor) {
+  __shared__ unsigned sh[kSigBins];
+  const int t = threadIdx.x;
+  const unsigned v = hist[t];
+  sh[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kSigBins; o <<= 1) {
+    const unsigned y = t >= o ? sh[t - o] : 0u;
+    __syncthreads();
+    sh[t] += y;
+    __syncthreads();
+  }
+  cursor[t] = sh[t] - v;
+}
+
+// Counting-sort scatter of pair indices by signature: per block, the bins'
+// counts reserve global ranges (one atomic per non-empty bin), then every pair
+// takes a rank inside its block's range. The order inside a bin is not
+// specified; pair results do not depend on it (each pair is evaluated and
+// combined on its own), only the warp convergence of the emit pass does.
+__global__ void __launch_bounds__(256) k_sig_scatter(int64_t n, const unsigned short* __restrict__ key,
+                                                      unsigned* __restrict__ cursor, int* __restrict__ order) {
+  __shared__ unsigned cnt[kSigBins];
+  __shared__ unsigned base[kSigBins];
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int b = threadIdx.x; b < kSigBins; b += blockDim.x) cnt[b] = 0u;
+  __syncthreads();
+  const unsigned kk = k < n ? key[k] : 0u;
+  if (k < n) atomicAdd(cnt + kk, 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kSigBins; b += blockDim.x) {
+    const unsigned c = cnt[b];
+    base[b] = c ? atomicAdd(cursor + b, c) : 0u;
+    cnt[b] = 0u;
+  }
+  __syncthreads();
+  if (k < n) {
+    const unsigned r = atomicAdd(cnt + kk, 1u);
+    order[base[kk] + r] = static_cast<int>(k);
+  }
 }
 
 __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const NormRec* __restrict__ nrec, int64_t n,
@@ -1341,6 +1435,28 @@ __global__ void k_pack_pairs(int64_t n, const int64_t* __restrict__ ip, const in
   }
 }
 
+// Streamed path: validate (range, sortedness) and convert to int32 pairs in
+// one pass.
+__global__ void k_pack_pairs32(int64_t n, const int64_t* __restrict__ ip, const int64_t* __restrict__ it,
+                               int64_t n_particles, int64_t n_tris, int* __restrict__ pp, int* __restrict__ pt,
+                               unsigned* __restrict__ flags) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t i = ip[k], t = it[k];
+  if (i < 0 || i >= n_particles || t < 0 || t >= n_tris) {
+    atomicOr(flags, 1u);  // out of range
+    pp[k] = 0;
+    pt[k] = 0;
+    return;
+  }
+  pp[k] = static_cast<int>(i);
+  pt[k] = static_cast<int>(t);
+  if (k > 0) {
+    const int64_t i0 = ip[k - 1], t0 = it[k - 1];
+    if (i0 > i || (i0 == i && t0 > t)) atomicOr(flags, 2u);  // unsorted
+  }
+}
+
 __global__ void k_unpack_keys(int64_t n, const unsigned long long* __restrict__ keys, int* __restrict__ pp,
                               int* __restrict__ pt) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1668,26 +1784,24 @@ sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, Nor
   cudaStream_t s = c->stream;
   sphbi_status st;
   const int64_t m = n + 1;
-  int* iota;
-  if ((st = scratch_t(c, kBufOrder, 2 * m, &iota)) != SPHBI_OK) return st;
-  k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, iota);
-  if ((st = check_launch(c, "k_iota")) != SPHBI_OK) return st;
   unsigned short* pk;
-  if ((st = scratch_t(c, kBufPreKey, 2 * m, &pk)) != SPHBI_OK) return st;
+  unsigned* hist;  // [kSigBins] histogram, [kSigBins] cursors
+  if ((st = scratch_t(c, kBufPreKey, m, &pk)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPreOrder, m, porder_out)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufNormRec, n, nrec_out)) != SPHBI_OK) return st;
-  k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, *nrec_out);
+  if ((st = scratch_t(c, kBufOrder, 2 * kSigBins, &hist)) != SPHBI_OK) return st;
+  SPHBI_CUDA_TRY(zero_async(hist, sizeof(unsigned) * kSigBins, s));
+  k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, *nrec_out, hist);
   if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
   if (c->no_sig_sort) {  // experiment: emit in pair order
     *porder_out = nullptr;
     return SPHBI_OK;
   }
-  size_t tmp_sort = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, pk, pk + m, iota, *porder_out, (int)n, 0, 9, s);
-  void* dtmp_sort;
-  if ((st = scratch(c, kBufCubTemp2, tmp_sort, &dtmp_sort)) != SPHBI_OK) return st;
-  cub::DeviceRadixSort::SortPairs(dtmp_sort, tmp_sort, pk, pk + m, iota, *porder_out, (int)n, 0, 9, s);
-  return check_launch(c, "radix sort pre-class");
+  // counting sort by signature (9-bit keys): no radix-sort passes, no memsets
+  k_sig_offsets<<<1, kSigBins, 0, s>>>(hist, hist + kSigBins);
+  if ((st = check_launch(c, "k_sig_offsets")) != SPHBI_OK) return st;
+  k_sig_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, pk, hist + kSigBins, *porder_out);
+  return check_launch(c, "k_sig_scatter");
 }
 
 // Two-pass K4 pipeline (after a slot overflow, or SPHBI_TWO_PASS=1): count
@@ -1852,12 +1966,17 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   unsigned* lcount;
   if ((st = scratch_t(c, kBufIdx, (kCapSec + 2 * kCapStub + kCapSeg) * n, &lists)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPipeCnt, kKinds, &lcount)) != SPHBI_OK) return st;
-  SPHBI_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned) * kKinds, s));
+  SPHBI_CUDA_TRY(zero_async(lcount, sizeof(unsigned) * kKinds, s));
   const long long scap = static_cast<long long>(kCapStub) * n;
   const SlotLists L{lists, {lists + kCapSec * n, lists + kCapSec * n + scap}, lists + kCapSec * n + 2 * scap, lcount,
                     scap};
+  auto mark = [&](int j) {
+    if (c->timeline && c->tl_chunk >= 0 && c->tl_chunk < 64) cudaEventRecord(c->tl2[c->tl_chunk][j], s);
+  };
+  mark(0);
   k_pipe_emit_slots<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr, dflags);
   if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
+  mark(1);
   const SlotItems items{jrec};
   // Piece-kernel grids without a host round trip: the kernels read their item
   // counts on the device and loop grid-stride, so any grid is correct; the
@@ -1881,8 +2000,12 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     for (int q = 0; q < kKinds; ++q) hc[q] = hp[q];
     dcount = nullptr;
   } else if (c->count_n == 0 && cudaEventQuery(c->count_ev) == cudaSuccess) {
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_counts, lcount, sizeof(unsigned) * kKinds, cudaMemcpyDeviceToHost, s));
-    SPHBI_CUDA_TRY(cudaEventRecord(c->count_ev, s));
+    // read back on the d2h stream: a device-to-host copy on the compute stream
+    // would wait behind bulk downloads queued on the copy engine
+    SPHBI_CUDA_TRY(cudaEventRecord(c->count_src_ev, s));
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->count_src_ev, 0));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_counts, lcount, sizeof(unsigned) * kKinds, cudaMemcpyDeviceToHost, c->d2h));
+    SPHBI_CUDA_TRY(cudaEventRecord(c->count_ev, c->d2h));
     c->count_n = n;
   } else {
     cudaGetLastError();
@@ -1927,8 +2050,10 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     k_pipe_sector<true><<<igrid(k_pipe_sector<true>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
     k_pipe_segment<true><<<igrid(k_pipe_segment<true>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
     if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+    mark(2);
     k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items,
                                                           ItemOuts{osec, {ostub, ostub + scap}, oseg}, stride, dout);
+    mark(3);
     return check_launch(c, "k_pipe_combine");
   }
   AccOut *osec, *ostub, *oseg;
@@ -1979,71 +2104,118 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
   if ((st = scratch_t(c, kBufTri, 6 * n_triangles, &dt)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutV, n_particles, &dov)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOutG, 2 * n_particles, &dog)) != SPHBI_OK) return st;
+  const auto tl_t0 = std::chrono::steady_clock::now();
+  if (c->timeline) SPHBI_CUDA_TRY(cudaEventRecord(c->tl[0], c->h2d));
   SPHBI_CUDA_TRY(cudaMemcpyAsync(dt, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
   if (tri_values) {
     if ((st = scratch_t(c, kBufVals, 3 * n_triangles, &dv)) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemcpyAsync(dv, tri_values, 24 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
   }
-  // particle-aligned chunks (pairs sorted by particle: boundaries by binary search)
-  const int nchunks = (int)std::min<int64_t>(64, std::max<int64_t>(2, n_particles >> c->stream_chunk_log2));
+  // Particle-aligned chunks (pairs sorted by particle: boundaries by binary
+  // search). Default: a ramp of relative sizes (c->stream_ramp, 1,2,3,4,3,2,1)
+  // -- the first upload and the last download are the only copies not hidden
+  // behind compute, so the end chunks are small, while the middle ones are
+  // large (each pipeline call has a fixed ~0.15 ms of launch / tail cost) and
+  // grow no faster than the copy engine (~1.5x the compute rate) stays ahead.
+  // SPHBI_STREAM_CHUNK_LOG2 selects equal chunks of 2^L particles instead.
+  std::vector<double> wts;
+  if (c->stream_chunk_log2 > 0) {
+    const int ne = (int)std::min<int64_t>(64, std::max<int64_t>(2, n_particles >> c->stream_chunk_log2));
+    wts.assign(ne, 1.0);
+  } else {
+    wts = c->stream_ramp;
+  }
+  const int nchunks = (int)wts.size();
   std::vector<int64_t> pb(nchunks + 1), qb(nchunks + 1);
-  for (int k = 0; k <= nchunks; ++k) {
-    pb[k] = n_particles * k / nchunks;
-    qb[k] = std::lower_bound(pair_particle, pair_particle + n_pairs, pb[k]) - pair_particle;
+  {
+    double wsum = 0.0, acc = 0.0;
+    for (double w : wts) wsum += w;
+    for (int k = 0; k <= nchunks; ++k) {
+      pb[k] = k == nchunks ? n_particles : static_cast<int64_t>(static_cast<double>(n_particles) * (acc / wsum));
+      if (k < nchunks) acc += wts[k];
+      qb[k] = std::lower_bound(pair_particle, pair_particle + n_pairs, pb[k]) - pair_particle;
+    }
   }
   qb[nchunks] = n_pairs;
   int64_t maxq = 0;
   for (int k = 0; k < nchunks; ++k) maxq = std::max(maxq, qb[k + 1] - qb[k]);
-  int64_t *ip[2], *it[2];
-  if ((st = scratch_t(c, kBufUserPairs0, maxq, &ip[0])) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufUserPairs1, maxq, &it[0])) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufUserPairs2, maxq, &ip[1])) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufUserPairs3, maxq, &it[1])) != SPHBI_OK) return st;
-  unsigned long long* keys;
-  int *pp, *pt;
-  double* pout;
-  int64_t* row_ptr;
-  if ((st = scratch_t(c, kBufKeysA, maxq, &keys)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPairP, maxq, &pp)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPairT, maxq, &pt)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufPairOut, 3 * maxq, &pout)) != SPHBI_OK) return st;
+  // the whole pair list gets a device copy (16 B per pair): uploads stream
+  // back to back, never waiting for a chunk's compute to free a buffer
+  int64_t *dip, *dit;
+  if ((st = scratch_t(c, kBufUserPairs0, n_pairs, &dip)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufUserPairs1, n_pairs, &dit)) != SPHBI_OK) return st;
+  // per-chunk compute scratch, one set per bank (chunk k runs on bank k & 1)
+  const int nbanks = c->aux && !c->one_bank ? 2 : 1;
+  int *pp[2], *pt[2];
+  double* pout[2];
+  int64_t* row_ptr[2];
   int64_t maxp = 0;
   for (int k = 0; k < nchunks; ++k) maxp = std::max(maxp, pb[k + 1] - pb[k]);
-  if ((st = scratch_t(c, kBufRowPtr, maxp + 1, &row_ptr)) != SPHBI_OK) return st;
+  for (int b = 0; b < nbanks; ++b) {
+    c->bank = b;
+    if ((st = scratch_t(c, kBufPairP, maxq, &pp[b])) == SPHBI_OK &&
+        (st = scratch_t(c, kBufPairT, maxq, &pt[b])) == SPHBI_OK &&
+        (st = scratch_t(c, kBufPairOut, 3 * maxq, &pout[b])) == SPHBI_OK)
+      st = scratch_t(c, kBufRowPtr, maxp + 1, &row_ptr[b]);
+    c->bank = 0;
+    if (st != SPHBI_OK) return st;
+  }
+  // chunk k computes on stream cs[k & 1]; c->stream / c->bank are switched
+  // for the pipeline calls and restored on every exit
+  struct Restore {
+    sphbi_ctx* c;
+    cudaStream_t s;
+    ~Restore() {
+      c->stream = s;
+      c->bank = 0;
+    }
+  } restore{c, s};
+  cudaStream_t cs2[2] = {s, nbanks == 2 ? c->aux : s};
+  if (nbanks == 2) {  // fork: the aux stream starts after the work already on s
+    SPHBI_CUDA_TRY(cudaEventRecord(c->ev[6], s));
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->aux, c->ev[6], 0));
+  }
   auto upload = [&](int k) -> sphbi_status {
-    const int b = k & 1;
-    if (k >= 2) SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->h2d, c->sev[1][(k - 2) % 64], 0));  // buffer b free
     const int64_t np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
     SPHBI_CUDA_TRY(cudaMemcpyAsync(dp + 2 * pb[k], particle_xy + 2 * pb[k], 16 * np, cudaMemcpyHostToDevice, c->h2d));
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(ip[b], pair_particle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
-    SPHBI_CUDA_TRY(cudaMemcpyAsync(it[b], pair_triangle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(dip + qb[k], pair_particle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(dit + qb[k], pair_triangle + qb[k], 8 * nq, cudaMemcpyHostToDevice, c->h2d));
     SPHBI_CUDA_TRY(cudaEventRecord(c->sev[0][k % 64], c->h2d));
+    if (c->timeline && k < 64) SPHBI_CUDA_TRY(cudaEventRecord(c->tl[1 + 3 * k], c->h2d));
     return SPHBI_OK;
   };
   if ((st = upload(0)) != SPHBI_OK) return st;
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks && (st = upload(k + 1)) != SPHBI_OK) return st;
-    const int b = k & 1;
+    const int q = k % nbanks;  // compute bank / stream
+    cudaStream_t cs = cs2[q];
     const int64_t p0 = pb[k], np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
-    SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[0][k % 64], 0));
-    if (np > 0) {
-      SPHBI_CUDA_TRY(cudaMemsetAsync(dov + p0, 0, 8 * np, s));
-      SPHBI_CUDA_TRY(cudaMemsetAsync(dog + 2 * p0, 0, 16 * np, s));
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(cs, c->sev[0][k % 64], 0));
+    if (c->timeline && k < 64) SPHBI_CUDA_TRY(cudaEventRecord(c->tl[193 + k], cs));
+    if (np > 0 && nq == 0) {  // otherwise k_reduce_rows writes every row of the chunk
+      SPHBI_CUDA_TRY(zero_async(dov + p0, 8 * np, cs));
+      SPHBI_CUDA_TRY(zero_async(dog + 2 * p0, 16 * np, cs));
     }
     if (nq > 0) {
       // validate (range, sortedness) and convert to int32 pairs
-      k_pack_pairs<<<grid_for(nq, 256), 256, 0, s>>>(nq, ip[b], it[b], n_particles, n_triangles, keys, dflags + 1);
-      if ((st = check_launch(c, "k_pack_pairs")) != SPHBI_OK) return st;
-      k_unpack_keys<<<grid_for(nq, 256), 256, 0, s>>>(nq, keys, pp, pt);
-      if ((st = check_launch(c, "k_unpack_keys")) != SPHBI_OK) return st;
-      const SceneSrc src{pp, pt, dp, dt, dv};
-      if ((st = run_pipeline(c, K, h, src, nq, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
-      k_row_ptr<<<grid_for(nq + 1, 256), 256, 0, s>>>(nq, pp, (int)p0, (int)np, row_ptr);
+      k_pack_pairs32<<<grid_for(nq, 256), 256, 0, cs>>>(nq, dip + qb[k], dit + qb[k], n_particles, n_triangles,
+                                                         pp[q], pt[q], dflags + 1);
+      if ((st = check_launch(c, "k_pack_pairs32")) != SPHBI_OK) return st;
+      const SceneSrc src{pp[q], pt[q], dp, dt, dv};
+      c->stream = cs;
+      c->bank = q;
+      c->tl_chunk = k;
+      if ((st = run_pipeline(c, K, h, src, nq, 0, 3, pout[q], dflags, ctr, nullptr)) != SPHBI_OK) return st;
+      c->tl_chunk = -1;
+      c->stream = s;
+      c->bank = 0;
+      k_row_ptr<<<grid_for(nq + 1, 256), 256, 0, cs>>>(nq, pp[q], (int)p0, (int)np, row_ptr[q]);
       if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
-      k_reduce_rows<<<grid_for(np, 256), 256, 0, s>>>((int)p0, (int)np, row_ptr, pout, dov, dog, 0);
+      k_reduce_rows<<<grid_for(np, 256), 256, 0, cs>>>((int)p0, (int)np, row_ptr[q], pout[q], dov, dog, 0);
       if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
     }
-    SPHBI_CUDA_TRY(cudaEventRecord(c->sev[1][k % 64], s));
+    SPHBI_CUDA_TRY(cudaEventRecord(c->sev[1][k % 64], cs));
+    if (c->timeline && k < 64) SPHBI_CUDA_TRY(cudaEventRecord(c->tl[2 + 3 * k], cs));
     SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->sev[1][k % 64], 0));
     if (np > 0) {
       if (out_value)
@@ -2052,9 +2224,32 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
         SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad + 2 * p0, dog + 2 * p0, 16 * np, cudaMemcpyDeviceToHost, c->d2h));
     }
     SPHBI_CUDA_TRY(cudaEventRecord(c->sev[2][k % 64], c->d2h));
+    if (c->timeline && k < 64) {
+      SPHBI_CUDA_TRY(cudaEventRecord(c->tl[3 + 3 * k], c->d2h));
+      c->tl_host[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl_t0).count();
+    }
+  }
+  if (nbanks == 2) {  // join
+    SPHBI_CUDA_TRY(cudaEventRecord(c->ev[7], c->aux));
+    SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->ev[7], 0));
   }
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->d2h));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->h2d));
+  if (c->timeline) {
+    SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    fprintf(stderr, "[sphbi timeline] %d chunks (ms: uploaded / compute start / computed / downloaded / host enqueued)\n",
+            nchunks);
+    for (int k = 0; k < nchunks && k < 64; ++k) {
+      float t[4];
+      for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&t[j], c->tl[0], c->tl[1 + 3 * k + j]);
+      cudaEventElapsedTime(&t[3], c->tl[0], c->tl[193 + k]);
+      fprintf(stderr, "  chunk %2d  pairs %9lld  %8.3f %8.3f %8.3f %8.3f %8.3f", k, (long long)(qb[k + 1] - qb[k]),
+              t[0], t[3], t[1], t[2], c->tl_host[k]);
+      float u[4];
+      for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&u[j], c->tl[0], c->tl2[k][j]);
+      fprintf(stderr, "   | sorted %.3f emitted %.3f pieces %.3f combined %.3f\n", u[0], u[1], u[2], u[3]);
+    }
+  }
   SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
   if (c->h_flags[1] & 1u) return fail(SPHBI_ERR_INVALID_ARGUMENT, "pair index out of range");
@@ -2125,6 +2320,19 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
     c->no_sig_sort = ns && ns[0] == '1';
     const char* cl = std::getenv("SPHBI_STREAM_CHUNK_LOG2");
     if (cl) c->stream_chunk_log2 = std::max(12, std::min(26, std::atoi(cl)));
+    if (const char* rp = std::getenv("SPHBI_STREAM_RAMP"); rp && *rp) {
+      std::vector<double> w;
+      for (const char* q = rp; *q;) {
+        char* e = nullptr;
+        const double v = std::strtod(q, &e);
+        if (e == q) break;
+        if (v > 0.0 && w.size() < 64) w.push_back(v);
+        q = *e == ',' ? e + 1 : e;
+      }
+      if (!w.empty()) c->stream_ramp = w;
+    }
+    const char* sb = std::getenv("SPHBI_STREAM_BANKS");
+    c->one_bank = sb && sb[0] == '1';
   }
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -2134,11 +2342,19 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (const char* t = std::getenv("SPHBI_TIMELINE"); t && t[0] == '1') {
+    c->timeline = true;
+    for (auto& e : c->tl) cudaEventCreate(&e);
+    for (auto& row : c->tl2)
+      for (auto& e : row) cudaEventCreate(&e);
+  }
   cudaMallocHost(&c->h_flags, 512);
   cudaMallocHost(&c->h_counts, 64);
   cudaEventCreateWithFlags(&c->count_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->count_src_ev, cudaEventDisableTiming);
   if (cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess) {
     cudaGetLastError();
     return fail(SPHBI_ERR_OUT_OF_MEMORY, "counter allocation failed");
@@ -2152,8 +2368,9 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   if (!c) return SPHBI_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (int i = 0; i < kNumBufs; ++i)
+  for (int i = 0; i < sphbi_ctx::kBanks * kNumBufs; ++i)
     if (c->buf[i]) cudaFree(c->buf[i]);
+  if (c->aux) cudaStreamDestroy(c->aux);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventDestroy(e);
@@ -2162,6 +2379,12 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   if (c->h_flags) cudaFreeHost(c->h_flags);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->count_ev) cudaEventDestroy(c->count_ev);
+  if (c->count_src_ev) cudaEventDestroy(c->count_src_ev);
+  for (auto& e : c->tl)
+    if (e) cudaEventDestroy(e);
+  for (auto& row : c->tl2)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
   if (c->d_counters) cudaFree(c->d_counters);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
@@ -2384,7 +2607,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
     if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;  // 8 x u32
-    SPHBI_CUDA_TRY(cudaMemsetAsync(sflags, 0, 32, s));
+    SPHBI_CUDA_TRY(zero_async(sflags, 32, s));
     unsigned long long* sctr = c->counters_on ? c->d_counters : nullptr;
     st = evaluate_streamed(c, K, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
                            pair_particle, pair_triangle, out_value, out_grad, sflags, sctr);
@@ -2483,10 +2706,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   }
   unsigned* dflags;
   if ((st = scratch_t(c, kBufFlags, 8, &dflags)) != SPHBI_OK) return st;
-  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, s));
+  SPHBI_CUDA_TRY(zero_async(dflags, 32, s));
   if (n_particles) {
-    SPHBI_CUDA_TRY(cudaMemsetAsync(dov, 0, 8 * n_particles, s));
-    SPHBI_CUDA_TRY(cudaMemsetAsync(dog, 0, 16 * n_particles, s));
+    SPHBI_CUDA_TRY(zero_async(dov, 8 * n_particles, s));
+    SPHBI_CUDA_TRY(zero_async(dog, 16 * n_particles, s));
   }
   unsigned long long* ctr = c->counters_on ? c->d_counters : nullptr;
   int64_t total_pairs = 0, candidates = 0;
@@ -2902,7 +3125,7 @@ static sphbi_status integrate_pairs_p3_impl(sphbi_ctx* c, const sphbi_kernel_des
     dn = v;
     dout = o;
   }
-  SPHBI_CUDA_TRY(cudaMemsetAsync(dflags, 0, 32, s));
+  SPHBI_CUDA_TRY(zero_async(dflags, 32, s));
   {
     const DirectSrc src{dq, dt, nullptr};  // geometry only; the field enters in k_p3_combine
     const P3Job job{P.get(), dn, nullptr};

@@ -400,6 +400,29 @@ def test_streamed_pinned_host_path_is_bitwise_identical(S, ctx):
                                     vp(ov.data_ptr()), vp(og.data_ptr()), None, None, None, N.MEM_HOST)
         assert rc == 0, N.last_error()
         assert np.array_equal(ov.numpy(), ref_v) and np.array_equal(og.numpy(), ref_g), order
+    # other chunkings (equal chunks, uneven ramps) and one compute stream vs two
+    import os
+    for env in ({"SPHBI_STREAM_CHUNK_LOG2": "17"}, {"SPHBI_STREAM_RAMP": "3,1,5,2"},
+                {"SPHBI_STREAM_RAMP": "1,2,3,4,3,2,1", "SPHBI_STREAM_BANKS": "1"}):
+        old_env = {key: os.environ.get(key) for key in env}
+        os.environ.update(env)
+        try:
+            c2 = S.Context(0)
+        finally:
+            for key, val in old_env.items():
+                if val is None:
+                    os.environ.pop(key, None)
+                else:
+                    os.environ[key] = val
+        ip, it = pin(sc.pairs[0]), pin(sc.pairs[1])
+        ov = torch.zeros(n, dtype=torch.float64).pin_memory()
+        og = torch.zeros((n, 2), dtype=torch.float64).pin_memory()
+        rc = c2.lib.sphbi_evaluate(c2.handle, ctypes.byref(desc), sc.h, n, vp(P.data_ptr()), T, vp(Tr.data_ptr()),
+                                   vp(V.data_ptr()), ip.shape[0], vp(ip.data_ptr()), vp(it.data_ptr()),
+                                   vp(ov.data_ptr()), vp(og.data_ptr()), None, None, None, N.MEM_HOST)
+        c2.close()
+        assert rc == 0, N.last_error()
+        assert np.array_equal(ov.numpy(), ref_v) and np.array_equal(og.numpy(), ref_g), env
 
 
 def test_heaviest_decomposition_t3_with_16_stubs(S, ctx, O):
