@@ -72,7 +72,7 @@ constexpr int kEvalBlock = 128;
 #define SPHBI_MINB_EMIT 4
 #endif
 #ifndef SPHBI_MINB_STUB
-#define SPHBI_MINB_STUB 4
+#define SPHBI_MINB_STUB 5
 #endif
 constexpr int kMaxChunkPairs = 1 << 22;  // 4 Mi pairs per evaluation chunk (item slots ~2 KB per pair: ~8 GB scratch)
 
