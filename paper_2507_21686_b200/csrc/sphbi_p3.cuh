@@ -236,36 +236,76 @@ SPHBI_HD void h24_half_disc(const P3Consts& P, H24& H) {
   }
 }
 
+// Weighted chain sums. Every stub-window / segment sum of a descriptor is
+// sum_k w_k F(k + off) with F a fixed linear combination of chain values at
+// shifted indices (p3_sp), so the k-sum is taken first, once per (family,
+// chain, shift): W[f][s + kW0] = sum_k w_f[k] C[k + s] (C[idx] = 0 for
+// idx < 0), s = -kW0 .. kW1. ~44 weighted sums per bound instead of the
+// descriptor x k x Chebyshev-term products.
+constexpr int kW0 = 5, kW1 = 4, kWN = kW0 + kW1 + 1;
+SPHBI_HD void p3_wsums(const P3Consts& P, const dd* C, int smin, dd (*W)[kWN]) {
+  for (int f = 0; f < 2; ++f)
+    for (int s = smin; s <= kW1; ++s) {
+      acc2 a{0.0, 0.0};
+      for (int k = s < 0 ? -s : 0; k <= P.deg; ++k) {
+        const dd w = P.w[f][k];
+        if (w.hi == 0.0) continue;
+        acc_add_dddd(a, w, C[k + s]);
+      }
+      W[f][s + kW0] = acc_dd(a);
+    }
+}
+// sum_k w_f[k] p3_sp(k + o, m, ...) from the weighted sums (m <= 4)
+SPHBI_HD dd p3_wsp(const dd (*WI)[kWN], const dd (*WX)[kWN], int f, int o, int m, dd D2) {
+  const dd(*W)[kWN] = (m & 1) ? WI : WX;
+  dd acc{0.0, 0.0};
+  dd pw = dd_make(1.0);  // (-D^2)^l
+  const int top = m / 2;
+  for (int l = 0; l <= top; ++l) {
+    const double bin = l == 0 ? 1.0 : (top == 1 ? 1.0 : (l == 1 ? 2.0 : 1.0));  // C(top, l), top <= 2
+    const int sh = o - 2 * l;
+    if (sh >= -kW0) acc = dd_add(acc, dd_mul_d(dd_mul(W[f][sh + kW0], pw), bin));
+    pw = dd_neg(dd_mul(pw, D2));
+  }
+  return acc;
+}
+// sum_k pc[f][off][k] Pt[k + off] (= sum_k w_k Pt[n] / (n + 1))
+SPHBI_HD dd p3_wpt(const P3Consts& P, const dd* Pt, int f, int off) {
+  acc2 a{0.0, 0.0};
+  for (int k = 0; k <= P.deg; ++k) {
+    const dd w = P.pc[f][off][k];
+    if (w.hi == 0.0 && w.lo == 0.0) continue;
+    acc_add_dddd(a, w, Pt[k + off]);
+  }
+  return acc_dd(a);
+}
+
 // segment {x >= d}, 0 < d < 1 (elementary_regions.hpp:130-167 generalised)
 SPHBI_HD void h24_segment(const P3Consts& P, double d, H24& H) {
   dd Pt[kP3Chain], I[kP3Chain], X[kP3Chain], R;
   const int M = P.deg + 6;
   p3_chains(1.0, d, M, Pt, I, X, R);
   const double acd = d <= 0.7 ? acos(d) : asin(R.hi);
+  dd WI[2][kWN];
+  p3_wsums(P, I, -3, WI);
   h24_zero(H);
   for (int dsi = 0; dsi < kP3Desc; ++dsi) {
     const P3Desc ds = p3desc(dsi);
-    acc2 ac{0, 0};
-    for (int k = 0; k <= P.deg; ++k) {
-      const dd w = P.w[ds.fam][k];
-      if (w.hi == 0.0) continue;
-      const int n = k + ds.off;
-      dd r;
-      if (ds.a == 0) {
-        r = dd_div_d_small(dd_mul_d(dd_sub(dd_make(acd), dd_mul_d(Pt[n], d)), 2.0), n + 1);  // 2/(n+1) inexact
-      } else {
-        r = dd{0.0, 0.0};
-        double dp = 1.0;  // d^p for p = 0..a-1
-        for (int p = 0; p < ds.a; ++p) {
-          const double u = uco(ds.a, p);
-          if (u != 0.0 && n - p >= 1) r = dd_add(r, dd_mul_d(I[n - p], u * dp));
-          dp *= d;
-        }
-        r = dd_mul_d(r, 2.0 / ds.a);
+    if (ds.a == 0) {
+      // sum_k w_k 2 (acd - Pt[n] d) / (n + 1)
+      const dd pv = dd_sub(dd_mul_d(P.pc1[ds.fam][ds.off], acd), dd_mul_d(p3_wpt(P, Pt, ds.fam, ds.off), d));
+      H.c[ds.ic] = dd_mul_d(pv, 2.0);
+    } else {
+      // sum_k w_k (2/a) sum_p U_(a-1)[p] d^p I[n - p]
+      dd r{0.0, 0.0};
+      double dp = 1.0;
+      for (int p = 0; p < ds.a; ++p) {
+        const double u = uco(ds.a, p);
+        if (u != 0.0) r = dd_add(r, dd_mul_d(WI[ds.fam][ds.off - p + kW0], u * dp));
+        dp *= d;
       }
-      acc_add_dddd(ac, w, r);
+      H.c[ds.ic] = dd_mul_d(r, 2.0 / ds.a);
     }
-    H.c[ds.ic] = acc_dd(ac);
   }
 }
 
@@ -281,35 +321,32 @@ SPHBI_HD void h24_stub_bound(const P3Consts& P, double x, double D, double beta,
     as = (kHalfPiHi - asin(R.hi / x)) + kHalfPiLo;
   const double amb = as - beta;
   const dd D2 = two_prod(D, D);
+  dd WI[2][kWN], WX[2][kWN];
+  p3_wsums(P, I, -kW0, WI);
+  p3_wsums(P, X, -kW0, WX);
   for (int dsi = 0; dsi < kP3Desc; ++dsi) {
     const P3Desc ds = p3desc(dsi);
-    double sab = 0.0, cab = 1.0;
-    if (ds.a > 0) dsincos(ds.a * beta, &sab, &cab);
-    acc2 acc_c{0, 0}, acc_s{0, 0};
-    for (int k = 0; k <= P.deg; ++k) {
-      const dd w = P.w[ds.fam][k];
-      if (w.hi == 0.0) continue;
-      const int n = k + ds.off;
-      if (ds.a == 0) {
-        const dd r = dd_add(dd_mul_d(X[n], amb), dd_div_d_small(dd_mul_d(Pt[n], D), n + 1));
-        acc_add_dddd(acc_c, w, r);
-        continue;
-      }
-      dd tsum{0.0, 0.0}, usum{0.0, 0.0};
-      for (int j = 0; j <= ds.a; ++j) {
-        const double t = tco(ds.a, j);
-        if (t != 0.0) tsum = dd_add(tsum, dd_mul_d(p3_sp(n, j, I, X, D2), t));
-        const double u = j < ds.a ? uco(ds.a, j) : 0.0;
-        if (u != 0.0 && n >= 1) usum = dd_add(usum, dd_mul_d(p3_sp(n - 1, j, I, X, D2), u));
-      }
-      const dd du = dd_mul_d(usum, D);
-      const dd rc = dd_mul_d(dd_sub(dd_mul_d(du, cab), dd_mul_d(tsum, sab)), 1.0 / ds.a);
-      const dd rs = dd_mul_d(dd_sub(dd_sub(X[n], dd_mul_d(tsum, cab)), dd_mul_d(du, sab)), 1.0 / ds.a);
-      acc_add_dddd(acc_c, w, rc);
-      acc_add_dddd(acc_s, w, rs);
+    const int f = ds.fam;
+    if (ds.a == 0) {
+      // sum_k w_k (X[n] amb + Pt[n] D / (n + 1))
+      const dd r = dd_add(dd_mul_d(WX[f][ds.off + kW0], amb), dd_mul_d(p3_wpt(P, Pt, f, ds.off), D));
+      H.c[ds.ic] = dd_add(H.c[ds.ic], dd_scale(r, sgn));
+      continue;
     }
-    H.c[ds.ic] = dd_add(H.c[ds.ic], dd_scale(acc_dd(acc_c), sgn));
-    if (ds.is >= 0) H.c[ds.is] = dd_add(H.c[ds.is], dd_scale(acc_dd(acc_s), sgn));
+    double sab, cab;
+    dsincos(ds.a * beta, &sab, &cab);
+    dd tsum{0.0, 0.0}, usum{0.0, 0.0};
+    for (int j = 0; j <= ds.a; ++j) {
+      const double t = tco(ds.a, j);
+      if (t != 0.0) tsum = dd_add(tsum, dd_mul_d(p3_wsp(WI, WX, f, ds.off, j, D2), t));
+      const double u = j < ds.a ? uco(ds.a, j) : 0.0;
+      if (u != 0.0) usum = dd_add(usum, dd_mul_d(p3_wsp(WI, WX, f, ds.off - 1, j, D2), u));
+    }
+    const dd du = dd_mul_d(usum, D);
+    const dd rc = dd_mul_d(dd_sub(dd_mul_d(du, cab), dd_mul_d(tsum, sab)), 1.0 / ds.a);
+    const dd rs = dd_mul_d(dd_sub(dd_sub(WX[f][ds.off + kW0], dd_mul_d(tsum, cab)), dd_mul_d(du, sab)), 1.0 / ds.a);
+    H.c[ds.ic] = dd_add(H.c[ds.ic], dd_scale(rc, sgn));
+    H.c[ds.is] = dd_add(H.c[ds.is], dd_scale(rs, sgn));
   }
 }
 

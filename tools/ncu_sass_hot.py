@@ -9,7 +9,7 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", kern, "--print-source", "sass",
-                      "--launch-count", "1"], capture_output=True, text=True).stdout
+                      "--launch-count", "1"] + (["--kernel-name-base", "demangled"] if False else []), capture_output=True, text=True).stdout
 lines = out.splitlines()
 i = next(j for j, l in enumerate(lines) if l.startswith('"Address"'))
 rows = [r for r in csv.DictReader(io.StringIO("\n".join(lines[i:]))) if r.get("Address", "").startswith("0x")]
