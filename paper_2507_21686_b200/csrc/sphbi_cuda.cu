@@ -214,8 +214,9 @@ sphbi_status scratch_t(sphbi_ctx* c, int slot, size_t count, T** out) {
   return st;
 }
 
-sphbi_status check_launch(sphbi_ctx* c, const char* what) {
-  c->launches += 1;
+// n: kernels launched since the previous check (c->launches counts kernels)
+sphbi_status check_launch(sphbi_ctx* c, const char* what, int n = 1) {
+  c->launches += n;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SPHBI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return SPHBI_OK;
@@ -243,9 +244,10 @@ __global__ void k_zero_words(int64_t n, unsigned* __restrict__ p) {
 // Zeroing as a kernel, not cudaMemsetAsync: on the streamed host path a memset
 // can be queued behind the bulk H2D / D2H transfers on a copy engine and stall
 // the compute stream until they drain (measured: +0.2-0.3 ms per chunk).
-cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s) {
+cudaError_t zero_async(sphbi_ctx* c, void* p, size_t bytes, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(bytes / 4);
   if (n <= 0) return cudaSuccess;
+  c->launches += 1;
   k_zero_words<<<static_cast<int>(std::min<int64_t>(grid_for(n, 256), 4096)), 256, 0, s>>>(n, static_cast<unsigned*>(p));
   return cudaGetLastError();
 }
@@ -1790,7 +1792,7 @@ sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, Nor
   if ((st = scratch_t(c, kBufPreOrder, m, porder_out)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufNormRec, n, nrec_out)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufOrder, 2 * kSigBins, &hist)) != SPHBI_OK) return st;
-  SPHBI_CUDA_TRY(zero_async(hist, sizeof(unsigned) * kSigBins, s));
+  SPHBI_CUDA_TRY(zero_async(c, hist, sizeof(unsigned) * kSigBins, s));
   k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, *nrec_out, hist);
   if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
   if (c->no_sig_sort) {  // experiment: emit in pair order
@@ -1867,7 +1869,7 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
       k_p3_stub<<<grid_for(n_stub, 128), 128, 0, s>>>(P, WorkN{(int64_t)n_stub, nullptr, 0}, istub, nullptr, qstub, dflags);
     if (n_sec) k_p3_sector<<<grid_for(n_sec, 128), 128, 0, s>>>(P, wsec, isec, nullptr, qsec);
     if (n_seg) k_p3_segment<<<grid_for(n_seg, 128), 128, 0, s>>>(P, wseg, iseg, nullptr, qseg);
-    if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
+    if ((st = check_launch(c, "P3 piece kernels", (n_stub > 0) + (n_sec > 0) + (n_seg > 0))) != SPHBI_OK) return st;
     k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, items, ItemOuts{qsec, {qstub, qstub}, qseg},
                                                   p3->nodes, p3->pt, stride, dout);
     return check_launch(c, "k_p3_combine");
@@ -1909,7 +1911,11 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
     if (n_sec) k_pipe_sector<false><<<grid_for(n_sec, 128), 128, 0, s>>>(K, wsec, isec, nullptr, osec);
     if (n_seg) k_pipe_segment<false><<<grid_for(n_seg, 128), 128, 0, s>>>(K, wseg, iseg, nullptr, oseg);
   }
-  if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+  {
+    int nl = (n_sec > 0) + (n_seg > 0);
+    for (int cl = 0; cl < 4; ++cl) nl += tot[1 + cl] > 0;
+    if ((st = check_launch(c, "piece kernels", nl)) != SPHBI_OK) return st;
+  }
   const void* so = f1 ? (const void*)ostub3 : (const void*)ostub;
   const ItemOuts io{osec, {so, so}, oseg};
   if (mode == 0) {
@@ -1966,7 +1972,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   unsigned* lcount;
   if ((st = scratch_t(c, kBufIdx, (kCapSec + 2 * kCapStub + kCapSeg) * n, &lists)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPipeCnt, kKinds, &lcount)) != SPHBI_OK) return st;
-  SPHBI_CUDA_TRY(zero_async(lcount, sizeof(unsigned) * kKinds, s));
+  SPHBI_CUDA_TRY(zero_async(c, lcount, sizeof(unsigned) * kKinds, s));
   const long long scap = static_cast<long long>(kCapStub) * n;
   const SlotLists L{lists, {lists + kCapSec * n, lists + kCapSec * n + scap}, lists + kCapSec * n + 2 * scap, lcount,
                     scap};
@@ -2031,7 +2037,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     for (int cl = 0; cl < 4; ++cl) k_p3_stub<<<igrid(k_p3_stub, 1 + cl), 128, 0, s>>>(P, wst[cl], istub, xst[cl], qst[cl], dflags);
     k_p3_sector<<<igrid(k_p3_sector, 0), 128, 0, s>>>(P, wsec, isec, L.sec, qsec);
     k_p3_segment<<<igrid(k_p3_segment, 5), 128, 0, s>>>(P, wseg, iseg, L.seg, qseg);
-    if ((st = check_launch(c, "P3 piece kernels")) != SPHBI_OK) return st;
+    if ((st = check_launch(c, "P3 piece kernels", 6)) != SPHBI_OK) return st;
     k_p3_combine<<<grid_for(n, 128), 128, 0, s>>>(K, P, nrec, n, h, items,
                                                   ItemOuts{qsec, {qstub, qstub + scap}, qseg}, p3->nodes, p3->pt,
                                                   stride, dout);
@@ -2049,7 +2055,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     k_pipe_stub<true, 3><<<igrid(k_pipe_stub<true, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3], dflags);
     k_pipe_sector<true><<<igrid(k_pipe_sector<true>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
     k_pipe_segment<true><<<igrid(k_pipe_segment<true>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
-    if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+    if ((st = check_launch(c, "piece kernels", 6)) != SPHBI_OK) return st;
     mark(2);
     k_pipe_combine<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items,
                                                           ItemOuts{osec, {ostub, ostub + scap}, oseg}, stride, dout);
@@ -2067,7 +2073,7 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   k_pipe_stub<false, 3><<<igrid(k_pipe_stub<false, 3>, 4), 128, 0, s>>>(K, wst[3], istub, xst[3], ost[3], dflags);
   k_pipe_sector<false><<<igrid(k_pipe_sector<false>, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
   k_pipe_segment<false><<<igrid(k_pipe_segment<false>, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
-  if ((st = check_launch(c, "piece kernels")) != SPHBI_OK) return st;
+  if ((st = check_launch(c, "piece kernels", 6)) != SPHBI_OK) return st;
   const ItemOuts io{osec, {ostub, ostub + scap}, oseg};
   if (mode == 0) {
     k_pipe_combine<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, h, items, io, stride, dout);
@@ -2193,8 +2199,8 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     SPHBI_CUDA_TRY(cudaStreamWaitEvent(cs, c->sev[0][k % 64], 0));
     if (c->timeline && k < 64) SPHBI_CUDA_TRY(cudaEventRecord(c->tl[193 + k], cs));
     if (np > 0 && nq == 0) {  // otherwise k_reduce_rows writes every row of the chunk
-      SPHBI_CUDA_TRY(zero_async(dov + p0, 8 * np, cs));
-      SPHBI_CUDA_TRY(zero_async(dog + 2 * p0, 16 * np, cs));
+      SPHBI_CUDA_TRY(zero_async(c, dov + p0, 8 * np, cs));
+      SPHBI_CUDA_TRY(zero_async(c, dog + 2 * p0, 16 * np, cs));
     }
     if (nq > 0) {
       // validate (range, sortedness) and convert to int32 pairs
@@ -2607,7 +2613,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       (!out_value || is_pinned(out_value)) && (!out_grad || is_pinned(out_grad))) {
     unsigned* sflags;
     if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;  // 8 x u32
-    SPHBI_CUDA_TRY(zero_async(sflags, 32, s));
+    SPHBI_CUDA_TRY(zero_async(c, sflags, 32, s));
     unsigned long long* sctr = c->counters_on ? c->d_counters : nullptr;
     st = evaluate_streamed(c, K, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
                            pair_particle, pair_triangle, out_value, out_grad, sflags, sctr);
@@ -2706,10 +2712,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   }
   unsigned* dflags;
   if ((st = scratch_t(c, kBufFlags, 8, &dflags)) != SPHBI_OK) return st;
-  SPHBI_CUDA_TRY(zero_async(dflags, 32, s));
+  SPHBI_CUDA_TRY(zero_async(c, dflags, 32, s));
   if (n_particles) {
-    SPHBI_CUDA_TRY(zero_async(dov, 8 * n_particles, s));
-    SPHBI_CUDA_TRY(zero_async(dog, 16 * n_particles, s));
+    SPHBI_CUDA_TRY(zero_async(c, dov, 8 * n_particles, s));
+    SPHBI_CUDA_TRY(zero_async(c, dog, 16 * n_particles, s));
   }
   unsigned long long* ctr = c->counters_on ? c->d_counters : nullptr;
   int64_t total_pairs = 0, candidates = 0;
@@ -3125,7 +3131,7 @@ static sphbi_status integrate_pairs_p3_impl(sphbi_ctx* c, const sphbi_kernel_des
     dn = v;
     dout = o;
   }
-  SPHBI_CUDA_TRY(zero_async(dflags, 32, s));
+  SPHBI_CUDA_TRY(zero_async(c, dflags, 32, s));
   {
     const DirectSrc src{dq, dt, nullptr};  // geometry only; the field enters in k_p3_combine
     const P3Job job{P.get(), dn, nullptr};

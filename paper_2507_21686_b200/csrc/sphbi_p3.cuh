@@ -237,63 +237,132 @@ SPHBI_HD void h24_half_disc(const P3Consts& P, H24& H) {
 }
 
 // Weighted chain sums. Every stub-window / segment sum of a descriptor is
-// sum_k w_k F(k + off) with F a fixed linear combination of chain values at
+// sum_k w_k F(k + off), F a fixed linear combination of chain values at
 // shifted indices (p3_sp), so the k-sum is taken first, once per (family,
-// chain, shift): W[f][s + kW0] = sum_k w_f[k] C[k + s] (C[idx] = 0 for
-// idx < 0), s = -kW0 .. kW1. ~44 weighted sums per bound instead of the
-// descriptor x k x Chebyshev-term products.
-constexpr int kW0 = 5, kW1 = 4, kWN = kW0 + kW1 + 1;
-SPHBI_HD void p3_wsums(const P3Consts& P, const dd* C, int smin, dd (*W)[kWN]) {
-  for (int f = 0; f < 2; ++f)
-    for (int s = smin; s <= kW1; ++s) {
-      acc2 a{0.0, 0.0};
-      for (int k = s < 0 ? -s : 0; k <= P.deg; ++k) {
-        const dd w = P.w[f][k];
-        if (w.hi == 0.0) continue;
-        acc_add_dddd(a, w, C[k + s]);
-      }
-      W[f][s + kW0] = acc_dd(a);
+// chain, shift): W(f, s) = sum_k w_f[k] C[k + s] (C[idx] = 0 for idx < 0).
+// The descriptor table needs 17 of them (T_a / U_(a-1) terms of p3_sp):
+//   family 0: X shifts 1..4, I shifts 2, 4;  family 1: X shifts -1..3, I shifts 0, 2;
+//   Pt sums with the weights pc[f][off] (= w_k / (n + 1)) for off 1, 3.
+// They are accumulated while the chains are generated (no chain arrays).
+struct P3W {
+  dd x0[4], i0[2], x1[5], i1[2], p[2][2];
+};
+SPHBI_HD dd p3w_x(const P3W& W, int f, int s) {
+  if (f == 0) return s >= 1 && s <= 4 ? W.x0[s - 1] : dd{0.0, 0.0};
+  return s >= -1 && s <= 3 ? W.x1[s + 1] : dd{0.0, 0.0};
+}
+SPHBI_HD dd p3w_i(const P3W& W, int f, int s) {
+  if (f == 0) return s == 2 ? W.i0[0] : (s == 4 ? W.i0[1] : dd{0.0, 0.0});
+  return s == 0 ? W.i1[0] : (s == 2 ? W.i1[1] : dd{0.0, 0.0});
+}
+SPHBI_HD void p3_acc_w(acc2& a, const dd* w, int deg, int k, dd c) {
+  if (k >= 0 && k <= deg) {
+    const dd wk = w[k];
+    if (wk.hi != 0.0) acc_add_dddd(a, wk, c);
+  }
+}
+// Chains at bound x (x >= D > 0) in double-double, as p3_chains, consumed on
+// the fly: Pt_m (Pt_0 = log((x+R)/D), Pt_1 = R), I_m (I_0 = 0), X_m = x^(m+1)/(m+1).
+SPHBI_HD void p3_wchain(const P3Consts& P, double x, double D, bool want_x, P3W& W, dd& Rout) {
+  ChainSeeds sd;
+  chain_seeds(x, D, sd);
+  const dd D2 = two_prod(D, D);
+  const dd R3 = dd_mul(dd_mul(sd.R, sd.R), sd.R);
+  const int deg = P.deg;
+  const int M = deg + 5;  // highest index used: deg + 4
+  acc2 ax0[4], ai0[2], ax1[5], ai1[2], ap[2][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ax0[q] = acc2{0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) ax1[q] = acc2{0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    ai0[q] = ai1[q] = acc2{0.0, 0.0};
+    ap[0][q] = ap[1][q] = acc2{0.0, 0.0};
+  }
+  dd Pm2{0.0, 0.0}, Pm1{0.0, 0.0}, Im2{0.0, 0.0}, Im1{0.0, 0.0};
+  dd xp = dd_make(1.0), xpm2 = dd_make(1.0);
+  dd xq = dd_make(x);
+#pragma unroll 1
+  for (int m = 0; m < M; ++m) {
+    dd Pt, I;
+    if (m == 0) {
+      Pt = sd.p0;
+      I = dd{0.0, 0.0};
+    } else if (m == 1) {
+      Pt = sd.R;
+      I = sd.i1;
+    } else {
+      xpm2 = xp;                // x^(m-2)
+      xp = dd_mul_d(xp, x);     // x^(m-1)
+      Pt = dd_div_d_small(dd_add(dd_mul(xp, sd.R), dd_mul_d(dd_mul(D2, Pm2), (double)(m - 1))), m);
+      I = dd_div_d_small(dd_add(dd_mul(xpm2, R3), dd_mul_d(dd_mul(D2, Im2), (double)(m - 2))), m + 1);
     }
+    Pm2 = Pm1;
+    Pm1 = Pt;
+    Im2 = Im1;
+    Im1 = I;
+    if (want_x) {
+      const dd X = dd_div_d_small(xq, m + 1);
+      xq = dd_mul_d(xq, x);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) p3_acc_w(ax0[q], P.w[0], deg, m - (q + 1), X);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) p3_acc_w(ax1[q], P.w[1], deg, m - (q - 1), X);
+    }
+    p3_acc_w(ai0[0], P.w[0], deg, m - 2, I);
+    p3_acc_w(ai0[1], P.w[0], deg, m - 4, I);
+    p3_acc_w(ai1[0], P.w[1], deg, m, I);
+    p3_acc_w(ai1[1], P.w[1], deg, m - 2, I);
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      p3_acc_w(ap[f][0], P.pc[f][1], deg, m - 1, Pt);
+      p3_acc_w(ap[f][1], P.pc[f][3], deg, m - 3, Pt);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) W.x0[q] = acc_dd(ax0[q]);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) W.x1[q] = acc_dd(ax1[q]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    W.i0[q] = acc_dd(ai0[q]);
+    W.i1[q] = acc_dd(ai1[q]);
+    W.p[0][q] = acc_dd(ap[0][q]);
+    W.p[1][q] = acc_dd(ap[1][q]);
+  }
+  Rout = sd.R;
 }
 // sum_k w_f[k] p3_sp(k + o, m, ...) from the weighted sums (m <= 4)
-SPHBI_HD dd p3_wsp(const dd (*WI)[kWN], const dd (*WX)[kWN], int f, int o, int m, dd D2) {
-  const dd(*W)[kWN] = (m & 1) ? WI : WX;
+SPHBI_HD dd p3_wsp(const P3W& W, int f, int o, int m, dd D2) {
   dd acc{0.0, 0.0};
   dd pw = dd_make(1.0);  // (-D^2)^l
   const int top = m / 2;
   for (int l = 0; l <= top; ++l) {
     const double bin = l == 0 ? 1.0 : (top == 1 ? 1.0 : (l == 1 ? 2.0 : 1.0));  // C(top, l), top <= 2
     const int sh = o - 2 * l;
-    if (sh >= -kW0) acc = dd_add(acc, dd_mul_d(dd_mul(W[f][sh + kW0], pw), bin));
+    const dd w = (m & 1) ? p3w_i(W, f, sh) : p3w_x(W, f, sh);
+    acc = dd_add(acc, dd_mul_d(dd_mul(w, pw), bin));
     pw = dd_neg(dd_mul(pw, D2));
   }
   return acc;
 }
-// sum_k pc[f][off][k] Pt[k + off] (= sum_k w_k Pt[n] / (n + 1))
-SPHBI_HD dd p3_wpt(const P3Consts& P, const dd* Pt, int f, int off) {
-  acc2 a{0.0, 0.0};
-  for (int k = 0; k <= P.deg; ++k) {
-    const dd w = P.pc[f][off][k];
-    if (w.hi == 0.0 && w.lo == 0.0) continue;
-    acc_add_dddd(a, w, Pt[k + off]);
-  }
-  return acc_dd(a);
-}
+// sum_k pc[f][off][k] Pt[k + off] (= sum_k w_k Pt[n] / (n + 1)), off in {1, 3}
+SPHBI_HD dd p3w_pt(const P3W& W, int f, int off) { return off == 1 ? W.p[f][0] : W.p[f][1]; }
 
 // segment {x >= d}, 0 < d < 1 (elementary_regions.hpp:130-167 generalised)
 SPHBI_HD void h24_segment(const P3Consts& P, double d, H24& H) {
-  dd Pt[kP3Chain], I[kP3Chain], X[kP3Chain], R;
-  const int M = P.deg + 6;
-  p3_chains(1.0, d, M, Pt, I, X, R);
+  P3W W;
+  dd R;
+  p3_wchain(P, 1.0, d, false, W, R);
   const double acd = d <= 0.7 ? acos(d) : asin(R.hi);
-  dd WI[2][kWN];
-  p3_wsums(P, I, -3, WI);
   h24_zero(H);
+#pragma unroll
   for (int dsi = 0; dsi < kP3Desc; ++dsi) {
     const P3Desc ds = p3desc(dsi);
     if (ds.a == 0) {
       // sum_k w_k 2 (acd - Pt[n] d) / (n + 1)
-      const dd pv = dd_sub(dd_mul_d(P.pc1[ds.fam][ds.off], acd), dd_mul_d(p3_wpt(P, Pt, ds.fam, ds.off), d));
+      const dd pv = dd_sub(dd_mul_d(P.pc1[ds.fam][ds.off], acd), dd_mul_d(p3w_pt(W, ds.fam, ds.off), d));
       H.c[ds.ic] = dd_mul_d(pv, 2.0);
     } else {
       // sum_k w_k (2/a) sum_p U_(a-1)[p] d^p I[n - p]
@@ -301,7 +370,7 @@ SPHBI_HD void h24_segment(const P3Consts& P, double d, H24& H) {
       double dp = 1.0;
       for (int p = 0; p < ds.a; ++p) {
         const double u = uco(ds.a, p);
-        if (u != 0.0) r = dd_add(r, dd_mul_d(WI[ds.fam][ds.off - p + kW0], u * dp));
+        if (u != 0.0) r = dd_add(r, dd_mul_d(p3w_i(W, ds.fam, ds.off - p), u * dp));
         dp *= d;
       }
       H.c[ds.ic] = dd_mul_d(r, 2.0 / ds.a);
@@ -311,9 +380,9 @@ SPHBI_HD void h24_segment(const P3Consts& P, double d, H24& H) {
 
 // stub radial window antiderivative at bound x, added with sign sgn
 SPHBI_HD void h24_stub_bound(const P3Consts& P, double x, double D, double beta, double sgn, H24& H) {
-  dd Pt[kP3Chain], I[kP3Chain], X[kP3Chain], R;
-  const int M = P.deg + 6;
-  p3_chains(x, D, M, Pt, I, X, R);
+  P3W W;
+  dd R;
+  p3_wchain(P, x, D, true, W, R);
   double as;
   if (D <= 0.7 * x)
     as = asin(D / x);
@@ -321,15 +390,13 @@ SPHBI_HD void h24_stub_bound(const P3Consts& P, double x, double D, double beta,
     as = (kHalfPiHi - asin(R.hi / x)) + kHalfPiLo;
   const double amb = as - beta;
   const dd D2 = two_prod(D, D);
-  dd WI[2][kWN], WX[2][kWN];
-  p3_wsums(P, I, -kW0, WI);
-  p3_wsums(P, X, -kW0, WX);
+#pragma unroll
   for (int dsi = 0; dsi < kP3Desc; ++dsi) {
     const P3Desc ds = p3desc(dsi);
     const int f = ds.fam;
     if (ds.a == 0) {
       // sum_k w_k (X[n] amb + Pt[n] D / (n + 1))
-      const dd r = dd_add(dd_mul_d(WX[f][ds.off + kW0], amb), dd_mul_d(p3_wpt(P, Pt, f, ds.off), D));
+      const dd r = dd_add(dd_mul_d(p3w_x(W, f, ds.off), amb), dd_mul_d(p3w_pt(W, f, ds.off), D));
       H.c[ds.ic] = dd_add(H.c[ds.ic], dd_scale(r, sgn));
       continue;
     }
@@ -338,13 +405,13 @@ SPHBI_HD void h24_stub_bound(const P3Consts& P, double x, double D, double beta,
     dd tsum{0.0, 0.0}, usum{0.0, 0.0};
     for (int j = 0; j <= ds.a; ++j) {
       const double t = tco(ds.a, j);
-      if (t != 0.0) tsum = dd_add(tsum, dd_mul_d(p3_wsp(WI, WX, f, ds.off, j, D2), t));
+      if (t != 0.0) tsum = dd_add(tsum, dd_mul_d(p3_wsp(W, f, ds.off, j, D2), t));
       const double u = j < ds.a ? uco(ds.a, j) : 0.0;
-      if (u != 0.0) usum = dd_add(usum, dd_mul_d(p3_wsp(WI, WX, f, ds.off - 1, j, D2), u));
+      if (u != 0.0) usum = dd_add(usum, dd_mul_d(p3_wsp(W, f, ds.off - 1, j, D2), u));
     }
     const dd du = dd_mul_d(usum, D);
     const dd rc = dd_mul_d(dd_sub(dd_mul_d(du, cab), dd_mul_d(tsum, sab)), 1.0 / ds.a);
-    const dd rs = dd_mul_d(dd_sub(dd_sub(WX[f][ds.off + kW0], dd_mul_d(tsum, cab)), dd_mul_d(du, sab)), 1.0 / ds.a);
+    const dd rs = dd_mul_d(dd_sub(dd_sub(p3w_x(W, f, ds.off), dd_mul_d(tsum, cab)), dd_mul_d(du, sab)), 1.0 / ds.a);
     H.c[ds.ic] = dd_add(H.c[ds.ic], dd_scale(rc, sgn));
     H.c[ds.is] = dd_add(H.c[ds.is], dd_scale(rs, sgn));
   }
