@@ -71,6 +71,9 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_EMIT
 #define SPHBI_MINB_EMIT 4
 #endif
+#ifndef SPHBI_MINB_P3
+#define SPHBI_MINB_P3 4
+#endif
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
@@ -1193,7 +1196,7 @@ __global__ void __launch_bounds__(128)
     h24_store(acc, out[k]);
   }
 }
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, SPHBI_MINB_P3)
     k_p3_stub(const __grid_constant__ P3Consts P, WorkN wn, const StubItem* __restrict__ items,
               const int* __restrict__ idx, H24Out* __restrict__ out, unsigned* status_or) {
   SPHBI_ITEM_LOOP(k) {
