@@ -172,6 +172,7 @@ struct sphbi_ctx {
   cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  bool no_sparse_find = false;  // SPHBI_NO_SPARSE_FIND=1: always walk all particles in cell order
   int stream_chunk_log2 = 0;    // SPHBI_STREAM_CHUNK_LOG2: equal chunks of 2^L particles (0: the ramp)
   std::vector<double> stream_ramp{1, 2, 3, 4, 3, 2, 1};  // SPHBI_STREAM_RAMP: relative chunk sizes
   // SPHBI_TIMELINE=1: the streamed path records timing events per chunk and
@@ -1290,6 +1291,20 @@ __global__ void k_iota(int n, int* __restrict__ out) {
   if (i < n) out[i] = i;
 }
 
+// Row pointers by binary search, one thread per row: balanced when most
+// particles have no pairs (a thread per pair would fill long gaps alone).
+__global__ void k_row_ptr_bs(int64_t npairs, const int* __restrict__ pp, int p_begin, int p_count,
+                             int64_t* __restrict__ row_ptr) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j > p_count) return;
+  const int target = p_begin + static_cast<int>(j);
+  int64_t lo = 0, hi = npairs;  // first k with pp[k] >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(pp + mid) < target) lo = mid + 1; else hi = mid;
+  }
+  row_ptr[j] = lo;
+}
 __global__ void k_row_ptr(int64_t npairs, const int* __restrict__ pp, int p_begin, int p_count,
                           int64_t* __restrict__ row_ptr) {
   // row_ptr[j] = first pair with particle >= p_begin + j, j in [0, p_count]
@@ -1575,7 +1590,19 @@ __global__ void k_tri_cell_fill(int64_t n_tris, const double* __restrict__ tri, 
     }
 }
 
-// cell_start[c] = first sorted entry with key >= c, c in [0, ncells]
+// cell_start[c] = first sorted entry with key >= c, c in [0, ncells]; by
+// binary search per cell (grids with more cells than entries)
+__global__ void k_cell_start_bs(int64_t n_entries, const unsigned* __restrict__ keys, int ncells,
+                                unsigned long long* __restrict__ cell_start) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c > ncells) return;
+  int64_t lo = 0, hi = n_entries;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(__ldg(keys + mid)) < c) lo = mid + 1; else hi = mid;
+  }
+  cell_start[c] = static_cast<unsigned long long>(lo);
+}
 __global__ void k_cell_start(int64_t n_entries, const unsigned* __restrict__ keys, int ncells,
                              unsigned long long* __restrict__ cell_start) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1591,6 +1618,24 @@ __global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid 
   const int cx = cell_coord(pxy[2 * i], g.x0, g.cell, g.nx);
   const int cy = cell_coord(pxy[2 * i + 1], g.y0, g.cell, g.ny);
   cell[i] = static_cast<unsigned>(cy * g.nx + cx);
+}
+// Sparse scenes (few cells hold triangles, e.g. a boundary strip around a
+// particle-filled domain): the cell of each particle, whether its cell list is
+// non-empty (flag), and a zero pair count for the others -- only the active
+// particles are walked, in index order (no particle sort).
+__global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy, Grid g,
+                                       const unsigned long long* __restrict__ cell_start, unsigned* __restrict__ cell,
+                                       unsigned char* __restrict__ active, unsigned long long* __restrict__ count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+  const int cx = cell_coord(p.x, g.x0, g.cell, g.nx);
+  const int cy = cell_coord(p.y, g.y0, g.cell, g.ny);
+  const unsigned c = static_cast<unsigned>(cy * g.nx + cx);
+  cell[i] = c;
+  const bool a = cell_start[c + 1] > cell_start[c];
+  active[i] = a ? 1 : 0;
+  if (!a) count[i] = 0;
 }
 
 // Count (fill == 0) or emit (fill == 1) the pairs of a set of particles.
@@ -1608,9 +1653,10 @@ __global__ void __launch_bounds__(kFindBlock)
                  const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
                  const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
                  unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
-                 int* __restrict__ pt) {
+                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (dcount) count = *dcount;  // device-side list length (sparse path)
   if ((pos & ~31ll) >= count) return;  // whole warps
   const bool valid = pos < count;
   int i = 0;
@@ -1723,6 +1769,16 @@ __global__ void k_chunk_bounds(int np, const unsigned long long* __restrict__ of
     out[2 * k + 1] = static_cast<long long>(off[p0]);
   }
   *nchunks = p0 < np ? -1 : k;
+}
+// row pointers of a particle-sorted pair list: per pair (dense rows) or per
+// row by binary search (sparse rows)
+static void launch_row_ptr(int64_t npairs, const int* pp, int p_begin, int p_count, int64_t* row_ptr,
+                           cudaStream_t s) {
+  if (npairs * 2 < static_cast<int64_t>(p_count))
+    k_row_ptr_bs<<<grid_for(static_cast<int64_t>(p_count) + 1, 256), 256, 0, s>>>(npairs, pp, p_begin, p_count,
+                                                                                   row_ptr);
+  else
+    k_row_ptr<<<grid_for(npairs + 1, 256), 256, 0, s>>>(npairs, pp, p_begin, p_count, row_ptr);
 }
 static int find_grid(int64_t count) {
   return static_cast<int>(((count + 31) / 32 * 32 + kFindBlock - 1) / kFindBlock);
@@ -2218,7 +2274,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
       c->tl_chunk = -1;
       c->stream = s;
       c->bank = 0;
-      k_row_ptr<<<grid_for(nq + 1, 256), 256, 0, cs>>>(nq, pp[q], (int)p0, (int)np, row_ptr[q]);
+      launch_row_ptr(nq, pp[q], (int)p0, (int)np, row_ptr[q], cs);
       if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
       k_reduce_rows<<<grid_for(np, 256), 256, 0, cs>>>((int)p0, (int)np, row_ptr[q], pout[q], dov, dog, 0);
       if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
@@ -2325,6 +2381,8 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
     c->two_pass = tp && tp[0] == '1';
     const char* ig = std::getenv("SPHBI_ITEM_GRID");
     c->item_grid = !ig ? 0 : (std::strcmp(ig, "sync") == 0 ? 1 : (std::strcmp(ig, "persist") == 0 ? 2 : 0));
+    const char* nsf = std::getenv("SPHBI_NO_SPARSE_FIND");
+    c->no_sparse_find = nsf && nsf[0] == '1';
     const char* ns = std::getenv("SPHBI_NO_SIG_SORT");
     c->no_sig_sort = ns && ns[0] == '1';
     const char* cl = std::getenv("SPHBI_STREAM_CHUNK_LOG2");
@@ -2782,7 +2840,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       // rows: all particles, accumulate (a particle may straddle chunks)
       const int pc = static_cast<int>(n_particles);
       if ((st = scratch_t(c, kBufRowPtr, pc + 1, &row_ptr)) != SPHBI_OK) return st;
-      k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp + done, 0, pc, row_ptr);
+      launch_row_ptr(cnt, pp + done, 0, pc, row_ptr, s);
       if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
       k_reduce_rows<<<grid_for(pc, 256), 256, 0, s>>>(0, pc, row_ptr, pout, dov, dog, 1);
       if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
@@ -2863,7 +2921,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       cub::DeviceRadixSort::SortPairs(dtmp, tmp, ka, kb, va, vb, (int)n_entries, 0, bits, s);
       if ((st = check_launch(c, "radix sort cell list")) != SPHBI_OK) return st;
     }
-    k_cell_start<<<grid_for((int64_t)n_entries + 1, 256), 256, 0, s>>>((int64_t)n_entries, kb, ncells, cell_start);
+    if (n_entries < static_cast<unsigned long long>(ncells))
+      k_cell_start_bs<<<grid_for((int64_t)ncells + 1, 256), 256, 0, s>>>((int64_t)n_entries, kb, ncells, cell_start);
+    else
+      k_cell_start<<<grid_for((int64_t)n_entries + 1, 256), 256, 0, s>>>((int64_t)n_entries, kb, ncells, cell_start);
     if ((st = check_launch(c, "k_cell_start")) != SPHBI_OK) return st;
     // K2: particle cells
     unsigned* pcell;
@@ -2871,10 +2932,32 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if ((st = scratch_t(c, kBufPartCell, n_particles, &pcell)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufPartCount, n_particles + 1, &pcount)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufPartOffset, n_particles + 1, &poff)) != SPHBI_OK) return st;
+    // Sparse scenes (fewer cell-list entries than a quarter of the particles,
+    // e.g. a boundary strip around a particle-filled domain): only the
+    // particles of non-empty cells are walked, listed in index order by a
+    // stable device compaction; otherwise all particles in cell order.
+    const bool sparse = n_entries * 4 < static_cast<unsigned long long>(n_particles) && !c->no_sparse_find;
+    int* sorder;
+    int* dactive_n = nullptr;
+    if (sparse) {
+      unsigned char* act;
+      if ((st = scratch_t(c, kBufPieceFlag, n_particles, &act)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufPartOrder, n_particles + 2, &sorder)) != SPHBI_OK) return st;
+      dactive_n = sorder + n_particles;
+      k_particle_cell_active<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, cell_start, pcell, act,
+                                                                        pcount);
+      if ((st = check_launch(c, "k_particle_cell_active")) != SPHBI_OK) return st;
+      size_t tmp = 0;
+      cub::CountingInputIterator<int> ids(0);
+      cub::DeviceSelect::Flagged(nullptr, tmp, ids, act, sorder, dactive_n, (int)n_particles, s);
+      void* dtmp;
+      if ((st = scratch(c, kBufCubTemp2, tmp, &dtmp)) != SPHBI_OK) return st;
+      cub::DeviceSelect::Flagged(dtmp, tmp, ids, act, sorder, dactive_n, (int)n_particles, s);
+      if ((st = check_launch(c, "select active particles")) != SPHBI_OK) return st;
+    } else {
     k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
     if ((st = check_launch(c, "k_particle_cell")) != SPHBI_OK) return st;
     // particles in cell order (the finder walks them so)
-    int* sorder;
     {
       unsigned* pcell_sorted;
       int* piota;
@@ -2891,11 +2974,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       cub::DeviceRadixSort::SortPairs(dtmp, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
       if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
     }
+    }
     // K3: count, scan
     const double h2 = h * h;
     const int np = static_cast<int>(n_particles);
     k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount,
-                                                      0, nullptr, nullptr);
+                                                      0, nullptr, nullptr, dactive_n);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
@@ -2941,7 +3025,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPairP, total_pairs, &gpp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPairT, total_pairs, &gpt)) != SPHBI_OK) return st;
       k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff,
-                                                        0, gpp, gpt);
+                                                        0, gpp, gpt, dactive_n);
       if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
     }
     // K4 + K5 in chunks of whole particles
@@ -2999,7 +3083,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           continue;
         }
         if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
-        k_row_ptr<<<grid_for(cnt + 1, 256), 256, 0, s>>>(cnt, pp, p0, p1 - p0, row_ptr);
+        launch_row_ptr(cnt, pp, p0, p1 - p0, row_ptr, s);
         if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
         k_reduce_rows<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, row_ptr, pout, dov, dog, 0);
         if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
@@ -3016,7 +3100,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   if (pair_list_capacity) *pair_list_capacity = total_pairs;
   if (bc) {
     if (!bc->pp && (st = bc->reserve(total_pairs)) != SPHBI_OK) return st;
-    k_row_ptr<<<grid_for(total_pairs + 1, 256), 256, 0, s>>>(total_pairs, bc->pp, 0, (int)n_particles, bc->row_ptr);
+    launch_row_ptr(total_pairs, bc->pp, 0, (int)n_particles, bc->row_ptr, s);
     if ((st = check_launch(c, "k_row_ptr(bases)")) != SPHBI_OK) return st;
   }
   // ---- outputs

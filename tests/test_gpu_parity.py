@@ -251,6 +251,28 @@ def test_cfg3_full_scene_runs_and_interior_is_zero(S, ctx):
     assert np.all(v >= -1e-12) and np.all(v <= 1.0 + 1e-12)
 
 
+def test_sparse_and_dense_pair_finders_agree(S, ctx):
+    """cfg3's strip covers a small part of the grid, so the finder walks only
+    the particles of non-empty cells (index order, no particle sort); forcing
+    the cell-ordered walk over all particles must give the same pair list and
+    bitwise the same sums."""
+    import os
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg3()
+    k = sc.kernels[0]
+    v1, g1, st1, pl1 = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
+    os.environ["SPHBI_NO_SPARSE_FIND"] = "1"
+    try:
+        c2 = S.Context(0)
+    finally:
+        os.environ.pop("SPHBI_NO_SPARSE_FIND", None)
+    v2, g2, st2, pl2 = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), ctx=c2, return_pairs=True)
+    c2.close()
+    assert st1.n_pairs == st2.n_pairs > 10000
+    assert np.array_equal(pl1, pl2)
+    assert np.array_equal(v1, v2) and np.array_equal(g1, g2)
+
+
 @pytest.mark.parametrize("kernel", ["wendland_c2", "cubic_spline"])
 def test_cfg5_reduced_scene(S, ctx, O, kernel):
     """cfg5 structure (Delaunay obstacle discs, uniform particles, h = 0.1) at
