@@ -271,11 +271,41 @@ SPHBI_HD void acc_add_region(PairAcc& a, const S9& S, const Frame& M, double sig
 // Cone / sector theta in [0, gamma], r in [0, L] (elementary_regions.hpp:65-83):
 //   p_n = gamma B_n, c_a = sin(a g)/a B_n, s_a = (1-cos(a g))/a B_n,
 //   B_n = L^(n+1)/(n+1).
-SPHBI_HD void cone_sums(const KernelConsts& K, double gamma, dd Pv, dd Qv, dd Pg, dd Rg, S9& S) {
-  double sg, cg;
-  dsincos(gamma, &sg, &cg);
+// Trigonometric factors of a piece: sin / cos / 1 - cos of the opening angle
+// gamma and sin / cos of the window angle beta. The pipeline's piece kernels
+// take them from the piece geometry (trig_from_geometry: ratios of the vectors
+// the angles are the atan2 of, ~1 ulp like sincos of the angle, and several
+// transcendental evaluations cheaper); the other sinks from the angles.
+struct PieceTrig {
+  double sg, cg, omc, sb, cb;
+};
+SPHBI_HD PieceTrig trig_from_angles(double gamma, double beta) {
+  PieceTrig t;
+  dsincos(gamma, &t.sg, &t.cg);
   const double sh = sin(0.5 * gamma);
-  const double omc = 2.0 * sh * sh;  // 1 - cos(gamma), cancellation-free
+  t.omc = 2.0 * sh * sh;  // 1 - cos(gamma), cancellation-free
+  dsincos(beta, &t.sb, &t.cb);
+  return t;
+}
+// gamma = atan2(wy, wx) with wy >= 0; beta = atan2(by, bx) (by >= 0; pass
+// bx = 1, by = 0 when there is no window)
+SPHBI_HD PieceTrig trig_from_geometry(double wx, double wy, double bx, double by) {
+  PieceTrig t;
+  const double rw = sqrt(wx * wx + wy * wy);
+  t.sg = wy / rw;
+  t.cg = wx / rw;
+  // 1 - cos = wy^2 / (rw (rw + wx)) without cancellation for wx >= 0
+  t.omc = wx >= 0.0 ? t.sg * (wy / (rw + wx)) : (rw - wx) / rw;
+  const double rb = sqrt(bx * bx + by * by);
+  t.sb = by / rb;
+  t.cb = bx / rb;
+  return t;
+}
+
+SPHBI_HD void cone_sums(const KernelConsts& K, double gamma, const PieceTrig& T, dd Pv, dd Qv, dd Pg, dd Rg,
+                        S9& S) {
+  const double sg = T.sg, cg = T.cg;
+  const double omc = T.omc;
   const dd sgcg = two_prod(sg, cg);  // sin(2g)/2
   const dd ggp = dd_add(dd_make(gamma), sgcg);
   const dd ggm = dd_sub(dd_make(gamma), sgcg);
@@ -576,13 +606,14 @@ SPHBI_HD void piece_half_disc(const KernelConsts& K, PairAcc& acc, const Frame& 
 }
 
 SPHBI_HD void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double L,
-                           double sign) {
+                           double sign, const PieceTrig* Tp = nullptr) {
+  const PieceTrig T = Tp ? *Tp : trig_from_angles(gamma, 0.0);
   S9 S;
   if (L >= 1.0) {
-    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+    cone_sums(K, gamma, T, K.pv1, K.qv1, K.pg1, K.rg1, S);
   } else {
     const int N = K.deg;
-    cone_sums(K, gamma, poly_dd(K.pv, N, L, 2), poly_dd(K.qv, N, L, 3), poly_dd(K.pg, N, L, 2),
+    cone_sums(K, gamma, T, poly_dd(K.pv, N, L, 2), poly_dd(K.qv, N, L, 3), poly_dd(K.pg, N, L, 2),
               poly_dd(K.rg, N, L, 1), S);
   }
   acc_add_region(acc, S, f, sign);
@@ -591,18 +622,18 @@ SPHBI_HD void piece_cone(const KernelConsts& K, PairAcc& acc, const Frame& f, do
 // Direct stub: cone [0,gamma] x [0,l] plus (when u > lo + eps) the radial
 // window [lo, u] at chord distance D and far-edge angle beta, in ONE frame.
 SPHBI_HD void piece_stub(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double l, double D,
-                         double beta, double lo, double u, bool window, double sign) {
+                         double beta, double lo, double u, bool window, double sign, const PieceTrig* Tp = nullptr) {
+  const PieceTrig T = Tp ? *Tp : trig_from_angles(gamma, window ? beta : 0.0);
   S9 S;
   if (l >= 1.0) {
-    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+    cone_sums(K, gamma, T, K.pv1, K.qv1, K.pg1, K.rg1, S);
   } else {
     const int N = K.deg;
-    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+    cone_sums(K, gamma, T, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
               poly_dd(K.rg, N, l, 1), S);
   }
   if (window) {
-    double sb, cb;
-    dsincos(beta, &sb, &cb);
+    const double sb = T.sb, cb = T.cb;
     const double s2b = 2.0 * sb * cb;
     const double c2b = (cb - sb) * (cb + sb);
     stub_bound_sums(K, u, D, beta, cb, sb, c2b, s2b, S, 1.0);
@@ -621,21 +652,20 @@ SPHBI_HD int stub_class(double D, double lo, double u, bool window) {
 
 template <int CLS>
 SPHBI_HD void piece_stub_k(const KernelConsts& K, PairAcc& acc, const Frame& f, double gamma, double l, double D,
-                           double beta, double lo, double u, bool window, double sign) {
+                           double beta, double lo, double u, bool window, double sign, const PieceTrig& T) {
   if (CLS == 3) {
-    piece_stub(K, acc, f, gamma, l, D, beta, lo, u, window, sign);
+    piece_stub(K, acc, f, gamma, l, D, beta, lo, u, window, sign, &T);
     return;
   }
   S9 S;
   if (l >= 1.0) {
-    cone_sums(K, gamma, K.pv1, K.qv1, K.pg1, K.rg1, S);
+    cone_sums(K, gamma, T, K.pv1, K.qv1, K.pg1, K.rg1, S);
   } else {
     const int N = K.deg;
-    cone_sums(K, gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
+    cone_sums(K, gamma, T, poly_dd(K.pv, N, l, 2), poly_dd(K.qv, N, l, 3), poly_dd(K.pg, N, l, 2),
               poly_dd(K.rg, N, l, 1), S);
   }
-  double sb, cb;
-  dsincos(beta, &sb, &cb);
+  const double sb = T.sb, cb = T.cb;
   const double s2b = 2.0 * sb * cb;
   const double c2b = (cb - sb) * (cb + sb);
   stub_bound_sums_k<(CLS == 0 || CLS == 2) ? 1 : 0>(K, u, D, beta, cb, sb, c2b, s2b, S, 1.0);
@@ -701,11 +731,9 @@ SPHBI_HD void piece_half_disc3(const KernelConsts& K, PairAcc3& acc, const Frame
   S.gy3 = dd{0.0, 0.0};
   acc3_add_region(acc, S, f, sign);
 }
-SPHBI_HD void cone_sums3(double gamma, dd Pv, dd Rg, S3& S) {
-  double sg, cg;
-  dsincos(gamma, &sg, &cg);
-  const double sh = sin(0.5 * gamma);
-  const double omc = 2.0 * sh * sh;
+SPHBI_HD void cone_sums3(double gamma, const PieceTrig& T, dd Pv, dd Rg, S3& S) {
+  const double sg = T.sg;
+  const double omc = T.omc;
   S.v3 = dd_mul_d(Pv, gamma);
   S.gx3 = dd_mul_d(Rg, sg);
   S.gy3 = dd_mul_d(Rg, omc);
@@ -765,29 +793,28 @@ SPHBI_HD void stub_bound_sums3(const KernelConsts& K, double x, double D, double
 }
 template <int CLS>
 SPHBI_HD void piece_stub3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double gamma, double l, double D,
-                          double beta, double lo, double u, bool window, double sign) {
+                          double beta, double lo, double u, bool window, double sign, const PieceTrig& T) {
   S3 S;
   if (l >= 1.0) {
-    cone_sums3(gamma, K.pv1, K.rg1, S);
+    cone_sums3(gamma, T, K.pv1, K.rg1, S);
   } else {
     const int N = K.deg;
-    cone_sums3(gamma, poly_dd(K.pv, N, l, 2), poly_dd(K.rg, N, l, 1), S);
+    cone_sums3(gamma, T, poly_dd(K.pv, N, l, 2), poly_dd(K.rg, N, l, 1), S);
   }
   if (CLS != 3 || window) {
-    double sb, cb;
-    dsincos(beta, &sb, &cb);
+    const double sb = T.sb, cb = T.cb;
     stub_bound_sums3<(CLS == 0 || CLS == 2) ? 1 : 0>(K, u, D, beta, cb, sb, S, 1.0);
     stub_bound_sums3<(CLS == 0 || CLS == 1) ? 2 : 0>(K, lo, D, beta, cb, sb, S, -1.0);
   }
   acc3_add_region(acc, S, f, sign);
 }
 SPHBI_HD void piece_cone3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double gamma, double L,
-                          double sign) {
+                          double sign, const PieceTrig& T) {
   S3 S;
   if (L >= 1.0)
-    cone_sums3(gamma, K.pv1, K.rg1, S);
+    cone_sums3(gamma, T, K.pv1, K.rg1, S);
   else
-    cone_sums3(gamma, poly_dd(K.pv, K.deg, L, 2), poly_dd(K.rg, K.deg, L, 1), S);
+    cone_sums3(gamma, T, poly_dd(K.pv, K.deg, L, 2), poly_dd(K.rg, K.deg, L, 1), S);
   acc3_add_region(acc, S, f, sign);
 }
 SPHBI_HD void piece_segment3(const KernelConsts& K, PairAcc3& acc, const Frame& f, double d, double sign) {
@@ -861,7 +888,7 @@ SPHBI_HD Frame rotation_taking_to_x(P2 v, Sink& c) {
 
 // Frame and opening angle of a sector (:352-360), given the rotation f taking
 // v1 onto +x: mirror so that v2 lies in the upper half plane, gamma = its angle.
-SPHBI_HD void sector_frame_angle(P2 v1, P2 v2, Frame& f, double& gamma) {
+SPHBI_HD void sector_frame_angle(P2 v1, P2 v2, Frame& f, double& gamma, PieceTrig* T = nullptr) {
   (void)v1;
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -870,14 +897,15 @@ SPHBI_HD void sector_frame_angle(P2 v1, P2 v2, Frame& f, double& gamma) {
     w2.y = -w2.y;
   }
   gamma = d_atan2(w2.y, w2.x);
+  if (T) *T = trig_from_geometry(w2.x, w2.y, 1.0, 0.0);
 }
 // Deferred sector (work-item pipeline): the same operations from the raw
 // chord points, in the (converged) piece kernel. v1 is a crossing point, so
 // its norm is ~1 and rotation_taking_to_x's degeneracy test cannot fire.
-SPHBI_HD void sector_from_raw(P2 v1, P2 v2, Frame& f, double& gamma) {
+SPHBI_HD void sector_from_raw(P2 v1, P2 v2, Frame& f, double& gamma, PieceTrig* T = nullptr) {
   const double n = p_norm(v1);
   f = Frame{v1.x / n, v1.y / n, -v1.y / n, v1.x / n};
-  sector_frame_angle(v1, v2, f, gamma);
+  sector_frame_angle(v1, v2, f, gamma, T);
 }
 
 // Frame and angles of a direct stub (:440-462): rotation taking v1 onto +x
@@ -885,7 +913,8 @@ SPHBI_HD void sector_from_raw(P2 v1, P2 v2, Frame& f, double& gamma) {
 // gamma = opening angle, beta = angle at v1 between the chord and the origin.
 // Identical operations whether called by the geometry pass or, deferred, by
 // the stub piece kernels.
-SPHBI_HD void stub_frame_angles(P2 v1, P2 v2, double r1, Frame& f, double& gamma, double& beta) {
+SPHBI_HD void stub_frame_angles(P2 v1, P2 v2, double r1, Frame& f, double& gamma, double& beta,
+                                PieceTrig* T = nullptr) {
   f = Frame{v1.x / r1, v1.y / r1, -v1.y / r1, v1.x / r1};
   P2 w2{f.m00 * v2.x + f.m01 * v2.y, f.m10 * v2.x + f.m11 * v2.y};
   if (w2.y < 0.0) {
@@ -895,7 +924,9 @@ SPHBI_HD void stub_frame_angles(P2 v1, P2 v2, double r1, Frame& f, double& gamma
   }
   gamma = d_atan2(w2.y, w2.x);
   const P2 cc = p_sub(v2, v1);
-  beta = d_atan2(fabs(cc.y * v1.x - cc.x * v1.y), -(cc.x * v1.x + cc.y * v1.y));
+  const double by = fabs(cc.y * v1.x - cc.x * v1.y), bx = -(cc.x * v1.x + cc.y * v1.y);
+  beta = d_atan2(by, bx);
+  if (T) *T = trig_from_geometry(w2.x, w2.y, bx, by);
 }
 
 // region_sector(v1, v2, l) (:349-366); the hot path always passes l = 1.

@@ -309,13 +309,14 @@ struct StubItem {
   double l, D, lo, u;
 };
 __device__ __forceinline__ void stub_item_geometry(const StubItem& it, Frame& f, double& gamma, double& beta,
-                                                   unsigned* status_or) {
-  stub_frame_angles(P2{it.v1x, it.v1y}, P2{it.v2x, it.v2y}, it.r1, f, gamma, beta);
+                                                   unsigned* status_or, PieceTrig* T = nullptr) {
+  stub_frame_angles(P2{it.v1x, it.v1y}, P2{it.v2x, it.v2y}, it.r1, f, gamma, beta, T);
   // stub_integral's beta validation (elementary_regions.hpp:179-183)
   if (it.window && !stub_beta_ok(beta)) atomicOr(status_or, kStatusDomain);
 }
-__device__ __forceinline__ void sector_item_geometry(const PieceItem& it, Frame& f, double& gamma) {
-  sector_from_raw(P2{it.m00, it.m01}, P2{it.m10, it.m11}, f, gamma);
+__device__ __forceinline__ void sector_item_geometry(const PieceItem& it, Frame& f, double& gamma,
+                                                     PieceTrig* T = nullptr) {
+  sector_from_raw(P2{it.m00, it.m01}, P2{it.m10, it.m11}, f, gamma, T);
 }
 
 struct AccOut {  // one piece's rotated contribution (9 dd)
@@ -720,14 +721,15 @@ __global__ void __launch_bounds__(128)
     // pad == 0: a sector from its raw chord points
     Frame f{it.m00, it.m01, it.m10, it.m11};
     double gamma = 0.0;
-    if (!it.pad) sector_item_geometry(it, f, gamma);
+    PieceTrig T{0.0, 1.0, 0.0, 0.0, 1.0};
+    if (!it.pad) sector_item_geometry(it, f, gamma, &T);
     if constexpr (F1) {
       PairAcc3 a;
       acc3_zero(a);
       if (it.pad)
         piece_half_disc3(K, a, f, it.sign);
       else
-        piece_cone3(K, a, f, gamma, 1.0, it.sign);
+        piece_cone3(K, a, f, gamma, 1.0, it.sign, T);
       acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
     } else {
       PairAcc a;
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(128)
       if (it.pad)
         piece_half_disc(K, a, f, it.sign);
       else
-        piece_cone(K, a, f, gamma, 1.0, it.sign);
+        piece_cone(K, a, f, gamma, 1.0, it.sign, &T);
       acc_to_out(a, static_cast<AccOut*>(out)[k]);
     }
   }
@@ -948,16 +950,17 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     const StubItem it = items[slot];
     Frame f;
     double gamma, beta;
-    stub_item_geometry(it, f, gamma, beta, status_or);
+    PieceTrig T;
+    stub_item_geometry(it, f, gamma, beta, status_or, &T);
     if constexpr (F1) {
       PairAcc3 a;
       acc3_zero(a);
-      piece_stub3<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign);
+      piece_stub3<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign, T);
       acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
     } else {
       PairAcc a;
       acc_zero(a);
-      piece_stub_k<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign);
+      piece_stub_k<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign, T);
       acc_to_out(a, static_cast<AccOut*>(out)[k]);
     }
   }
