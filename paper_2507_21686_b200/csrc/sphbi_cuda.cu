@@ -149,10 +149,10 @@ struct sphbi_ctx {
   // scratch banks: the streamed host path runs consecutive particle chunks on
   // two compute streams (own scratch each), so one chunk's pipeline tail
   // overlaps the next chunk's work; everything else uses bank 0
-  static constexpr int kBanks = 2;
+  static constexpr int kBanks = 3;
   int bank = 0;
-  cudaStream_t aux = nullptr;  // second compute stream (bank 1)
-  bool one_bank = false;       // SPHBI_STREAM_BANKS=1: chunks on one stream (experiment)
+  cudaStream_t aux[kBanks - 1] = {};  // compute streams of banks 1.. (bank 0: c->stream)
+  int stream_banks = 2;               // SPHBI_STREAM_BANKS: compute streams of the e2e path (1..3)
   void* buf[kBanks * kNumBufs] = {};
   size_t cap[kBanks * kNumBufs] = {};
   cudaEvent_t ev[8] = {};
@@ -2212,11 +2212,11 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
   int64_t *dip, *dit;
   if ((st = scratch_t(c, kBufUserPairs0, n_pairs, &dip)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufUserPairs1, n_pairs, &dit)) != SPHBI_OK) return st;
-  // per-chunk compute scratch, one set per bank (chunk k runs on bank k & 1)
-  const int nbanks = c->aux && !c->one_bank ? 2 : 1;
-  int *pp[2], *pt[2];
-  double* pout[2];
-  int64_t* row_ptr[2];
+  // per-chunk compute scratch, one set per bank (chunk k runs on bank k % nbanks)
+  const int nbanks = std::max(1, std::min(c->stream_banks, static_cast<int>(sphbi_ctx::kBanks)));
+  int *pp[sphbi_ctx::kBanks], *pt[sphbi_ctx::kBanks];
+  double* pout[sphbi_ctx::kBanks];
+  int64_t* row_ptr[sphbi_ctx::kBanks];
   int64_t maxp = 0;
   for (int k = 0; k < nchunks; ++k) maxp = std::max(maxp, pb[k + 1] - pb[k]);
   for (int b = 0; b < nbanks; ++b) {
@@ -2228,7 +2228,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     c->bank = 0;
     if (st != SPHBI_OK) return st;
   }
-  // chunk k computes on stream cs[k & 1]; c->stream / c->bank are switched
+  // chunk k computes on stream cs2[k % nbanks]; c->stream / c->bank are switched
   // for the pipeline calls and restored on every exit
   struct Restore {
     sphbi_ctx* c;
@@ -2238,10 +2238,10 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
       c->bank = 0;
     }
   } restore{c, s};
-  cudaStream_t cs2[2] = {s, nbanks == 2 ? c->aux : s};
-  if (nbanks == 2) {  // fork: the aux stream starts after the work already on s
+  cudaStream_t cs2[sphbi_ctx::kBanks] = {s, c->aux[0], c->aux[1]};
+  if (nbanks > 1) {  // fork: the aux streams start after the work already on s
     SPHBI_CUDA_TRY(cudaEventRecord(c->ev[6], s));
-    SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->aux, c->ev[6], 0));
+    for (int b = 1; b < nbanks; ++b) SPHBI_CUDA_TRY(cudaStreamWaitEvent(cs2[b], c->ev[6], 0));
   }
   auto upload = [&](int k) -> sphbi_status {
     const int64_t np = pb[k + 1] - pb[k], nq = qb[k + 1] - qb[k];
@@ -2297,8 +2297,8 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
       c->tl_host[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl_t0).count();
     }
   }
-  if (nbanks == 2) {  // join
-    SPHBI_CUDA_TRY(cudaEventRecord(c->ev[7], c->aux));
+  for (int b = 1; b < nbanks; ++b) {  // join
+    SPHBI_CUDA_TRY(cudaEventRecord(c->ev[7], cs2[b]));
     SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->ev[7], 0));
   }
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->d2h));
@@ -2402,7 +2402,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
       if (!w.empty()) c->stream_ramp = w;
     }
     const char* sb = std::getenv("SPHBI_STREAM_BANKS");
-    c->one_bank = sb && sb[0] == '1';
+    if (sb && *sb) c->stream_banks = std::max(1, std::min(static_cast<int>(sphbi_ctx::kBanks), std::atoi(sb)));
   }
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -2412,7 +2412,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+  for (auto& a : c->aux) cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   if (const char* t = std::getenv("SPHBI_TIMELINE"); t && t[0] == '1') {
@@ -2440,7 +2440,8 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < sphbi_ctx::kBanks * kNumBufs; ++i)
     if (c->buf[i]) cudaFree(c->buf[i]);
-  if (c->aux) cudaStreamDestroy(c->aux);
+  for (auto& a : c->aux)
+    if (a) cudaStreamDestroy(a);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& row : c->sev)
     for (auto& e : row) cudaEventDestroy(e);
