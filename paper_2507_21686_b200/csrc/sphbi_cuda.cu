@@ -121,8 +121,6 @@ enum ScratchSlot {
   kBufOutB,
   kBufOutS,
   kBufPartial,
-  kBufUserPairs2,
-  kBufUserPairs3,
   kBufClass,
   kBufOrder,
   kBufCubTemp2,

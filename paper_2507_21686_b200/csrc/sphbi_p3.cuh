@@ -153,51 +153,6 @@ SPHBI_HD double uco(int a, int j) {
   }
 }
 
-// Raw radial chains at bound x (x >= D > 0), double-double:
-//   Pt[m] = P~_m (P~_0 = log((x+R)/D), P~_1 = R), I[m] = I_m(x; D) (I_0 unused),
-//   X[p]  = x^(p+1)/(p+1)
-SPHBI_HD void p3_chains(double x, double D, int M, dd* Pt, dd* I, dd* X, dd& Rout) {
-  ChainSeeds sd;
-  chain_seeds(x, D, sd);
-  const dd D2 = two_prod(D, D);
-  const dd R3 = dd_mul(dd_mul(sd.R, sd.R), sd.R);
-  Pt[0] = sd.p0;
-  Pt[1] = sd.R;
-  I[0] = dd{0.0, 0.0};
-  I[1] = sd.i1;
-  dd xp = dd_make(1.0);  // x^(m-1) at step m
-  dd xpm2 = dd_make(1.0);
-  for (int m = 2; m < M; ++m) {
-    xpm2 = xp;                    // x^(m-2)
-    xp = dd_mul_d(xp, x);         // x^(m-1)
-    Pt[m] = dd_div_d_small(dd_add(dd_mul(xp, sd.R), dd_mul_d(dd_mul(D2, Pt[m - 2]), (double)(m - 1))), m);
-    I[m] = dd_div_d_small(dd_add(dd_mul(xpm2, R3), dd_mul_d(dd_mul(D2, I[m - 2]), (double)(m - 2))), m + 1);
-  }
-  dd xq = dd_make(x);  // x^(p+1)
-  for (int p = 0; p < M; ++p) {
-    X[p] = dd_div_d_small(xq, p + 1);
-    xq = dd_mul_d(xq, x);
-  }
-  Rout = sd.R;
-}
-
-// int^x r^n (1 - D^2/r^2)^(m/2) dr with the chains' constants (m <= 4, n >= 0)
-SPHBI_HD dd p3_sp(int n, int m, const dd* I, const dd* X, dd D2) {
-  dd acc{0.0, 0.0};
-  dd pw = dd_make(1.0);  // (-D^2)^l
-  const int top = m / 2;
-  for (int l = 0; l <= top; ++l) {
-    const double bin = l == 0 ? 1.0 : (top == 1 ? 1.0 : (l == 1 ? 2.0 : 1.0));  // C(top, l), top <= 2
-    const int idx = n - 2 * l;
-    if (idx >= 0) {
-      const dd term = (m & 1) ? I[idx] : X[idx];
-      acc = dd_add(acc, dd_mul_d(dd_mul(term, pw), bin));
-    }
-    pw = dd_neg(dd_mul(pw, D2));
-  }
-  return acc;
-}
-
 // ---- region harmonic sums (region frame) ---------------------------------
 SPHBI_HD void h24_cone(const P3Consts& P, double gamma, double L, H24& H) {
   for (int d = 0; d < kP3Desc; ++d) {
@@ -238,9 +193,9 @@ SPHBI_HD void h24_half_disc(const P3Consts& P, H24& H) {
 
 // Weighted chain sums. Every stub-window / segment sum of a descriptor is
 // sum_k w_k F(k + off), F a fixed linear combination of chain values at
-// shifted indices (p3_sp), so the k-sum is taken first, once per (family,
+// shifted indices (the Chebyshev / binomial terms of p3_wsp), so the k-sum is taken first, once per (family,
 // chain, shift): W(f, s) = sum_k w_f[k] C[k + s] (C[idx] = 0 for idx < 0).
-// The descriptor table needs 17 of them (T_a / U_(a-1) terms of p3_sp):
+// The descriptor table needs 17 of them (T_a / U_(a-1) terms of p3_wsp):
 //   family 0: X shifts 1..4, I shifts 2, 4;  family 1: X shifts -1..3, I shifts 0, 2;
 //   Pt sums with the weights pc[f][off] (= w_k / (n + 1)) for off 1, 3.
 // They are accumulated while the chains are generated (no chain arrays).
@@ -261,7 +216,7 @@ SPHBI_HD void p3_acc_w(acc2& a, const dd* w, int deg, int k, dd c) {
     if (wk.hi != 0.0) acc_add_dddd(a, wk, c);
   }
 }
-// Chains at bound x (x >= D > 0) in double-double, as p3_chains, consumed on
+// Chains at bound x (x >= D > 0) in double-double, consumed on
 // the fly: Pt_m (Pt_0 = log((x+R)/D), Pt_1 = R), I_m (I_0 = 0), X_m = x^(m+1)/(m+1).
 SPHBI_HD void p3_wchain(const P3Consts& P, double x, double D, bool want_x, P3W& W, dd& Rout) {
   ChainSeeds sd;
@@ -333,7 +288,8 @@ SPHBI_HD void p3_wchain(const P3Consts& P, double x, double D, bool want_x, P3W&
   }
   Rout = sd.R;
 }
-// sum_k w_f[k] p3_sp(k + o, m, ...) from the weighted sums (m <= 4)
+// sum_k w_f[k] int^x r^(k+o) (1 - D^2/r^2)^(m/2) dr from the weighted sums (m <= 4):
+// sum_l C(m/2, l) (-D^2)^l W(f, o - 2l), W over I (odd m) or X (even m)
 SPHBI_HD dd p3_wsp(const P3W& W, int f, int o, int m, dd D2) {
   dd acc{0.0, 0.0};
   dd pw = dd_make(1.0);  // (-D^2)^l
