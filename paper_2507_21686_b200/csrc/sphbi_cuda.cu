@@ -291,20 +291,22 @@ __global__ void __launch_bounds__(kEvalBlock)
 // Sector items carry their raw chord points (pad == 0: m00, m01 = v1 and
 // m10, m11 = v2; the sector kernel derives frame and angle, sector_from_raw);
 // half discs (pad == 1) and segments (a = d) carry their frame.
-struct PieceItem {
+struct __align__(16) PieceItem {  // 64 B: four 16-B vector accesses
   int pair;
   int pad;
   double sign, m00, m01, m10, m11;
   double a;
+  double pad2;
 };
 // Direct stub: cone (gamma, l) + radial window [lo, u] at distance D. The
 // geometry pass stores the raw stub (v1, v2, r1 = |v1|); the stub kernels
 // derive frame, gamma and beta (stub_frame_angles), in converged warps.
-struct StubItem {
+struct __align__(16) StubItem {  // 96 B: six 16-B vector accesses
   int pair;
   int window;
   double sign, v1x, v1y, v2x, v2y, r1;
   double l, D, lo, u;
+  double pad;
 };
 __device__ __forceinline__ void stub_item_geometry(const StubItem& it, Frame& f, double& gamma, double& beta,
                                                    unsigned* status_or, PieceTrig* T = nullptr) {
@@ -317,10 +319,10 @@ __device__ __forceinline__ void sector_item_geometry(const PieceItem& it, Frame&
   sector_from_raw(P2{it.m00, it.m01}, P2{it.m10, it.m11}, f, gamma, T);
 }
 
-struct AccOut {  // one piece's rotated contribution (9 dd)
+struct __align__(16) AccOut {  // one piece's rotated contribution (9 dd)
   double v[18];
 };
-struct AccOut3 {  // constant field: v3, g13, g23 only (3 dd)
+struct __align__(16) AccOut3 {  // constant field: v3, g13, g23 only (3 dd)
   double v[6];
 };
 SPHBI_HD void acc3_to_out(const PairAcc3& a, AccOut3& o) {
@@ -379,6 +381,7 @@ __device__ __forceinline__ StubItem make_stub_item(int pair, P2 v1, P2 v2, doubl
   it.D = D;
   it.lo = lo;
   it.u = u;
+  it.pad = 0.0;
   return it;
 }
 __device__ __forceinline__ PieceItem make_sector_item(int pair, P2 v1, P2 v2, double sign) {
@@ -391,6 +394,7 @@ __device__ __forceinline__ PieceItem make_sector_item(int pair, P2 v1, P2 v2, do
   it.m10 = v2.x;
   it.m11 = v2.y;
   it.a = 0.0;
+  it.pad2 = 0.0;
   return it;
 }
 
@@ -414,6 +418,7 @@ struct EmitSink {
     it.m10 = f.m10;
     it.m11 = f.m11;
     it.a = a;
+    it.pad2 = 0.0;
     *dst++ = it;
   }
   int disc_n;
@@ -653,7 +658,7 @@ constexpr int kRecRoute = 1, kRecPlane = 2;
 // of one kind sit at consecutive list positions (the emitting warp appended
 // them together), and the piece kernels write each output at its list
 // position, so combine reads them coalesced, in emission order.
-struct JRec {
+struct __align__(16) JRec {
   int k;
   int flags;   // kRecRoute | kRecPlane | nsec << 8 | nseg << 12
   int disc_n;
@@ -778,6 +783,7 @@ struct SlotSink {
     it.m10 = f.m10;
     it.m11 = f.m11;
     it.a = a;
+    it.pad2 = 0.0;
     return it;
   }
   __device__ void disc(double sign) { disc_n += sign > 0.0 ? 1 : -1; }
@@ -1168,7 +1174,7 @@ __global__ void __launch_bounds__(128)
 // particle frame), and the P3 combine adds a pair's items, builds the cubic
 // field polynomial from its 10 nodal values and contracts.
 // ---------------------------------------------------------------------------
-struct H24Out {
+struct __align__(16) H24Out {
   double v[2 * kP3Sums];
 };
 __device__ __forceinline__ void h24_store(const H24& H, H24Out& o) {
