@@ -952,6 +952,16 @@ SPHBI_HD void region_sector(Sink& c, P2 v1, P2 v2, double sign, double l = 1.0) 
   }
 }
 
+// Radial window [lo, u] of a direct stub (:440-475): u = min(r1, 1), lo =
+// max(l, D) snapped onto D; a window exists when u > lo + eps. Shared by the
+// geometry pass and the stub kernels, which re-derive it from (r1, l, D).
+SPHBI_HD bool stub_window(double r1, double l, double D, double& lo, double& u) {
+  u = fmin(r1, 1.0);
+  lo = fmax(l, D);
+  if (lo - D <= 256.0 * kDblEps * D) lo = D;
+  return u > lo + kGeomEps;
+}
+
 // stub_integral validation (elementary_regions.hpp:179-183)
 SPHBI_HD bool stub_beta_ok(double beta) { return beta >= 0.0 && beta < kHalfPiHi; }
 
@@ -961,10 +971,8 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
                           double sign) {
   const double D = fabs(area2) / p_norm(b);
   const double l = fmin(r2, 1.0);
-  const double u = fmin(r1, 1.0);
-  double lo = fmax(l, D);
-  if (lo - D <= 256.0 * kDblEps * D) lo = D;
-  const bool window = u > lo + kGeomEps;
+  double lo, u;
+  const bool window = stub_window(r1, l, D, lo, u);
   if constexpr (Sink::kAngles == 0) {
     c.stub(Frame{1.0, 0.0, 0.0, 1.0}, 0.0, l, D, 0.0, lo, u, window, sign);
     return;

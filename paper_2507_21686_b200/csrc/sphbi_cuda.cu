@@ -301,18 +301,22 @@ struct __align__(16) PieceItem {  // 64 B: four 16-B vector accesses
 // Direct stub: cone (gamma, l) + radial window [lo, u] at distance D. The
 // geometry pass stores the raw stub (v1, v2, r1 = |v1|); the stub kernels
 // derive frame, gamma and beta (stub_frame_angles), in converged warps.
-struct __align__(16) StubItem {  // 96 B: six 16-B vector accesses
+// 64 B (four 16-B vector accesses): the window bounds and flag are re-derived
+// from (r1, l, D) by stub_window, the sign is a flag bit.
+struct __align__(16) StubItem {
   int pair;
-  int window;
-  double sign, v1x, v1y, v2x, v2y, r1;
-  double l, D, lo, u;
-  double pad;
+  int flags;  // bit 0: negative sign
+  double v1x, v1y, v2x, v2y, r1;
+  double l, D;
+  __device__ double sign() const { return (flags & 1) ? -1.0 : 1.0; }
+  __device__ bool window(double& lo, double& u) const { return stub_window(r1, l, D, lo, u); }
 };
 __device__ __forceinline__ void stub_item_geometry(const StubItem& it, Frame& f, double& gamma, double& beta,
                                                    unsigned* status_or, PieceTrig* T = nullptr) {
   stub_frame_angles(P2{it.v1x, it.v1y}, P2{it.v2x, it.v2y}, it.r1, f, gamma, beta, T);
   // stub_integral's beta validation (elementary_regions.hpp:179-183)
-  if (it.window && !stub_beta_ok(beta)) atomicOr(status_or, kStatusDomain);
+  double lo, u;
+  if (it.window(lo, u) && !stub_beta_ok(beta)) atomicOr(status_or, kStatusDomain);
 }
 __device__ __forceinline__ void sector_item_geometry(const PieceItem& it, Frame& f, double& gamma,
                                                      PieceTrig* T = nullptr) {
@@ -366,12 +370,11 @@ struct CountSink {
 };
 
 // Raw stub / sector items (Sink::kAngles == 1)
-__device__ __forceinline__ StubItem make_stub_item(int pair, P2 v1, P2 v2, double r1, double l, double D, double lo,
-                                                   double u, bool window, double sign) {
+__device__ __forceinline__ StubItem make_stub_item(int pair, P2 v1, P2 v2, double r1, double l, double D,
+                                                   double sign) {
   StubItem it;
   it.pair = pair;
-  it.window = window ? 1 : 0;
-  it.sign = sign;
+  it.flags = sign < 0.0 ? 1 : 0;
   it.v1x = v1.x;
   it.v1y = v1.y;
   it.v2x = v2.x;
@@ -379,9 +382,6 @@ __device__ __forceinline__ StubItem make_stub_item(int pair, P2 v1, P2 v2, doubl
   it.r1 = r1;
   it.l = l;
   it.D = D;
-  it.lo = lo;
-  it.u = u;
-  it.pad = 0.0;
   return it;
 }
 __device__ __forceinline__ PieceItem make_sector_item(int pair, P2 v1, P2 v2, double sign) {
@@ -433,7 +433,7 @@ struct EmitSink {
   __device__ void sector_raw(P2 v1, P2 v2, double, double sign) { *sector_items++ = make_sector_item(pair, v1, v2, sign); }
   __device__ void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window,
                            double sign) {
-    const StubItem it = make_stub_item(pair, v1, v2, r1, l, D, lo, u, window, sign);
+    const StubItem it = make_stub_item(pair, v1, v2, r1, l, D, sign);
     switch (stub_class(D, lo, u, window)) {
       case 0: *stub0++ = it; break;
       case 1: *stub1++ = it; break;
@@ -815,7 +815,7 @@ struct SlotSink {
                            double sign) {
     const int cls = stub_class(D, lo, u, window);
     if (nstub < kCapStub) {
-      stubs[nstub] = make_stub_item(pair, v1, v2, r1, l, D, lo, u, window, sign);
+      stubs[nstub] = make_stub_item(pair, v1, v2, r1, l, D, sign);
       cls_bits |= static_cast<unsigned>(cls) << (2 * nstub);
     } else {
       overflow = true;
@@ -956,15 +956,17 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_STUB)
     double gamma, beta;
     PieceTrig T;
     stub_item_geometry(it, f, gamma, beta, status_or, &T);
+    double lo, u;
+    const bool window = it.window(lo, u);
     if constexpr (F1) {
       PairAcc3 a;
       acc3_zero(a);
-      piece_stub3<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign, T);
+      piece_stub3<CLS>(K, a, f, gamma, it.l, it.D, beta, lo, u, window, it.sign(), T);
       acc3_to_out(a, static_cast<AccOut3*>(out)[k]);
     } else {
       PairAcc a;
       acc_zero(a);
-      piece_stub_k<CLS>(K, a, f, gamma, it.l, it.D, beta, it.lo, it.u, it.window != 0, it.sign, T);
+      piece_stub_k<CLS>(K, a, f, gamma, it.l, it.D, beta, lo, u, window, it.sign(), T);
       acc_to_out(a, static_cast<AccOut*>(out)[k]);
     }
   }
@@ -1215,12 +1217,13 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_P3)
     stub_item_geometry(it, f, gamma, beta, status_or);
     H24 H, acc;
     h24_cone(P, gamma, it.l, H);
-    if (it.window) {
-      h24_stub_bound(P, it.u, it.D, beta, 1.0, H);
-      h24_stub_bound(P, it.lo, it.D, beta, -1.0, H);
+    double lo, u;
+    if (it.window(lo, u)) {
+      h24_stub_bound(P, u, it.D, beta, 1.0, H);
+      h24_stub_bound(P, lo, it.D, beta, -1.0, H);
     }
     h24_zero(acc);
-    h24_accumulate(acc, H, f, it.sign);
+    h24_accumulate(acc, H, f, it.sign());
     h24_store(acc, out[k]);
   }
 }
