@@ -524,6 +524,23 @@ __device__ __forceinline__ void load_norm(const NormRec* __restrict__ r, int64_t
   perm[2] = (pc >> 4) & 3;
 }
 
+// Crossing count of segment pq with the unit circle for the signature only
+// (a sort key: exactness is not needed, convergence is): segment_circle_
+// crossings' root tests with the divisions by 2a multiplied out.
+__device__ __forceinline__ int crossing_count_key(P2 p, P2 q) {
+  const P2 d = p_sub(q, p);
+  const double a = p_norm2(d);
+  if (a < kGeomEps * kGeomEps) return 0;
+  const double b = 2.0 * p_dot(p, d);
+  const double cc = p_norm2(p) - 1.0;
+  const double disc = b * b - 4.0 * a * cc;
+  if (disc <= 0.0) return 0;
+  const double rt = sqrt(disc);
+  const double lo = -1e-12 * 2.0 * a, hi = (1.0 + 1e-12) * 2.0 * a;  // lam * 2a in [lo, hi]
+  const double r0 = -b - rt, r1 = -b + rt;
+  return (r0 >= lo && r0 <= hi ? 1 : 0) + (r1 >= lo && r1 <= hi ? 1 : 0);
+}
+
 // Signature bins: 3 inside bits + 3 x 2 crossing-count bits.
 constexpr int kSigBins = 512;
 
@@ -563,8 +580,7 @@ __global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h,
     }
     for (int i = 0; i < 3; ++i) {
       if (p_norm2(nv[i]) <= 1.0) kk |= 1u << i;
-      const Crossings x = segment_circle_crossings(nv[i], nv[(i + 1) % 3]);
-      kk |= static_cast<unsigned>(x.count) << (3 + 2 * i);
+      kk |= static_cast<unsigned>(crossing_count_key(nv[i], nv[(i + 1) % 3])) << (3 + 2 * i);
     }
     key[k] = static_cast<unsigned short>(kk);
   }
