@@ -541,8 +541,9 @@ __device__ __forceinline__ int crossing_count_key(P2 p, P2 q) {
   return (r0 >= lo && r0 <= hi ? 1 : 0) + (r1 >= lo && r1 <= hi ? 1 : 0);
 }
 
-// Signature bins: 3 inside bits + 3 x 2 crossing-count bits.
-constexpr int kSigBins = 512;
+// Signature bins: 3 inside bits + 3 x 2 crossing-count bits + particle on a
+// vertex + particle on an edge line (those take the degenerate branches).
+constexpr int kSigBins = 2048;
 
 // Block-level signature histogram, added to the global one (one atomic per
 // non-empty bin and block).
@@ -578,30 +579,49 @@ __global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h,
       r.pad2 = 0.0;
       nrec[k] = r;
     }
+    bool on_vertex = false, on_edge = false;
     for (int i = 0; i < 3; ++i) {
-      if (p_norm2(nv[i]) <= 1.0) kk |= 1u << i;
-      kk |= static_cast<unsigned>(crossing_count_key(nv[i], nv[(i + 1) % 3])) << (3 + 2 * i);
+      const double r2 = p_norm2(nv[i]);
+      if (r2 <= 1.0) kk |= 1u << i;
+      on_vertex |= r2 < 1e-18;
+      const P2 a = nv[i], b = nv[(i + 1) % 3];
+      const double cr = a.x * b.y - a.y * b.x, e2 = p_norm2(p_sub(b, a));
+      on_edge |= cr * cr < 1e-18 * e2;
+      kk |= static_cast<unsigned>(crossing_count_key(a, b)) << (3 + 2 * i);
     }
+    kk |= (on_vertex ? 1u : 0u) << 9;
+    kk |= (on_edge ? 1u : 0u) << 10;
     key[k] = static_cast<unsigned short>(kk);
   }
   sig_hist_add(sh, kk, k < n, hist);  // the whole block reaches its barriers
 }
 
 // Exclusive scan of the signature histogram -> per-bin cursors (one block).
-__global__ void __launch_bounds__(kSigBins) k_sig_offsets(const unsigned* __restrict__ hist,
-                                                          unsigned* __restrict__ cursor) {
-  __shared__ unsigned sh[kSigBins];
+constexpr int kSigScanThreads = 1024, kSigPerThread = kSigBins / kSigScanThreads;
+__global__ void __launch_bounds__(kSigScanThreads) k_sig_offsets(const unsigned* __restrict__ hist,
+                                                                 unsigned* __restrict__ cursor) {
+  __shared__ unsigned sh[kSigScanThreads];
   const int t = threadIdx.x;
-  const unsigned v = hist[t];
-  sh[t] = v;
+  unsigned loc[kSigPerThread], tot = 0u;
+#pragma unroll
+  for (int q = 0; q < kSigPerThread; ++q) {
+    loc[q] = hist[t * kSigPerThread + q];
+    tot += loc[q];
+  }
+  sh[t] = tot;
   __syncthreads();
-  for (int o = 1; o < kSigBins; o <<= 1) {
+  for (int o = 1; o < kSigScanThreads; o <<= 1) {
     const unsigned y = t >= o ? sh[t - o] : 0u;
     __syncthreads();
     sh[t] += y;
     __syncthreads();
   }
-  cursor[t] = sh[t] - v;
+  unsigned run = sh[t] - tot;
+#pragma unroll
+  for (int q = 0; q < kSigPerThread; ++q) {
+    cursor[t * kSigPerThread + q] = run;
+    run += loc[q];
+  }
 }
 
 // Counting-sort scatter of pair indices by signature: per block, the bins'
@@ -1885,7 +1905,7 @@ sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, Nor
     return SPHBI_OK;
   }
   // counting sort by signature (9-bit keys): no radix-sort passes, no memsets
-  k_sig_offsets<<<1, kSigBins, 0, s>>>(hist, hist + kSigBins);
+  k_sig_offsets<<<1, kSigScanThreads, 0, s>>>(hist, hist + kSigBins);
   if ((st = check_launch(c, "k_sig_offsets")) != SPHBI_OK) return st;
   k_sig_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, pk, hist + kSigBins, *porder_out);
   return check_launch(c, "k_sig_scatter");
