@@ -233,8 +233,14 @@ SPHBI_HD double glibc_hypot_kernel(double ax, double ay) {
   return h;
 }
 
-// Out of line on the device: ~15 call sites per pair; scalar-only interface.
-SPHBI_HDNI double glibc_hypot(double x, double y) {
+// Out of line on the device by default: ~15 call sites per pair; scalar-only
+// interface (SPHBI_HYPOT_INLINE inlines it, for code-shape experiments).
+#ifdef SPHBI_HYPOT_INLINE
+SPHBI_HD
+#else
+SPHBI_HDNI
+#endif
+double glibc_hypot(double x, double y) {
   x = fabs(x);
   y = fabs(y);
   const double ax = x < y ? y : x;
