@@ -1000,16 +1000,16 @@ SPHBI_HD void stub_direct(Sink& c, P2 v1, P2 v2, double r1, double r2, double ar
 // constants are the reference's; only the order in which pieces reach the
 // sink differs (immaterial: pieces are summed in double-double).
 // ---------------------------------------------------------------------------
-// segment_circle_crossings (:494-509)
+// segment_circle_crossings (:494-509). Only the count and the last crossing
+// (points.back()) are ever read, so only those are kept.
 struct Crossings {
   int count;
-  P2 pts[2];
+  P2 last;
 };
 SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
   Crossings out;
   out.count = 0;
-  out.pts[0] = P2{0.0, 0.0};
-  out.pts[1] = P2{0.0, 0.0};
+  out.last = P2{0.0, 0.0};
   const P2 d = p_sub(q, p);
   const double a = p_norm2(d);
   if (a < kGeomEps * kGeomEps) return out;
@@ -1020,16 +1020,16 @@ SPHBI_HD Crossings segment_circle_crossings(P2 p, P2 q) {
   const double rt = sqrt(disc);
   const double lam0 = (-b - rt) / (2.0 * a), lam1 = (-b + rt) / (2.0 * a);
   if (lam0 >= -1e-12 && lam0 <= 1.0 + 1e-12) {
-    out.pts[out.count] = P2{p.x + lam0 * d.x, p.y + lam0 * d.y};
+    out.last = P2{p.x + lam0 * d.x, p.y + lam0 * d.y};
     out.count++;
   }
   if (lam1 >= -1e-12 && lam1 <= 1.0 + 1e-12) {
-    out.pts[out.count] = P2{p.x + lam1 * d.x, p.y + lam1 * d.y};
+    out.last = P2{p.x + lam1 * d.x, p.y + lam1 * d.y};
     out.count++;
   }
   return out;
 }
-SPHBI_HD P2 last_crossing(const Crossings& x) { return x.count == 2 ? x.pts[1] : x.pts[0]; }
+SPHBI_HD P2 last_crossing(const Crossings& x) { return x.last; }
 
 // region_segment body (:369-423).
 template <class Sink>
@@ -1077,12 +1077,15 @@ constexpr int kMaxStubStack = 4;
 
 template <class Sink>
 SPHBI_HD void stub_process(Sink& c, P2 v1_in, P2 v2_in, double sign) {
-  StubTask st[kMaxStubStack];
-  st[0] = StubTask{v1_in, v2_in};
-  int top = 1;
-  while (top > 0) {
-    --top;
-    P2 v1 = st[top].v1, v2 = st[top].v2;
+  // LIFO of pending tasks: its top entry lives in registers (a split's second
+  // child, the common case), older entries in a small array touched only by
+  // nested splits. Pop order is the reference's (first child (v1, foot), then
+  // (v2, foot)); the depth limit is kMaxStubStack pending entries.
+  StubTask deep[kMaxStubStack];
+  StubTask pend{P2{0.0, 0.0}, P2{0.0, 0.0}};
+  int npend = 0;  // pending entries: pend + deep[0 .. npend - 2]
+  P2 v1 = v1_in, v2 = v2_in;
+  for (;;) {
     double r1 = p_norm(v1), r2 = p_norm(v2);
     if (r1 < r2) {
       const P2 tv = v1;
@@ -1093,26 +1096,38 @@ SPHBI_HD void stub_process(Sink& c, P2 v1_in, P2 v2_in, double sign) {
       r2 = tr;
     }
     const double area2 = p_cross(v1, v2);
+    bool next = true;
     if (r2 < kGeomEps || fabs(area2) < kGeomEps * r1 * fmax(r2, 1.0)) {
       c.bump(kStubDegenerate);
-      continue;
+    } else {
+      const P2 b = p_sub(v1, v2);
+      const double dot_a = -(v2.x * b.x + v2.y * b.y);
+      if (dot_a <= kGeomEps) {
+        c.bump(kStubDirect);
+        stub_direct(c, v1, v2, r1, r2, area2, b, sign);
+      } else {
+        c.bump(kStubSplit);
+        const double t = dot_a / p_norm2(b);
+        const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
+        if (npend + 2 > kMaxStubStack) {
+          c.status |= kStatusStack;
+        } else {
+          // push (v2, foot), then continue with (v1, foot) (push + pop)
+          if (npend > 0) deep[npend - 1] = pend;
+          pend = StubTask{v2, foot};
+          ++npend;
+          v2 = foot;
+          next = false;
+        }
+      }
     }
-    const P2 b = p_sub(v1, v2);
-    const double dot_a = -(v2.x * b.x + v2.y * b.y);
-    if (dot_a <= kGeomEps) {
-      c.bump(kStubDirect);
-      stub_direct(c, v1, v2, r1, r2, area2, b, sign);
-      continue;
+    if (next) {
+      if (npend == 0) break;
+      v1 = pend.v1;
+      v2 = pend.v2;
+      --npend;
+      if (npend > 0) pend = deep[npend - 1];
     }
-    c.bump(kStubSplit);
-    const double t = dot_a / p_norm2(b);
-    const P2 foot{v2.x + t * b.x, v2.y + t * b.y};
-    if (top + 2 > kMaxStubStack) {
-      c.status |= kStatusStack;
-      continue;
-    }
-    st[top++] = StubTask{v2, foot};
-    st[top++] = StubTask{v1, foot};
   }
 }
 

@@ -69,7 +69,7 @@ constexpr int kEvalBlock = 128;
 #define SPHBI_MINB_COUNT 5
 #endif
 #ifndef SPHBI_MINB_EMIT
-#define SPHBI_MINB_EMIT 4
+#define SPHBI_MINB_EMIT 5
 #endif
 #ifndef SPHBI_MINB_P3
 #define SPHBI_MINB_P3 4
@@ -802,12 +802,20 @@ struct SlotSink {
   unsigned status;
   int pair;
   int disc_n;  // signed count of full discs
-  bool overflow;
   PieceItem *sec, *seg;
   StubItem* stubs;
-  unsigned cls_bits;  // 2 bits per stub slot: its class (stub_class)
-  int nsec, nseg, nstub, c0, c1, c2, c3;
+  unsigned cls_bits;  // 2 bits per stub slot: its class (stub_class); per-class counts derived at the end
+  int nsec, nseg, nstub;
   unsigned long long* counters;
+  __device__ bool overflowed() const { return nsec > kCapSec || nseg > kCapSeg || nstub > kCapStub; }
+  // stubs of class c among the first min(nstub, kCapStub) slots
+  __device__ int class_count(int c) const {
+    const int m = min(nstub, kCapStub);
+    const unsigned valid = (m >= 16 ? 0xffffffffu : ((1u << (2 * m)) - 1u)) & 0x55555555u;
+    const unsigned lo = cls_bits & 0x55555555u, hi = (cls_bits >> 1) & 0x55555555u;
+    const unsigned sel = c == 0 ? ~(lo | hi) : c == 1 ? (lo & ~hi) : c == 2 ? (hi & ~lo) : (hi & lo);
+    return __popc(sel & valid);
+  }
   __device__ void bump(int w) { bump_counter(counters, w); }
   __device__ PieceItem piece(const Frame& f, double sign, double a) const {
     PieceItem it;
@@ -828,23 +836,15 @@ struct SlotSink {
       PieceItem it = piece(f, sign, 0.0);
       it.pad = 1;  // tagged: evaluated as a half disc by k_pipe_sector
       sec[nsec] = it;
-    } else {
-      overflow = true;
     }
     ++nsec;
   }
   __device__ void sector_raw(P2 v1, P2 v2, double, double sign) {
-    if (nsec < kCapSec)
-      sec[nsec] = make_sector_item(pair, v1, v2, sign);
-    else
-      overflow = true;
+    if (nsec < kCapSec) sec[nsec] = make_sector_item(pair, v1, v2, sign);
     ++nsec;
   }
   __device__ void segment(const Frame& f, double d, double sign) {
-    if (nseg < kCapSeg)
-      seg[nseg] = piece(f, sign, d);
-    else
-      overflow = true;
+    if (nseg < kCapSeg) seg[nseg] = piece(f, sign, d);
     ++nseg;
   }
   __device__ void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window,
@@ -853,14 +853,8 @@ struct SlotSink {
     if (nstub < kCapStub) {
       stubs[nstub] = make_stub_item(pair, v1, v2, r1, l, D, sign);
       cls_bits |= static_cast<unsigned>(cls) << (2 * nstub);
-    } else {
-      overflow = true;
     }
     ++nstub;
-    c0 += cls == 0;
-    c1 += cls == 1;
-    c2 += cls == 2;
-    c3 += cls == 3;
   }
 };
 
@@ -898,40 +892,30 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     e.status = 0;
     e.pair = static_cast<int>(k);
     e.disc_n = 0;
-    e.overflow = false;
     // slots by emission position: a warp writes one contiguous region
     e.sec = sec_slots + kCapSec * j;
     e.seg = seg_slots + kCapSeg * j;
     e.stubs = stub_slots + kCapStub * j;
     e.cls_bits = 0u;
-    e.nsec = e.nseg = e.nstub = e.c0 = e.c1 = e.c2 = e.c3 = 0;
+    e.nsec = e.nseg = e.nstub = 0;
     e.counters = counters;
     const bool nondeg_route = integrate_normalized(e, nv);
-    if (e.overflow) {
+    if (e.overflowed()) {
       // the call is redone with the two-pass pipeline (dflags[1] bit 2); keep
       // this pass in bounds
       atomicOr(status_or + 1, 4u);
       e.nsec = min(e.nsec, kCapSec);
       e.nseg = min(e.nseg, kCapSeg);
-      e.nstub = min(e.nstub, kCapStub);
-      e.c0 = e.c1 = e.c2 = e.c3 = 0;
-      for (int q = 0; q < e.nstub; ++q) {
-        const int c = (e.cls_bits >> (2 * q)) & 3;
-        e.c0 += c == 0;
-        e.c1 += c == 1;
-        e.c2 += c == 2;
-        e.c3 += c == 3;
-      }
     }
     if (nondeg_route) flags |= kRecRoute;
     flags |= (e.nsec << 8) | (e.nseg << 12);
     disc_n = e.disc_n;
     if (e.status) atomicOr(status_or, e.status);
     my[0] = e.nsec;
-    my[1] = e.c0;
-    my[2] = e.c1;
-    my[3] = e.c2;
-    my[4] = e.c3;
+    my[1] = e.class_count(0);
+    my[2] = e.class_count(1);
+    my[3] = e.class_count(2);
+    my[4] = e.class_count(3);
     my[5] = e.nseg;
     cls_bits = e.cls_bits;
   }
