@@ -159,18 +159,33 @@ inline void reset_branch_counters() { branch_counters() = BranchCounters{}; }
 namespace detail {
 
 // ---- device plumbing ---------------------------------------------------------
-inline sphbi_ctx* device_context() {
-  static std::once_flag once;
-  static sphbi_ctx* ctx = nullptr;
-  static sphbi_status created = SPHBI_ERR_INTERNAL;
-  std::call_once(once, [] {
+// One device context per host thread: the reference's functions are pure and
+// reentrant with thread_local BranchCounters (:180-183), so concurrent callers
+// must not share scratch buffers, streams or device route counters. (A
+// context is also internally locked per C-ABI call, sphbi_cuda.h.)
+struct ThreadContext {
+  sphbi_ctx* ctx = nullptr;
+  sphbi_status created = SPHBI_ERR_INTERNAL;
+  std::string error;
+  ThreadContext() {
     const char* env = std::getenv("SPHBI_DEVICE");
     created = sphbi_ctx_create(env ? std::atoi(env) : 0, &ctx);
-    if (created == SPHBI_OK) sphbi_ctx_enable_counters(ctx, 1);
-  });
-  if (created != SPHBI_OK)
-    throw std::runtime_error(std::string("sphbi: no B200 device context: ") + sphbi_last_error());
-  return ctx;
+    if (created == SPHBI_OK)
+      sphbi_ctx_enable_counters(ctx, 1);
+    else
+      error = sphbi_last_error();
+  }
+  ~ThreadContext() {
+    if (ctx) sphbi_ctx_destroy(ctx);
+  }
+  ThreadContext(const ThreadContext&) = delete;
+  ThreadContext& operator=(const ThreadContext&) = delete;
+};
+
+inline sphbi_ctx* device_context() {
+  thread_local ThreadContext tc;
+  if (tc.created != SPHBI_OK) throw std::runtime_error("sphbi: no B200 device context: " + tc.error);
+  return tc.ctx;
 }
 
 inline void check(sphbi_status st) {

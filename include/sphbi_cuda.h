@@ -23,6 +23,16 @@
  *   sphbi_bases_create / _apply <- integrate_triangle_bases :828-846 over a scene +
  *                              gradient_variant_weights :860-894 + combine_basis :706-717
  *
+ *   sphbi_pair_counts       <- (none) the count pass of the SPEC.md:711 neighbour search,
+ *                              for the multi-GPU shard cut
+ *
+ * Threading: a context may be shared by host threads -- every call holds the
+ * context's lock for its duration, so concurrent calls on one context are
+ * serialised (and the device route counters then mix their counts). For
+ * concurrency, and for per-thread counters as the reference keeps them
+ * (thread_local BranchCounters, triangle_integrator.hpp:180-183), give each
+ * host thread its own context, as the C++ headers and the Python package do.
+ *
  * Error convention: every call returns a sphbi_status; nothing throws across
  * the ABI. The C++ wrappers map statuses back onto the reference's exception
  * types (std::domain_error, std::invalid_argument, sphbi::UnsupportedForm,
@@ -151,6 +161,17 @@ sphbi_status sphbi_evaluate(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, dou
                             const int64_t* pair_particle, const int64_t* pair_triangle,
                             double* out_value, double* out_grad, int64_t* pair_list_out,
                             int64_t* pair_list_capacity, sphbi_stats* stats, sphbi_memory mem);
+
+/* ---- device count pass (multi-GPU work balance) --------
+ * The pair finder of sphbi_evaluate (same grid, same exact predicate) run as a
+ * count only: counts[i] = number of triangles t with d(p_i, closed T_t) < h,
+ * *total (optional) = their sum. counts is device memory when mem ==
+ * SPHBI_MEM_DEVICE, else host memory. No reference interface (the reference
+ * has no pair finder). Used to cut particle shards at equal
+ * pair counts (paper_2507_21686_b200/shard.py). */
+sphbi_status sphbi_pair_counts(sphbi_ctx* ctx, double h, int64_t n_particles, const double* particle_xy,
+                               int64_t n_triangles, const double* tri_xy, int64_t* counts, int64_t* total,
+                               sphbi_stats* stats, sphbi_memory mem);
 
 /* ---- P3 (10-node cubic Lagrange) boundary fields -------------------------
  * BASELINE.json configs[3]. No reference interface: the reference's term

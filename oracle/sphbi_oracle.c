@@ -36,6 +36,26 @@ typedef long double LD;
 typedef long double _Complex LC;
 typedef double _Complex DC;
 
+/* Region results (BasisTriple, triangle_integrator.hpp:218-230) are
+ * std::complex<double> in the reference: every region's basis triple is
+ * rounded to FP64 and regions are combined in FP64. -DORACLE_WIDE_BASIS keeps
+ * them in long double instead (a diagnostic build, oracle/_ref/
+ * libsphbi_oracle_wide.so, used only to measure how much of the reference's
+ * own error comes from that rounding; never the parity oracle). */
+#ifdef ORACLE_WIDE_BASIS
+typedef LC BC;
+typedef LD BR;
+#define BCMPLX CMPLXL
+#define BRE creall
+#define BIM cimagl
+#else
+typedef DC BC;
+typedef double BR;
+#define BCMPLX CMPLX
+#define BRE creal
+#define BIM cimag
+#endif
+
 /* status codes == include/sphbi_cuda.h */
 enum { ST_OK = 0, ST_DOMAIN = 1, ST_INVALID = 2, ST_UNSUPPORTED = 3, ST_SINGULAR = 4, ST_LOGIC = 5 };
 
@@ -605,13 +625,13 @@ static Mat2 mirrored_y(Mat2 m) {
 }
 
 typedef struct { /* :218-230 */
-  DC value[3], grad_x[3], grad_y[3];
+  BC value[3], grad_x[3], grad_y[3];
 } Basis;
 static void add_scaled(Basis* a, const Basis* o, double w) {
   for (int i = 0; i < 3; ++i) {
-    a->value[i] = CMPLX(creal(a->value[i]) + w * creal(o->value[i]), cimag(a->value[i]) + w * cimag(o->value[i]));
-    a->grad_x[i] = CMPLX(creal(a->grad_x[i]) + w * creal(o->grad_x[i]), cimag(a->grad_x[i]) + w * cimag(o->grad_x[i]));
-    a->grad_y[i] = CMPLX(creal(a->grad_y[i]) + w * creal(o->grad_y[i]), cimag(a->grad_y[i]) + w * cimag(o->grad_y[i]));
+    a->value[i] = BCMPLX(BRE(a->value[i]) + w * BRE(o->value[i]), BIM(a->value[i]) + w * BIM(o->value[i]));
+    a->grad_x[i] = BCMPLX(BRE(a->grad_x[i]) + w * BRE(o->grad_x[i]), BIM(a->grad_x[i]) + w * BIM(o->grad_x[i]));
+    a->grad_y[i] = BCMPLX(BRE(a->grad_y[i]) + w * BRE(o->grad_y[i]), BIM(a->grad_y[i]) + w * BIM(o->grad_y[i]));
   }
 }
 static Basis zero_basis(void) {
@@ -794,9 +814,9 @@ static Basis p3_assemble(Mat2 frame, const FamEval* fam) {
   const LC gx = cx_add(cx_scale(gxp, (LD)frame.m[0][0]), cx_scale(gyp, (LD)frame.m[1][0]));
   const LC gy = cx_add(cx_scale(gxp, (LD)frame.m[0][1]), cx_scale(gyp, (LD)frame.m[1][1]));
   Basis out = zero_basis();
-  out.value[0] = CMPLX((double)re_(v), (double)im_(v));
-  out.grad_x[0] = CMPLX((double)re_(gx), (double)im_(gx));
-  out.grad_y[0] = CMPLX((double)re_(gy), (double)im_(gy));
+  out.value[0] = BCMPLX((BR)re_(v), (BR)im_(v));
+  out.grad_x[0] = BCMPLX((BR)re_(gx), (BR)im_(gx));
+  out.grad_y[0] = BCMPLX((BR)re_(gy), (BR)im_(gy));
   return out;
 }
 
@@ -842,9 +862,9 @@ static Basis assemble_region(const Table* table, Mat2 frame, const P2* ref, cons
   for (int i = 0; i < 3; ++i) {
     const LC gx = cx_add(cx_scale(gxp[i], (LD)frame.m[0][0]), cx_scale(gyp[i], (LD)frame.m[1][0]));
     const LC gy = cx_add(cx_scale(gxp[i], (LD)frame.m[0][1]), cx_scale(gyp[i], (LD)frame.m[1][1]));
-    out.value[i] = CMPLX((double)re_(v[i]), (double)im_(v[i]));
-    out.grad_x[i] = CMPLX((double)re_(gx), (double)im_(gx));
-    out.grad_y[i] = CMPLX((double)re_(gy), (double)im_(gy));
+    out.value[i] = BCMPLX((BR)re_(v[i]), (BR)im_(v[i]));
+    out.grad_x[i] = BCMPLX((BR)re_(gx), (BR)im_(gx));
+    out.grad_y[i] = BCMPLX((BR)re_(gy), (BR)im_(gy));
   }
   return out;
 }
@@ -1185,28 +1205,28 @@ static void canonicalize_triangle(P2* v, int* perm) { /* :680-694 */
   }
 }
 
-static void finalize(DC v, DC gx, DC gy, double normalization, double h, double* out4) { /* :696-704 */
-  double im = fabs(cimag(v));
-  if (fabs(cimag(gx)) > im) im = fabs(cimag(gx));
-  if (fabs(cimag(gy)) > im) im = fabs(cimag(gy));
-  out4[0] = creal(v) * normalization;
-  out4[1] = creal(gx) * normalization / h;
-  out4[2] = creal(gy) * normalization / h;
+static void finalize(BC v, BC gx, BC gy, double normalization, double h, double* out4) { /* :696-704 */
+  double im = fabs((double)BIM(v));
+  if (fabs((double)BIM(gx)) > im) im = fabs((double)BIM(gx));
+  if (fabs((double)BIM(gy)) > im) im = fabs((double)BIM(gy));
+  out4[0] = (double)(BRE(v) * normalization);
+  out4[1] = (double)(BRE(gx) * normalization / h);
+  out4[2] = (double)(BRE(gy) * normalization / h);
   out4[3] = im;
 }
 
 static void combine_basis(const Basis* b, const double* values, double normalization, double h,
                           double* out4) { /* :706-717 */
-  double vr = 0, vi = 0, xr = 0, xi = 0, yr = 0, yi = 0;
+  BR vr = 0, vi = 0, xr = 0, xi = 0, yr = 0, yi = 0;
   for (int i = 0; i < 3; ++i) {
-    vr += values[i] * creal(b->value[i]);
-    vi += values[i] * cimag(b->value[i]);
-    xr += values[i] * creal(b->grad_x[i]);
-    xi += values[i] * cimag(b->grad_x[i]);
-    yr += values[i] * creal(b->grad_y[i]);
-    yi += values[i] * cimag(b->grad_y[i]);
+    vr += values[i] * BRE(b->value[i]);
+    vi += values[i] * BIM(b->value[i]);
+    xr += values[i] * BRE(b->grad_x[i]);
+    xi += values[i] * BIM(b->grad_x[i]);
+    yr += values[i] * BRE(b->grad_y[i]);
+    yi += values[i] * BIM(b->grad_y[i]);
   }
-  finalize(CMPLX(vr, vi), CMPLX(xr, xi), CMPLX(yr, yi), normalization, h, out4);
+  finalize(BCMPLX(vr, vi), BCMPLX(xr, xi), BCMPLX(yr, yi), normalization, h, out4);
 }
 
 /* integrate_triangle (:808-822) */
@@ -1363,9 +1383,9 @@ int oracle_integrate_region(int kind, const double* a, const double* ref6, const
     }
   }
   for (int i = 0; i < 3; ++i) {
-    out9[3 * i] = creal(b.value[i]);
-    out9[3 * i + 1] = creal(b.grad_x[i]);
-    out9[3 * i + 2] = creal(b.grad_y[i]);
+    out9[3 * i] = (double)BRE(b.value[i]);
+    out9[3 * i + 1] = (double)BRE(b.grad_x[i]);
+    out9[3 * i + 2] = (double)BRE(b.grad_y[i]);
   }
   return g_status;
 }

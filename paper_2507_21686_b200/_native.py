@@ -71,6 +71,7 @@ EXPORTED_SYMBOLS = (
     "sphbi_integrate_pairs",
     "sphbi_integrate_regions",
     "sphbi_evaluate",
+    "sphbi_pair_counts",
     "sphbi_integrate_pairs_p3",
     "sphbi_evaluate_p3",
     "sphbi_measure_fp64_peak",
@@ -114,6 +115,8 @@ def load() -> ctypes.CDLL:
     lib.sphbi_evaluate.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64, P,
                                    ctypes.c_int64, P, P, ctypes.c_int64, P, P, P, P, P,
                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats), ctypes.c_int]
+    lib.sphbi_pair_counts.argtypes = [P, ctypes.c_double, ctypes.c_int64, P, ctypes.c_int64, P, P,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats), ctypes.c_int]
     lib.sphbi_integrate_pairs_p3.argtypes = [P, ctypes.POINTER(KernelDesc), ctypes.c_double, ctypes.c_int64,
                                              P, P, P, P, P, ctypes.c_int]
     lib.sphbi_evaluate_p3.argtypes = lib.sphbi_evaluate.argtypes

@@ -17,6 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "_lib" / "libsphbi_cuda.so"
+SCENES_LIB = PKG / "_lib" / "libsphbi_scenes.so"
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -51,6 +52,19 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             print(r.stderr[-2000:])
     return LIB
+
+
+def build_scenes(force: bool = False) -> Path:
+    """Scene-generation helper (Bridson Poisson-disk sampler for the cfg5
+    obstacle meshes); plain C, not on the evaluation path."""
+    src = CSRC / "poisson_disk.c"
+    if force or _stale(SCENES_LIB, [src]):
+        SCENES_LIB.parent.mkdir(parents=True, exist_ok=True)
+        r = subprocess.run(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", str(src), "-o", str(SCENES_LIB), "-lm"],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"scene helper build failed:\n{r.stderr[-4000:]}")
+    return SCENES_LIB
 
 
 def build_checkers(force: bool = False) -> None:
@@ -91,5 +105,6 @@ def build_dropin_tests(force: bool = False) -> None:
 
 if __name__ == "__main__":
     build_native(force=True, verbose=True)
+    build_scenes(force=True)
     build_checkers(force=True)
     build_dropin_tests(force=True)

@@ -236,21 +236,37 @@ SPHBI_HD void acc_zero(PairAcc& a) {
 
 SPHBI_HD dd dd_scale(dd a, double s) { return s == 1.0 ? a : (s == -1.0 ? dd_neg(a) : dd_mul_d(a, s)); }
 
-// acc += sign * (M^T S M) (see header comment): tau' = M tau; g = M^T g'.
+// The frames are FP64 rotations or reflections (rows (c, s), (-s, c) or
+// (c, s), (s, -c)), orthonormal only to rounding: M^T M = delta I with
+// delta = c^2 + s^2 = 1 + e, |e| ~ 1e-16. The reference solves the hat planes
+// in the region frame from the vertices mapped by M (triangle_integrator.hpp:
+// 248-269), i.e. its tau' = M^-T tau exactly, M^-1 = M^T / delta; the
+// gradient covector is back-mapped with M^T (:291-299). Rotating the tau
+// channels with M^T instead leaves a relative error e that the plane slope
+// of a sliver triangle (1e3..1e4 in the unit-disc frame) lifts above the
+// parity floor, so x / delta = x (1 - e) + O(e^2) is applied in dd.
+SPHBI_HD double frame_excess(const Frame& M) {
+  const dd q = dd_add(two_prod(M.m00, M.m00), two_prod(M.m01, M.m01));
+  return (q.hi - 1.0) + q.lo;  // exact: q.hi is within a few ulp of 1
+}
+SPHBI_HD dd dd_unscale(dd x, double e) { return dd_add_d(x, -x.hi * e); }
+
+// acc += sign * (M^-1 S, M^T G' M^-T) (see header comment and frame_excess).
 SPHBI_HD void acc_add_region(PairAcc& a, const S9& S, const Frame& M, double sign) {
-  // value covector
-  const dd v1 = dd_dot2_d(S.v1, M.m00, S.v2, M.m10);
-  const dd v2 = dd_dot2_d(S.v1, M.m01, S.v2, M.m11);
+  const double e = frame_excess(M);
+  // value covector M^-1 S_v = M^T S_v / delta
+  const dd v1 = dd_unscale(dd_dot2_d(S.v1, M.m00, S.v2, M.m10), e);
+  const dd v2 = dd_unscale(dd_dot2_d(S.v1, M.m01, S.v2, M.m11), e);
   // A = M^T G'
   const dd a00 = dd_dot2_d(S.gx1, M.m00, S.gy1, M.m10);
   const dd a01 = dd_dot2_d(S.gx2, M.m00, S.gy2, M.m10);
   const dd a10 = dd_dot2_d(S.gx1, M.m01, S.gy1, M.m11);
   const dd a11 = dd_dot2_d(S.gx2, M.m01, S.gy2, M.m11);
-  // G = A M
-  const dd g00 = dd_dot2_d(a00, M.m00, a01, M.m10);
-  const dd g01 = dd_dot2_d(a00, M.m01, a01, M.m11);
-  const dd g10 = dd_dot2_d(a10, M.m00, a11, M.m10);
-  const dd g11 = dd_dot2_d(a10, M.m01, a11, M.m11);
+  // G = A M^-T = A M / delta
+  const dd g00 = dd_unscale(dd_dot2_d(a00, M.m00, a01, M.m10), e);
+  const dd g01 = dd_unscale(dd_dot2_d(a00, M.m01, a01, M.m11), e);
+  const dd g10 = dd_unscale(dd_dot2_d(a10, M.m00, a11, M.m10), e);
+  const dd g11 = dd_unscale(dd_dot2_d(a10, M.m01, a11, M.m11), e);
   const dd g3x = dd_dot2_d(S.gx3, M.m00, S.gy3, M.m10);
   const dd g3y = dd_dot2_d(S.gx3, M.m01, S.gy3, M.m11);
   a.v1 = dd_add(a.v1, dd_scale(v1, sign));

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -138,6 +139,10 @@ enum ScratchSlot {
 };
 
 struct sphbi_ctx {
+  // Every C-ABI call on a context holds this lock for its whole duration: the
+  // scratch banks, pinned staging words, overflow flags, stream and device
+  // counters below are per-context state (recursive: entry points may nest).
+  std::recursive_mutex mtx;
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -181,6 +186,11 @@ struct sphbi_ctx {
   cudaEvent_t tl2[64][4] = {};  // per chunk: pre-classified / emitted / pieces done / combined
   int tl_chunk = -1;
 };
+
+// Holds the context's lock for the rest of the enclosing C-ABI call (no-op for NULL).
+#define SPHBI_LOCK(ctxp)                                                     \
+  std::unique_lock<std::recursive_mutex> sphbi_lock_;                         \
+  if (sphbi_ctx* lc_ = (ctxp)) sphbi_lock_ = std::unique_lock<std::recursive_mutex>(lc_->mtx)
 
 namespace {
 
@@ -2364,6 +2374,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
 extern "C" {
 
 sphbi_status sphbi_measure_fp64_peak(sphbi_ctx* c, double* tflops, double* ms_out) {
+  SPHBI_LOCK(c);
   if (!c || !tflops) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL argument");
   cudaSetDevice(c->device);
   int sms = 0;
@@ -2463,6 +2474,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
 
 sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
   if (!c) return SPHBI_OK;
+  { std::lock_guard<std::recursive_mutex> wait_for_calls(c->mtx); }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < sphbi_ctx::kBanks * kNumBufs; ++i)
@@ -2490,24 +2502,28 @@ sphbi_status sphbi_ctx_destroy(sphbi_ctx* c) {
 }
 
 sphbi_status sphbi_ctx_set_stream(sphbi_ctx* c, void* s) {
+  SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
   return SPHBI_OK;
 }
 
 sphbi_status sphbi_ctx_synchronize(sphbi_ctx* c) {
+  SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return SPHBI_OK;
 }
 
 sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* c, int enable) {
+  SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   c->counters_on = enable != 0;
   return SPHBI_OK;
 }
 
 sphbi_status sphbi_read_counters(sphbi_ctx* c, uint64_t out[SPHBI_NUM_COUNTERS], int reset) {
+  SPHBI_LOCK(c);
   if (!c || !out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL argument");
   cudaSetDevice(c->device);
   SPHBI_CUDA_TRY(cudaMemcpyAsync(out, c->d_counters, sizeof(uint64_t) * kNumCounters,
@@ -2588,6 +2604,7 @@ static sphbi_status integrate_pairs_impl(sphbi_ctx* c, const sphbi_kernel_desc* 
 sphbi_status sphbi_integrate_regions(sphbi_ctx* c, const sphbi_kernel_desc* kernel, int64_t n,
                                      const int32_t* kind, const double* args, const double* ref_xy,
                                      double* out, uint32_t* status_out) {
+  SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   KernelConsts K;
   sphbi_status st = make_consts(kernel, &K);
@@ -2637,6 +2654,7 @@ struct sphbi_basis_cache {
   size_t stage_cap = 0;
   unsigned* flags = nullptr;
   sphbi_status reserve(int64_t total) {
+    release();  // an overflow retry reserves again
     n_pairs = total;
     const size_t np = static_cast<size_t>(total > 0 ? total : 1);
     if (cudaMalloc(&pp, 4 * np) != cudaSuccess || cudaMalloc(&pt, 4 * np) != cudaSuccess ||
@@ -2655,6 +2673,7 @@ struct sphbi_basis_cache {
     bases = stage = nullptr;
     row_ptr = nullptr;
     flags = nullptr;
+    stage_cap = 0;
   }
 };
 
@@ -2673,7 +2692,8 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
                             int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
                             sphbi_memory mem, const double* nodal10 = nullptr,
-                            sphbi_basis_cache* bc = nullptr, const PieceSet* pieces = nullptr) {
+                            sphbi_basis_cache* bc = nullptr, const PieceSet* pieces = nullptr,
+                            int64_t* counts_out = nullptr) {
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
   if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
@@ -2821,6 +2841,8 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     total_pairs = n_pairs;
     if (n_pairs > 0) {
       if (!pair_particle || !pair_triangle) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL pair arrays");
+      if (n_pairs >= (int64_t(1) << 31))  // the pair sort and row pointers index pairs with int
+        return fail(SPHBI_ERR_INVALID_ARGUMENT, "explicit pair lists are limited to 2^31 - 1 pairs per call");
       const int64_t *ip = pair_particle, *it = pair_triangle;
       if (mem == SPHBI_MEM_HOST) {
         int64_t *a, *b;
@@ -3027,6 +3049,22 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     total_pairs = static_cast<int64_t>(*htot);
+    if (counts_out) {  // sphbi_pair_counts: the count pass only
+      const cudaMemcpyKind kind = mem == SPHBI_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(counts_out, pcount, 8 * n_particles, kind, s));
+      SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+      if (pair_list_capacity) *pair_list_capacity = total_pairs;
+      if (timing) {
+        cudaEventRecord(c->ev[1], s);
+        cudaEventSynchronize(c->ev[1]);
+        float a = 0;
+        cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+        stats->ms_pairs = a;
+        stats->n_pairs = total_pairs;
+        stats->n_candidates = candidates;
+      }
+      return SPHBI_OK;
+    }
     // chunk boundaries (particle index, pair offset), computed on the device
     std::vector<long long> cb;
     if (total_pairs > kMaxChunkPairs) {
@@ -3182,6 +3220,7 @@ extern "C" {
 sphbi_status sphbi_integrate_pairs(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
                                    const double* query_xy, const double* tri_xy, const double* values,
                                    int32_t mode, double* out, uint32_t* status_out, sphbi_memory mem) {
+  SPHBI_LOCK(c);
   if (c) c->overflowed = false;
   sphbi_status st = integrate_pairs_impl(c, kernel, h, n, query_xy, tri_xy, values, mode, out, status_out, mem);
   if (c && c->overflowed) {
@@ -3199,6 +3238,7 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
                             const int64_t* pair_triangle, double* out_value, double* out_grad,
                             int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
                             sphbi_memory mem) {
+  SPHBI_LOCK(c);
   if (c) c->overflowed = false;
   sphbi_status st = evaluate_impl(c, kernel, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
                                   pair_particle, pair_triangle, out_value, out_grad, pair_list_out,
@@ -3211,6 +3251,39 @@ sphbi_status sphbi_evaluate(sphbi_ctx* c, const sphbi_kernel_desc* kernel, doubl
                        mem);
     c->force_exact = false;
   }
+  return st;
+}
+
+sphbi_status sphbi_pair_counts(sphbi_ctx* c, double h, int64_t n_particles, const double* particle_xy,
+                               int64_t n_triangles, const double* tri_xy, int64_t* counts, int64_t* total,
+                               sphbi_stats* stats, sphbi_memory mem) {
+  SPHBI_LOCK(c);
+  if (!counts && n_particles > 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "counts is NULL");
+  sphbi_kernel_desc unit{};  // the count pass never evaluates: any valid kernel
+  unit.n_coefficients = 1;
+  unit.coefficients[0] = 1.0;
+  unit.normalization = 1.0;
+  int64_t tot = 0;
+  sphbi_status st = SPHBI_OK;
+  if (n_particles > 0 && n_triangles > 0) {
+    st = evaluate_impl(c, &unit, h, n_particles, particle_xy, n_triangles, tri_xy, nullptr, -1, nullptr, nullptr,
+                       nullptr, nullptr, nullptr, &tot, stats, mem, nullptr, nullptr, nullptr, counts);
+  } else {
+    if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");
+    if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (n_particles > 0) {
+      if (mem == SPHBI_MEM_HOST) {
+        std::memset(counts, 0, 8 * n_particles);
+      } else {
+        cudaSetDevice(c->device);
+        SPHBI_CUDA_TRY(cudaMemsetAsync(counts, 0, 8 * n_particles, c->stream));
+        SPHBI_CUDA_TRY(cudaStreamSynchronize(c->stream));
+      }
+    }
+  }
+  if (st == SPHBI_OK && total) *total = tot;
   return st;
 }
 
@@ -3271,6 +3344,7 @@ static sphbi_status integrate_pairs_p3_impl(sphbi_ctx* c, const sphbi_kernel_des
 sphbi_status sphbi_integrate_pairs_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, double h, int64_t n,
                                       const double* query_xy, const double* tri_xy, const double* nodal10,
                                       double* out, uint32_t* status_out, sphbi_memory mem) {
+  SPHBI_LOCK(c);
   return retry_exact(c, [&] {
     return integrate_pairs_p3_impl(c, kernel, h, n, query_xy, tri_xy, nodal10, out, status_out, mem);
   });
@@ -3282,6 +3356,7 @@ sphbi_status sphbi_evaluate_p3(sphbi_ctx* c, const sphbi_kernel_desc* kernel, do
                                const int64_t* pair_triangle, double* out_value, double* out_grad,
                                int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
                                sphbi_memory mem) {
+  SPHBI_LOCK(c);
   if (!nodal10 && n_triangles > 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "nodal10 is NULL");
   static const double kNoNodes = 0.0;
   return retry_exact(c, [&] {
@@ -3296,6 +3371,7 @@ sphbi_status sphbi_bases_create(sphbi_ctx* c, const sphbi_kernel_desc* kernel, d
                                 const double* particle_xy, int64_t n_triangles, const double* tri_xy,
                                 int64_t n_pairs, const int64_t* pair_particle, const int64_t* pair_triangle,
                                 sphbi_stats* stats, sphbi_memory mem, sphbi_basis_cache** out) {
+  SPHBI_LOCK(c);
   if (!out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
@@ -3327,6 +3403,7 @@ sphbi_status sphbi_bases_info(const sphbi_basis_cache* bc, int64_t* n_particles,
 }
 
 sphbi_status sphbi_bases_read(const sphbi_basis_cache* bc, int64_t* pair_list, double* bases, sphbi_memory mem) {
+  SPHBI_LOCK(bc ? bc->ctx : nullptr);
   if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
   sphbi_ctx* c = bc->ctx;
   cudaSetDevice(c->device);
@@ -3355,6 +3432,7 @@ sphbi_status sphbi_bases_apply(sphbi_basis_cache* bc, int32_t variant, const dou
                                const double* tri_densities, const double* particle_a0,
                                const double* particle_rho0, double* out_value, double* out_grad, double* ms_apply,
                                sphbi_memory mem) {
+  SPHBI_LOCK(bc ? bc->ctx : nullptr);
   if (!bc) return fail(SPHBI_ERR_INVALID_ARGUMENT, "basis cache is NULL");
   if (variant < 0 || variant > 2) return fail(SPHBI_ERR_INVALID_ARGUMENT, "unknown gradient variant");
   if (bc->n_triangles > 0 && !tri_values) return fail(SPHBI_ERR_INVALID_ARGUMENT, "tri_values is NULL");
@@ -3479,14 +3557,17 @@ static sphbi_status bases_pairs_impl(sphbi_basis_cache* bc, const double* pair_w
 
 sphbi_status sphbi_bases_apply_pairs(sphbi_basis_cache* bc, const double* pair_weights, double* out_value,
                                      double* out_grad, sphbi_memory mem) {
+  SPHBI_LOCK(bc ? bc->ctx : nullptr);
   return bases_pairs_impl(bc, pair_weights, 0, out_value, out_grad, mem);
 }
 
 sphbi_status sphbi_boundary_normals(sphbi_basis_cache* bc, double* out_normal, sphbi_memory mem) {
+  SPHBI_LOCK(bc ? bc->ctx : nullptr);
   return bases_pairs_impl(bc, nullptr, 1, nullptr, out_normal, mem);
 }
 
 sphbi_status sphbi_bases_destroy(sphbi_basis_cache* bc) {
+  SPHBI_LOCK(bc ? bc->ctx : nullptr);
   if (!bc) return SPHBI_OK;
   cudaSetDevice(bc->ctx->device);
   cudaStreamSynchronize(bc->ctx->stream);
@@ -3503,6 +3584,7 @@ sphbi_status sphbi_evaluate_piecewise(sphbi_ctx* c, int32_t n_pieces, const sphb
                                       const int64_t* pair_triangle, double* out_value, double* out_grad,
                                       int64_t* pair_list_out, int64_t* pair_list_capacity, sphbi_stats* stats,
                                       sphbi_memory mem) {
+  SPHBI_LOCK(c);
   if (n_pieces < 1 || n_pieces > kMaxPieces || !pieces || !scales)
     return fail(SPHBI_ERR_INVALID_ARGUMENT, "piecewise kernel: 1..4 pieces with scales");
   if (!(h > 0.0)) return fail(SPHBI_ERR_DOMAIN, "integrate_triangle: support h must be > 0");

@@ -262,20 +262,62 @@ def cfg4(spacing_div: int = 4, max_particles: Optional[int] = None) -> Scene:
                                                           "field": "p3", "vertex_ids": vid})
 
 
-def cfg5(n_particles: int = 16_000_000, n_discs: int = 500, target_tris: int = 2_000_000,
-         domain: float = 100.0, spacing: float = 0.05) -> Scene:
-    """100x100 domain, 500 non-overlapping obstacle discs meshed by Delaunay
-    triangulation of min-spacing-0.05 points (jittered hex lattice) with a
-    centroid-inside filter (~2M triangles); 16M uniform particles; Wendland C2 and
-    the 2-piece cubic spline, h = 0.1."""
+def _poisson_disk_lib():
+    import ctypes
+
+    from . import build as B
+
+    lib = ctypes.CDLL(str(B.build_scenes()))
+    lib.sphbi_poisson_disk.restype = ctypes.c_int64
+    lib.sphbi_poisson_disk.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_int64]
+    return lib
+
+
+def poisson_disk(seed: int, radius: float, spacing: float, k: int = 30) -> np.ndarray:
+    """Bridson Poisson-disk samples (min spacing `spacing`) inside the disc of
+    the given radius about the origin (csrc/poisson_disk.c)."""
+    lib = _poisson_disk_lib()
+    cap = int(4.0 * radius * radius / (spacing * spacing)) + 64
+    while True:
+        buf = np.zeros((cap, 2))
+        n = lib.sphbi_poisson_disk(seed, radius, spacing, k, buf.ctypes.data, cap)
+        if n < 0:
+            raise RuntimeError("poisson_disk: bad arguments")
+        if n <= cap:
+            return np.ascontiguousarray(buf[:n])
+        cap = int(n)
+
+
+def _disc_mesh(seed: int, radius: float, spacing: float) -> np.ndarray:
+    """Delaunay triangulation of fresh Poisson-disk points of one obstacle
+    disc, triangles whose centroid lies outside the disc dropped; (m, 6)."""
     from scipy.spatial import Delaunay
 
+    pts = poisson_disk(seed, radius, spacing)
+    t = pts[Delaunay(pts).simplices]  # (m, 3, 2)
+    cen = t.mean(axis=1)
+    return t[np.hypot(cen[:, 0], cen[:, 1]) <= radius].reshape(-1, 6)
+
+
+_CFG5_MESH = {}
+
+
+def cfg5_mesh(n_discs: int = 500, target_tris: int = 2_000_000, domain: float = 100.0, spacing: float = 0.05,
+              h: float = 0.1):
+    """The cfg5 obstacle mesh (BASELINE.json configs[4]): n_discs non-overlapping
+    discs of a common radius R (gap >= 2h), centres uniform; each disc meshed
+    by a Delaunay triangulation of its own Bridson Poisson-disk points (min
+    spacing 0.05) with a centroid-inside filter. R is tuned from a pilot disc's
+    triangle density so the total is ~target_tris. Returns (triangles, info)."""
+    key = (n_discs, target_tris, domain, spacing, h)
+    if key in _CFG5_MESH:
+        return _CFG5_MESH[key]
     rng = np.random.default_rng(SEED_BASE + 5)
-    h = 0.1
-    s = spacing * 1.2  # hex spacing; jitter keeps the min spacing >= `spacing`
-    jit = (s - spacing) / 2.0 * 0.999
-    dens_tri = 2.0 * 2.0 / (math.sqrt(3.0) * s * s)
-    R = math.sqrt(target_tris / (n_discs * math.pi * dens_tri))
+    pilot_r = 1.5
+    pilot = _disc_mesh(int(rng.integers(1 << 62)), pilot_r, spacing)
+    density = pilot.shape[0] / (math.pi * pilot_r * pilot_r)
+    R = math.sqrt(target_tris / (n_discs * math.pi * density))
     centres = []
     tries = 0
     while len(centres) < n_discs and tries < 200000:
@@ -284,28 +326,29 @@ def cfg5(n_particles: int = 16_000_000, n_discs: int = 500, target_tris: int = 2
         if all((c[0] - q[0]) ** 2 + (c[1] - q[1]) ** 2 > (2 * R + 2 * h) ** 2 for q in centres):
             centres.append(c)
     centres = np.array(centres)
-    # one hex patch reused per disc, with fresh jitter per disc
-    rows = int(math.ceil(2 * R / (s * math.sqrt(3) / 2))) + 2
-    cols = int(math.ceil(2 * R / s)) + 2
-    jj, ii = np.meshgrid(np.arange(rows), np.arange(cols), indexing="ij")
-    hx = (ii - cols / 2) * s + (jj % 2) * s / 2
-    hy = (jj - rows / 2) * s * math.sqrt(3) / 2
-    base = np.stack([hx.ravel(), hy.ravel()], axis=1)
-    base = base[np.hypot(base[:, 0], base[:, 1]) <= R + 1e-9]
-    tris = []
-    for c in centres:
-        pts = base + rng.uniform(-jit, jit, base.shape)
-        pts = pts[np.hypot(pts[:, 0], pts[:, 1]) <= R]
-        dl = Delaunay(pts)
-        t = pts[dl.simplices]  # (m,3,2)
-        cen = t.mean(axis=1)
-        t = t[np.hypot(cen[:, 0], cen[:, 1]) <= R]
-        tris.append((t + c).reshape(-1, 6))
+    seeds = rng.integers(1 << 62, size=len(centres))
+    tris = [(_disc_mesh(int(sd), R, spacing).reshape(-1, 3, 2) + c).reshape(-1, 6) for sd, c in zip(seeds, centres)]
     tris = np.ascontiguousarray(np.concatenate(tris, axis=0))
+    info = {"R": R, "triangles": int(tris.shape[0]), "discs": int(len(centres)), "mesh": "bridson+delaunay",
+            "pilot_tri_density": density}
+    _CFG5_MESH[key] = (tris, info)
+    return tris, info
+
+
+def cfg5(n_particles: int = 16_000_000, n_discs: int = 500, target_tris: int = 2_000_000,
+         domain: float = 100.0, spacing: float = 0.05) -> Scene:
+    """100x100 domain, 500 non-overlapping obstacle discs, each meshed by a
+    Delaunay triangulation of its own Bridson Poisson-disk points (min spacing
+    0.05) with a centroid-inside filter (~2M triangles, cfg5_mesh); 16M uniform
+    particles over the whole domain (also inside obstacles: the literal
+    reading); Wendland C2 and the 2-piece cubic spline,
+    h = 0.1."""
+    h = 0.1
+    tris, info = cfg5_mesh(n_discs, target_tris, domain, spacing, h)
+    rng = np.random.default_rng(SEED_BASE + 5 + 1000)
     P = rng.uniform(0.0, domain, (n_particles, 2))
     kernels = [wendland_c2()] + cubic_spline_pieces()
-    return Scene("cfg5", P, tris, None, kernels, h,
-                 info={"R": R, "triangles": int(tris.shape[0]), "discs": int(len(centres))})
+    return Scene("cfg5", P, tris, None, kernels, h, info=dict(info))
 
 
 def subsample(scene: Scene, n: int, seed: int = 0) -> Scene:

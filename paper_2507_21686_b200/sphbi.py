@@ -317,22 +317,62 @@ class Context:
         return int(self.lib.sphbi_ctx_launch_count(self.handle))
 
 
-_ctx_lock = threading.Lock()
-_default_ctx: dict = {}
+_tls = threading.local()
 
 
 def default_context(device: int = 0) -> Context:
-    with _ctx_lock:
-        c = _default_ctx.get(device)
-        if c is None:
-            c = Context(device)
-            c.enable_counters(True)
-            _default_ctx[device] = c
-        return c
+    """This host thread's context on `device` (created on first use, route
+    counters on). One context per thread, as the C++ drop-in does: the
+    reference's functions are reentrant with thread_local counters, and ctypes
+    releases the GIL during device calls."""
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(device)
+    if c is None:
+        c = Context(device)
+        c.enable_counters(True)
+        ctxs[device] = c
+    return c
 
 
 def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def _tri_values(tri_values, T: int, allow_p3: bool = True):
+    """Validated per-triangle field values: (T,3) barycentric (a flat array of
+    3T is accepted) or, where allowed, (T,10) P3 nodal values. Returns
+    (array or None, is_p3). The C side reads 24 T (or 80 T) bytes from the
+    pointer, so a short array must never reach it."""
+    if tri_values is None:
+        return None, False
+    v = np.ascontiguousarray(tri_values, dtype=np.float64)
+    if allow_p3 and v.ndim == 2 and v.shape == (T, 10):
+        return v, True
+    if v.ndim == 2 and v.shape == (T, 3):
+        return v, False
+    if v.ndim == 1 and v.shape[0] == 3 * T:
+        return v.reshape(T, 3), False
+    want = "(T,3) or (T,10)" if allow_p3 else "(T,3)"
+    raise InvalidArgument(f"tri_values must have shape {want} with T = {T}, got {v.shape}")
+
+
+def _pair_arrays(pairs, what: str = "pairs"):
+    ip = np.ascontiguousarray(pairs[0], dtype=np.int64).reshape(-1)
+    it = np.ascontiguousarray(pairs[1], dtype=np.int64).reshape(-1)
+    if ip.shape != it.shape:
+        raise InvalidArgument(f"{what}: pair_particle and pair_triangle differ in length")
+    return ip, it
+
+
+def _per_particle(a, n: int, what: str):
+    if a is None:
+        return None
+    v = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    if v.shape[0] != n:
+        raise InvalidArgument(f"{what}: one value per particle ({n}) required, got {v.shape[0]}")
+    return v
 
 
 def _as_table(table) -> KernelTermTable:
@@ -553,14 +593,8 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
     p = np.ascontiguousarray(particles_xy, dtype=np.float64).reshape(-1, 2)
     t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
     n, T = p.shape[0], t.shape[0]
-    fn = ctx.lib.sphbi_evaluate
-    v = None
-    if tri_values is not None:
-        v = np.ascontiguousarray(tri_values, dtype=np.float64)
-        if v.ndim == 2 and v.shape[1] == 10:  # P3 nodal values (configs[3])
-            fn = ctx.lib.sphbi_evaluate_p3
-        else:
-            v = v.reshape(-1, 3)
+    v, p3 = _tri_values(tri_values, T)
+    fn = ctx.lib.sphbi_evaluate_p3 if p3 else ctx.lib.sphbi_evaluate  # P3 nodal values: configs[3]
     out_v = np.zeros(n, dtype=np.float64)
     out_g = np.zeros((n, 2), dtype=np.float64)
     stats = N.Stats()
@@ -582,8 +616,7 @@ def evaluate(particles_xy, h: float, tri_xy, table, tri_values=None, pairs=None,
         if return_pairs:
             return out_v, out_g, es, plist[: cap.value]
         return out_v, out_g, es
-    ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
-    it = np.ascontiguousarray(pairs[1], dtype=np.int64)
+    ip, it = _pair_arrays(pairs, "evaluate")
     _raise(fn(ctx.handle, ctypes.byref(desc), float(h), n, _ptr(p), T, _ptr(t), _ptr(v),
                                   ip.shape[0], _ptr(ip), _ptr(it), _ptr(out_v), _ptr(out_g), None, None,
                                   ctypes.byref(stats), N.MEM_HOST), "evaluate")
@@ -610,7 +643,7 @@ def evaluate_piecewise(particles_xy, h: float, tri_xy, pieces, tri_values=None, 
     p = np.ascontiguousarray(particles_xy, dtype=np.float64).reshape(-1, 2)
     t = np.ascontiguousarray(tri_xy, dtype=np.float64).reshape(-1, 6)
     n, T = p.shape[0], t.shape[0]
-    v = None if tri_values is None else np.ascontiguousarray(tri_values, dtype=np.float64).reshape(-1, 3)
+    v, _ = _tri_values(tri_values, T, allow_p3=False)
     out_v = np.zeros(n, dtype=np.float64)
     out_g = np.zeros((n, 2), dtype=np.float64)
     stats = N.Stats()
@@ -620,8 +653,7 @@ def evaluate_piecewise(particles_xy, h: float, tri_xy, pieces, tri_values=None, 
         ip = it = None
         npairs = -1
     else:
-        ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
-        it = np.ascontiguousarray(pairs[1], dtype=np.int64)
+        ip, it = _pair_arrays(pairs, "evaluate_piecewise")
         npairs = ip.shape[0]
     plist = None
     if return_pairs:
@@ -670,8 +702,7 @@ class BasisCache:
                                         _ptr(t), -1, None, None, ctypes.byref(stats), N.MEM_HOST,
                                         ctypes.byref(h_out))
         else:
-            ip = np.ascontiguousarray(pairs[0], dtype=np.int64)
-            it = np.ascontiguousarray(pairs[1], dtype=np.int64)
+            ip, it = _pair_arrays(pairs, "BasisCache")
             st = lib.sphbi_bases_create(self.ctx.handle, ctypes.byref(desc), float(h), self.n, _ptr(p), self.T,
                                         _ptr(t), ip.shape[0], _ptr(ip), _ptr(it), ctypes.byref(stats),
                                         N.MEM_HOST, ctypes.byref(h_out))
@@ -694,11 +725,10 @@ class BasisCache:
         """Per-particle sums of integrate_triangle with the vertex weights
         gradient_variant_weights(variant, a0[p], rho0[p], tri_values[t], tri_densities[t])."""
         var = _VARIANT_CODE[variant] if isinstance(variant, str) else int(variant)
-        f64 = lambda a, shape: None if a is None else np.ascontiguousarray(a, dtype=np.float64).reshape(shape)
-        vals = f64(tri_values, (-1, 3))
-        dens = f64(tri_densities, (-1, 3))
-        pa = f64(a0, (-1,))
-        pr = f64(rho0, (-1,))
+        vals, _ = _tri_values(tri_values, self.T, allow_p3=False)
+        dens, _ = _tri_values(tri_densities, self.T, allow_p3=False)
+        pa = _per_particle(a0, self.n, "a0")
+        pr = _per_particle(rho0, self.n, "rho0")
         out_v = np.zeros(self.n, dtype=np.float64)
         out_g = np.zeros((self.n, 2), dtype=np.float64)
         ms = ctypes.c_double(0.0)
