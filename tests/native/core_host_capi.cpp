@@ -186,6 +186,62 @@ void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, co
   }
 }
 
+
+// piece log of one affine-field pair (analysis only): per piece 16 params
+// (type, sign, f00, f01, f10, f11, p0..p9) + the piece's own 9 moment sums
+// (PairAcc v1 v2 v3 g11 g12 g21 g22 g13 g23, hi + lo) in the particle frame
+struct LinLogSink {
+  static constexpr int kAngles = 2;
+  const KernelConsts* K;
+  unsigned status;
+  unsigned long long* counters;
+  double* rec;
+  int n, cap;
+  SPHBI_HD void bump(int) {}
+  void put(int type, const Frame& f, double sign, const double* prm, int np, const PairAcc& a) {
+    if (n >= cap) return;
+    double* r = rec + n * 34;
+    r[0] = type; r[1] = sign; r[2] = f.m00; r[3] = f.m01; r[4] = f.m10; r[5] = f.m11;
+    for (int i = 0; i < 10; ++i) r[6 + i] = i < np ? prm[i] : 0.0;
+    const dd* m[9] = {&a.v1, &a.v2, &a.v3, &a.g11, &a.g12, &a.g21, &a.g22, &a.g13, &a.g23};
+    for (int i = 0; i < 9; ++i) { r[16 + 2 * i] = m[i]->hi; r[17 + 2 * i] = m[i]->lo; }
+    ++n;
+  }
+  void disc(double sign) { PairAcc a; acc_zero(a); piece_disc(*K, a, sign); put(0, Frame{1, 0, 0, 1}, sign, nullptr, 0, a); }
+  void half_disc(const Frame& f, double sign) { PairAcc a; acc_zero(a); piece_half_disc(*K, a, f, sign); put(1, f, sign, nullptr, 0, a); }
+  void sector(const Frame& f, double gamma, double L, double sign) {
+    PairAcc a; acc_zero(a); piece_cone(*K, a, f, gamma, L, sign);
+    const double prm[2] = {gamma, L}; put(2, f, sign, prm, 2, a);
+  }
+  void stub(const Frame& f, double gamma, double l, double D, double beta, double lo, double u, bool window,
+            double sign) {
+    PairAcc a; acc_zero(a); piece_stub(*K, a, f, gamma, l, D, beta, lo, u, window, sign);
+    const double prm[7] = {gamma, l, D, beta, lo, u, window ? 1.0 : 0.0};
+    put(3, f, sign, prm, 7, a);
+  }
+  void segment(const Frame& f, double d, double sign) {
+    PairAcc a; acc_zero(a); piece_segment(*K, a, f, d, sign); const double prm[1] = {d}; put(4, f, sign, prm, 1, a);
+  }
+};
+// returns the piece count; nv6 receives the canonical normalized vertices,
+// planes9 the hat planes (t1, t2, t3 per vertex as hi + lo), perm3 the permutation
+int core_host_lin_pieces(const double* coef, int ncoef, double c2, double qx, double qy, double h,
+                         const double* tri6, double* rec, int cap, double* nv6, int* perm3) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  canonicalize(v, perm3);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) {
+    nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+    nv6[2 * i] = nv[i].x;
+    nv6[2 * i + 1] = nv[i].y;
+  }
+  LinLogSink s{&K, 0u, nullptr, rec, 0, cap};
+  integrate_normalized(s, nv);
+  return s.n;
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 // region-level evaluation with the device core (sphbi_integrate_regions' math, host build)

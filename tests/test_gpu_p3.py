@@ -2,9 +2,12 @@
 the product path (libsphbi_cuda.so, sphbi_integrate_pairs_p3 /
 sphbi_evaluate_p3 through the C-ABI) against the extended oracle and the
 high-precision golden values (tests/golden/p3_truth.npz). Tolerance as in
-test_gpu_parity.py; the absolute floor is scaled by the field's sup on the
-support disc only for the N(0,1)-nodes-on-random-triangles stress rows
-(kind 1), see oracle_lib.p3_ratio.
+test_gpu_parity.py, literal floor 1e-13 C/h^2 against the 40-digit truth for
+every row. The N(0,1)-nodes-on-random-triangles stress rows (kind 1: the cubic
+extrapolated over the support disc reaches 1e2..1e4) are checked against the
+truth only: there the extended CPU oracle's own error (the reference's
+complex long-double machinery, per-region FP64 rounding) exceeds the literal
+floor, so it cannot arbitrate (its kind-1 deviation is printed).
 """
 import sys
 from pathlib import Path
@@ -50,10 +53,9 @@ def test_p3_pairs_vs_golden_truth_and_oracle(S, ctx, O):
         q, tri, nodes, kind = g["q"][i], g["tri"][i], g["nodes"][i], int(g["kind"][i])
         table = S.table1_terms(S.PolyKernel(list(coef), c2))
         out = S.integrate_pairs_p3(q, h, tri, nodes, table, ctx=ctx)[0]
-        sup = OL.p3_field_sup(q, h, tri, nodes) if kind == 1 else 1.0
-        rt = OL.p3_ratio(out, g["truth"][i], c2, h, sup)
+        rt = OL.p3_ratio(out, g["truth"][i], c2, h, 1.0)
         st, want = OL.oracle_p3(O, coef, c2, q, h, np.ascontiguousarray(tri), np.ascontiguousarray(nodes))
-        ro = OL.p3_ratio(out, want, c2, h, sup if kind == 1 else 1.0)
+        ro = OL.p3_ratio(out, want, c2, h, 1.0)
         worst_t, worst_o = max(worst_t, rt), max(worst_o, ro)
         assert rt <= 1.0, (i, kind, out, g["truth"][i])
         if kind != 1:

@@ -215,22 +215,19 @@ def _cpu_pairs(O, P, T, h):
     return OL.cpu_pairs_grid(O, P, T, h)
 
 
-def test_cfg3_cell_list_pairs_bit_exact_and_parity(S, ctx, O):
-    """Star-shaped boundary strip (8,192 triangles), Wendland C6, h = 0.01: the
-    device cell list must find exactly the brute-force pair list (exact
-    predicate), and the per-particle sums must match the oracle. Run on the
-    particles of a seeded window (the full 1M-particle scene runs in the bench)."""
+def test_cfg3_full_scene_pairs_bit_exact_and_parity(S, ctx, O):
+    """cfg3 at full size: star-shaped boundary strip (8,192 triangles),
+    1,001,724 jittered-lattice particles, Wendland C6, h = 0.01. The device
+    cell list must find exactly the CPU exact-predicate pair list over ALL
+    particles, and every particle's sums must match the oracle."""
     from paper_2507_21686_b200 import scenes
     sc = scenes.cfg3()
-    # particles within 3h of the wall, plus 2000 deep interior ones
-    r = np.hypot(sc.particles[:, 0], sc.particles[:, 1])
-    near = np.argsort(-r)[:30000]
-    far = np.random.default_rng(0).choice(sc.particles.shape[0], 2000, replace=False)
-    P = sc.particles[np.unique(np.concatenate([near, far]))]
+    P = sc.particles
     k = sc.kernels[0]
     v, g, st, plist = S.evaluate(P, sc.h, sc.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
     ref_pairs = _cpu_pairs(O, P, sc.triangles, sc.h)
     assert plist.shape == ref_pairs.shape and np.array_equal(plist, ref_pairs)
+    assert st.n_pairs == ref_pairs.shape[0] > 50_000
     st_o, vo, go = OL.oracle_scene_sums(O, P, sc.triangles, None, k.coefficients, k.normalization, sc.h,
                                         ref_pairs[:, 0], ref_pairs[:, 1], threads=16)
     assert st_o == 0

@@ -119,8 +119,9 @@ def test_piecewise_argument_errors(S):
 def test_cubic_spline_one_pass_linear_field_cfg2(S, O):
     """Linear N(0,1) vertex field on cfg2's stress triangles (20% slivers,
     d/h in {0, 1e-12, U(0, 1.2)}), own-triangle pairs (mode A, explicit list),
-    h = 0.05; the inner piece sees the pairs within h/2. (Cell-list pairing with
-    a steep linear field over slivers is the known accuracy limit.)"""
+    h = 0.05; the inner piece sees the pairs within h/2. The same path with
+    cell-list pairing at BASELINE density is
+    test_gpu_adjudicated.py::test_cfg2_mode_b_cubic_spline_one_pass_linear_field."""
     from paper_2507_21686_b200 import scenes
     sc = scenes.cfg2(T=2048, per_tri=16, linear_field=True)
     ks = scenes.cubic_spline_pieces()

@@ -27,7 +27,7 @@ every particle, and that every particle with |gpu - raw| > tol has flagged
 pairs on which the reference misses the exact value by more than the
 tolerance.
 
-Run:  python tools/make_adjudicated.py [cfg2b|cfg5lin|all]   (~10 min on 8 cores)
+Run:  python tools/make_adjudicated.py [cfg2b|cfg2bcubic|cfg5lin|all]   (~10 min on 8 cores)
 """
 from __future__ import annotations
 
@@ -143,6 +143,23 @@ def main(which):
             report(f"cfg2b/{tag}", d, k, sc.h)
             out.update({f"{tag}_{key}": v for key, v in d.items()})
         np.savez_compressed(GOLD / "adjudicated_cfg2b.npz", **out)
+    if which in ("cfg2bcubic", "all"):
+        # the 2-piece cubic spline (one-pass piecewise path) with cell-list
+        # pairing and the linear field over the first 128 cfg2b particles
+        sc, idx = cfg2b_scene()
+        idx = idx[:128]
+        out = {"idx": idx, "h": sc.h}
+        raw = adj = None
+        for j, k in enumerate(scenes.cubic_spline_pieces()):
+            h = sc.h * k.support_scale
+            print(f"cfg2bcubic piece {j}", flush=True)
+            d = adjudicate(sc.particles[idx], sc.triangles, sc.values, k, h)
+            report(f"cfg2bcubic/{j}", d, k, h)
+            out.update({f"p{j}_{key}": v for key, v in d.items()})
+            raw = d["raw"] if raw is None else raw + d["raw"]
+            adj = d["adj"] if adj is None else adj + d["adj"]
+        out["raw"], out["adj"] = raw, adj
+        np.savez_compressed(GOLD / "adjudicated_cfg2bcubic.npz", **out)
     if which in ("cfg5lin", "all"):
         sc, idx, vals = cfg5lin_scene()
         k = sc.kernels[0]
