@@ -154,7 +154,9 @@ sphbi_status sphbi_integrate_regions(sphbi_ctx* ctx, const sphbi_kernel_desc* ke
  * Outputs may be NULL. pair_list_out (optional, device memory only when
  * mem == SPHBI_MEM_DEVICE): receives the found pairs as int64 (particle,
  * triangle) interleaved, sorted, when its capacity *pair_list_capacity
- * suffices; *pair_list_capacity is set to the pair count. */
+ * suffices; *pair_list_capacity is set to the pair count. With mem ==
+ * SPHBI_MEM_DEVICE, particle_xy, tri_xy and out_grad must be 16-byte aligned
+ * (double2 accesses), else SPHBI_ERR_INVALID_ARGUMENT. */
 sphbi_status sphbi_evaluate(sphbi_ctx* ctx, const sphbi_kernel_desc* kernel, double h,
                             int64_t n_particles, const double* particle_xy, int64_t n_triangles,
                             const double* tri_xy, const double* tri_values, int64_t n_pairs,

@@ -2699,6 +2699,11 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   if (n_particles < 0 || n_triangles < 0) return fail(SPHBI_ERR_INVALID_ARGUMENT, "negative size");
   if (n_particles >= (1ll << 31) || n_triangles >= (1ll << 31))
     return fail(SPHBI_ERR_INVALID_ARGUMENT, "particle / triangle counts must be < 2^31");
+  if (mem == SPHBI_MEM_DEVICE) {  // the kernels move particles and gradients as double2
+    auto misaligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; };
+    if (misaligned(particle_xy) || misaligned(out_grad) || misaligned(tri_xy))
+      return fail(SPHBI_ERR_INVALID_ARGUMENT, "device particle / triangle / gradient arrays must be 16-byte aligned");
+  }
   KernelConsts K;
   sphbi_status st = SPHBI_OK;
   if (pieces) {

@@ -144,7 +144,9 @@ class ShardedScene:
             self.ranges = shard_ranges(self.n, self.world)
         else:
             raise ValueError(f"unknown balance {balance!r}")
-        self.m = max(1, max(e - b for b, e in self.ranges))
+        # shard slot length: a multiple of 64 records, so each rank's value and
+        # gradient blocks start 512-B aligned (the reduction stores double2)
+        self.m = -(-max(1, max(e - b for b, e in self.ranges)) // 64) * 64
         self.buf = torch.zeros(self.world * 3 * self.m, dtype=torch.float64, device=self.device)
 
     # ---- work balance -------------------------------------------------
@@ -171,7 +173,7 @@ class ShardedScene:
         import torch
 
         blocks = shard_ranges(self.n, self.world)
-        mb = max(1, max(e - b for b, e in blocks))
+        mb = -(-max(1, max(e - b for b, e in blocks)) // 64) * 64
         cbuf = torch.zeros(self.world * mb, dtype=torch.int64, device=self.device)
         b, e = blocks[self.rank]
         local = cbuf[self.rank * mb:(self.rank + 1) * mb]

@@ -242,6 +242,82 @@ int core_host_lin_pieces(const double* coef, int ncoef, double c2, double qx, do
   return s.n;
 }
 
+// Host emulation of the device work-item pipeline's piece math (analysis
+// only): raw sector / stub items evaluated as k_pipe_sector / k_pipe_stub do
+// (frames and angles re-derived from the raw geometry, window classes, trig
+// factors from the piece geometry -- or, with trig_angles, from the angles).
+struct PipeEmuSink {
+  static constexpr int kAngles = 1;
+  const KernelConsts* K;
+  PairAcc acc;
+  unsigned status;
+  unsigned long long* counters;
+  bool trig_angles;
+  int disc_n;
+  SPHBI_HD void bump(int) {}
+  void disc(double sign) { disc_n += sign > 0.0 ? 1 : -1; }
+  void half_disc(const Frame& f, double sign) { piece_half_disc(*K, acc, f, sign); }
+  void sector_raw(P2 v1, P2 v2, double, double sign) {
+    Frame f;
+    double gamma;
+    PieceTrig T;
+    sector_from_raw(v1, v2, f, gamma, &T);
+    if (trig_angles) T = trig_from_angles(gamma, 0.0);
+    piece_cone(*K, acc, f, gamma, 1.0, sign, &T);
+  }
+  void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window, double sign) {
+    Frame f;
+    double gamma, beta;
+    PieceTrig T;
+    stub_frame_angles(v1, v2, r1, f, gamma, beta, &T);
+    if (trig_angles) T = trig_from_angles(gamma, window ? beta : 0.0);
+    switch (stub_class(D, lo, u, window)) {
+      case 0: piece_stub_k<0>(*K, acc, f, gamma, l, D, beta, lo, u, window, sign, T); break;
+      case 1: piece_stub_k<1>(*K, acc, f, gamma, l, D, beta, lo, u, window, sign, T); break;
+      case 2: piece_stub_k<2>(*K, acc, f, gamma, l, D, beta, lo, u, window, sign, T); break;
+      default: piece_stub_k<3>(*K, acc, f, gamma, l, D, beta, lo, u, window, sign, T); break;
+    }
+  }
+  void segment(const Frame& f, double d, double sign) { piece_segment(*K, acc, f, d, sign); }
+};
+int core_host_eval_pair_pipe(const double* coef, int ncoef, double c2, double qx, double qy, double h,
+                             const double* tri6, const double* vals3, int trig_angles, double* out4) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  PipeEmuSink c;
+  c.K = &K;
+  acc_zero(c.acc);
+  c.status = 0;
+  c.counters = nullptr;
+  c.trig_angles = trig_angles != 0;
+  c.disc_n = 0;
+  integrate_normalized(c, nv);
+  PairAcc a;
+  acc_zero(a);
+  if (c.disc_n) piece_disc(K, a, static_cast<double>(c.disc_n));
+  const dd* src[9] = {&c.acc.v1, &c.acc.v2, &c.acc.v3, &c.acc.g11, &c.acc.g12, &c.acc.g21, &c.acc.g22, &c.acc.g13, &c.acc.g23};
+  dd* dst[9] = {&a.v1, &a.v2, &a.v3, &a.g11, &a.g12, &a.g21, &a.g22, &a.g13, &a.g23};
+  for (int i = 0; i < 9; ++i) *dst[i] = dd_add(*dst[i], *src[i]);
+  HatPlanes H;
+  if (!hat_planes(nv, H)) { for (int i = 0; i < 4; ++i) out4[i] = 0.0; return (int)c.status; }
+  const double av[3] = {vals3[perm[0]], vals3[perm[1]], vals3[perm[2]]};
+  dd tau1{0, 0}, tau2{0, 0}, tau3{0, 0};
+  for (int i = 0; i < 3; ++i) {
+    tau1 = dd_add(tau1, dd_mul_d(H.t1[i], av[i]));
+    tau2 = dd_add(tau2, dd_mul_d(H.t2[i], av[i]));
+    tau3 = dd_add(tau3, dd_mul_d(H.t3[i], av[i]));
+  }
+  double raw[3];
+  combine_plane(a, tau1, tau2, tau3, raw);
+  finalize(raw, K.c2, h, out4);
+  return (int)c.status;
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 // region-level evaluation with the device core (sphbi_integrate_regions' math, host build)

@@ -524,3 +524,43 @@ np.savez(sys.argv[1], **out)
             res.append(np.load(f))
         for key in res[0].files:
             assert np.array_equal(res[0][key], res[1][key]), key
+
+
+def test_concurrent_host_threads(S):
+    """The reference is reentrant (pure functions, thread_local counters); the
+    drop-in gives each host thread its own context (default_context) and locks
+    a shared one per call: 4 threads x 20 batches, on per-thread contexts and
+    on one shared context, all bitwise equal to the single-threaded result."""
+    import threading
+    rng = np.random.default_rng(77)
+    batches = []
+    for _ in range(20):
+        n = int(rng.integers(1, 600))
+        rows = [OL.random_config(rng) for _ in range(n)]
+        Q = np.array([r[2] / r[3] for r in rows])
+        T = np.array([r[0] / r[3] for r in rows])
+        V = np.array([r[1] for r in rows])
+        batches.append((Q, T, V))
+    tab = S.table1_terms(S.wendland4())
+    want = [S.integrate_pairs(Q, 1.0, T, V, tab) for Q, T, V in batches]
+    shared = S.Context(0)
+    errors = []
+
+    def run(ctx_kind):
+        try:
+            for i, (Q, T, V) in enumerate(batches):
+                c = shared if ctx_kind == "shared" else None
+                got = S.integrate_pairs(Q, 1.0, T, V, tab, ctx=c)
+                if not np.array_equal(got, want[i]):
+                    errors.append((ctx_kind, i))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((ctx_kind, repr(e)))
+
+    for kind in ("per-thread", "shared"):
+        th = [threading.Thread(target=run, args=(kind,)) for _ in range(4)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    shared.close()
+    assert not errors, errors[:5]
