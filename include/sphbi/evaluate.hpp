@@ -29,6 +29,7 @@ inline std::vector<IntegralResult> evaluate(const std::vector<Point2>& particles
                                             EvaluateStats* stats = nullptr) {
   if (!(h > 0.0)) throw std::domain_error("integrate_triangle: support h must be > 0");
   sphbi_ctx* ctx = detail::device_context();
+  const detail::ScopedEdgeDecomposition decomposition(ctx);
   const sphbi_kernel_desc d = detail::kernel_desc(table);
   const std::size_t n = particles.size(), T = mesh.size();
   std::vector<double> pxy(2 * n), tri(6 * T), vals(3 * T, 1.0);
@@ -93,6 +94,7 @@ class BasisSweep {
       : n_(particles.size()), T_(mesh.size()) {
     if (!(h > 0.0)) throw std::domain_error("integrate_triangle_bases: support h must be > 0");
     sphbi_ctx* ctx = detail::device_context();
+    const detail::ScopedEdgeDecomposition decomposition(ctx);
     const sphbi_kernel_desc d = detail::kernel_desc(table);
     std::vector<double> pxy(2 * n_), tri(6 * T_);
     for (std::size_t i = 0; i < n_; ++i) {

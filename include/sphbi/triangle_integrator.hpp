@@ -170,8 +170,12 @@ struct ThreadContext {
   ThreadContext() {
     const char* env = std::getenv("SPHBI_DEVICE");
     created = sphbi_ctx_create(env ? std::atoi(env) : 0, &ctx);
-    if (created == SPHBI_OK)
+    if (created == SPHBI_OK) {
+      // the reference's own decomposition and all 19 route counters
+      // (BranchCounters, :158-178) for the drop-in single-pair API
       sphbi_ctx_enable_counters(ctx, 1);
+      sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_REFERENCE);
+    }
     else
       error = sphbi_last_error();
   }
@@ -187,6 +191,17 @@ inline sphbi_ctx* device_context() {
   if (tc.created != SPHBI_OK) throw std::runtime_error("sphbi: no B200 device context: " + tc.error);
   return tc.ctx;
 }
+
+// The batched scene entry points (sphbi::evaluate, BasisSweep) run the
+// product's edge-sum decomposition; the thread context stays on the
+// reference's route-faithful one for the single-pair API.
+struct ScopedEdgeDecomposition {
+  sphbi_ctx* ctx;
+  explicit ScopedEdgeDecomposition(sphbi_ctx* c) : ctx(c) { sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_EDGES); }
+  ~ScopedEdgeDecomposition() { sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_REFERENCE); }
+  ScopedEdgeDecomposition(const ScopedEdgeDecomposition&) = delete;
+  ScopedEdgeDecomposition& operator=(const ScopedEdgeDecomposition&) = delete;
+};
 
 inline void check(sphbi_status st) {
   if (st == SPHBI_OK) return;

@@ -31,6 +31,9 @@ ERR_INTERNAL = 9
 MEM_HOST = 0
 MEM_DEVICE = 1
 
+DECOMP_EDGES = 0
+DECOMP_REFERENCE = 1
+
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int64_p = ctypes.POINTER(ctypes.c_int64)
 c_uint32_p = ctypes.POINTER(ctypes.c_uint32)
@@ -64,6 +67,7 @@ EXPORTED_SYMBOLS = (
     "sphbi_ctx_set_stream",
     "sphbi_ctx_synchronize",
     "sphbi_ctx_enable_counters",
+    "sphbi_ctx_set_decomposition",
     "sphbi_read_counters",
     "sphbi_last_error",
     "sphbi_ctx_launch_count",
@@ -104,6 +108,7 @@ def load() -> ctypes.CDLL:
     lib.sphbi_ctx_set_stream.argtypes = [P, P]
     lib.sphbi_ctx_synchronize.argtypes = [P]
     lib.sphbi_ctx_enable_counters.argtypes = [P, ctypes.c_int]
+    lib.sphbi_ctx_set_decomposition.argtypes = [P, ctypes.c_int32]
     lib.sphbi_read_counters.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.sphbi_last_error.restype = ctypes.c_char_p
     lib.sphbi_ctx_launch_count.argtypes = [P]

@@ -1382,6 +1382,33 @@ SPHBI_HD bool integrate_normalized(Sink& c, const P2* v) {
   return true;
 }
 
+// Edge-sum decomposition (the scene path's default): the triangle clipped to
+// the unit support disc is the signed sum over its edges (a, b) of the
+// origin-anchored triangles (0, a, b) clipped to the disc, each of which is
+// exactly the reference's region_stub (:426-484: a direct cone + radial
+// window, or a split at the perpendicular foot; it clips at radius 1 for
+// vertices on either side of the circle). Mathematically the same integral as
+// the reference's vertex-count dispatch into wedges / t2 / t3 (:637-674), but
+// without the auxiliary points at distance 3 whose sectors and segments cancel
+// by O(1) per pair, and with at most six stub pieces instead of up to ~20
+// regions for a triangle with all vertices inside. The degenerate test is the
+// reference's (:640); the route counters of the reference's dispatch are not
+// bumped here (counting callers use integrate_normalized).
+template <class Sink>
+SPHBI_HD bool integrate_edges(Sink& c, const P2* v) {
+  const double area = signed_area(v[0], v[1], v[2]);
+  if (fabs(area) < kGeomEps) return false;
+  const double orient = area > 0.0 ? 1.0 : -1.0;
+#pragma unroll 1
+  for (int e = 0; e < 3; ++e) {
+    const P2 a = v[e], b = v[e == 2 ? 0 : e + 1];
+    const double cr = p_cross(a, b);
+    if (cr == 0.0) continue;  // origin on the edge line: zero-area origin triangle
+    stub_process(c, a, b, cr > 0.0 ? orient : -orient);
+  }
+  return true;
+}
+
 // Region-level entry points (test surface, triangle_integrator.hpp:335-632).
 template <class Sink>
 SPHBI_HD void region_segment(Sink& c, P2 t0, P2 t1, P2 keep, double sign) {

@@ -144,6 +144,9 @@ struct sphbi_ctx {
   // counters below are per-context state (recursive: entry points may nest).
   std::recursive_mutex mtx;
   int device = 0;
+  // geometry passes: edge-sum decomposition (default) or the reference's
+  // route-faithful dispatch (SPHBI_DECOMP_REFERENCE; sphbi_ctx_set_decomposition)
+  bool edges = true;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   unsigned long long* d_counters = nullptr;
@@ -359,6 +362,18 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
   dd* x[9] = {&a.v1, &a.v2, &a.v3, &a.g11, &a.g12, &a.g21, &a.g22, &a.g13, &a.g23};
 #pragma unroll
   for (int i = 0; i < 9; ++i) *x[i] = dd_add(*x[i], dd{o[2 * i], o[2 * i + 1]});
+}
+
+// The decomposition the geometry passes run (sphbi_ctx_set_decomposition):
+// the edge sum of clipped origin triangles (integrate_edges, default) or the
+// reference's vertex-count dispatch into wedges / t2 / t3 (integrate_normalized,
+// bit-faithful routes and route counters).
+template <bool EDGES, class Sink>
+__device__ __forceinline__ bool decompose(Sink& c, const P2* nv) {
+  if constexpr (EDGES)
+    return integrate_edges(c, nv);
+  else
+    return integrate_normalized(c, nv);
 }
 
 // Work-item kinds: 0 sector, 1..4 stub classes (stub_class), 5 segment.
@@ -661,6 +676,7 @@ __global__ void __launch_bounds__(256) k_sig_scatter(int64_t n, const unsigned s
   }
 }
 
+template <bool EDGES>
 __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const NormRec* __restrict__ nrec, int64_t n,
                                                     unsigned* __restrict__ cnt, unsigned char* __restrict__ cls,
                                                     unsigned long long* counters, unsigned* status_or,
@@ -680,7 +696,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const Norm
   for (int j = 0; j < kKinds; ++j) c.n[j] = 0u;
   c.status = 0u;
   c.counters = counters;
-  integrate_normalized(c, nv);
+  decompose<EDGES>(c, nv);
   for (int j = 0; j < kKinds; ++j) cnt[j * m + k] = c.n[j];
   // decomposition signature: pairs with equal signatures follow the same
   // control flow in the emit pass, which runs them in signature order
@@ -713,7 +729,7 @@ struct __align__(16) JRec {
   int pad[2];
 };
 
-template <class Src>
+template <bool EDGES, class Src>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
@@ -738,7 +754,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.stub2 = stub_items + stub_base.z + off[3 * m + k];
   e.stub3 = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
-  const bool nondeg_route = integrate_normalized(e, nv);
+  const bool nondeg_route = decompose<EDGES>(e, nv);
   rec[k] = PairRec{nondeg_route ? kRecRoute : 0, e.disc_n};
   if (e.status) atomicOr(status_or, e.status);
 }
@@ -881,6 +897,7 @@ struct SlotLists {
   long long stub_cap;  // kCapStub * n
 };
 
+template <bool EDGES>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit_slots(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
                       const int* __restrict__ order, PieceItem* __restrict__ sec_slots,
@@ -909,7 +926,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     e.cls_bits = 0u;
     e.nsec = e.nseg = e.nstub = 0;
     e.counters = counters;
-    const bool nondeg_route = integrate_normalized(e, nv);
+    const bool nondeg_route = decompose<EDGES>(e, nv);
     if (e.overflowed()) {
       // the call is redone with the two-pass pipeline (dflags[1] bit 2); keep
       // this pass in bounds
@@ -1926,7 +1943,10 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
   unsigned char* cls;
   if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
-  k_pipe_count<<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
+  if (c->edges)
+    k_pipe_count<true><<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
+  else
+    k_pipe_count<false><<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
   if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
@@ -1953,8 +1973,12 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
   if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
-  k_pipe_emit<<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder, stub_base,
-                                               dflags);
+  if (c->edges)
+    k_pipe_emit<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder,
+                                                       stub_base, dflags);
+  else
+    k_pipe_emit<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder,
+                                                        stub_base, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
   const DenseItems items{rec, off, m, stub_base};
   const WorkN wsec{(int64_t)n_sec, nullptr, 0}, wseg{(int64_t)n_seg, nullptr, 0};
@@ -2079,7 +2103,12 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if (c->timeline && c->tl_chunk >= 0 && c->tl_chunk < 64) cudaEventRecord(c->tl2[c->tl_chunk][j], s);
   };
   mark(0);
-  k_pipe_emit_slots<<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr, dflags);
+  if (c->edges)
+    k_pipe_emit_slots<true><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr,
+                                                             dflags);
+  else
+    k_pipe_emit_slots<false><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr,
+                                                              dflags);
   if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
   mark(1);
   const SlotItems items{jrec};
@@ -2439,6 +2468,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
       }
       if (!w.empty()) c->stream_ramp = w;
     }
+    if (const char* dm = std::getenv("SPHBI_DECOMP"); dm && std::strcmp(dm, "reference") == 0) c->edges = false;
     const char* sb = std::getenv("SPHBI_STREAM_BANKS");
     if (sb && *sb) c->stream_banks = std::max(1, std::min(static_cast<int>(sphbi_ctx::kBanks), std::atoi(sb)));
   }
@@ -2519,6 +2549,15 @@ sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* c, int enable) {
   SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
   c->counters_on = enable != 0;
+  return SPHBI_OK;
+}
+
+sphbi_status sphbi_ctx_set_decomposition(sphbi_ctx* c, int32_t mode) {
+  SPHBI_LOCK(c);
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (mode != SPHBI_DECOMP_EDGES && mode != SPHBI_DECOMP_REFERENCE)
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "unknown decomposition mode");
+  c->edges = mode == SPHBI_DECOMP_EDGES;
   return SPHBI_OK;
 }
 

@@ -308,6 +308,15 @@ class Context:
     def enable_counters(self, enable: bool = True):
         _raise(self.lib.sphbi_ctx_enable_counters(self.handle, 1 if enable else 0))
 
+    def set_decomposition(self, mode: str = "edges"):
+        """'edges' (default: signed edge sum of clipped origin triangles) or
+        'reference' (the reference's wedge / t2 / t3 dispatch with all 19 route
+        counters); include/sphbi_cuda.h sphbi_ctx_set_decomposition."""
+        code = {"edges": N.DECOMP_EDGES, "reference": N.DECOMP_REFERENCE}.get(mode)
+        if code is None:
+            raise InvalidArgument(f"unknown decomposition {mode!r}")
+        _raise(self.lib.sphbi_ctx_set_decomposition(self.handle, code))
+
     def read_counters(self, reset: bool = False) -> np.ndarray:
         out = (ctypes.c_uint64 * N.NUM_COUNTERS)()
         _raise(self.lib.sphbi_read_counters(self.handle, out, 1 if reset else 0))

@@ -164,7 +164,7 @@ struct KindCountSink {
   void segment(const Frame&, double, double) { ++n[5]; }
 };
 void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
-                        const double* tri6, double h, unsigned* mx, unsigned long long* sum) {
+                        const double* tri6, double h, unsigned* mx, unsigned long long* sum, int edges) {
   for (int64_t k = 0; k < npairs; ++k) {
     const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
     P2 v[3] = {{tri6[6 * t], tri6[6 * t + 1]}, {tri6[6 * t + 2], tri6[6 * t + 3]}, {tri6[6 * t + 4], tri6[6 * t + 5]}};
@@ -173,7 +173,7 @@ void core_host_kind_max(int64_t npairs, const int64_t* pp, const int64_t* pt, co
     P2 nv[3];
     for (int j = 0; j < 3; ++j) nv[j] = P2{(v[j].x - pxy[2 * i]) / h, (v[j].y - pxy[2 * i + 1]) / h};
     KindCountSink s{0u, {0, 0, 0, 0, 0, 0}};
-    integrate_normalized(s, nv);
+    if (edges) integrate_edges(s, nv); else integrate_normalized(s, nv);
     unsigned tot = 0;
     for (int j = 0; j < 6; ++j) {
       if (s.n[j] > mx[j]) mx[j] = s.n[j];
@@ -281,7 +281,7 @@ struct PipeEmuSink {
   void segment(const Frame& f, double d, double sign) { piece_segment(*K, acc, f, d, sign); }
 };
 int core_host_eval_pair_pipe(const double* coef, int ncoef, double c2, double qx, double qy, double h,
-                             const double* tri6, const double* vals3, int trig_angles, double* out4) {
+                             const double* tri6, const double* vals3, int trig_angles, double* out4, int edges) {
   KernelConsts K;
   if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
   P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
@@ -296,7 +296,7 @@ int core_host_eval_pair_pipe(const double* coef, int ncoef, double c2, double qx
   c.counters = nullptr;
   c.trig_angles = trig_angles != 0;
   c.disc_n = 0;
-  integrate_normalized(c, nv);
+  if (edges) integrate_edges(c, nv); else integrate_normalized(c, nv);
   PairAcc a;
   acc_zero(a);
   if (c.disc_n) piece_disc(K, a, static_cast<double>(c.disc_n));
@@ -316,6 +316,23 @@ int core_host_eval_pair_pipe(const double* coef, int ncoef, double c2, double qx
   combine_plane(a, tau1, tau2, tau3, raw);
   finalize(raw, K.c2, h, out4);
   return (int)c.status;
+}
+
+int core_host_eval_pairs_pipe(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
+                              const double* tri6, const double* vals3, const double* coef, int ncoef, double c2,
+                              double h, int nthreads, int edges, double* out4) {
+  auto work = [&](int tid) {
+    for (int64_t k = tid; k < npairs; k += nthreads) {
+      const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
+      core_host_eval_pair_pipe(coef, ncoef, c2, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, vals3 + 3 * t, 0,
+                               out4 + 4 * k, edges);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  return 0;
 }
 
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }

@@ -362,6 +362,7 @@ def test_branch_coverage_all_routes(S, ctx):
     suite's own configurations (test_triangle_integrator.cpp:704-727)."""
     c = S.Context(0)
     c.enable_counters(True)
+    c.set_decomposition("reference")  # the reference's routes (the default edge sum bumps stub routes only)
     c.read_counters(reset=True)
     tab = S.table1_terms(S.wendland4())
     ti = FROZEN["triangle_integrator"]
