@@ -193,11 +193,11 @@ inline sphbi_ctx* device_context() {
 }
 
 // The batched scene entry points (sphbi::evaluate, BasisSweep) run the
-// product's edge-sum decomposition; the thread context stays on the
+// product's default (hybrid) decomposition; the thread context stays on the
 // reference's route-faithful one for the single-pair API.
 struct ScopedEdgeDecomposition {
   sphbi_ctx* ctx;
-  explicit ScopedEdgeDecomposition(sphbi_ctx* c) : ctx(c) { sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_EDGES); }
+  explicit ScopedEdgeDecomposition(sphbi_ctx* c) : ctx(c) { sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_HYBRID); }
   ~ScopedEdgeDecomposition() { sphbi_ctx_set_decomposition(ctx, SPHBI_DECOMP_REFERENCE); }
   ScopedEdgeDecomposition(const ScopedEdgeDecomposition&) = delete;
   ScopedEdgeDecomposition& operator=(const ScopedEdgeDecomposition&) = delete;

@@ -101,19 +101,23 @@ sphbi_status sphbi_ctx_synchronize(sphbi_ctx* ctx);
 sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* ctx, int enable);
 sphbi_status sphbi_read_counters(sphbi_ctx* ctx, uint64_t out[SPHBI_NUM_COUNTERS], int reset);
 /* Decomposition of a pair into elementary regions used by the evaluation
- * kernels. Both give the same integral (to rounding; parity-tested):
- *   SPHBI_DECOMP_EDGES (default): the clipped triangle as the signed sum over
- *     its edges of clipped origin-anchored triangles (the reference's
- *     region_stub, triangle_integrator.hpp:426-484) -- fewer pieces, less
- *     cancellation; only the stub route counters are bumped.
+ * kernels. All give the same integral (to rounding; parity-tested):
+ *   SPHBI_DECOMP_HYBRID (default): the reference's single wedge for pairs with
+ *     at most one vertex inside the support, the edge sum for two or three.
+ *   SPHBI_DECOMP_EDGES: the clipped triangle as the signed sum over its edges
+ *     of clipped origin-anchored triangles (the reference's region_stub,
+ *     triangle_integrator.hpp:426-484).
  *   SPHBI_DECOMP_REFERENCE: the reference's own vertex-count dispatch into
  *     wedges / t2 / t3 (integrate_normalized, :637-674), bit-faithful branch
  *     routes and all 19 route counters (BranchCounters, :158-178). The C++
  *     drop-in headers select it for the single-pair API.
- * The environment variable SPHBI_DECOMP=reference sets it at context creation. */
+ * Route counters count the routes the selected decomposition takes. The
+ * environment variable SPHBI_DECOMP=reference|edges|hybrid sets the mode at
+ * context creation. */
 typedef enum sphbi_decomposition {
   SPHBI_DECOMP_EDGES = 0,
-  SPHBI_DECOMP_REFERENCE = 1
+  SPHBI_DECOMP_REFERENCE = 1,
+  SPHBI_DECOMP_HYBRID = 2
 } sphbi_decomposition;
 sphbi_status sphbi_ctx_set_decomposition(sphbi_ctx* ctx, int32_t mode);
 /* Message of the last failing call on this host thread. */

@@ -33,6 +33,7 @@ MEM_DEVICE = 1
 
 DECOMP_EDGES = 0
 DECOMP_REFERENCE = 1
+DECOMP_HYBRID = 2
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int64_p = ctypes.POINTER(ctypes.c_int64)

@@ -978,8 +978,10 @@ SPHBI_HD bool stub_window(double r1, double l, double D, double& lo, double& u) 
   return u > lo + kGeomEps;
 }
 
-// stub_integral validation (elementary_regions.hpp:179-183)
-SPHBI_HD bool stub_beta_ok(double beta) { return beta >= 0.0 && beta < kHalfPiHi; }
+// stub_integral validation (elementary_regions.hpp:179-183): beta < pi/2 in
+// the reference's long double (EvalReal, :333), i.e. beta <= the double
+// nearest pi/2 from below
+SPHBI_HD bool stub_beta_ok(double beta) { return beta >= 0.0 && beta <= kHalfPiHi; }
 
 // Direct stub: cone [0,gamma] x [0,l] plus the radial window (:440-475).
 template <class Sink>
@@ -1399,6 +1401,16 @@ SPHBI_HD bool integrate_edges(Sink& c, const P2* v) {
   const double area = signed_area(v[0], v[1], v[2]);
   if (fabs(area) < kGeomEps) return false;
   const double orient = area > 0.0 ? 1.0 : -1.0;
+  // no vertex inside the support and no edge through it: the reference's
+  // wedge gives exactly zero, or the exact full disc when the triangle
+  // encloses the support (:524-530); so does this, instead of three clipped
+  // sectors cancelling to rounding
+  if (p_norm(v[0]) > 1.0 + kOnCircleTol && p_norm(v[1]) > 1.0 + kOnCircleTol && p_norm(v[2]) > 1.0 + kOnCircleTol &&
+      segment_circle_crossings(v[0], v[1]).count == 0 && segment_circle_crossings(v[1], v[2]).count == 0 &&
+      segment_circle_crossings(v[2], v[0]).count == 0) {
+    if (point_in_triangle(P2{0.0, 0.0}, v[0], v[1], v[2])) c.disc(1.0);
+    return true;
+  }
 #pragma unroll 1
   for (int e = 0; e < 3; ++e) {
     const P2 a = v[e], b = v[e == 2 ? 0 : e + 1];
@@ -1406,6 +1418,44 @@ SPHBI_HD bool integrate_edges(Sink& c, const P2* v) {
     if (cr == 0.0) continue;  // origin on the edge line: zero-area origin triangle
     stub_process(c, a, b, cr > 0.0 ? orient : -orient);
   }
+  return true;
+}
+
+// Hybrid decomposition (the scene path's default): the reference's single
+// wedge for pairs with at most one vertex inside the support (a sector, <= 2
+// stubs, <= 1 segment: fewer and cheaper pieces than three clipped origin
+// triangles whose far vertices lie outside), the edge sum for two or three
+// vertices inside (where the reference's t2 / t3 route builds 8..20 regions
+// around auxiliary points). Same dispatch test as integrate_normalized (:644).
+template <class Sink>
+SPHBI_HD bool integrate_hybrid(Sink& c, const P2* v) {
+  const bool i0 = p_norm(v[0]) <= 1.0 + kOnCircleTol, i1 = p_norm(v[1]) <= 1.0 + kOnCircleTol,
+             i2 = p_norm(v[2]) <= 1.0 + kOnCircleTol;
+  const int inside_count = (i0 ? 1 : 0) + (i1 ? 1 : 0) + (i2 ? 1 : 0);
+  if (inside_count >= 2) return integrate_edges(c, v);
+  if (fabs(signed_area(v[0], v[1], v[2])) < kGeomEps) {
+    c.bump(kDispatchDegenerate);
+    return false;
+  }
+  int k0;
+  if (inside_count == 0) {
+    c.bump(kDispatchWedgeOutside);
+    const double r0 = p_norm(v[0]), r1 = p_norm(v[1]), r2 = p_norm(v[2]);
+    k0 = 0;
+    double rk = r0;
+    if (r1 < rk) {
+      k0 = 1;
+      rk = r1;
+    }
+    if (r2 < rk) k0 = 2;
+  } else {
+    c.bump(kDispatchWedgeSingle);
+    k0 = i0 ? 0 : (i1 ? 1 : 2);
+  }
+  const P2 a = k0 == 0 ? v[0] : (k0 == 1 ? v[1] : v[2]);
+  const P2 b = k0 == 0 ? v[1] : (k0 == 1 ? v[2] : v[0]);
+  const P2 cc = k0 == 0 ? v[2] : (k0 == 1 ? v[0] : v[1]);
+  wedge_body(c, a, b, cc, 1.0);
   return true;
 }
 

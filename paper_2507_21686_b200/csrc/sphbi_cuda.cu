@@ -144,9 +144,9 @@ struct sphbi_ctx {
   // counters below are per-context state (recursive: entry points may nest).
   std::recursive_mutex mtx;
   int device = 0;
-  // geometry passes: edge-sum decomposition (default) or the reference's
-  // route-faithful dispatch (SPHBI_DECOMP_REFERENCE; sphbi_ctx_set_decomposition)
-  bool edges = true;
+  // geometry passes: hybrid (default), edge sum, or the reference's
+  // route-faithful dispatch (sphbi_ctx_set_decomposition, SPHBI_DECOMP)
+  int decomp = SPHBI_DECOMP_HYBRID;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   unsigned long long* d_counters = nullptr;
@@ -368,13 +368,25 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
 // the edge sum of clipped origin triangles (integrate_edges, default) or the
 // reference's vertex-count dispatch into wedges / t2 / t3 (integrate_normalized,
 // bit-faithful routes and route counters).
-template <bool EDGES, class Sink>
+template <int DECOMP, class Sink>
 __device__ __forceinline__ bool decompose(Sink& c, const P2* nv) {
-  if constexpr (EDGES)
+  if constexpr (DECOMP == SPHBI_DECOMP_EDGES)
     return integrate_edges(c, nv);
+  else if constexpr (DECOMP == SPHBI_DECOMP_HYBRID)
+    return integrate_hybrid(c, nv);
   else
     return integrate_normalized(c, nv);
 }
+// launches a geometry kernel instantiated for the context's decomposition
+#define SPHBI_DECOMP_LAUNCH(c, KERNEL, GRID, BLOCK, STREAM, ...)                       \
+  do {                                                                                 \
+    if ((c)->decomp == SPHBI_DECOMP_HYBRID)                                            \
+      KERNEL<SPHBI_DECOMP_HYBRID><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);            \
+    else if ((c)->decomp == SPHBI_DECOMP_EDGES)                                        \
+      KERNEL<SPHBI_DECOMP_EDGES><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);             \
+    else                                                                               \
+      KERNEL<SPHBI_DECOMP_REFERENCE><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);         \
+  } while (0)
 
 // Work-item kinds: 0 sector, 1..4 stub classes (stub_class), 5 segment.
 constexpr int kKinds = 6;
@@ -676,7 +688,7 @@ __global__ void __launch_bounds__(256) k_sig_scatter(int64_t n, const unsigned s
   }
 }
 
-template <bool EDGES>
+template <int DECOMP>
 __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const NormRec* __restrict__ nrec, int64_t n,
                                                     unsigned* __restrict__ cnt, unsigned char* __restrict__ cls,
                                                     unsigned long long* counters, unsigned* status_or,
@@ -696,7 +708,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_COUNT) k_pipe_count(const Norm
   for (int j = 0; j < kKinds; ++j) c.n[j] = 0u;
   c.status = 0u;
   c.counters = counters;
-  decompose<EDGES>(c, nv);
+  decompose<DECOMP>(c, nv);
   for (int j = 0; j < kKinds; ++j) cnt[j * m + k] = c.n[j];
   // decomposition signature: pairs with equal signatures follow the same
   // control flow in the emit pass, which runs them in signature order
@@ -729,7 +741,7 @@ struct __align__(16) JRec {
   int pad[2];
 };
 
-template <bool EDGES, class Src>
+template <int DECOMP, class Src>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit(const __grid_constant__ KernelConsts K, Src src, const NormRec* __restrict__ nrec, int64_t n,
                 const unsigned long long* __restrict__ off, PieceItem* __restrict__ sector_items,
@@ -754,7 +766,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
   e.stub2 = stub_items + stub_base.z + off[3 * m + k];
   e.stub3 = stub_items + stub_base.w + off[4 * m + k];
   e.seg_items = seg_items + off[5 * m + k];
-  const bool nondeg_route = decompose<EDGES>(e, nv);
+  const bool nondeg_route = decompose<DECOMP>(e, nv);
   rec[k] = PairRec{nondeg_route ? kRecRoute : 0, e.disc_n};
   if (e.status) atomicOr(status_or, e.status);
 }
@@ -897,7 +909,7 @@ struct SlotLists {
   long long stub_cap;  // kCapStub * n
 };
 
-template <bool EDGES>
+template <int DECOMP>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     k_pipe_emit_slots(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
                       const int* __restrict__ order, PieceItem* __restrict__ sec_slots,
@@ -926,7 +938,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     e.cls_bits = 0u;
     e.nsec = e.nseg = e.nstub = 0;
     e.counters = counters;
-    const bool nondeg_route = decompose<EDGES>(e, nv);
+    const bool nondeg_route = decompose<DECOMP>(e, nv);
     if (e.overflowed()) {
       // the call is redone with the two-pass pipeline (dflags[1] bit 2); keep
       // this pass in bounds
@@ -1943,10 +1955,7 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
   if ((st = scratch_t(c, kBufPartial, n, &rec)) != SPHBI_OK) return st;
   unsigned char* cls;
   if ((st = scratch_t(c, kBufClass, 2 * m, &cls)) != SPHBI_OK) return st;
-  if (c->edges)
-    k_pipe_count<true><<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
-  else
-    k_pipe_count<false><<<grid_for(m, 128), 128, 0, s>>>(nrec, n, cnt, cls, ctr, dflags, porder);
+  SPHBI_DECOMP_LAUNCH(c, k_pipe_count, grid_for(m, 128), 128, s, nrec, n, cnt, cls, ctr, dflags, porder);
   if ((st = check_launch(c, "k_pipe_count")) != SPHBI_OK) return st;
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)m, s);
@@ -1973,12 +1982,15 @@ sphbi_status run_pipeline_dense(sphbi_ctx* c, const KernelConsts& K, double h, c
   if ((st = scratch_t(c, kBufItemsC, n_sec, &isec)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufItemsB, n_stub, &istub)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufItemsS, n_seg, &iseg)) != SPHBI_OK) return st;
-  if (c->edges)
-    k_pipe_emit<true><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder,
-                                                       stub_base, dflags);
+  if (c->decomp == SPHBI_DECOMP_HYBRID)
+    k_pipe_emit<SPHBI_DECOMP_HYBRID><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec,
+                                                                      porder, stub_base, dflags);
+  else if (c->decomp == SPHBI_DECOMP_EDGES)
+    k_pipe_emit<SPHBI_DECOMP_EDGES><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec,
+                                                                     porder, stub_base, dflags);
   else
-    k_pipe_emit<false><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg, rec, porder,
-                                                        stub_base, dflags);
+    k_pipe_emit<SPHBI_DECOMP_REFERENCE><<<grid_for(n, 128), 128, 0, s>>>(K, src, nrec, n, off, isec, istub, iseg,
+                                                                         rec, porder, stub_base, dflags);
   if ((st = check_launch(c, "k_pipe_emit")) != SPHBI_OK) return st;
   const DenseItems items{rec, off, m, stub_base};
   const WorkN wsec{(int64_t)n_sec, nullptr, 0}, wseg{(int64_t)n_seg, nullptr, 0};
@@ -2103,12 +2115,8 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if (c->timeline && c->tl_chunk >= 0 && c->tl_chunk < 64) cudaEventRecord(c->tl2[c->tl_chunk][j], s);
   };
   mark(0);
-  if (c->edges)
-    k_pipe_emit_slots<true><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr,
-                                                             dflags);
-  else
-    k_pipe_emit_slots<false><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg, jrec, L, ctr,
-                                                              dflags);
+  SPHBI_DECOMP_LAUNCH(c, k_pipe_emit_slots, grid_for(n, 128), 128, s, K, nrec, n, porder, isec, istub, iseg, jrec,
+                      L, ctr, dflags);
   if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
   mark(1);
   const SlotItems items{jrec};
@@ -2468,7 +2476,11 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
       }
       if (!w.empty()) c->stream_ramp = w;
     }
-    if (const char* dm = std::getenv("SPHBI_DECOMP"); dm && std::strcmp(dm, "reference") == 0) c->edges = false;
+    if (const char* dm = std::getenv("SPHBI_DECOMP"); dm && *dm) {
+      if (std::strcmp(dm, "reference") == 0) c->decomp = SPHBI_DECOMP_REFERENCE;
+      if (std::strcmp(dm, "edges") == 0) c->decomp = SPHBI_DECOMP_EDGES;
+      if (std::strcmp(dm, "hybrid") == 0) c->decomp = SPHBI_DECOMP_HYBRID;
+    }
     const char* sb = std::getenv("SPHBI_STREAM_BANKS");
     if (sb && *sb) c->stream_banks = std::max(1, std::min(static_cast<int>(sphbi_ctx::kBanks), std::atoi(sb)));
   }
@@ -2555,9 +2567,9 @@ sphbi_status sphbi_ctx_enable_counters(sphbi_ctx* c, int enable) {
 sphbi_status sphbi_ctx_set_decomposition(sphbi_ctx* c, int32_t mode) {
   SPHBI_LOCK(c);
   if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
-  if (mode != SPHBI_DECOMP_EDGES && mode != SPHBI_DECOMP_REFERENCE)
+  if (mode != SPHBI_DECOMP_EDGES && mode != SPHBI_DECOMP_REFERENCE && mode != SPHBI_DECOMP_HYBRID)
     return fail(SPHBI_ERR_INVALID_ARGUMENT, "unknown decomposition mode");
-  c->edges = mode == SPHBI_DECOMP_EDGES;
+  c->decomp = mode;
   return SPHBI_OK;
 }
 

@@ -308,11 +308,12 @@ class Context:
     def enable_counters(self, enable: bool = True):
         _raise(self.lib.sphbi_ctx_enable_counters(self.handle, 1 if enable else 0))
 
-    def set_decomposition(self, mode: str = "edges"):
-        """'edges' (default: signed edge sum of clipped origin triangles) or
-        'reference' (the reference's wedge / t2 / t3 dispatch with all 19 route
-        counters); include/sphbi_cuda.h sphbi_ctx_set_decomposition."""
-        code = {"edges": N.DECOMP_EDGES, "reference": N.DECOMP_REFERENCE}.get(mode)
+    def set_decomposition(self, mode: str = "hybrid"):
+        """'hybrid' (default: the reference's wedge for <= 1 vertex inside the
+        support, the signed edge sum of clipped origin triangles for 2 or 3),
+        'edges' or 'reference' (the reference's wedge / t2 / t3 dispatch with
+        all 19 route counters); include/sphbi_cuda.h sphbi_ctx_set_decomposition."""
+        code = {"edges": N.DECOMP_EDGES, "reference": N.DECOMP_REFERENCE, "hybrid": N.DECOMP_HYBRID}.get(mode)
         if code is None:
             raise InvalidArgument(f"unknown decomposition {mode!r}")
         _raise(self.lib.sphbi_ctx_set_decomposition(self.handle, code))

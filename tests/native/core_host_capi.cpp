@@ -335,6 +335,27 @@ int core_host_eval_pairs_pipe(int64_t npairs, const int64_t* pp, const int64_t* 
   return 0;
 }
 
+// per pair: inside count and the piece counts by kind under one decomposition
+void core_host_kind_counts(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
+                           const double* tri6, double h, int edges, int* out7) {
+  for (int64_t k = 0; k < npairs; ++k) {
+    const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
+    P2 v[3] = {{tri6[6 * t], tri6[6 * t + 1]}, {tri6[6 * t + 2], tri6[6 * t + 3]}, {tri6[6 * t + 4], tri6[6 * t + 5]}};
+    int perm[3];
+    canonicalize(v, perm);
+    P2 nv[3];
+    int inside = 0;
+    for (int j = 0; j < 3; ++j) {
+      nv[j] = P2{(v[j].x - pxy[2 * i]) / h, (v[j].y - pxy[2 * i + 1]) / h};
+      inside += p_norm(nv[j]) <= 1.0 + kOnCircleTol ? 1 : 0;
+    }
+    KindCountSink s{0u, {0, 0, 0, 0, 0, 0}};
+    if (edges) integrate_edges(s, nv); else integrate_normalized(s, nv);
+    out7[7 * k] = inside;
+    for (int j = 0; j < 6; ++j) out7[7 * k + 1 + j] = static_cast<int>(s.n[j]);
+  }
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 // region-level evaluation with the device core (sphbi_integrate_regions' math, host build)
