@@ -311,6 +311,61 @@ def fp64_roofline(workload, pairs, k4_ms, fp64_peak):
     return roof
 
 
+def secondary_configs(ctx, names):
+    """The other BASELINE.json configs measured in the same run (N = 1, rank
+    0): device pair-evals/s through sphbi_evaluate with device-resident inputs
+    (pair finding + evaluation + reduction, best of 3 after a warm-up), and
+    the reference CPU path on a bounded seeded pair sample of the same scene
+    (cfg4: the extended oracle; the reference has no P3 path)."""
+    sys.path.insert(0, str(ROOT / "tools"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import bench_configs as BC
+    import oracle_lib as OL
+    from paper_2507_21686_b200 import scenes
+
+    out = {}
+    for name in names:
+        t0 = time.perf_counter()
+        repeat, pairs, note = 1, None, ""
+        if name == "cfg1":
+            sc = scenes.cfg1()
+            repeat = 200
+            note = "single triangle, 4,096 particles: latency-bound, mean of 200 back-to-back calls"
+        elif name == "cfg2a":
+            sc = scenes.cfg2()
+            pairs = sc.pairs
+            note = "own-triangle pairs (mode A, explicit pair list)"
+        elif name == "cfg2b":
+            sc = scenes.subsample(scenes.cfg2(), 16384, seed=2)
+            sc.pairs = None
+            note = "full cell-list pairing (mode B, ~12.5k pairs per particle) on a seeded 16,384-particle subsample"
+        elif name == "cfg3":
+            sc = scenes.cfg3()
+            note = "1M particles, boundary strip: pair finding dominates"
+        else:
+            sc = scenes.cfg4()
+            note = "4M particles, P3 (cubic) field, degree-12 kernel"
+        k = sc.kernels[0]
+        r = BC.run_device(ctx, sc, k, sc.h, 3, pairs=pairs, repeat=repeat)
+        dev_ms = r["ms_pairs"] + r["ms_eval"] + r["ms_reduce"]
+        row = {"pairs": r["pairs"], "ms_device": dev_ms, "ms_pair_finding": r["ms_pairs"],
+               "value": r["pairs"] / (dev_ms * 1e-3), "unit": UNIT, "kernel": k.name, "h": sc.h,
+               "particles": int(sc.particles.shape[0]), "triangles": int(sc.triangles.shape[0]), "note": note}
+        if name in ("cfg3", "cfg4"):
+            row["pair_finding_GBps_algorithmic"] = 28.0 * sc.particles.shape[0] / (r["ms_pairs"] * 1e-3) / 1e9
+        if pairs is None:
+            idx = np.sort(np.random.default_rng(11).choice(sc.particles.shape[0], min(65536, sc.particles.shape[0]),
+                                                           replace=False))
+            pr = OL.cpu_pairs_grid(OL.oracle(), np.ascontiguousarray(sc.particles[idx]), sc.triangles, sc.h)
+            pairs = (idx[pr[:, 0]], pr[:, 1])
+        if pairs[0].shape[0]:
+            row["cpu_baseline"] = BC.cpu_rate(sc, k, sc.h, pairs, 8192 if name in ("cfg4", "cfg2b") else 32768)
+            row["gpu_over_cpu"] = row["value"] / row["cpu_baseline"]["value"]
+        row["wall_s"] = time.perf_counter() - t0
+        out[name] = row
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -321,6 +376,8 @@ def main():
     ap.add_argument("--balance", default="pairs", choices=["pairs", "count"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--configs", default="cfg1,cfg2a,cfg2b,cfg3,cfg4",
+                    help="secondary BASELINE.json configs measured in the same run at N = 1 ('' for none)")
     args = ap.parse_args()
     if args.impl == "ours":
         args.warmup = max(args.warmup, 3)
@@ -528,6 +585,9 @@ def main():
                    **host_info()}
 
     clocks = sampler.summary()
+    others = None
+    if rank == 0 and world == 1 and args.configs and args.workload == "cfg5":
+        others = secondary_configs(ctx, [c for c in args.configs.split(",") if c])
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -546,6 +606,8 @@ def main():
         }
         if balance_ms is not None:
             line["setup_ms"] = {"shard_cut": balance_ms, "count_pass": S.count_ms}
+        if others:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:

@@ -819,8 +819,14 @@ SPHBI_HD void piece_stub3(const KernelConsts& K, PairAcc3& acc, const Frame& f, 
   }
   if (CLS != 3 || window) {
     const double sb = T.sb, cb = T.cb;
-    stub_bound_sums3<(CLS == 0 || CLS == 2) ? 1 : 0>(K, u, D, beta, cb, sb, S, 1.0);
-    stub_bound_sums3<(CLS == 0 || CLS == 1) ? 2 : 0>(K, lo, D, beta, cb, sb, S, -1.0);
+    // both bounds through one copy of the bound code, run twice: the
+    // kernel's size, not its FP64 work, limited it (instruction-fetch
+    // stalls). x == 1 (far bound on the circle) and x == D (snapped right
+    // limit) are recognised at run time -- warp-uniform within a window
+    // class -- with the same operations and results as the compile-time
+    // specialisations.
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) stub_bound_sums3<0>(K, b == 0 ? u : lo, D, beta, cb, sb, S, b == 0 ? 1.0 : -1.0);
   }
   acc3_add_region(acc, S, f, sign);
 }

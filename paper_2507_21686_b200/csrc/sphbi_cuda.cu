@@ -70,7 +70,7 @@ constexpr int kEvalBlock = 128;
 #define SPHBI_MINB_COUNT 5
 #endif
 #ifndef SPHBI_MINB_EMIT
-#define SPHBI_MINB_EMIT 5
+#define SPHBI_MINB_EMIT 6
 #endif
 #ifndef SPHBI_MINB_P3
 #define SPHBI_MINB_P3 4
@@ -3153,11 +3153,36 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
                                                         0, gpp, gpt, dactive_n);
       if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
     }
-    // K4 + K5 in chunks of whole particles
+    // K4 + K5 in chunks of whole particles. Several chunks (cfg5: ~40): they
+    // alternate between the context's compute streams, each with its own
+    // scratch bank, so one chunk's latency-bound geometry pass and kernel
+    // tails overlap the next chunk's FP64-bound piece kernels (the e2e
+    // streamed path does the same, evaluate_streamed).
+    const int nbanks = (!cb.empty() && !bc && !pieces && !pair_list_out)
+                           ? std::max(1, std::min(c->stream_banks, static_cast<int>(sphbi_ctx::kBanks)))
+                           : 1;
+    cudaStream_t cs2[sphbi_ctx::kBanks] = {s, c->aux[0], c->aux[1]};
+    struct RestoreBank {
+      sphbi_ctx* c;
+      cudaStream_t s;
+      ~RestoreBank() {
+        c->stream = s;
+        c->bank = 0;
+      }
+    } restore_bank{c, s};
+    if (nbanks > 1) {
+      if (timing) cudaEventRecord(c->ev[1], s);
+      SPHBI_CUDA_TRY(cudaEventRecord(c->ev[6], s));  // fork: the pair list is complete on s
+      for (int b = 1; b < nbanks; ++b) SPHBI_CUDA_TRY(cudaStreamWaitEvent(cs2[b], c->ev[6], 0));
+    }
     int p0 = 0;
     int64_t written = 0;
     size_t chunk = 0;
     while (p0 < np) {
+      const int q = static_cast<int>(chunk % static_cast<size_t>(nbanks));
+      c->stream = cs2[q];
+      c->bank = q;
+      cudaStream_t s = cs2[q];  // this chunk's stream (shadows the call's stream)
       // chunk [p0, p1): off[p1] - off[p0] <= budget (at least one particle)
       unsigned long long base = 0;
       int p1 = np;
@@ -3200,9 +3225,9 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           }
           written += cnt;
         }
-        if (timing && p0 == 0) cudaEventRecord(c->ev[1], s);
+        if (timing && p0 == 0 && nbanks == 1) cudaEventRecord(c->ev[1], s);
         if ((st = eval_chunk(pp, pt, cnt, pout, dflags, ctr, static_cast<int64_t>(base))) != SPHBI_OK) return st;
-        if (timing && p1 >= np) cudaEventRecord(c->ev[2], s);
+        if (timing && p1 >= np && nbanks == 1) cudaEventRecord(c->ev[2], s);
         if (bc) {
           p0 = p1;
           continue;
@@ -3214,6 +3239,15 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
         if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
       }
       p0 = p1;
+    }
+    c->stream = s;
+    c->bank = 0;
+    if (nbanks > 1) {  // join; ms_eval then spans evaluation and reduction of all chunks
+      for (int b = 1; b < nbanks; ++b) {
+        SPHBI_CUDA_TRY(cudaEventRecord(c->ev[7], cs2[b]));
+        SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->ev[7], 0));
+      }
+      if (timing) cudaEventRecord(c->ev[2], s);
     }
     if (timing) cudaEventRecord(c->ev[3], s);
     (void)candidates;
