@@ -244,7 +244,7 @@ def run_reference(args, rank, world):
     pairs_done = 0
     kind = "reference"
     if args.workload == "cfg5":
-        per_step = 4096  # particles per step: ~45k pairs, ~1 s on 16 cores
+        per_step = 16384  # particles per step: ~180k pairs, ~3 s on 16 cores
         for s in range(args.warmup + args.steps):
             idx = np.sort(rng.choice(sc.particles.shape[0], per_step, replace=False))
             P = sc.particles[idx]
@@ -354,7 +354,8 @@ def secondary_configs(ctx, names):
         if name in ("cfg3", "cfg4"):
             row["pair_finding_GBps_algorithmic"] = 28.0 * sc.particles.shape[0] / (r["ms_pairs"] * 1e-3) / 1e9
         if pairs is None:
-            idx = np.sort(np.random.default_rng(11).choice(sc.particles.shape[0], min(65536, sc.particles.shape[0]),
+            m = 256 if name == "cfg2b" else 65536  # cfg2b: ~12.5k pairs per particle
+            idx = np.sort(np.random.default_rng(11).choice(sc.particles.shape[0], min(m, sc.particles.shape[0]),
                                                            replace=False))
             pr = OL.cpu_pairs_grid(OL.oracle(), np.ascontiguousarray(sc.particles[idx]), sc.triangles, sc.h)
             pairs = (idx[pr[:, 0]], pr[:, 1])
