@@ -1433,12 +1433,20 @@ SPHBI_HD bool integrate_edges(Sink& c, const P2* v) {
 // triangles whose far vertices lie outside), the edge sum for two or three
 // vertices inside (where the reference's t2 / t3 route builds 8..20 regions
 // around auxiliary points). Same dispatch test as integrate_normalized (:644).
+// the inside test of the reference's dispatch (:644), shared by the hybrid
+// router and the signature of the geometry pass (k_pre_class), which groups
+// the pairs so that each group's emit launch runs only its own route
+SPHBI_HD int inside_count_of(const P2* v) {
+  return (p_norm(v[0]) <= 1.0 + kOnCircleTol ? 1 : 0) + (p_norm(v[1]) <= 1.0 + kOnCircleTol ? 1 : 0) +
+         (p_norm(v[2]) <= 1.0 + kOnCircleTol ? 1 : 0);
+}
+// The reference's single-wedge dispatch (:637-660) for pairs with at most one
+// vertex inside the support.
 template <class Sink>
-SPHBI_HD bool integrate_hybrid(Sink& c, const P2* v) {
+SPHBI_HD bool integrate_single_wedge(Sink& c, const P2* v) {
   const bool i0 = p_norm(v[0]) <= 1.0 + kOnCircleTol, i1 = p_norm(v[1]) <= 1.0 + kOnCircleTol,
              i2 = p_norm(v[2]) <= 1.0 + kOnCircleTol;
   const int inside_count = (i0 ? 1 : 0) + (i1 ? 1 : 0) + (i2 ? 1 : 0);
-  if (inside_count >= 2) return integrate_edges(c, v);
   if (fabs(signed_area(v[0], v[1], v[2])) < kGeomEps) {
     c.bump(kDispatchDegenerate);
     return false;
@@ -1463,6 +1471,11 @@ SPHBI_HD bool integrate_hybrid(Sink& c, const P2* v) {
   const P2 cc = k0 == 0 ? v[2] : (k0 == 1 ? v[0] : v[1]);
   wedge_body(c, a, b, cc, 1.0);
   return true;
+}
+template <class Sink>
+SPHBI_HD bool integrate_hybrid(Sink& c, const P2* v) {
+  if (inside_count_of(v) >= 2) return integrate_edges(c, v);
+  return integrate_single_wedge(c, v);
 }
 
 // Region-level entry points (test surface, triangle_integrator.hpp:335-632).

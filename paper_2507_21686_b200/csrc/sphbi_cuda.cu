@@ -72,6 +72,9 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_EMIT
 #define SPHBI_MINB_EMIT 6
 #endif
+#ifndef SPHBI_MINB_EMIT_WEDGE
+#define SPHBI_MINB_EMIT_WEDGE 5
+#endif
 #ifndef SPHBI_MINB_P3
 #define SPHBI_MINB_P3 4
 #endif
@@ -368,12 +371,17 @@ __device__ __forceinline__ void acc_add_out(PairAcc& a, const double* o) {
 // the edge sum of clipped origin triangles (integrate_edges, default) or the
 // reference's vertex-count dispatch into wedges / t2 / t3 (integrate_normalized,
 // bit-faithful routes and route counters).
+// kDecompWedgeGroup: the hybrid's <= 1-inside group alone (its own emit
+// launch over the pairs the signature sort put first)
+constexpr int kDecompWedgeGroup = 16;
 template <int DECOMP, class Sink>
 __device__ __forceinline__ bool decompose(Sink& c, const P2* nv) {
   if constexpr (DECOMP == SPHBI_DECOMP_EDGES)
     return integrate_edges(c, nv);
   else if constexpr (DECOMP == SPHBI_DECOMP_HYBRID)
     return integrate_hybrid(c, nv);
+  else if constexpr (DECOMP == kDecompWedgeGroup)
+    return integrate_single_wedge(c, nv);
   else
     return integrate_normalized(c, nv);
 }
@@ -579,7 +587,8 @@ __device__ __forceinline__ int crossing_count_key(P2 p, P2 q) {
 }
 
 // Signature bins: 3 inside bits + 3 x 2 crossing-count bits + particle on a
-// vertex + particle on an edge line (those take the degenerate branches).
+// vertex or an edge line (the degenerate branches) + the hybrid group (>= 2
+// vertices inside: edge sum), the most significant bit.
 constexpr int kSigBins = 2048;
 
 // Block-level signature histogram, added to the global one (one atomic per
@@ -617,6 +626,7 @@ __global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h,
       nrec[k] = r;
     }
     bool on_vertex = false, on_edge = false;
+    const bool group1 = inside_count_of(nv) >= 2;  // the hybrid's edge-sum group (bit 10, sorts last)
     for (int i = 0; i < 3; ++i) {
       const double r2 = p_norm2(nv[i]);
       if (r2 <= 1.0) kk |= 1u << i;
@@ -626,8 +636,8 @@ __global__ void __launch_bounds__(256) k_pre_class(Src src, int64_t n, double h,
       on_edge |= cr * cr < 1e-18 * e2;
       kk |= static_cast<unsigned>(crossing_count_key(a, b)) << (3 + 2 * i);
     }
-    kk |= (on_vertex ? 1u : 0u) << 9;
-    kk |= (on_edge ? 1u : 0u) << 10;
+    kk |= (on_vertex || on_edge ? 1u : 0u) << 9;
+    kk |= (group1 ? 1u : 0u) << 10;
     key[k] = static_cast<unsigned short>(kk);
   }
   sig_hist_add(sh, kk, k < n, hist);  // the whole block reaches its barriers
@@ -656,6 +666,7 @@ __global__ void __launch_bounds__(kSigScanThreads) k_sig_offsets(const unsigned*
   unsigned run = sh[t] - tot;
 #pragma unroll
   for (int q = 0; q < kSigPerThread; ++q) {
+    if (t * kSigPerThread + q == kSigBins / 2) cursor[kSigBins] = run;  // first pair of group 1
     cursor[t * kSigPerThread + q] = run;
     run += loc[q];
   }
@@ -910,17 +921,23 @@ struct SlotLists {
 };
 
 template <int DECOMP>
-__global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
+__global__ void __launch_bounds__(128, DECOMP == 16 ? SPHBI_MINB_EMIT_WEDGE : SPHBI_MINB_EMIT)
     k_pipe_emit_slots(const __grid_constant__ KernelConsts K, const NormRec* __restrict__ nrec, int64_t n,
                       const int* __restrict__ order, PieceItem* __restrict__ sec_slots,
                       StubItem* __restrict__ stub_slots, PieceItem* __restrict__ seg_slots,
-                      JRec* __restrict__ jrec, SlotLists L, unsigned long long* counters, unsigned* status_or) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+                      JRec* __restrict__ jrec, SlotLists L, unsigned long long* counters, unsigned* status_or,
+                      const unsigned* __restrict__ split = nullptr, int part = 0) {
+  // split (hybrid groups): part 0 emits positions [0, *split), part 1 [*split, n)
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t jb = split && part == 1 ? static_cast<int64_t>(*split) : 0;
+  const int64_t je = split && part == 0 ? static_cast<int64_t>(*split) : n;
+  const int64_t j = jb + j0;
+  if (jb + static_cast<int64_t>(blockIdx.x) * blockDim.x >= je) return;  // whole block beyond the range
   int64_t k = 0;
   int my[kKinds] = {0, 0, 0, 0, 0, 0};
   unsigned cls_bits = 0u;
   int flags = 0, disc_n = 0;
-  if (j < n) {
+  if (j < je) {
     k = order ? order[j] : j;
     P2 nv[3];
     int perm[3];
@@ -979,7 +996,7 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EMIT)
     // classes 1 and 3 (kinds 2, 4) fill their buffers from the back
     pos[q] = (q == 2 || q == 4) ? static_cast<unsigned>(L.stub_cap) - base - total + (x - v) : base + x - v;
   }
-  if (j >= n) return;
+  if (j >= je) return;
   {
     JRec r;
     r.k = static_cast<int>(k);
@@ -1709,23 +1726,83 @@ __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy
 
 // Count (fill == 0) or emit (fill == 1) the pairs of a set of particles.
 // A warp takes 32 particles -- 32 consecutive entries of `order` (particles
-// sorted by cell: neighbouring warps read the same cell lists and triangles
-// from L1/L2) or, with order == NULL, the index range p0 + [32w, 32w + 32).
-// Particles with an empty cell list are done at once; the warp then walks
-// each remaining particle's list with all 32 lanes, 32 candidates at a time
-// (cfg2 mode B: ~15k candidates per particle; cfg3/cfg5: tens). Hits are
-// compacted with a ballot in lane order, so a particle's pairs come out in
-// ascending triangle id (stably sorted cell lists) -- the CPU finder's list.
+// sorted by cell: neighbouring lanes share cell lists, so their candidate
+// loads coalesce / hit L1) or, with order == NULL, the index range
+// p0 + [32w, 32w + 32). Two regimes, chosen per particle by its cell list's
+// length:
+//  * short lists (<= kFindLaneMax candidates; cfg3/cfg5: tens): every lane
+//    walks its own particle's list, in list order, 32 particles at once --
+//    no shuffles or ballots, the exact-predicate evaluations of consecutive
+//    candidates are independent (instruction-level parallelism);
+//  * long lists (cfg2 mode B: ~15k candidates per particle): the warp walks
+//    each remaining particle's list with all 32 lanes, 32 candidates at a
+//    time, and compacts the hits with a ballot in lane order.
+// Either way a particle's pairs come out in ascending triangle id (stably
+// sorted cell lists) -- the CPU finder's list.
 constexpr int kFindBlock = 256;
+constexpr unsigned long long kFindLaneMax = 96;
+__device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
+  const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
+  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  tv[0] = a.x;
+  tv[1] = a.y;
+  tv[2] = b.x;
+  tv[3] = b.y;
+  tv[4] = c.x;
+  tv[5] = c.y;
+}
+// one particle's candidate list [qb, qe) walked by the whole warp (32
+// candidates at a time, hits compacted in lane order); returns the hit count
+__device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, double qy, unsigned long long qb,
+                                                        unsigned long long qe, unsigned long long qo, int qi,
+                                                        const int* __restrict__ cell_tris,
+                                                        const double* __restrict__ tri, double h2, int fill,
+                                                        int* __restrict__ pp, int* __restrict__ pt) {
+  unsigned long long n = 0;
+  for (unsigned long long k0 = qb; k0 < qe; k0 += 32) {
+    const unsigned long long k = k0 + lane;
+    bool hit = false;
+    int t = 0;
+    if (k < qe) {
+      t = __ldg(cell_tris + k);
+      double tv[6];
+      load_tri6(tri, t, tv);
+      hit = pair_dist2(qx, qy, tv) < h2;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (fill && hit) {
+      const unsigned long long q = qo + n + __popc(m & ((1u << lane) - 1u));
+      pp[q] = qi;
+      pt[q] = t;
+    }
+    n += __popc(m);
+  }
+  return n;
+}
+
 __global__ void __launch_bounds__(kFindBlock)
     k_find_pairs(int64_t count, const int* __restrict__ order, int p0, const double* __restrict__ pxy,
                  const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
                  const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
                  unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
-                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr) {
+                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0) {
   const int lane = threadIdx.x & 31;
   const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (dcount) count = *dcount;  // device-side list length (sparse path)
+  if (warp_per_particle) {
+    // scenes with long cell lists (cfg2 mode B: ~15k candidates per particle):
+    // one warp per particle, so a small particle set still fills the GPU
+    const int64_t w = pos >> 5;
+    if (w >= count) return;
+    const int i = order ? order[w] : p0 + static_cast<int>(w);
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    const unsigned c = pcell[i];
+    const unsigned long long b = cell_start[c], e = cell_start[c + 1];
+    const unsigned long long o = fill ? count_or_offset[i] - base : 0;
+    const unsigned long long n = walk_warp(lane, p.x, p.y, b, e, o, i, cell_tris, tri, h2, fill, pp, pt);
+    if (!fill && lane == 0) count_or_offset[i] = n;
+    return;
+  }
   if ((pos & ~31ll) >= count) return;  // whole warps
   const bool valid = pos < count;
   int i = 0;
@@ -1740,9 +1817,26 @@ __global__ void __launch_bounds__(kFindBlock)
     b = cell_start[c];
     e = cell_start[c + 1];
     if (fill) o = count_or_offset[i] - base;
-    else if (e == b) count_or_offset[i] = 0;
   }
-  unsigned todo = __ballot_sync(0xffffffffu, valid && e > b);
+  // short lists: one lane per particle
+  if (valid && e - b <= kFindLaneMax) {
+    unsigned long long n = 0;
+    for (unsigned long long k = b; k < e; ++k) {
+      const int t = __ldg(cell_tris + k);
+      double tv[6];
+      load_tri6(tri, t, tv);
+      if (pair_dist2(px, py, tv) < h2) {
+        if (fill) {
+          pp[o + n] = i;
+          pt[o + n] = t;
+        }
+        ++n;
+      }
+    }
+    if (!fill) count_or_offset[i] = n;
+  }
+  // long lists: the whole warp per particle
+  unsigned todo = __ballot_sync(0xffffffffu, valid && e - b > kFindLaneMax);
   while (todo) {
     const int src = __ffs(todo) - 1;
     todo &= todo - 1;
@@ -1750,30 +1844,7 @@ __global__ void __launch_bounds__(kFindBlock)
     const unsigned long long qb = __shfl_sync(0xffffffffu, b, src), qe = __shfl_sync(0xffffffffu, e, src);
     unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
     const int qi = __shfl_sync(0xffffffffu, i, src);
-    unsigned long long n = 0;
-    for (unsigned long long k0 = qb; k0 < qe; k0 += 32) {
-      const unsigned long long k = k0 + lane;
-      bool hit = false;
-      int t = 0;
-      if (k < qe) {
-        t = __ldg(cell_tris + k);
-        double tv[6];
-#pragma unroll
-        for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * (int64_t)t + j);
-        hit = pair_dist2(qx, qy, tv) < h2;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (fill) {
-        if (hit) {
-          const unsigned long long q = qo + __popc(m & ((1u << lane) - 1u));
-          pp[q] = qi;
-          pt[q] = t;
-        }
-        qo += __popc(m);
-      } else {
-        n += __popc(m);
-      }
-    }
+    const unsigned long long n = walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, fill, pp, pt);
     if (!fill && lane == src) count_or_offset[qi] = n;
   }
 }
@@ -1908,6 +1979,12 @@ int rgrid(sphbi_ctx* c, F* fn) {
 
 // Canonical normalized vertices (NormRec) + pre-classification key, pairs
 // sorted by key (shared by both pipelines).
+// the current bank's signature histogram / cursors (pre_classify); the word
+// after the cursors holds the first position of the hybrid's group 1
+unsigned* hist_cursor_of(sphbi_ctx* c) {
+  return static_cast<unsigned*>(c->buf[kBufOrder + c->bank * kNumBufs]) + kSigBins;
+}
+
 template <class Src>
 sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, NormRec** nrec_out,
                           int** porder_out) {
@@ -1919,7 +1996,7 @@ sphbi_status pre_classify(sphbi_ctx* c, double h, const Src& src, int64_t n, Nor
   if ((st = scratch_t(c, kBufPreKey, m, &pk)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufPreOrder, m, porder_out)) != SPHBI_OK) return st;
   if ((st = scratch_t(c, kBufNormRec, n, nrec_out)) != SPHBI_OK) return st;
-  if ((st = scratch_t(c, kBufOrder, 2 * kSigBins, &hist)) != SPHBI_OK) return st;
+  if ((st = scratch_t(c, kBufOrder, 2 * kSigBins + 4, &hist)) != SPHBI_OK) return st;
   SPHBI_CUDA_TRY(zero_async(c, hist, sizeof(unsigned) * kSigBins, s));
   k_pre_class<<<grid_for(n, 256), 256, 0, s>>>(src, n, h, pk, *nrec_out, hist);
   if ((st = check_launch(c, "k_pre_class")) != SPHBI_OK) return st;
@@ -2115,8 +2192,20 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
     if (c->timeline && c->tl_chunk >= 0 && c->tl_chunk < 64) cudaEventRecord(c->tl2[c->tl_chunk][j], s);
   };
   mark(0);
-  SPHBI_DECOMP_LAUNCH(c, k_pipe_emit_slots, grid_for(n, 128), 128, s, K, nrec, n, porder, isec, istub, iseg, jrec,
-                      L, ctr, dflags);
+  if (c->decomp == SPHBI_DECOMP_HYBRID && porder) {
+    // two lean launches over the signature-sorted pairs: the <= 1-inside group
+    // (reference wedge) first, then the edge-sum group; the split position is
+    // the group boundary k_sig_offsets recorded (no host round trip)
+    const unsigned* split = hist_cursor_of(c) + kSigBins;
+    k_pipe_emit_slots<kDecompWedgeGroup><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg,
+                                                                        jrec, L, ctr, dflags, split, 0);
+    if ((st = check_launch(c, "k_pipe_emit_slots(wedge group)")) != SPHBI_OK) return st;
+    k_pipe_emit_slots<SPHBI_DECOMP_EDGES><<<grid_for(n, 128), 128, 0, s>>>(K, nrec, n, porder, isec, istub, iseg,
+                                                                         jrec, L, ctr, dflags, split, 1);
+  } else {
+    SPHBI_DECOMP_LAUNCH(c, k_pipe_emit_slots, grid_for(n, 128), 128, s, K, nrec, n, porder, isec, istub, iseg, jrec,
+                        L, ctr, dflags);
+  }
   if ((st = check_launch(c, "k_pipe_emit_slots")) != SPHBI_OK) return st;
   mark(1);
   const SlotItems items{jrec};
@@ -3084,11 +3173,15 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
     }
     }
-    // K3: count, scan
+    // K3: count, scan. Long cell lists (mean entries per cell > 512, e.g. cfg2
+    // mode B) are walked one warp per particle, short ones one lane per particle.
     const double h2 = h * h;
     const int np = static_cast<int>(n_particles);
-    k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount,
-                                                      0, nullptr, nullptr, dactive_n);
+    const int wpp = !sparse && n_entries > 512ull * static_cast<unsigned long long>(ncells) ? 1 : 0;
+    const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
+                          : find_grid(np);
+    k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
+                                              nullptr, nullptr, dactive_n, wpp);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
@@ -3149,8 +3242,8 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if (resident && total_pairs > 0) {
       if ((st = scratch_t(c, kBufPairP, total_pairs, &gpp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPairT, total_pairs, &gpt)) != SPHBI_OK) return st;
-      k_find_pairs<<<find_grid(np), kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff,
-                                                        0, gpp, gpt, dactive_n);
+      k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff, 0, gpp,
+                                                gpt, dactive_n, wpp);
       if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
     }
     // K4 + K5 in chunks of whole particles. Several chunks (cfg5: ~40): they
@@ -3201,8 +3294,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
         } else {
           if ((st = scratch_t(c, kBufPairP, cnt, &pp)) != SPHBI_OK) return st;
           if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
-          k_find_pairs<<<find_grid(p1 - p0), kFindBlock, 0, s>>>(p1 - p0, nullptr, p0, dp, pcell, cell_start, vb,
-                                                                 dt, h2, 1, poff, (long long)base, pp, pt);
+          const int cgrid = wpp ? static_cast<int>((static_cast<int64_t>(p1 - p0) * 32 + kFindBlock - 1) / kFindBlock)
+                                : find_grid(p1 - p0);
+          k_find_pairs<<<cgrid, kFindBlock, 0, s>>>(p1 - p0, nullptr, p0, dp, pcell, cell_start, vb, dt, h2, 1, poff,
+                                                    (long long)base, pp, pt, nullptr, wpp);
           if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
         }
         if (pair_list_out && pair_list_capacity && *pair_list_capacity >= total_pairs) {
