@@ -2975,6 +2975,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     SPHBI_CUDA_TRY(zero_async(c, dog, 16 * n_particles, s));
   }
   unsigned long long* ctr = c->counters_on ? c->d_counters : nullptr;
+  bool outputs_copied = false;  // host outputs already copied per chunk
   int64_t total_pairs = 0, candidates = 0;
   int* pp = nullptr;
   int* pt = nullptr;
@@ -3263,10 +3264,14 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
         c->bank = 0;
       }
     } restore_bank{c, s};
+    // host outputs: each chunk's rows go back on the copy stream as soon as
+    // they are reduced, behind the later chunks' compute
+    const bool chunk_d2h = nbanks > 1 && mem == SPHBI_MEM_HOST;
     if (nbanks > 1) {
       if (timing) cudaEventRecord(c->ev[1], s);
       SPHBI_CUDA_TRY(cudaEventRecord(c->ev[6], s));  // fork: the pair list is complete on s
       for (int b = 1; b < nbanks; ++b) SPHBI_CUDA_TRY(cudaStreamWaitEvent(cs2[b], c->ev[6], 0));
+      if (chunk_d2h) SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->ev[6], 0));
     }
     int p0 = 0;
     int64_t written = 0;
@@ -3333,10 +3338,24 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
         k_reduce_rows<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, row_ptr, pout, dov, dog, 0);
         if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
       }
+      if (chunk_d2h && p1 > p0) {
+        SPHBI_CUDA_TRY(cudaEventRecord(c->sev[1][chunk % 64], s));
+        SPHBI_CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->sev[1][chunk % 64], 0));
+        if (out_value)
+          SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value + p0, dov + p0, 8 * (p1 - p0), cudaMemcpyDeviceToHost, c->d2h));
+        if (out_grad)
+          SPHBI_CUDA_TRY(
+              cudaMemcpyAsync(out_grad + 2 * p0, dog + 2 * p0, 16 * (p1 - p0), cudaMemcpyDeviceToHost, c->d2h));
+      }
       p0 = p1;
     }
     c->stream = s;
     c->bank = 0;
+    if (chunk_d2h) {
+      outputs_copied = true;
+      SPHBI_CUDA_TRY(cudaEventRecord(c->ev[5], c->d2h));
+      SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->ev[5], 0));
+    }
     if (nbanks > 1) {  // join; ms_eval then spans evaluation and reduction of all chunks
       for (int b = 1; b < nbanks; ++b) {
         SPHBI_CUDA_TRY(cudaEventRecord(c->ev[7], cs2[b]));
@@ -3358,7 +3377,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if ((st = check_launch(c, "k_row_ptr(bases)")) != SPHBI_OK) return st;
   }
   // ---- outputs
-  if (mem == SPHBI_MEM_HOST && n_particles) {
+  if (mem == SPHBI_MEM_HOST && n_particles && !outputs_copied) {
     if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, dov, 8 * n_particles, cudaMemcpyDeviceToHost, s));
     if (out_grad) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, dog, 16 * n_particles, cudaMemcpyDeviceToHost, s));
   }
