@@ -3266,7 +3266,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     } restore_bank{c, s};
     // host outputs: each chunk's rows go back on the copy stream as soon as
     // they are reduced, behind the later chunks' compute
-    const bool chunk_d2h = nbanks > 1 && mem == SPHBI_MEM_HOST;
+    // (pinned outputs only: a copy to pageable memory blocks the host thread
+    // until it completes, which would serialise the chunk launches)
+    const bool chunk_d2h = nbanks > 1 && mem == SPHBI_MEM_HOST && (!out_value || is_pinned(out_value)) &&
+                           (!out_grad || is_pinned(out_grad));
     if (nbanks > 1) {
       if (timing) cudaEventRecord(c->ev[1], s);
       SPHBI_CUDA_TRY(cudaEventRecord(c->ev[6], s));  // fork: the pair list is complete on s
