@@ -1780,30 +1780,13 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
   return n;
 }
 
-__global__ void __launch_bounds__(kFindBlock)
-    k_find_pairs(int64_t count, const int* __restrict__ order, int p0, const double* __restrict__ pxy,
-                 const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
-                 const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
-                 unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
-                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0) {
-  const int lane = threadIdx.x & 31;
-  const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (dcount) count = *dcount;  // device-side list length (sparse path)
-  if (warp_per_particle) {
-    // scenes with long cell lists (cfg2 mode B: ~15k candidates per particle):
-    // one warp per particle, so a small particle set still fills the GPU
-    const int64_t w = pos >> 5;
-    if (w >= count) return;
-    const int i = order ? order[w] : p0 + static_cast<int>(w);
-    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
-    const unsigned c = pcell[i];
-    const unsigned long long b = cell_start[c], e = cell_start[c + 1];
-    const unsigned long long o = fill ? count_or_offset[i] - base : 0;
-    const unsigned long long n = walk_warp(lane, p.x, p.y, b, e, o, i, cell_tris, tri, h2, fill, pp, pt);
-    if (!fill && lane == 0) count_or_offset[i] = n;
-    return;
-  }
-  if ((pos & ~31ll) >= count) return;  // whole warps
+// 32 consecutive list positions (one warp; see k_find_pairs)
+__device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int* __restrict__ order, int p0,
+                                           const double* __restrict__ pxy, const unsigned* __restrict__ pcell,
+                                           const unsigned long long* __restrict__ cell_start,
+                                           const int* __restrict__ cell_tris, const double* __restrict__ tri,
+                                           double h2, int fill, unsigned long long* __restrict__ count_or_offset,
+                                           long long base, int* __restrict__ pp, int* __restrict__ pt, int lane) {
   const bool valid = pos < count;
   int i = 0;
   double px = 0.0, py = 0.0;
@@ -1848,6 +1831,40 @@ __global__ void __launch_bounds__(kFindBlock)
     if (!fill && lane == src) count_or_offset[qi] = n;
   }
 }
+
+__global__ void __launch_bounds__(kFindBlock)
+    k_find_pairs(int64_t count, const int* __restrict__ order, int p0, const double* __restrict__ pxy,
+                 const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
+                 const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
+                 unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
+                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (dcount) count = *dcount;  // device-side list length (sparse path)
+  if (warp_per_particle) {
+    // scenes with long cell lists (cfg2 mode B: ~15k candidates per particle):
+    // one warp per particle, so a small particle set still fills the GPU
+    const int64_t w = pos >> 5;
+    if (w >= count) return;
+    const int i = order ? order[w] : p0 + static_cast<int>(w);
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    const unsigned c = pcell[i];
+    const unsigned long long b = cell_start[c], e = cell_start[c + 1];
+    const unsigned long long o = fill ? count_or_offset[i] - base : 0;
+    const unsigned long long n = walk_warp(lane, p.x, p.y, b, e, o, i, cell_tris, tri, h2, fill, pp, pt);
+    if (!fill && lane == 0) count_or_offset[i] = n;
+    return;
+  }
+  // grid-stride over groups of 32 list positions: the sparse path's list
+  // length is known only on the device, so its grid is capped (a grid sized
+  // for every particle was mostly empty blocks)
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t pos0 = pos; (pos0 & ~31ll) < count; pos0 += stride) {
+    find_group(pos0, count, order, p0, pxy, pcell, cell_start, cell_tris, tri, h2, fill, count_or_offset, base, pp,
+               pt, lane);
+  }
+}
+
 // Piecewise kernels: the pairs of an inner piece with
 // support h_j <= h are the chunk's pairs that pass the same exact predicate at
 // h_j (so its pair list is bit-identical to a separate pass at h_j).
@@ -3180,7 +3197,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     const int np = static_cast<int>(n_particles);
     const int wpp = !sparse && n_entries > 512ull * static_cast<unsigned long long>(ncells) ? 1 : 0;
     const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
-                          : find_grid(np);
+                          : (sparse ? std::min(find_grid(np), 8 * c->sms) : find_grid(np));
     k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
                                               nullptr, nullptr, dactive_n, wpp);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
