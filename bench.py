@@ -367,6 +367,15 @@ def secondary_configs(ctx, names):
     return out
 
 
+def allreduce_scalar(dist, dev, value, op, dtype):
+    """all_reduce of one number (NCCL on the device, gloo on the host)."""
+    import torch
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=dtype, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=op)
+    return t.item()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -394,12 +403,21 @@ def main():
     from paper_2507_21686_b200 import shard
     from paper_2507_21686_b200.sphbi import Context, PolyKernel, _raise, table1_terms
 
+    if os.environ.get("SPHBI_BENCH_BACKEND", "nccl") != "nccl":
+        local = local % torch.cuda.device_count()  # functional multi-rank check on fewer GPUs
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink (one process per GPU). SPHBI_BENCH_BACKEND=gloo runs
+        # the same sharded path with several ranks on ONE GPU (NCCL refuses
+        # that) -- a functional check of the multi-rank code, not a measurement
+        backend = os.environ.get("SPHBI_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     sc = load_scene(args.workload, rank)
     k = sc.kernels[0]
@@ -478,12 +496,8 @@ def main():
     total_ms = sum(step_ms)
     pairs_step = local_pairs
     if dist:
-        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-        pc = torch.tensor([local_pairs], device=dev, dtype=torch.int64)
-        dist.all_reduce(pc)
-        pairs_step = int(pc.item())
+        total_ms = float(allreduce_scalar(dist, dev, total_ms, dist.ReduceOp.MAX, torch.float64))
+        pairs_step = int(allreduce_scalar(dist, dev, local_pairs, dist.ReduceOp.SUM, torch.int64))
     ms_per_step = total_ms / args.steps
     value = pairs_step / (ms_per_step * 1e-3)
 
@@ -554,9 +568,7 @@ def main():
             e2e_ms.append(a.elapsed_time(bb))
         e2e_total = sum(e2e_ms)
         if dist:
-            tt = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_total = float(tt.item())
+            e2e_total = float(allreduce_scalar(dist, dev, e2e_total, dist.ReduceOp.MAX, torch.float64))
         e2e = {"value": pairs_step / (e2e_total / args.steps * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps}
 

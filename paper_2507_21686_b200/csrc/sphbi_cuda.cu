@@ -81,7 +81,10 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
-constexpr int kMaxChunkPairs = 1 << 22;  // 4 Mi pairs per evaluation chunk (item slots ~2 KB per pair: ~8 GB scratch)
+#ifndef SPHBI_CHUNK_LOG2
+#define SPHBI_CHUNK_LOG2 22
+#endif
+constexpr int kMaxChunkPairs = 1 << SPHBI_CHUNK_LOG2;  // 4 Mi pairs per evaluation chunk (item slots ~2 KB per pair: ~8 GB scratch)
 
 }  // namespace
 
