@@ -141,6 +141,7 @@ enum ScratchSlot {
   kBufPiecePT,
   kBufPieceOut,
   kBufPieceFlag,
+  kBufStage,
   kNumBufs
 };
 
@@ -1783,13 +1784,21 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
   return n;
 }
 
+// Staged hits: the count pass of the short-list walk also keeps each
+// particle's first kFindStage hits (triangle ids, walk order = ascending) in a
+// particle-major staging area, so the fill becomes a compaction
+// (k_stage_compact) instead of a second walk over every candidate; particles
+// with more hits than slots are walked again there.
+constexpr int kFindStage = 32;
+
 // 32 consecutive list positions (one warp; see k_find_pairs)
 __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int* __restrict__ order, int p0,
                                            const double* __restrict__ pxy, const unsigned* __restrict__ pcell,
                                            const unsigned long long* __restrict__ cell_start,
                                            const int* __restrict__ cell_tris, const double* __restrict__ tri,
                                            double h2, int fill, unsigned long long* __restrict__ count_or_offset,
-                                           long long base, int* __restrict__ pp, int* __restrict__ pt, int lane) {
+                                           long long base, int* __restrict__ pp, int* __restrict__ pt, int lane,
+                                           int* __restrict__ stage) {
   const bool valid = pos < count;
   int i = 0;
   double px = 0.0, py = 0.0;
@@ -1815,6 +1824,8 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
         if (fill) {
           pp[o + n] = i;
           pt[o + n] = t;
+        } else if (stage && n < kFindStage) {
+          stage[static_cast<int64_t>(i) * kFindStage + n] = t;
         }
         ++n;
       }
@@ -1840,7 +1851,8 @@ __global__ void __launch_bounds__(kFindBlock)
                  const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
                  const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
                  unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
-                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0) {
+                 int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0,
+                 int* __restrict__ stage = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (dcount) count = *dcount;  // device-side list length (sparse path)
@@ -1864,7 +1876,46 @@ __global__ void __launch_bounds__(kFindBlock)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t pos0 = pos; (pos0 & ~31ll) < count; pos0 += stride) {
     find_group(pos0, count, order, p0, pxy, pcell, cell_start, cell_tris, tri, h2, fill, count_or_offset, base, pp,
-               pt, lane);
+               pt, lane, stage);
+  }
+}
+
+// Fill from the staging area: thread per particle of [p_begin, p_begin + p_count)
+// (index order), its hits to pair positions off[i] - base. Particles with
+// more than kFindStage hits or a long cell list (walked by the whole warp in
+// the count pass, not staged) re-walk their list here (lane walk, fill mode).
+__global__ void __launch_bounds__(256)
+    k_stage_compact(int p_begin, int p_count, const int* __restrict__ stage,
+                    const unsigned long long* __restrict__ off, long long base, const double* __restrict__ pxy,
+                    const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
+                    const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2,
+                    int* __restrict__ pp, int* __restrict__ pt) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= p_count) return;
+  const int i = p_begin + static_cast<int>(r);
+  const unsigned long long o = off[i] - base, n = off[i + 1] - off[i];
+  const unsigned c = pcell[i];
+  const unsigned long long cb = cell_start[c], ce = cell_start[c + 1];
+  // staged by the count pass: short lists (lane walk) with <= kFindStage hits
+  if (n <= static_cast<unsigned long long>(kFindStage) && ce - cb <= kFindLaneMax) {
+    const int* src = stage + static_cast<int64_t>(i) * kFindStage;
+    for (unsigned long long q = 0; q < n; ++q) {
+      pp[o + q] = i;
+      pt[o + q] = src[q];
+    }
+    return;
+  }
+  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+  unsigned long long m = 0;
+  for (unsigned long long k = cb; k < ce; ++k) {
+    const int t = __ldg(cell_tris + k);
+    double tv[6];
+    load_tri6(tri, t, tv);
+    if (pair_dist2(p.x, p.y, tv) < h2) {
+      pp[o + m] = i;
+      pt[o + m] = t;
+      ++m;
+    }
   }
 }
 
@@ -3201,8 +3252,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     const int wpp = !sparse && n_entries > 512ull * static_cast<unsigned long long>(ncells) ? 1 : 0;
     const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
                           : (sparse ? std::min(find_grid(np), 8 * c->sms) : find_grid(np));
+    int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
+    if (!wpp && (st = scratch_t(c, kBufStage, static_cast<size_t>(np) * kFindStage, &stage)) != SPHBI_OK) return st;
     k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
-                                              nullptr, nullptr, dactive_n, wpp);
+                                              nullptr, nullptr, dactive_n, wpp, stage);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
@@ -3263,8 +3316,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if (resident && total_pairs > 0) {
       if ((st = scratch_t(c, kBufPairP, total_pairs, &gpp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPairT, total_pairs, &gpt)) != SPHBI_OK) return st;
-      k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff, 0, gpp,
-                                                gpt, dactive_n, wpp);
+      if (stage)
+        k_stage_compact<<<grid_for(np, 256), 256, 0, s>>>(0, np, stage, poff, 0, dp, pcell, cell_start, vb, dt, h2,
+                                                          gpp, gpt);
+      else
+        k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 1, poff, 0, gpp,
+                                                  gpt, dactive_n, wpp);
       if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
     }
     // K4 + K5 in chunks of whole particles. Several chunks (cfg5: ~40): they
@@ -3324,8 +3381,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
           const int cgrid = wpp ? static_cast<int>((static_cast<int64_t>(p1 - p0) * 32 + kFindBlock - 1) / kFindBlock)
                                 : find_grid(p1 - p0);
-          k_find_pairs<<<cgrid, kFindBlock, 0, s>>>(p1 - p0, nullptr, p0, dp, pcell, cell_start, vb, dt, h2, 1, poff,
-                                                    (long long)base, pp, pt, nullptr, wpp);
+          if (stage)
+            k_stage_compact<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, stage, poff, (long long)base, dp,
+                                                                   pcell, cell_start, vb, dt, h2, pp, pt);
+          else
+            k_find_pairs<<<cgrid, kFindBlock, 0, s>>>(p1 - p0, nullptr, p0, dp, pcell, cell_start, vb, dt, h2, 1,
+                                                      poff, (long long)base, pp, pt, nullptr, wpp);
           if ((st = check_launch(c, "k_find_pairs(fill)")) != SPHBI_OK) return st;
         }
         if (pair_list_out && pair_list_capacity && *pair_list_capacity >= total_pairs) {
