@@ -492,6 +492,7 @@ def main():
             local_pairs = pairs_of(st)
         torch.cuda.synchronize()
     launches = ctx.launch_count() - launches0
+    arithmetic = ctx.last_precision()  # what the constant-field pipelines ran (sphbi_ctx_set_precision: auto)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     pairs_step = local_pairs
@@ -607,7 +608,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.workload == "cfg5" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; scenes.py)",
-            "config": bench_config(args.workload, sc, world, pairs_step),
+            "config": dict(bench_config(args.workload, sc, world, pairs_step),
+                           arithmetic={"fp64": "FP64 (a-priori error bound below the parity floor: fp64_path_ok)",
+                                       "dd": "double-double"}[arithmetic]),
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roof,

@@ -120,6 +120,27 @@ typedef enum sphbi_decomposition {
   SPHBI_DECOMP_HYBRID = 2
 } sphbi_decomposition;
 sphbi_status sphbi_ctx_set_decomposition(sphbi_ctx* ctx, int32_t mode);
+/* Arithmetic of the constant-field (tri_values == NULL: A == 1) pipelines.
+ * The reference evaluates in x87 long double (triangle_integrator.hpp:247,
+ * :333); the device carries its sums in double-double. With A == 1 no plane
+ * slope multiplies a piece's sums, so straight FP64 evaluation errs by at
+ * most ~2 u sum_k |b_k| per pair in the unit-disc frame (u = 2^-53), against
+ * an ABSOLUTE parity floor of 1e-13 / max(h, h^2) in the same units.
+ *   SPHBI_PRECISION_AUTO (default): FP64 when 4 u sum|b_k| sqrt(max pairs per
+ *     particle) <= half that floor (single pairs: max pairs = 1), else
+ *     double-double. Affine / P3 fields and the basis cache always run
+ *     double-double.
+ *   SPHBI_PRECISION_DD / SPHBI_PRECISION_FP64: forced.
+ * Environment variable SPHBI_PRECISION=auto|dd|fp64 sets the mode at context
+ * creation. sphbi_ctx_last_precision reports what the last constant-field
+ * call ran (SPHBI_PRECISION_DD or SPHBI_PRECISION_FP64). */
+typedef enum sphbi_precision {
+  SPHBI_PRECISION_AUTO = 0,
+  SPHBI_PRECISION_DD = 1,
+  SPHBI_PRECISION_FP64 = 2
+} sphbi_precision;
+sphbi_status sphbi_ctx_set_precision(sphbi_ctx* ctx, int32_t mode);
+int32_t sphbi_ctx_last_precision(sphbi_ctx* ctx);
 /* Message of the last failing call on this host thread. */
 const char* sphbi_last_error(void);
 /* Device kernel launches issued by this context so far (evidence counter). */

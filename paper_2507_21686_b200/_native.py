@@ -69,6 +69,8 @@ EXPORTED_SYMBOLS = (
     "sphbi_ctx_synchronize",
     "sphbi_ctx_enable_counters",
     "sphbi_ctx_set_decomposition",
+    "sphbi_ctx_set_precision",
+    "sphbi_ctx_last_precision",
     "sphbi_read_counters",
     "sphbi_last_error",
     "sphbi_ctx_launch_count",
@@ -110,6 +112,9 @@ def load() -> ctypes.CDLL:
     lib.sphbi_ctx_synchronize.argtypes = [P]
     lib.sphbi_ctx_enable_counters.argtypes = [P, ctypes.c_int]
     lib.sphbi_ctx_set_decomposition.argtypes = [P, ctypes.c_int32]
+    lib.sphbi_ctx_set_precision.argtypes = [P, ctypes.c_int32]
+    lib.sphbi_ctx_last_precision.argtypes = [P]
+    lib.sphbi_ctx_last_precision.restype = ctypes.c_int32
     lib.sphbi_read_counters.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.sphbi_last_error.restype = ctypes.c_char_p
     lib.sphbi_ctx_launch_count.argtypes = [P]

@@ -851,6 +851,166 @@ SPHBI_HD void piece_segment3(const KernelConsts& K, PairAcc3& acc, const Frame& 
   acc3_add_region(acc, S, f, sign);
 }
 
+// ---------------------------------------------------------------------------
+// constant field in plain FP64 (precision policy, sphbi_ctx_set_precision).
+// With A == 1 no plane slope multiplies a region's sums, every quantity below
+// is O(kappa) in the unit-disc frame (kappa = sum_k |b_k|, the size of the
+// monomial coefficients) and the parity rule's floor is ABSOLUTE
+// (1e-13 C/h^2, i.e. 1e-13 / max(h, h^2) in these units), so the rounding
+// error of straight FP64 evaluation -- a few u * kappa per piece, u = 2^-53 --
+// sits far below it for the named configurations. The forward recurrences
+// have positive terms (relative error ~ m u); the seeds switch to their
+// series where the closed forms cancel. The host selects this path only when
+// its a-priori bound clears the floor with a safety factor (fp64_path_ok).
+// ---------------------------------------------------------------------------
+struct S3f {
+  double v3, gx3, gy3;
+};
+// sum_{k=0}^{deg} c_k x^(k+off) on the leading parts of the dd coefficients
+SPHBI_HD double poly_f(const dd* c, int deg, double x, int off) {
+  double r = c[deg].hi;
+  for (int k = deg - 1; k >= 0; --k) r = fma(r, x, c[k].hi);
+  for (int j = 0; j < off; ++j) r *= x;
+  return r;
+}
+// Chain sums sPv = sum_k b_k/(k+2) P~_(k+1), sIg = sum_k w_k/2 I_k at bound x
+// (radial_chains3 in FP64; the same division-free scaled recurrences).
+SPHBI_HD void radial_chains3f(const KernelConsts& K, double x, double D, double& sPv, double& sIg, double& R) {
+  const int N = K.deg;
+  R = sqrt((x - D) * (x + D));
+  const double s = R / D;
+  const double D2 = D * D;
+  double p0, i1;
+  if (s < 0.125) {
+    // asinh(s) and f(s) = s sqrt(1+s^2) - asinh(s) by their Maclaurin series
+    // (|s| < 1/8: 10 terms reach 1e-19 relative); closed forms cancel here
+    const double s2 = s * s;
+    double a = 0.0097616095291941736;   // 46189/262144 / 19 ... asinh coefficients, high to low
+    a = fma(a, s2, -0.011551800896139706);
+    a = fma(a, s2, 0.013964843750000000);
+    a = fma(a, s2, -0.017352764423076923);
+    a = fma(a, s2, 0.022372159090909091);
+    a = fma(a, s2, -0.030381944444444444);
+    a = fma(a, s2, 0.044642857142857144);
+    a = fma(a, s2, -0.075);
+    a = fma(a, s2, 0.16666666666666666);
+    p0 = s - a * s2 * s;  // asinh s = s - s^3/6 + 3/40 s^5 - ...
+    // f(s)/s^3 = 2/3 - s^2/5 + 3/28 s^4 - 5/72 s^6 + 35/704 s^8 - 63/1664 s^10 + 77/2560 s^12 - ...
+    double t = -0.024643841911764706;
+    t = fma(t, s2, 0.030078125);
+    t = fma(t, s2, -0.037860576923076923);
+    t = fma(t, s2, 0.049715909090909091);
+    t = fma(t, s2, -0.069444444444444444);
+    t = fma(t, s2, 0.10714285714285714);
+    t = fma(t, s2, -0.2);
+    t = fma(t, s2, 0.66666666666666663);
+    i1 = 0.5 * D2 * (t * s2 * s);
+  } else {
+    p0 = log((x + R) / D);
+    i1 = 0.5 * (x * R - D2 * p0);
+  }
+  const double R3 = R * R * R;
+  double um2 = p0, um1 = R, vm2 = 0.0, vm1 = i1;
+  double aPv = K.wpv[1].hi * um1;
+  double aIg = K.wig[1].hi * vm1;
+  double xpm2 = 1.0, xpm1 = x;
+  for (int m = 2; m <= N + 2; ++m) {
+    const double um = fma(xpm1 * R, K.dfac[m - 2], (double)(m - 1) * D2 * um2);
+    const double vm = fma(xpm2 * R3, K.efac[m - 2], (double)(m - 2) * D2 * vm2);
+    aPv = fma(K.wpv[m].hi, um, aPv);
+    aIg = fma(K.wig[m].hi, vm, aIg);
+    um2 = um1;
+    um1 = um;
+    vm2 = vm1;
+    vm1 = vm;
+    xpm2 = xpm1;
+    xpm1 *= x;
+  }
+  sPv = aPv;
+  sIg = aIg;
+}
+// S += sgn * (stub window antiderivative at bound x), tau3 channels, FP64
+SPHBI_HD void stub_bound_sums3f(const KernelConsts& K, double x, double D, double beta, double cb, double sb,
+                                S3f& S, double sgn) {
+  double sPv = 0.0, sIg = 0.0, R = 0.0;
+  if (x != D) radial_chains3f(K, x, D, sPv, sIg, R);
+  double as;
+  if (D <= 0.7 * x)
+    as = asin(D / x);
+  else
+    as = (kHalfPiHi - asin(R / x)) + kHalfPiLo;
+  const double amb = as - beta;
+  const int N = K.deg;
+  const bool one = x == 1.0;
+  const double Pv = one ? K.pv1.hi : poly_f(K.pv, N, x, 2);
+  const double Tg = one ? K.tg1.hi : poly_f(K.tg, N, x, 0);
+  const double Rg = one ? K.rg1.hi : poly_f(K.rg, N, x, 1);
+  S.v3 = fma(sgn, fma(Pv, amb, sPv * D), S.v3);
+  S.gx3 = fma(sgn, 2.0 * (cb * D * Tg - sb * sIg), S.gx3);
+  S.gy3 = fma(sgn, Rg - 2.0 * (cb * sIg + sb * D * Tg), S.gy3);
+}
+// out[0..2] = sign * (v3, M^T (gx3, gy3))
+SPHBI_HD void s3f_rotate(const S3f& S, const Frame& M, double sign, double* out) {
+  out[0] = sign * S.v3;
+  out[1] = sign * fma(S.gx3, M.m00, S.gy3 * M.m10);
+  out[2] = sign * fma(S.gx3, M.m01, S.gy3 * M.m11);
+}
+SPHBI_HD void piece_stub3f(const KernelConsts& K, const Frame& f, double gamma, double l, double D, double beta,
+                           double lo, double u, bool window, double sign, const PieceTrig& T, double* out) {
+  const bool full = l >= 1.0;
+  const double Pv = full ? K.pv1.hi : poly_f(K.pv, K.deg, l, 2);
+  const double Rg = full ? K.rg1.hi : poly_f(K.rg, K.deg, l, 1);
+  S3f S{Pv * gamma, Rg * T.sg, Rg * T.omc};
+  if (window) {
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) stub_bound_sums3f(K, b == 0 ? u : lo, D, beta, T.cb, T.sb, S, b == 0 ? 1.0 : -1.0);
+  }
+  s3f_rotate(S, f, sign, out);
+}
+SPHBI_HD void piece_cone3f(const KernelConsts& K, const Frame& f, double gamma, double L, double sign,
+                           const PieceTrig& T, double* out) {
+  const bool full = L >= 1.0;
+  const double Pv = full ? K.pv1.hi : poly_f(K.pv, K.deg, L, 2);
+  const double Rg = full ? K.rg1.hi : poly_f(K.rg, K.deg, L, 1);
+  const S3f S{Pv * gamma, Rg * T.sg, Rg * T.omc};
+  s3f_rotate(S, f, sign, out);
+}
+SPHBI_HD void piece_half_disc3f(const KernelConsts& K, const Frame& f, double sign, double* out) {
+  const S3f S{K.pv1.hi * kPiHi, 2.0 * K.rg1.hi, 0.0};
+  s3f_rotate(S, f, sign, out);
+}
+SPHBI_HD void piece_segment3f(const KernelConsts& K, const Frame& f, double d, double sign, double* out) {
+  double sPv, sIg, R;
+  radial_chains3f(K, 1.0, d, sPv, sIg, R);
+  const double acd = d <= 0.7 ? acos(d) : asin(R);
+  const S3f S{2.0 * (K.pv1.hi * acd - sPv * d), 4.0 * sIg, 0.0};
+  s3f_rotate(S, f, sign, out);
+}
+// A signed count of full unit discs: (v3, g13, g23) += n * (2 pi Pv(1), 0, 0)
+SPHBI_HD double disc_value3f(const KernelConsts& K, int disc_n) { return (double)disc_n * (2.0 * kPiHi) * K.pv1.hi; }
+
+// A-priori selection of the FP64 constant-field path. Measured (tools/
+// prec_study.py: host build of this file, FP64 against the double-double path
+// over the five configurations' pairs and the reference suites' random
+// configurations): the per-pair difference in the unit-disc frame stays below
+// 2.0 u sum_k |b_k| (Wendland C2 1.2, C4 2.0, C6 1.3). The selection takes
+// twice that per pair, lets a particle's pairs add like a random walk
+// (sqrt(max_row)), and demands half of the floor 1e-13 / max(h, h^2):
+//   cfg1 / cfg5 (C2, h = 0.25 / 0.1) and cfg2 mode A (C4, one pair per row)
+//   select FP64; cfg2 mode B (rows of ~2e4 pairs), cfg3 (C6: sum |b_k| = 3718)
+//   and the reference suites' h >= 0.5 stay double-double.
+inline double kernel_kappa(const KernelConsts& K) {
+  double s = 0.0;
+  for (int k = 0; k <= K.deg; ++k) s += fabs(K.b[k]);
+  return s;
+}
+inline bool fp64_path_ok(const KernelConsts& K, double h, double max_row) {
+  const double u = 1.1102230246251565e-16;
+  const double per_pair = 4.0 * u * kernel_kappa(K);
+  const double floor_norm = 1e-13 / (h > 1.0 ? h * h : h);
+  return per_pair * sqrt(max_row < 1.0 ? 1.0 : max_row) <= 0.5 * floor_norm;
+}
+
 SPHBI_HD void bump_counter(unsigned long long* counters, int which) {
   if (counters) {
 #if defined(__CUDA_ARCH__)

@@ -81,6 +81,9 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
+#ifndef SPHBI_MINB_STUBF
+#define SPHBI_MINB_STUBF 6
+#endif
 #ifndef SPHBI_CHUNK_LOG2
 #define SPHBI_CHUNK_LOG2 22
 #endif
@@ -154,6 +157,11 @@ struct sphbi_ctx {
   // geometry passes: hybrid (default), edge sum, or the reference's
   // route-faithful dispatch (sphbi_ctx_set_decomposition, SPHBI_DECOMP)
   int decomp = SPHBI_DECOMP_HYBRID;
+  // constant-field arithmetic: auto (FP64 where fp64_path_ok's a-priori bound
+  // clears the parity floor, else double-double), or forced either way
+  // (sphbi_ctx_set_precision, SPHBI_PRECISION)
+  int precision = SPHBI_PRECISION_AUTO;
+  bool fp64_now = false;  // this call's constant-field pipelines run the FP64 piece kernels
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   unsigned long long* d_counters = nullptr;
@@ -253,6 +261,22 @@ sphbi_status make_consts(const sphbi_kernel_desc* k, KernelConsts* K) {
   return SPHBI_OK;
 }
 
+// Constant-field precision selection (sphbi_ctx_set_precision): the longest
+// row (pairs per particle) for which the FP64 path's a-priori error bound
+// clears the parity floor (fp64_path_ok); 0: double-double, INT64_MAX: forced.
+int64_t fp64_row_limit(const sphbi_ctx* c, const KernelConsts& K, double h) {
+  if (c->precision == SPHBI_PRECISION_DD || c->force_exact || c->two_pass) return 0;
+  if (c->precision == SPHBI_PRECISION_FP64) return INT64_MAX;
+  if (!fp64_path_ok(K, h, 1.0)) return 0;
+  int64_t lo = 1, hi = int64_t(1) << 40;  // largest m with fp64_path_ok(K, h, m)
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (fp64_path_ok(K, h, static_cast<double>(mid))) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+constexpr unsigned kFlagLongRow = 8u;  // dflags[1]: a row exceeds the FP64 path's row limit
+
 int grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return static_cast<int>(g < 1 ? 1 : g);
@@ -348,6 +372,9 @@ struct __align__(16) AccOut {  // one piece's rotated contribution (9 dd)
 };
 struct __align__(16) AccOut3 {  // constant field: v3, g13, g23 only (3 dd)
   double v[6];
+};
+struct __align__(16) AccOut3f {  // constant field, FP64 path: v3, g13, g23 (+ pad)
+  double v[4];
 };
 SPHBI_HD void acc3_to_out(const PairAcc3& a, AccOut3& o) {
   o.v[0] = a.v3.hi;
@@ -1074,6 +1101,67 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Constant field in plain FP64 (sphbi_core.cuh: piece_*3f; selected per call
+// by fp64_path_ok): the same work lists and item slots, 32-byte item outputs,
+// one stub kernel for the four window classes (each launch still runs one
+// class, so warps stay converged on the x == 1 / x == D recognitions).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void out3f_store(AccOut3f* out, int64_t k, const double* o) {
+  double2* q = reinterpret_cast<double2*>(out + k);
+  q[0] = make_double2(o[0], o[1]);
+  q[1] = make_double2(o[2], 0.0);
+}
+__global__ void __launch_bounds__(128, SPHBI_MINB_STUBF)
+    k_pipe_stub_f(const __grid_constant__ KernelConsts K, WorkN wn, const StubItem* __restrict__ items,
+                  const int* __restrict__ idx, AccOut3f* __restrict__ out, unsigned* status_or) {
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const StubItem it = items[slot];
+    Frame f;
+    double gamma, beta;
+    PieceTrig T;
+    stub_item_geometry(it, f, gamma, beta, status_or, &T);
+    double lo, u;
+    const bool window = it.window(lo, u);
+    double o[3];
+    piece_stub3f(K, f, gamma, it.l, it.D, beta, lo, u, window, it.sign(), T, o);
+    out3f_store(out, k, o);
+  }
+}
+__global__ void __launch_bounds__(128)
+    k_pipe_sector_f(const __grid_constant__ KernelConsts K, WorkN wn, const PieceItem* __restrict__ items,
+                    const int* __restrict__ idx, AccOut3f* __restrict__ out) {
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    Frame f{it.m00, it.m01, it.m10, it.m11};
+    double o[3];
+    if (it.pad) {
+      piece_half_disc3f(K, f, it.sign, o);
+    } else {
+      double gamma;
+      PieceTrig T;
+      sector_item_geometry(it, f, gamma, &T);
+      piece_cone3f(K, f, gamma, 1.0, it.sign, T, o);
+    }
+    out3f_store(out, k, o);
+  }
+}
+__global__ void __launch_bounds__(128)
+    k_pipe_segment_f(const __grid_constant__ KernelConsts K, WorkN wn, const PieceItem* __restrict__ items,
+                     const int* __restrict__ idx, AccOut3f* __restrict__ out) {
+  SPHBI_ITEM_LOOP(k) {
+    const int64_t slot = idx ? idx[k] : k;
+    const PieceItem it = items[slot];
+    const Frame f{it.m00, it.m01, it.m10, it.m11};
+    double o[3];
+    piece_segment3f(K, f, it.a, it.sign, o);
+    out3f_store(out, k, o);
+  }
+}
+
 // A pair's items in a fixed summation order: sectors, stub classes 0..3,
 // segments, each in emission order -- identical on both pipelines, so their
 // results agree bit for bit.
@@ -1213,6 +1301,30 @@ __global__ void __launch_bounds__(128)
     }
   }
   for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
+}
+
+// combine, constant field on the FP64 path (slot path only): the pair's items
+// in the same fixed order, plain FP64 sums; the plane is exactly (0, 0, 1).
+__global__ void __launch_bounds__(128)
+    k_pipe_combine_f(const __grid_constant__ KernelConsts K, int64_t n, double h, SlotItems items, ItemOuts io,
+                     int stride, double* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const JRec r = items.get(j);
+  double o[4] = {0.0, 0.0, 0.0, 0.0};
+  if ((r.flags & kRecRoute) && (r.flags & kRecPlane)) {
+    double raw[3] = {0.0, 0.0, 0.0};
+    items.each(j, r, [&](int kind, unsigned long long q) {
+      const double2* p = reinterpret_cast<const double2*>(static_cast<const AccOut3f*>(item_base(io, kind)) + q);
+      const double2 a = p[0], b = p[1];
+      raw[0] += a.x;
+      raw[1] += a.y;
+      raw[2] += b.x;
+    });
+    if (r.disc_n) raw[0] += disc_value3f(K, r.disc_n);
+    finalize(raw, K.c2, h, o);
+  }
+  for (int q = 0; q < stride; ++q) out[stride * r.k + q] = o[q];
 }
 
 // combine, vertex-basis mode: per pair and vertex i (original order) the
@@ -1527,10 +1639,13 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 __global__ void k_pack_pairs(int64_t n, const int64_t* __restrict__ ip, const int64_t* __restrict__ it,
                              int64_t n_particles, int64_t n_tris, unsigned long long* __restrict__ keys,
-                             unsigned* __restrict__ flags) {
+                             unsigned* __restrict__ flags, int64_t row_limit = 0) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t i = ip[k], t = it[k];
+  // a sorted list has a row longer than row_limit iff some entry equals the
+  // one row_limit positions before it (FP64-path selection, kFlagLongRow)
+  if (row_limit > 0 && k >= row_limit && ip[k - row_limit] == i) atomicOr(flags, 8u);
   if (i < 0 || i >= n_particles || t < 0 || t >= n_tris) {
     atomicOr(flags, 1u);  // out of range
     keys[k] = 0ull;
@@ -1549,10 +1664,12 @@ __global__ void k_pack_pairs(int64_t n, const int64_t* __restrict__ ip, const in
 // one pass.
 __global__ void k_pack_pairs32(int64_t n, const int64_t* __restrict__ ip, const int64_t* __restrict__ it,
                                int64_t n_particles, int64_t n_tris, int* __restrict__ pp, int* __restrict__ pt,
-                               unsigned* __restrict__ flags) {
+                               unsigned* __restrict__ flags, int64_t row_limit = 0, int64_t before = 0) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t i = ip[k], t = it[k];
+  // `before` entries of the same list precede ip[0] on the device (earlier chunks)
+  if (row_limit > 0 && k + before >= row_limit && ip[k - row_limit] == i) atomicOr(flags, 8u);
   if (i < 0 || i >= n_particles || t < 0 || t >= n_tris) {
     atomicOr(flags, 1u);  // out of range
     pp[k] = 0;
@@ -1568,10 +1685,11 @@ __global__ void k_pack_pairs32(int64_t n, const int64_t* __restrict__ ip, const 
 }
 
 __global__ void k_unpack_keys(int64_t n, const unsigned long long* __restrict__ keys, int* __restrict__ pp,
-                              int* __restrict__ pt) {
+                              int* __restrict__ pt, unsigned* __restrict__ flags = nullptr, int64_t row_limit = 0) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const unsigned long long key = keys[k];
+  if (row_limit > 0 && k >= row_limit && (keys[k - row_limit] >> 32) == (key >> 32)) atomicOr(flags, 8u);
   pp[k] = static_cast<int>(key >> 32);
   pt[k] = static_cast<int>(key & 0xffffffffull);
 }
@@ -1798,7 +1916,8 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
                                            const int* __restrict__ cell_tris, const double* __restrict__ tri,
                                            double h2, int fill, unsigned long long* __restrict__ count_or_offset,
                                            long long base, int* __restrict__ pp, int* __restrict__ pt, int lane,
-                                           int* __restrict__ stage) {
+                                           int* __restrict__ stage, unsigned long long row_limit,
+                                           unsigned* __restrict__ row_flag) {
   const bool valid = pos < count;
   int i = 0;
   double px = 0.0, py = 0.0;
@@ -1830,7 +1949,10 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
         ++n;
       }
     }
-    if (!fill) count_or_offset[i] = n;
+    if (!fill) {
+      count_or_offset[i] = n;
+      if (row_limit && n > row_limit) atomicOr(row_flag, 8u);  // a row too long for the FP64 path
+    }
   }
   // long lists: the whole warp per particle
   unsigned todo = __ballot_sync(0xffffffffu, valid && e - b > kFindLaneMax);
@@ -1842,7 +1964,10 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
     unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
     const int qi = __shfl_sync(0xffffffffu, i, src);
     const unsigned long long n = walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, fill, pp, pt);
-    if (!fill && lane == src) count_or_offset[qi] = n;
+    if (!fill && lane == src) {
+      count_or_offset[qi] = n;
+      if (row_limit && n > row_limit) atomicOr(row_flag, 8u);
+    }
   }
 }
 
@@ -1852,7 +1977,8 @@ __global__ void __launch_bounds__(kFindBlock)
                  const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
                  unsigned long long* __restrict__ count_or_offset, long long base, int* __restrict__ pp,
                  int* __restrict__ pt, const int* __restrict__ dcount = nullptr, int warp_per_particle = 0,
-                 int* __restrict__ stage = nullptr) {
+                 int* __restrict__ stage = nullptr, unsigned long long row_limit = 0,
+                 unsigned* __restrict__ row_flag = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (dcount) count = *dcount;  // device-side list length (sparse path)
@@ -1867,7 +1993,10 @@ __global__ void __launch_bounds__(kFindBlock)
     const unsigned long long b = cell_start[c], e = cell_start[c + 1];
     const unsigned long long o = fill ? count_or_offset[i] - base : 0;
     const unsigned long long n = walk_warp(lane, p.x, p.y, b, e, o, i, cell_tris, tri, h2, fill, pp, pt);
-    if (!fill && lane == 0) count_or_offset[i] = n;
+    if (!fill && lane == 0) {
+      count_or_offset[i] = n;
+      if (row_limit && n > row_limit) atomicOr(row_flag, 8u);
+    }
     return;
   }
   // grid-stride over groups of 32 list positions: the sparse path's list
@@ -1876,7 +2005,7 @@ __global__ void __launch_bounds__(kFindBlock)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t pos0 = pos; (pos0 & ~31ll) < count; pos0 += stride) {
     find_group(pos0, count, order, p0, pxy, pcell, cell_start, cell_tris, tri, h2, fill, count_or_offset, base, pp,
-               pt, lane, stage);
+               pt, lane, stage, row_limit, row_flag);
   }
 }
 
@@ -2339,6 +2468,23 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
                                                   stride, dout);
     return check_launch(c, "k_p3_combine");
   }
+  if (f1 && c->fp64_now) {
+    AccOut3f *osec, *ostub, *oseg;
+    if ((st = scratch_t(c, kBufOutC, kCapSec * n, &osec)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutB, 2 * scap, &ostub)) != SPHBI_OK) return st;
+    if ((st = scratch_t(c, kBufOutS, kCapSeg * n, &oseg)) != SPHBI_OK) return st;
+    AccOut3f* ost[4] = {ostub, ostub, ostub + scap, ostub + scap};
+    for (int cl = 0; cl < 4; ++cl)
+      k_pipe_stub_f<<<igrid(k_pipe_stub_f, 1 + cl), 128, 0, s>>>(K, wst[cl], istub, xst[cl], ost[cl], dflags);
+    k_pipe_sector_f<<<igrid(k_pipe_sector_f, 0), 128, 0, s>>>(K, wsec, isec, L.sec, osec);
+    k_pipe_segment_f<<<igrid(k_pipe_segment_f, 5), 128, 0, s>>>(K, wseg, iseg, L.seg, oseg);
+    if ((st = check_launch(c, "piece kernels (FP64)", 6)) != SPHBI_OK) return st;
+    mark(2);
+    k_pipe_combine_f<<<grid_for(n, 128), 128, 0, s>>>(K, n, h, items, ItemOuts{osec, {ostub, ostub + scap}, oseg},
+                                                      stride, dout);
+    mark(3);
+    return check_launch(c, "k_pipe_combine_f");
+  }
   if (f1) {
     AccOut3 *osec, *ostub, *oseg;
     if ((st = scratch_t(c, kBufOutC, kCapSec * n, &osec)) != SPHBI_OK) return st;
@@ -2398,7 +2544,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
                                const double* particle_xy, int64_t n_triangles, const double* tri_xy,
                                const double* tri_values, int64_t n_pairs, const int64_t* pair_particle,
                                const int64_t* pair_triangle, double* out_value, double* out_grad,
-                               unsigned* dflags, unsigned long long* ctr) {
+                               unsigned* dflags, unsigned long long* ctr, int64_t row_limit) {
   cudaStream_t s = c->stream;
   sphbi_status st;
   double *dp, *dt, *dv = nullptr, *dov, *dog;
@@ -2501,7 +2647,8 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     if (nq > 0) {
       // validate (range, sortedness) and convert to int32 pairs
       k_pack_pairs32<<<grid_for(nq, 256), 256, 0, cs>>>(nq, dip + qb[k], dit + qb[k], n_particles, n_triangles,
-                                                         pp[q], pt[q], dflags + 1);
+                                                         pp[q], pt[q], dflags + 1,
+                                                         row_limit < nq + qb[k] ? row_limit : 0, qb[k]);
       if ((st = check_launch(c, "k_pack_pairs32")) != SPHBI_OK) return st;
       const SceneSrc src{pp[q], pt[q], dp, dt, dv};
       c->stream = cs;
@@ -2560,6 +2707,7 @@ sphbi_status evaluate_streamed(sphbi_ctx* c, const KernelConsts& K, double h, in
     return SPHBI_ERR_INTERNAL;
   }
   if (c->h_flags[1] & 2u) return SPHBI_ERR_INTERNAL;  // unsorted: caller falls back
+  if (c->h_flags[1] & kFlagLongRow) return SPHBI_ERR_INTERNAL;  // a row beyond the FP64 path's limit: likewise
   return SPHBI_OK;
 }
 
@@ -2635,6 +2783,12 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
         q = *e == ',' ? e + 1 : e;
       }
       if (!w.empty()) c->stream_ramp = w;
+    }
+    if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
+      const std::string v(pm);
+      if (v == "dd") c->precision = SPHBI_PRECISION_DD;
+      else if (v == "fp64") c->precision = SPHBI_PRECISION_FP64;
+      else c->precision = SPHBI_PRECISION_AUTO;
     }
     if (const char* dm = std::getenv("SPHBI_DECOMP"); dm && *dm) {
       if (std::strcmp(dm, "reference") == 0) c->decomp = SPHBI_DECOMP_REFERENCE;
@@ -2733,6 +2887,19 @@ sphbi_status sphbi_ctx_set_decomposition(sphbi_ctx* c, int32_t mode) {
   return SPHBI_OK;
 }
 
+sphbi_status sphbi_ctx_set_precision(sphbi_ctx* c, int32_t mode) {
+  SPHBI_LOCK(c);
+  if (!c) return fail(SPHBI_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (mode != SPHBI_PRECISION_AUTO && mode != SPHBI_PRECISION_DD && mode != SPHBI_PRECISION_FP64)
+    return fail(SPHBI_ERR_INVALID_ARGUMENT, "unknown precision mode");
+  c->precision = mode;
+  return SPHBI_OK;
+}
+int32_t sphbi_ctx_last_precision(sphbi_ctx* c) {
+  SPHBI_LOCK(c);
+  return c && c->fp64_now ? SPHBI_PRECISION_FP64 : SPHBI_PRECISION_DD;
+}
+
 sphbi_status sphbi_read_counters(sphbi_ctx* c, uint64_t out[SPHBI_NUM_COUNTERS], int reset) {
   SPHBI_LOCK(c);
   if (!c || !out) return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL argument");
@@ -2766,6 +2933,7 @@ static sphbi_status integrate_pairs_impl(sphbi_ctx* c, const sphbi_kernel_desc* 
   if (!query_xy || !tri_xy || !out || (mode == 0 && !values))
     return fail(SPHBI_ERR_INVALID_ARGUMENT, "NULL input/output array");
   cudaSetDevice(c->device);
+  c->fp64_now = false;  // affine fields / vertex bases: double-double
   const int nout = mode == 0 ? 4 : 12;
   const double *dq = query_xy, *dt = tri_xy, *dv = values;
   double* dout = out;
@@ -2935,6 +3103,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     std::memset(stats, 0, sizeof(*stats));
     cudaEventRecord(c->ev[0], s);
   }
+  // constant-field arithmetic (sphbi_ctx_set_precision): FP64 when no row of
+  // the pair list is longer than row_limit, decided where the rows are known
+  c->fp64_now = false;
+  const int64_t row_limit = (!tri_values && !nodal10 && !bc && !pieces && !counts_out) ? fp64_row_limit(c, K, h) : 0;
   // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
   if (!p3 && !bc && !pieces && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&
@@ -2943,8 +3115,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if ((st = scratch_t(c, kBufFlags, 8, &sflags)) != SPHBI_OK) return st;  // 8 x u32
     SPHBI_CUDA_TRY(zero_async(c, sflags, 32, s));
     unsigned long long* sctr = c->counters_on ? c->d_counters : nullptr;
+    // optimistic: the chunks run the FP64 kernels while the upload-side
+    // validation checks the rows; a longer row falls back to the general path
+    c->fp64_now = row_limit > 0;
     st = evaluate_streamed(c, K, h, n_particles, particle_xy, n_triangles, tri_xy, tri_values, n_pairs,
-                           pair_particle, pair_triangle, out_value, out_grad, sflags, sctr);
+                           pair_particle, pair_triangle, out_value, out_grad, sflags, sctr, row_limit);
+    if (st != SPHBI_OK) c->fp64_now = false;
     if (st == SPHBI_OK) {
       if (pair_list_capacity) *pair_list_capacity = n_pairs;
       if (c->h_flags[0]) return fail(status_from_bits(c->h_flags[0]), "pair evaluation: reference-domain error on device");
@@ -3072,7 +3248,8 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       }
       unsigned long long *ka, *kb;
       if ((st = scratch_t(c, kBufKeysA, n_pairs, &ka)) != SPHBI_OK) return st;
-      k_pack_pairs<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, ip, it, n_particles, n_triangles, ka, dflags + 1);
+      k_pack_pairs<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, ip, it, n_particles, n_triangles, ka, dflags + 1,
+                                                          row_limit < n_pairs ? row_limit : 0);
       if ((st = check_launch(c, "k_pack_pairs")) != SPHBI_OK) return st;
       SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
       SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
@@ -3090,8 +3267,19 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       }
       if ((st = scratch_t(c, kBufPairP, n_pairs, &pp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPairT, n_pairs, &pt)) != SPHBI_OK) return st;
-      k_unpack_keys<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, keys, pp, pt);
+      const bool was_sorted = !(c->h_flags[1] & 2u);
+      k_unpack_keys<<<grid_for(n_pairs, 256), 256, 0, s>>>(n_pairs, keys, pp, pt, dflags + 1,
+                                                           !was_sorted && row_limit < n_pairs ? row_limit : 0);
       if ((st = check_launch(c, "k_unpack_keys")) != SPHBI_OK) return st;
+      if (row_limit > 0) {
+        // a list that came sorted was checked by k_pack_pairs (flags already
+        // here); a list sorted on the device only now
+        if (!was_sorted && row_limit < n_pairs) {
+          SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
+          SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        c->fp64_now = !(c->h_flags[1] & kFlagLongRow);
+      }
     }
     if (timing) cudaEventRecord(c->ev[1], s);
     if (bc && (st = bc->reserve(n_pairs)) != SPHBI_OK) return st;
@@ -3255,7 +3443,9 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
     if (!wpp && (st = scratch_t(c, kBufStage, static_cast<size_t>(np) * kFindStage, &stage)) != SPHBI_OK) return st;
     k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
-                                              nullptr, nullptr, dactive_n, wpp, stage);
+                                              nullptr, nullptr, dactive_n, wpp, stage,
+                                              row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull,
+                                              dflags + 1);
     if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
@@ -3270,8 +3460,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // the pairs need more than one evaluation chunk (chunk boundaries)
     unsigned long long* htot = reinterpret_cast<unsigned long long*>(c->h_flags + 32);
     SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
+    if (row_limit > 0) SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     total_pairs = static_cast<int64_t>(*htot);
+    c->fp64_now = row_limit > 0 && !(c->h_flags[1] & kFlagLongRow);
     if (counts_out) {  // sphbi_pair_counts: the count pass only
       const cudaMemcpyKind kind = mem == SPHBI_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
       SPHBI_CUDA_TRY(cudaMemcpyAsync(counts_out, pcount, 8 * n_particles, kind, s));

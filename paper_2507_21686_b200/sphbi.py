@@ -318,6 +318,20 @@ class Context:
             raise InvalidArgument(f"unknown decomposition {mode!r}")
         _raise(self.lib.sphbi_ctx_set_decomposition(self.handle, code))
 
+    def set_precision(self, mode: str = "auto"):
+        """Arithmetic of the constant-field (tri_values=None) pipelines: 'auto'
+        (plain FP64 where its a-priori error bound clears the parity floor,
+        else double-double), 'dd' or 'fp64'; include/sphbi_cuda.h
+        sphbi_ctx_set_precision. Affine and P3 fields always run double-double."""
+        code = {"auto": 0, "dd": 1, "fp64": 2}.get(mode)
+        if code is None:
+            raise InvalidArgument(f"unknown precision {mode!r}")
+        _raise(self.lib.sphbi_ctx_set_precision(self.handle, code))
+
+    def last_precision(self) -> str:
+        """'fp64' or 'dd': what the last constant-field call on this context ran."""
+        return "fp64" if int(self.lib.sphbi_ctx_last_precision(self.handle)) == 2 else "dd"
+
     def read_counters(self, reset: bool = False) -> np.ndarray:
         out = (ctypes.c_uint64 * N.NUM_COUNTERS)()
         _raise(self.lib.sphbi_read_counters(self.handle, out, 1 if reset else 0))

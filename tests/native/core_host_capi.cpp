@@ -356,6 +356,131 @@ void core_host_kind_counts(int64_t npairs, const int64_t* pp, const int64_t* pt,
   }
 }
 
+// Host emulation of the constant-field (A == 1) piece kernels, in either
+// precision: the double-double tau3 path (k_pipe_*<1>) or the plain FP64 path
+// (k_pipe_*_f). Pieces are evaluated exactly as the device kernels do (raw
+// items -> frames / trig from geometry -> piece sums -> rotation), summed per
+// pair in the combine kernels' arithmetic.
+}  // extern "C"
+template <bool FAST>
+struct F1EmuSink {
+  static constexpr int kAngles = 1;
+  const KernelConsts* K;
+  PairAcc3 acc;     // dd path
+  double f[3];      // FP64 path
+  unsigned status;
+  unsigned long long* counters;
+  int disc_n;
+  SPHBI_HD void bump(int) {}
+  void add3(const double* o) { for (int i = 0; i < 3; ++i) f[i] += o[i]; }
+  void disc(double sign) { disc_n += sign > 0.0 ? 1 : -1; }
+  void half_disc(const Frame& fr, double sign) {
+    if (FAST) { double o[3]; piece_half_disc3f(*K, fr, sign, o); add3(o); }
+    else piece_half_disc3(*K, acc, fr, sign);
+  }
+  void sector_raw(P2 v1, P2 v2, double, double sign) {
+    Frame fr;
+    double gamma;
+    PieceTrig T;
+    sector_from_raw(v1, v2, fr, gamma, &T);
+    if (FAST) { double o[3]; piece_cone3f(*K, fr, gamma, 1.0, sign, T, o); add3(o); }
+    else piece_cone3(*K, acc, fr, gamma, 1.0, sign, T);
+  }
+  void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window, double sign) {
+    Frame fr;
+    double gamma, beta;
+    PieceTrig T;
+    stub_frame_angles(v1, v2, r1, fr, gamma, beta, &T);
+    if (FAST) {
+      double o[3];
+      piece_stub3f(*K, fr, gamma, l, D, beta, lo, u, window, sign, T, o);
+      add3(o);
+      return;
+    }
+    switch (stub_class(D, lo, u, window)) {
+      case 0: piece_stub3<0>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
+      case 1: piece_stub3<1>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
+      case 2: piece_stub3<2>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
+      default: piece_stub3<3>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
+    }
+  }
+  void segment(const Frame& fr, double d, double sign) {
+    if (FAST) { double o[3]; piece_segment3f(*K, fr, d, sign, o); add3(o); }
+    else piece_segment3(*K, acc, fr, d, sign);
+  }
+};
+template <bool FAST>
+static void f1_pair(const KernelConsts& K, double qx, double qy, double h, const double* tri6, int decomp,
+                    double* out3) {
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  F1EmuSink<FAST> c;
+  c.K = &K;
+  acc3_zero(c.acc);
+  c.f[0] = c.f[1] = c.f[2] = 0.0;
+  c.status = 0;
+  c.counters = nullptr;
+  c.disc_n = 0;
+  const bool route = decomp == 2 ? integrate_hybrid(c, nv) : decomp == 1 ? integrate_edges(c, nv)
+                                                                        : integrate_normalized(c, nv);
+  out3[0] = out3[1] = out3[2] = 0.0;
+  if (!route || !hat_planes_nondeg(nv)) return;
+  double raw[3];
+  if (FAST) {
+    raw[0] = c.f[0] + disc_value3f(K, c.disc_n);
+    raw[1] = c.f[1];
+    raw[2] = c.f[2];
+  } else {
+    PairAcc a;
+    acc_zero(a);
+    if (c.disc_n) piece_disc(K, a, static_cast<double>(c.disc_n));
+    a.v3 = dd_add(a.v3, c.acc.v3);
+    a.g13 = dd_add(a.g13, c.acc.g13);
+    a.g23 = dd_add(a.g23, c.acc.g23);
+    combine_plane(a, dd{0, 0}, dd{0, 0}, dd{1.0, 0}, raw);
+  }
+  double o4[4];
+  finalize(raw, K.c2, h, o4);
+  out3[0] = o4[0];
+  out3[1] = o4[1];
+  out3[2] = o4[2];
+}
+extern "C" {
+// per pair (value, gx, gy) of the constant field; fast = 0 dd, 1 FP64;
+// decomp 0 reference, 1 edges, 2 hybrid
+int core_host_eval_pairs_f1(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
+                            const double* tri6, const double* coef, int ncoef, double c2, double h, int nthreads,
+                            int decomp, int fast, double* out3) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, c2, &K)) return -1;
+  if (nthreads < 1) nthreads = 1;
+  auto work = [&](int tid) {
+    for (int64_t k = tid; k < npairs; k += nthreads) {
+      const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
+      if (fast) f1_pair<true>(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, decomp, out3 + 3 * k);
+      else f1_pair<false>(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, decomp, out3 + 3 * k);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  return 0;
+}
+double core_host_kappa(const double* coef, int ncoef) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, 1.0, &K)) return -1.0;
+  return kernel_kappa(K);
+}
+int core_host_fp64_ok(const double* coef, int ncoef, double h, double max_row) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, 1.0, &K)) return -1;
+  return fp64_path_ok(K, h, max_row) ? 1 : 0;
+}
+
 double core_host_glibc_hypot(double x, double y) { return glibc_hypot(x, y); }
 
 // region-level evaluation with the device core (sphbi_integrate_regions' math, host build)

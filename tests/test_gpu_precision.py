@@ -1,0 +1,93 @@
+"""GPU tier: the constant-field precision policy (sphbi_ctx_set_precision).
+Each named configuration's field == 1 run is evaluated with the double-double
+kernels and with the FP64 kernels; both must meet the literal parity rule
+against the oracle, and 'auto' must pick what fp64_path_ok prescribes."""
+import numpy as np
+import pytest
+
+import oracle_lib as OL
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2507_21686_b200 import sphbi
+    return sphbi
+
+
+@pytest.fixture(scope="module")
+def O():
+    return OL.oracle()
+
+
+def _table(S, k):
+    return S.table1_terms(S.PolyKernel(list(k.coefficients), k.normalization))
+
+
+def _scene(name):
+    from paper_2507_21686_b200 import scenes
+    if name == "cfg1":
+        return scenes.cfg1(), "fp64"
+    if name == "cfg2a":
+        return scenes.cfg2(T=4096), "fp64"
+    if name == "cfg3":
+        sc = scenes.cfg3(target_particles=200_000)
+        return sc, "dd"
+    if name == "cfg5":
+        return scenes.cfg5(n_particles=60_000, n_discs=6, target_tris=20_000, domain=12.0), "fp64"
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2a", "cfg3", "cfg5"])
+def test_precisions_meet_parity_and_auto_selects(S, O, name):
+    sc, expect = _scene(name)
+    k = sc.kernels[0]
+    res = {}
+    for mode in ("dd", "fp64", "auto"):
+        ctx = S.Context(0)
+        ctx.set_precision(mode)
+        v, g, st, pl = S.evaluate(sc.particles, sc.h, sc.triangles, _table(S, k), pairs=sc.pairs, ctx=ctx,
+                                  return_pairs=True)
+        res[mode] = (np.concatenate([v[:, None], g], axis=1), pl, ctx.last_precision())
+        ctx.close()
+    assert res["dd"][2] == "dd" and res["fp64"][2] == "fp64"
+    assert res["auto"][2] == expect, (name, res["auto"][2])
+    assert np.array_equal(res["dd"][1], res["fp64"][1])  # the pair list does not depend on the arithmetic
+    assert np.array_equal(res["auto"][0], res[expect][0])  # auto is bit for bit the path it selected
+    pl = res["dd"][1]
+    st_o, vo, go = OL.oracle_scene_sums(O, sc.particles, sc.triangles, None, k.coefficients, k.normalization, sc.h,
+                                        pl[:, 0], pl[:, 1], threads=16)
+    assert st_o == 0
+    want = np.concatenate([vo[:, None], go], axis=1)
+    r_dd = OL.parity_ratio(res["dd"][0], want, k.normalization, sc.h)
+    r_f = OL.parity_ratio(res["fp64"][0], want, k.normalization, sc.h)
+    r_x = OL.parity_ratio(res["fp64"][0], res["dd"][0], k.normalization, sc.h)
+    print(f"{name}: dd {r_dd:.4f}  fp64 {r_f:.4f}  fp64 vs dd {r_x:.4f} (tolerances)")
+    assert r_dd <= 1.0
+    assert r_f <= 1.0
+    # where auto selects FP64 its distance from the dd result is a small part of the tolerance
+    if expect == "fp64":
+        assert r_x <= 0.1
+
+
+def test_auto_falls_back_to_dd_on_long_rows(S):
+    """cfg2 mode B rows (~1e4 pairs per particle) exceed the FP64 path's row
+    limit: device cell list and explicit (sorted and unsorted) pair lists."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg2(T=8192)
+    sub = scenes.subsample(sc, 256, seed=3)
+    k = sc.kernels[0]
+    ctx = S.Context(0)
+    v, g, st, pl = S.evaluate(sub.particles, sc.h, sc.triangles, _table(S, k), ctx=ctx, return_pairs=True)
+    assert ctx.last_precision() == "dd"
+    assert np.bincount(pl[:, 0]).max() > 500
+    v1, g1, st1 = S.evaluate(sub.particles, sc.h, sc.triangles, _table(S, k), pairs=(pl[:, 0], pl[:, 1]), ctx=ctx)
+    assert ctx.last_precision() == "dd"
+    assert np.array_equal(v1, v) and np.array_equal(g1, g)
+    perm = np.random.default_rng(0).permutation(pl.shape[0])
+    v2, g2, st2 = S.evaluate(sub.particles, sc.h, sc.triangles, _table(S, k), pairs=(pl[perm, 0], pl[perm, 1]),
+                             ctx=ctx)
+    assert ctx.last_precision() == "dd"
+    assert np.array_equal(v2, v) and np.array_equal(g2, g)
+    ctx.close()
