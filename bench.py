@@ -52,7 +52,7 @@ UNIT = "pair-evals/s"
 PROFILES = ROOT / "profiles"
 # ncu FP64 instruction counts of the K4 kernels (tools/ncu_fp64.py); the frozen
 # first-kernel F_pair of BASELINE.md §5 stays in F_pair.json
-FP64_PROFILE = {"cfg5": PROFILES / "r02_fp64_cfg5.json", "cfg2a": PROFILES / "r02_fp64_cfg2a.json"}
+FP64_PROFILE = {"cfg5": PROFILES / "r02m_fp64_cfg5.json", "cfg2a": PROFILES / "r02m_fp64_cfg2a.json"}
 F_PAIR_FILE = PROFILES / "F_pair.json"
 
 

@@ -519,7 +519,8 @@ np.savez(sys.argv[1], **out)
         res = []
         for flag in ("0", "1"):
             f = os.path.join(d, f"r{flag}.npz")
-            env = dict(os.environ, SPHBI_TWO_PASS=flag)
+            # the two-pass pipeline is the double-double fallback: compare like with like
+            env = dict(os.environ, SPHBI_TWO_PASS=flag, SPHBI_PRECISION="dd")
             r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True)
             assert r.returncode == 0, r.stderr[-2000:]
             res.append(np.load(f))
