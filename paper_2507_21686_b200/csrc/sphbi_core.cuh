@@ -1004,11 +1004,21 @@ inline double kernel_kappa(const KernelConsts& K) {
   for (int k = 0; k <= K.deg; ++k) s += fabs(K.b[k]);
   return s;
 }
-inline bool fp64_path_ok(const KernelConsts& K, double h, double max_row) {
+// the FP64 path's error budget per pair in OUTPUT units (value C2 x, gradient
+// C2 / h x the unit-disc quantities)
+inline double fp64_pair_error(const KernelConsts& K, double h) {
   const double u = 1.1102230246251565e-16;
-  const double per_pair = 4.0 * u * kernel_kappa(K);
-  const double floor_norm = 1e-13 / (h > 1.0 ? h * h : h);
-  return per_pair * sqrt(max_row < 1.0 ? 1.0 : max_row) <= 0.5 * floor_norm;
+  return 4.0 * u * kernel_kappa(K) * fabs(K.c2) * (h < 1.0 ? 1.0 / h : 1.0);
+}
+// one kernel, or the pieces of a piecewise kernel (piece 0 carries the full
+// support and the normalisation the parity floor 1e-13 C/h^2 refers to)
+inline bool fp64_pieces_ok(const KernelConsts* K, const double* h, int n, double max_row) {
+  double err = 0.0;
+  for (int j = 0; j < n; ++j) err += fp64_pair_error(K[j], h[j]);
+  return err * sqrt(max_row < 1.0 ? 1.0 : max_row) <= 0.5 * 1e-13 * fabs(K[0].c2) / (h[0] * h[0]);
+}
+inline bool fp64_path_ok(const KernelConsts& K, double h, double max_row) {
+  return fp64_pieces_ok(&K, &h, 1, max_row);
 }
 
 SPHBI_HD void bump_counter(unsigned long long* counters, int which) {

@@ -264,14 +264,14 @@ sphbi_status make_consts(const sphbi_kernel_desc* k, KernelConsts* K) {
 // Constant-field precision selection (sphbi_ctx_set_precision): the longest
 // row (pairs per particle) for which the FP64 path's a-priori error bound
 // clears the parity floor (fp64_path_ok); 0: double-double, INT64_MAX: forced.
-int64_t fp64_row_limit(const sphbi_ctx* c, const KernelConsts& K, double h) {
+int64_t fp64_row_limit(const sphbi_ctx* c, const KernelConsts* K, const double* h, int n_pieces) {
   if (c->precision == SPHBI_PRECISION_DD || c->force_exact || c->two_pass) return 0;
   if (c->precision == SPHBI_PRECISION_FP64) return INT64_MAX;
-  if (!fp64_path_ok(K, h, 1.0)) return 0;
-  int64_t lo = 1, hi = int64_t(1) << 40;  // largest m with fp64_path_ok(K, h, m)
+  if (!fp64_pieces_ok(K, h, n_pieces, 1.0)) return 0;
+  int64_t lo = 1, hi = int64_t(1) << 40;  // largest m with fp64_pieces_ok(.., m)
   while (lo < hi) {
     const int64_t mid = lo + (hi - lo + 1) / 2;
-    if (fp64_path_ok(K, h, static_cast<double>(mid))) lo = mid; else hi = mid - 1;
+    if (fp64_pieces_ok(K, h, n_pieces, static_cast<double>(mid))) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -3106,7 +3106,9 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   // constant-field arithmetic (sphbi_ctx_set_precision): FP64 when no row of
   // the pair list is longer than row_limit, decided where the rows are known
   c->fp64_now = false;
-  const int64_t row_limit = (!tri_values && !nodal10 && !bc && !pieces && !counts_out) ? fp64_row_limit(c, K, h) : 0;
+  const int64_t row_limit = (tri_values || nodal10 || bc || counts_out) ? 0
+                            : pieces ? fp64_row_limit(c, pieces->K, pieces->h, pieces->n)
+                                     : fp64_row_limit(c, &K, &h, 1);
   // ---- streamed fast path: pinned host buffers, particle-sorted explicit pairs
   if (!p3 && !bc && !pieces && mem == SPHBI_MEM_HOST && n_pairs >= (1 << 20) && pair_particle && pair_triangle && !timing &&
       !pair_list_out && is_pinned(particle_xy) && is_pinned(pair_particle) && is_pinned(pair_triangle) &&

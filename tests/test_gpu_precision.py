@@ -47,8 +47,11 @@ def test_precisions_meet_parity_and_auto_selects(S, O, name):
     for mode in ("dd", "fp64", "auto"):
         ctx = S.Context(0)
         ctx.set_precision(mode)
-        v, g, st, pl = S.evaluate(sc.particles, sc.h, sc.triangles, _table(S, k), pairs=sc.pairs, ctx=ctx,
-                                  return_pairs=True)
+        if sc.pairs is not None:  # explicit list (cfg2 mode A)
+            v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, _table(S, k), pairs=sc.pairs, ctx=ctx)
+            pl = np.stack(sc.pairs, axis=1)
+        else:
+            v, g, st, pl = S.evaluate(sc.particles, sc.h, sc.triangles, _table(S, k), ctx=ctx, return_pairs=True)
         res[mode] = (np.concatenate([v[:, None], g], axis=1), pl, ctx.last_precision())
         ctx.close()
     assert res["dd"][2] == "dd" and res["fp64"][2] == "fp64"
