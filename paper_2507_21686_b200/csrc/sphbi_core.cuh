@@ -873,81 +873,46 @@ SPHBI_HD double poly_f(const dd* c, int deg, double x, int off) {
   for (int j = 0; j < off; ++j) r *= x;
   return r;
 }
-// Chain sums sPv = sum_k b_k/(k+2) P~_(k+1), sIg = sum_k w_k/2 I_k at bound x
-// (radial_chains3 in FP64; the same division-free scaled recurrences).
-SPHBI_HD void radial_chains3f(const KernelConsts& K, double x, double D, double& sPv, double& sIg, double& R) {
+// Difference of the chain sums between two radial bounds u >= lo >= D of one
+// chord distance D (R_x = sqrt(x^2 - D^2) given):
+//   dPv = sPv(u) - sPv(lo),  sPv(x) = sum_k b_k/(k+2) P~_(k+1)(x)
+//   dIg = sIg(u) - sIg(lo),  sIg(x) = sum_k w_k/2 I_k(x)
+// The recurrences (radial_chains3's division-free scaled forms) are linear in
+// the chain values, so they run ONCE on the differences: one logarithm
+//   P~_0(u) - P~_0(lo) = log((u + R_u) / (lo + R_lo))
+// seeds both chains (no chord distance in it: nothing blows up for a particle
+// on the edge line), I_1's seed is (u R_u - lo R_lo - D^2 dP~_0) / 2. Every
+// term is O(1) and the path is judged in absolute terms (see above), so the
+// closed forms need no series near x = D.
+SPHBI_HD void chain_diff3f(const KernelConsts& K, double u, double Ru, double lo, double Rlo, double D,
+                           double& dPv, double& dIg) {
   const int N = K.deg;
-  R = sqrt((x - D) * (x + D));
-  const double s = R / D;
   const double D2 = D * D;
-  double p0, i1;
-  if (s < 0.125) {
-    // asinh(s) and f(s) = s sqrt(1+s^2) - asinh(s) by their Maclaurin series
-    // (|s| < 1/8: 10 terms reach 1e-19 relative); closed forms cancel here
-    const double s2 = s * s;
-    double a = 0.0097616095291941736;   // 46189/262144 / 19 ... asinh coefficients, high to low
-    a = fma(a, s2, -0.011551800896139706);
-    a = fma(a, s2, 0.013964843750000000);
-    a = fma(a, s2, -0.017352764423076923);
-    a = fma(a, s2, 0.022372159090909091);
-    a = fma(a, s2, -0.030381944444444444);
-    a = fma(a, s2, 0.044642857142857144);
-    a = fma(a, s2, -0.075);
-    a = fma(a, s2, 0.16666666666666666);
-    p0 = s - a * s2 * s;  // asinh s = s - s^3/6 + 3/40 s^5 - ...
-    // f(s)/s^3 = 2/3 - s^2/5 + 3/28 s^4 - 5/72 s^6 + 35/704 s^8 - 63/1664 s^10 + 77/2560 s^12 - ...
-    double t = -0.024643841911764706;
-    t = fma(t, s2, 0.030078125);
-    t = fma(t, s2, -0.037860576923076923);
-    t = fma(t, s2, 0.049715909090909091);
-    t = fma(t, s2, -0.069444444444444444);
-    t = fma(t, s2, 0.10714285714285714);
-    t = fma(t, s2, -0.2);
-    t = fma(t, s2, 0.66666666666666663);
-    i1 = 0.5 * D2 * (t * s2 * s);
-  } else {
-    p0 = log((x + R) / D);
-    i1 = 0.5 * (x * R - D2 * p0);
-  }
-  const double R3 = R * R * R;
-  double um2 = p0, um1 = R, vm2 = 0.0, vm1 = i1;
+  const double dp0 = log((u + Ru) / (lo + Rlo));
+  const double di1 = 0.5 * ((u * Ru - lo * Rlo) - D2 * dp0);
+  const double R3u = Ru * Ru * Ru, R3l = Rlo * Rlo * Rlo;
+  double um2 = dp0, um1 = Ru - Rlo, vm2 = 0.0, vm1 = di1;
   double aPv = K.wpv[1].hi * um1;
   double aIg = K.wig[1].hi * vm1;
-  double xpm2 = 1.0, xpm1 = x;
+  double pu = Ru, pl = Rlo;    // x^(m-2) R   at the two bounds (m = 2: R)
+  double qu = R3u, ql = R3l;   // x^(m-2) R^3
   for (int m = 2; m <= N + 2; ++m) {
-    const double um = fma(xpm1 * R, K.dfac[m - 2], (double)(m - 1) * D2 * um2);
-    const double vm = fma(xpm2 * R3, K.efac[m - 2], (double)(m - 2) * D2 * vm2);
+    const double pu1 = pu * u, pl1 = pl * lo;  // x^(m-1) R
+    const double um = fma(K.dfac[m - 2], pu1 - pl1, (double)(m - 1) * D2 * um2);
+    const double vm = fma(K.efac[m - 2], qu - ql, (double)(m - 2) * D2 * vm2);
     aPv = fma(K.wpv[m].hi, um, aPv);
     aIg = fma(K.wig[m].hi, vm, aIg);
     um2 = um1;
     um1 = um;
     vm2 = vm1;
     vm1 = vm;
-    xpm2 = xpm1;
-    xpm1 *= x;
+    pu = pu1;
+    pl = pl1;
+    qu *= u;
+    ql *= lo;
   }
-  sPv = aPv;
-  sIg = aIg;
-}
-// S += sgn * (stub window antiderivative at bound x), tau3 channels, FP64
-SPHBI_HD void stub_bound_sums3f(const KernelConsts& K, double x, double D, double beta, double cb, double sb,
-                                S3f& S, double sgn) {
-  double sPv = 0.0, sIg = 0.0, R = 0.0;
-  if (x != D) radial_chains3f(K, x, D, sPv, sIg, R);
-  double as;
-  if (D <= 0.7 * x)
-    as = asin(D / x);
-  else
-    as = (kHalfPiHi - asin(R / x)) + kHalfPiLo;
-  const double amb = as - beta;
-  const int N = K.deg;
-  const bool one = x == 1.0;
-  const double Pv = one ? K.pv1.hi : poly_f(K.pv, N, x, 2);
-  const double Tg = one ? K.tg1.hi : poly_f(K.tg, N, x, 0);
-  const double Rg = one ? K.rg1.hi : poly_f(K.rg, N, x, 1);
-  S.v3 = fma(sgn, fma(Pv, amb, sPv * D), S.v3);
-  S.gx3 = fma(sgn, 2.0 * (cb * D * Tg - sb * sIg), S.gx3);
-  S.gy3 = fma(sgn, Rg - 2.0 * (cb * sIg + sb * D * Tg), S.gy3);
+  dPv = aPv;
+  dIg = aIg;
 }
 // out[0..2] = sign * (v3, M^T (gx3, gy3))
 SPHBI_HD void s3f_rotate(const S3f& S, const Frame& M, double sign, double* out) {
@@ -955,17 +920,89 @@ SPHBI_HD void s3f_rotate(const S3f& S, const Frame& M, double sign, double* out)
   out[1] = sign * fma(S.gx3, M.m00, S.gy3 * M.m10);
   out[2] = sign * fma(S.gx3, M.m01, S.gy3 * M.m11);
 }
-SPHBI_HD void piece_stub3f(const KernelConsts& K, const Frame& f, double gamma, double l, double D, double beta,
-                           double lo, double u, bool window, double sign, const PieceTrig& T, double* out) {
-  const bool full = l >= 1.0;
-  const double Pv = full ? K.pv1.hi : poly_f(K.pv, K.deg, l, 2);
-  const double Rg = full ? K.rg1.hi : poly_f(K.rg, K.deg, l, 1);
-  S3f S{Pv * gamma, Rg * T.sg, Rg * T.omc};
-  if (window) {
-#pragma unroll 1
-    for (int b = 0; b < 2; ++b) stub_bound_sums3f(K, b == 0 ? u : lo, D, beta, T.cb, T.sb, S, b == 0 ? 1.0 : -1.0);
+// Direct stub from its raw item (region_stub's direct branch, triangle_
+// integrator.hpp:440-475): origin triangle (0, v1, v2), |v1| = r1 >= |v2|,
+// chord distance D, clipped to the unit disc. In the frame with v1 on +x and
+// v2 above, the chord point at radius x sits at polar angle
+//   theta(x) = asin(D / x) - beta     (beta: the triangle's angle at v1),
+// theta(r1) = 0 and theta(|v2|) = gamma, the opening angle. With l = lo = |v2|
+// (a window exists only when v2 is inside the disc) the cone term Pv(l) gamma
+// cancels the window's lower boundary term Pv(lo) theta(lo) identically, and
+// the upper one vanishes unless the chord leaves the disc (u = 1 < r1):
+//   v3  = Pv(u) theta(u) + D dPv
+//   gx3 = Rg(l) sin(gamma) + 2 D cos(beta) dTg - 2 sin(beta) dIg
+//   gy3 = Rg(u) - Rg(l) cos(gamma) - 2 cos(beta) dIg - 2 D sin(beta) dTg
+// (d. = value at u minus value at l), theta(1) = atan of the angle difference
+// of asin(D) and beta from their sines and cosines. One logarithm and at most
+// one arctangent per stub instead of the two arcsines, two arctangents and two
+// logarithms of the per-bound form; the reference's snap of lo onto D (:463,
+// a device for its right-limit evaluation) is not needed here.
+// Without a window (both ends outside or on the circle): the cone alone,
+//   v3 = Pv(l) gamma, gx3 = Rg(l) sin(gamma), gy3 = Rg(l) (1 - cos(gamma)).
+// Returns false when the triangle's angle at v1 is obtuse with a window
+// present (stub_integral's beta validation, elementary_regions.hpp:179-183).
+SPHBI_HD bool stub_item3f(const KernelConsts& K, P2 v1, P2 v2, double r1, double l, double sign, double* out) {
+  const double ir1 = 1.0 / r1;
+  const double c1 = v1.x * ir1, s1 = v1.y * ir1;
+  double w2x = fma(c1, v2.x, s1 * v2.y);
+  double w2y = fma(c1, v2.y, -(s1 * v2.x));
+  Frame f{c1, s1, -s1, c1};
+  if (w2y < 0.0) {  // mirror so that v2 lies above
+    f.m10 = s1;
+    f.m11 = -c1;
+    w2y = -w2y;
+  }
+  const double irw = 1.0 / sqrt(fma(w2x, w2x, w2y * w2y));
+  const double sg = w2y * irw, cg = w2x * irw;
+  const int N = K.deg;
+  const bool lfull = l >= 1.0;
+  const double Rgl = lfull ? K.rg1.hi : poly_f(K.rg, N, l, 1);
+  const double u = fmin(r1, 1.0);
+  S3f S;
+  bool ok = true;
+  if (!(u > l + kGeomEps)) {
+    const double Pvl = lfull ? K.pv1.hi : poly_f(K.pv, N, l, 2);
+    const double omc = cg >= 0.0 ? sg * sg / (1.0 + cg) : 1.0 - cg;  // 1 - cos(gamma), cancellation-free
+    S.v3 = Pvl * atan2(w2y, w2x);
+    S.gx3 = Rgl * sg;
+    S.gy3 = Rgl * omc;
+  } else {
+    // beta from the chord direction at v1: (bx, by) = |v2 - v1| r1 (cos, sin)
+    const double ccx = v2.x - v1.x, ccy = v2.y - v1.y;
+    const double by = fabs(fma(ccy, v1.x, -(ccx * v1.y))), bx = -fma(ccx, v1.x, ccy * v1.y);
+    ok = bx >= -1e-15 * by;  // beta <= pi/2 to rounding, as the double-double path's stub_beta_ok
+    const double irb = 1.0 / sqrt(fma(bx, bx, by * by));
+    const double sb = by * irb, cb = bx * irb;
+    // Chord distance and the chord points' distances from the chord's foot,
+    // R(x) = +-sqrt(x^2 - D^2) (the coordinate along the chord, zero at the foot,
+    // positive towards v1; every chain term is odd in it), from the chord vector (v2 - v1 is exact or nearly
+    // so for a short chord, where |v1 x v2| / |v1 - v2| cancels): D = r1 sin
+    // (beta) -- consistent with beta by construction --, R(l) = -v2 . c,
+    // R(r1) = -v1 . c (c the unit chord vector). Through sqrt(x^2 - D^2) an end
+    // point next to the foot would be ill-conditioned (d R / d D = -D / R), and
+    // the cancellation theta(l) = gamma above holds for the geometric values.
+    const double icc = irb * r1;  // 1 / |v2 - v1|
+    const double D = by * icc;
+    const double Rlo = -fma(v2.x, ccx, v2.y * ccy) * icc;  // signed: a computed foot may sit a few ulp past the true one
+    const double Ru = r1 > 1.0 ? sqrt(fmax((1.0 - D) * (1.0 + D), 0.0)) : bx * icc;
+    double dPv, dIg;
+    chain_diff3f(K, u, Ru, l, Rlo, D, dPv, dIg);
+    const bool one = u == 1.0;
+    const double Tgl = poly_f(K.tg, N, l, 0);
+    const double Tgu = one ? K.tg1.hi : poly_f(K.tg, N, u, 0);
+    const double Rgu = one ? K.rg1.hi : poly_f(K.rg, N, u, 1);
+    double v3 = D * dPv;
+    if (r1 > 1.0) {  // the chord leaves the disc: theta(1) = asin(D) - beta
+      const double th = atan(fma(D, cb, -(Ru * sb)) / fma(Ru, cb, D * sb));
+      v3 = fma(K.pv1.hi, th, v3);
+    }
+    const double dTg = Tgu - Tgl;
+    S.v3 = v3;
+    S.gx3 = fma(Rgl, sg, 2.0 * (D * cb * dTg - sb * dIg));
+    S.gy3 = (Rgu - Rgl * cg) - 2.0 * fma(cb, dIg, D * sb * dTg);
   }
   s3f_rotate(S, f, sign, out);
+  return ok;
 }
 SPHBI_HD void piece_cone3f(const KernelConsts& K, const Frame& f, double gamma, double L, double sign,
                            const PieceTrig& T, double* out) {
@@ -979,9 +1016,11 @@ SPHBI_HD void piece_half_disc3f(const KernelConsts& K, const Frame& f, double si
   const S3f S{K.pv1.hi * kPiHi, 2.0 * K.rg1.hi, 0.0};
   s3f_rotate(S, f, sign, out);
 }
+// Circular segment {x >= d}: the chains between the chord's foot (R = 0) and the circle
 SPHBI_HD void piece_segment3f(const KernelConsts& K, const Frame& f, double d, double sign, double* out) {
-  double sPv, sIg, R;
-  radial_chains3f(K, 1.0, d, sPv, sIg, R);
+  const double R = sqrt((1.0 - d) * (1.0 + d));
+  double sPv, sIg;
+  chain_diff3f(K, 1.0, R, d, 0.0, d, sPv, sIg);
   const double acd = d <= 0.7 ? acos(d) : asin(R);
   const S3f S{2.0 * (K.pv1.hi * acd - sPv * d), 4.0 * sIg, 0.0};
   s3f_rotate(S, f, sign, out);

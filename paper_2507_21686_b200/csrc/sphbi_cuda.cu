@@ -1119,14 +1119,9 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_STUBF)
   SPHBI_ITEM_LOOP(k) {
     const int64_t slot = idx ? idx[k] : k;
     const StubItem it = items[slot];
-    Frame f;
-    double gamma, beta;
-    PieceTrig T;
-    stub_item_geometry(it, f, gamma, beta, status_or, &T);
-    double lo, u;
-    const bool window = it.window(lo, u);
     double o[3];
-    piece_stub3f(K, f, gamma, it.l, it.D, beta, lo, u, window, it.sign(), T, o);
+    if (!stub_item3f(K, P2{it.v1x, it.v1y}, P2{it.v2x, it.v2y}, it.r1, it.l, it.sign(), o))
+      atomicOr(status_or, kStatusDomain);
     out3f_store(out, k, o);
   }
 }

@@ -387,16 +387,16 @@ struct F1EmuSink {
     else piece_cone3(*K, acc, fr, gamma, 1.0, sign, T);
   }
   void stub_raw(P2 v1, P2 v2, double r1, double l, double D, double lo, double u, bool window, double sign) {
+    if (FAST) {
+      double o[3];
+      if (!stub_item3f(*K, v1, v2, r1, l, sign, o)) status |= kStatusDomain;
+      add3(o);
+      return;
+    }
     Frame fr;
     double gamma, beta;
     PieceTrig T;
     stub_frame_angles(v1, v2, r1, fr, gamma, beta, &T);
-    if (FAST) {
-      double o[3];
-      piece_stub3f(*K, fr, gamma, l, D, beta, lo, u, window, sign, T, o);
-      add3(o);
-      return;
-    }
     switch (stub_class(D, lo, u, window)) {
       case 0: piece_stub3<0>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
       case 1: piece_stub3<1>(*K, acc, fr, gamma, l, D, beta, lo, u, window, sign, T); break;
