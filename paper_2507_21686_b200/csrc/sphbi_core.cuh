@@ -67,6 +67,10 @@ struct KernelConsts {
   dd wig[kMaxKernelDegree + 4];   // weight of V_m in sIg  (wh[m] / e_m)
   double dfac[kMaxKernelDegree + 4];  // m!!
   double efac[kMaxKernelDegree + 4];  // e_m
+  // FP64 edge form (edge_sum3f): weight of U_m in the normal-gradient chain
+  // sum, w_(m+1) / (m + 2) / m!!, and Q(x) = sum_k w_k / (k (k + 1)) x^k
+  double wgn[kMaxKernelDegree + 4];
+  double qg[kMaxKernelDegree + 1];
 };
 
 // Exact quotient of a double by a small positive integer, as a dd.
@@ -122,7 +126,9 @@ inline bool build_kernel_consts(const double* coef, int ncoef, double c2, Kernel
     const int ki = m - 2;  // I_m carries b[m-2] and wh[m]
     K->wiv[m] = (ki >= 0 && ki <= deg) ? dd_mul(dd_make(K->b[ki]), inv_e) : z;
     K->wig[m] = (m >= 1 && m <= deg) ? dd_mul(dd_make(K->wh[m]), inv_e) : z;
+    K->wgn[m] = (m + 1 <= deg) ? K->rg[m + 1].hi / K->dfac[m] : 0.0;
   }
+  for (int k = 0; k <= deg; ++k) K->qg[k] = k >= 1 ? K->rg[k].hi / k : 0.0;
   return true;
 }
 
@@ -1025,6 +1031,121 @@ SPHBI_HD void piece_segment3f(const KernelConsts& K, const Frame& f, double d, d
   const S3f S{2.0 * (K.pv1.hi * acd - sPv * d), 4.0 * sIg, 0.0};
   s3f_rotate(S, f, sign, out);
 }
+// ---------------------------------------------------------------------------
+// The whole pair in FP64, edge by edge (no pieces, no work items). The
+// triangle clipped to the unit support disc is the signed sum over its edges
+// (a -> b) of the origin triangles (0, a, b) clipped to the disc (the edge sum
+// of integrate_edges). With t the unit chord vector, n = (t.y, -t.x), the chord
+// coordinate s = p . t (zero at the foot) and the signed chord distance
+// Ds = a . n = (a x b) / |b - a|, a ray's polar angle obeys d(theta) =
+// Ds / x^2 ds, x = sqrt(Ds^2 + s^2), so over the part of the chord inside the
+// disc (|s| < sc = sqrt(1 - Ds^2)):
+//   value     = Ds [ sum_k b_k/(k+2) P~_(k+1)(s) ]        P~_m(s) = int_0^s x^(m-1) ds
+//   gradient  = n Ds^2 [ sum_k w_k/(k+1) P~_(k-1)(s) ] + t Ds [ Q(x) ],
+//               Q(x) = sum_k w_k / (k (k + 1)) x^k
+// (P~_0 = asinh(s / D), P~_1 = s, P~_m = (x^(m-1) s + (m-1) D^2 P~_(m-2)) / m:
+// the stub chain of elementary_regions.hpp:175-232 in the chord coordinate, odd
+// in s, valid through the foot -- no split, no cone term), and over the parts
+// of the chord outside the disc the integrand is the disc's constant:
+//   value     = Pv(1) (theta(s1) - theta(s0)),  theta differences by one atan2
+//   gradient  = Rg(1) ( n [s / x] - t Ds [1 / x] )
+// One logarithm per edge (the chains run once, on the difference between the
+// two ends), at most two arctangents, no other transcendental. Every term is
+// O(kappa) and the result is judged against the absolute parity floor (see the
+// FP64 notes above); fp64_path_ok's bound was measured on this form too.
+// ---------------------------------------------------------------------------
+// contribution of s in [s0, s1] with the chord outside the disc
+SPHBI_HD void edge_outside3f(double pv1, double rg1, double Ds, double D2, double s0, double x0, double s1,
+                             double x1, double& V, double& Gn, double& Gt) {
+  const double ang = atan2(fabs(Ds) * (s1 - s0), fma(s0, s1, D2));  // theta(s1) - theta(s0) in (0, pi), for Ds > 0
+  V += pv1 * (Ds < 0.0 ? -ang : ang);
+  const double ix0 = 1.0 / x0, ix1 = 1.0 / x1;
+  Gn = fma(rg1, s1 * ix1 - s0 * ix0, Gn);
+  Gt = fma(rg1 * Ds, ix0 - ix1, Gt);
+}
+SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
+  const int N = K.deg;
+  const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
+  // the three edges through one copy of the code: (a, b, c) rotate in registers
+  P2 a = v[0], b = v[1], c = v[2];
+  double ra = sqrt(fma(a.x, a.x, a.y * a.y)), rb = sqrt(fma(b.x, b.x, b.y * b.y)),
+         rc = sqrt(fma(c.x, c.x, c.y * c.y));
+  double V = 0.0, Gx = 0.0, Gy = 0.0;
+#pragma unroll 1
+  for (int e = 0; e < 3; ++e) {
+    if (e > 0) {
+      const P2 t = a;
+      a = b;
+      b = c;
+      c = t;
+      const double tr = ra;
+      ra = rb;
+      rb = rc;
+      rc = tr;
+    }
+    const double ex = b.x - a.x, ey = b.y - a.y;
+    const double L2 = fma(ex, ex, ey * ey);
+    if (!(L2 > 0.0)) continue;
+    const double iL = 1.0 / sqrt(L2);
+    const double tx = ex * iL, ty = ey * iL;
+    // origin on the edge line (incl. on an end point): zero-area origin
+    // triangle, as integrate_edges. Plain products: a x b is exactly zero then.
+    if (a.x * b.y - a.y * b.x == 0.0) continue;
+    const double Ds = (a.x * ey - a.y * ex) * iL;
+    if (Ds == 0.0) continue;
+    const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
+    const double D = fabs(Ds), D2 = Ds * Ds;
+    double Ve = 0.0, Gn = 0.0, Gt = 0.0;
+    const double sc = D < 1.0 ? sqrt((1.0 - D) * (1.0 + D)) : 0.0;
+    if (!(D < 1.0) || sa >= sc || sb <= -sc) {
+      edge_outside3f(pv1, rg1, Ds, D2, sa, ra, sb, rb, Ve, Gn, Gt);
+    } else {
+      // inside part [slo, shi] and the (up to two) outside parts
+      double slo = sa, xlo = ra, shi = sb, xhi = rb;
+      if (sa < -sc) {
+        edge_outside3f(pv1, rg1, Ds, D2, sa, ra, -sc, 1.0, Ve, Gn, Gt);
+        slo = -sc;
+        xlo = 1.0;
+      }
+      if (sb > sc) {
+        edge_outside3f(pv1, rg1, Ds, D2, sc, 1.0, sb, rb, Ve, Gn, Gt);
+        shi = sc;
+        xhi = 1.0;
+      }
+      // x + s without cancellation on the far side of the foot
+      const double nh = shi >= 0.0 ? xhi + shi : D2 / (xhi - shi);
+      const double nl = slo >= 0.0 ? xlo + slo : D2 / (xlo - slo);
+      double um2 = log(nh / nl), um1 = shi - slo;  // differences of U_0 = P~_0, U_1 = P~_1
+      double aPv = K.wpv[1].hi * um1;
+      double aGn = fma(K.wgn[0], um2, K.wgn[1] * um1);
+      double ph = shi, pl = slo;  // x^(m-2) s at the two ends
+      for (int m = 2; m <= N + 1; ++m) {
+        ph *= xhi;
+        pl *= xlo;
+        const double um = fma(K.dfac[m - 2], ph - pl, (double)(m - 1) * D2 * um2);
+        aPv = fma(K.wpv[m].hi, um, aPv);
+        aGn = fma(K.wgn[m], um, aGn);
+        um2 = um1;
+        um1 = um;
+      }
+      double qh = K.qg[N], ql = K.qg[N];
+      for (int k = N - 1; k >= 0; --k) {
+        qh = fma(qh, xhi, K.qg[k]);
+        ql = fma(ql, xlo, K.qg[k]);
+      }
+      Ve = fma(Ds, aPv, Ve);
+      Gn = fma(D2, aGn, Gn);
+      Gt = fma(Ds, qh - ql, Gt);
+    }
+    V += Ve;
+    Gx += fma(Gn, ty, Gt * tx);   // n = (t.y, -t.x)
+    Gy += fma(Gt, ty, -(Gn * tx));
+  }
+  raw3[0] = V;
+  raw3[1] = Gx;
+  raw3[2] = Gy;
+}
+
 // A signed count of full unit discs: (v3, g13, g23) += n * (2 pi Pv(1), 0, 0)
 SPHBI_HD double disc_value3f(const KernelConsts& K, int disc_n) { return (double)disc_n * (2.0 * kPiHi) * K.pv1.hi; }
 

@@ -81,6 +81,9 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
+#ifndef SPHBI_MINB_EDGE
+#define SPHBI_MINB_EDGE 6
+#endif
 #ifndef SPHBI_MINB_STUBF
 #define SPHBI_MINB_STUBF 6
 #endif
@@ -161,7 +164,8 @@ struct sphbi_ctx {
   // clears the parity floor, else double-double), or forced either way
   // (sphbi_ctx_set_precision, SPHBI_PRECISION)
   int precision = SPHBI_PRECISION_AUTO;
-  bool fp64_now = false;  // this call's constant-field pipelines run the FP64 piece kernels
+  bool fp64_now = false;  // this call's constant-field pairs run in FP64
+  bool fp64_pieces = false;  // SPHBI_FP64_PIECES=1: FP64 through the work-item pipeline (k_pipe_*_f) instead of the edge kernel
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   unsigned long long* d_counters = nullptr;
@@ -1322,6 +1326,34 @@ __global__ void __launch_bounds__(128)
   for (int q = 0; q < stride; ++q) out[stride * r.k + q] = o[q];
 }
 
+// ---------------------------------------------------------------------------
+// K4 on the FP64 constant-field path: ONE kernel, thread per pair. The pair is
+// evaluated edge by edge in closed form (sphbi_core.cuh edge_sum3f): no
+// decomposition into pieces, no work items, no sort -- 72 B in, 24 B out per
+// pair. Same canonical order and normalisation as every other path (the
+// result is bitwise independent of the triangle's vertex order), same
+// degenerate-triangle rule (integrate_normalized :640 / hat planes :255-269).
+// ---------------------------------------------------------------------------
+template <class Src>
+__global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
+    k_edge_pairs_f(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h, int stride,
+                   double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6], a3[3];
+  src.load(k, qx, qy, t6, a3);
+  P2 nv[3];
+  int perm[3];
+  normalized_pair(qx, qy, h, t6, nv, perm);
+  double o[4] = {0.0, 0.0, 0.0, 0.0};
+  if (!(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes_nondeg(nv)) {
+    double raw[3];
+    edge_sum3f(K, nv, raw);
+    finalize(raw, K.c2, h, o);
+  }
+  for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
+}
+
 // combine, vertex-basis mode: per pair and vertex i (original order) the
 // finalized (value, grad_x, grad_y[, imag = 0]) of the hat field of vertex i;
 // stride 12 (integrate_triangle_bases' layout) or 9 (basis cache, no imag).
@@ -2353,6 +2385,11 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   if (n <= 0) return SPHBI_OK;
   if (c->force_exact || c->two_pass) return run_pipeline_dense(c, K, h, src, n, mode, stride, dout, dflags, ctr, p3);
   const bool f1 = mode == 0 && src.vals == nullptr;
+  if (f1 && c->fp64_now && !c->fp64_pieces) {
+    // FP64 constant-field path: the whole pair in one kernel (edge form)
+    k_edge_pairs_f<<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
+    return check_launch(c, "k_edge_pairs_f");
+  }
   const int64_t cap = slot_chunk(mode, f1);
   if (n > cap) {
     for (int64_t o = 0; o < n; o += cap) {
@@ -2779,6 +2816,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
       }
       if (!w.empty()) c->stream_ramp = w;
     }
+    if (const char* fp = std::getenv("SPHBI_FP64_PIECES"); fp && fp[0] == '1') c->fp64_pieces = true;
     if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
       const std::string v(pm);
       if (v == "dd") c->precision = SPHBI_PRECISION_DD;

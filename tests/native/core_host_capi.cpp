@@ -448,8 +448,24 @@ static void f1_pair(const KernelConsts& K, double qx, double qy, double h, const
   out3[1] = o4[1];
   out3[2] = o4[2];
 }
+// the whole pair by the FP64 edge form (k_edge_pairs_f)
+static void f1_pair_edges(const KernelConsts& K, double qx, double qy, double h, const double* tri6, double* out3) {
+  P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
+  int perm[3];
+  canonicalize(v, perm);
+  P2 nv[3];
+  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  out3[0] = out3[1] = out3[2] = 0.0;
+  if (fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps || !hat_planes_nondeg(nv)) return;
+  double raw[3], o4[4];
+  edge_sum3f(K, nv, raw);
+  finalize(raw, K.c2, h, o4);
+  out3[0] = o4[0];
+  out3[1] = o4[1];
+  out3[2] = o4[2];
+}
 extern "C" {
-// per pair (value, gx, gy) of the constant field; fast = 0 dd, 1 FP64;
+// per pair (value, gx, gy) of the constant field; fast = 0 dd, 1 FP64 pieces, 2 FP64 edge form;
 // decomp 0 reference, 1 edges, 2 hybrid
 int core_host_eval_pairs_f1(int64_t npairs, const int64_t* pp, const int64_t* pt, const double* pxy,
                             const double* tri6, const double* coef, int ncoef, double c2, double h, int nthreads,
@@ -460,7 +476,8 @@ int core_host_eval_pairs_f1(int64_t npairs, const int64_t* pp, const int64_t* pt
   auto work = [&](int tid) {
     for (int64_t k = tid; k < npairs; k += nthreads) {
       const int64_t i = pp ? pp[k] : k, t = pt ? pt[k] : k;
-      if (fast) f1_pair<true>(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, decomp, out3 + 3 * k);
+      if (fast == 2) f1_pair_edges(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, out3 + 3 * k);
+      else if (fast) f1_pair<true>(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, decomp, out3 + 3 * k);
       else f1_pair<false>(K, pxy[2 * i], pxy[2 * i + 1], h, tri6 + 6 * t, decomp, out3 + 3 * k);
     }
   };

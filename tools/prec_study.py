@@ -24,6 +24,7 @@ from paper_2507_21686_b200 import scenes  # noqa: E402
 
 P, D, I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int64
 U = 2.0 ** -53
+FAST = 2  # 1: FP64 piece kernels' math, 2: the FP64 edge form (the product's FP64 path)
 
 
 def f1(C, pp, pt, pxy, tri, coef, c2, h, fast, decomp=2, threads=16):
@@ -63,7 +64,7 @@ def study(name, sc, O, R, C, max_pairs=None, ref_check=True):
     t0 = time.time()
     a = f1(C, pp, pt, sc.particles, sc.triangles, coef, c2, h, 0)
     t1 = time.time()
-    b = f1(C, pp, pt, sc.particles, sc.triangles, coef, c2, h, 1)
+    b = f1(C, pp, pt, sc.particles, sc.triangles, coef, c2, h, FAST)
     t2 = time.time()
     # unit-disc frame: value / C2, gradient * h / C2
     scale = np.array([1.0 / c2, h / c2, h / c2])
