@@ -1054,6 +1054,15 @@ SPHBI_HD void piece_segment3f(const KernelConsts& K, const Frame& f, double d, d
 // O(kappa) and the result is judged against the absolute parity floor (see the
 // FP64 notes above); fp64_path_ok's bound was measured on this form too.
 // ---------------------------------------------------------------------------
+// a x b by Kahan's difference of products: accurate to a few ulp of the true
+// value for any a, b -- a vertex 1e-12 from the particle (cfg2's stress
+// placements) would lose its digits in a x (b - a), and the folded form below
+// needs every vertex direction seen alike from its two edges.
+SPHBI_HD double cross_exact(P2 a, P2 b) {
+  const double p = a.x * b.y, q = a.y * b.x;
+  const double ep = fma(a.x, b.y, -p), eq = fma(a.y, b.x, -q);
+  return (p - q) + (ep - eq);
+}
 // contribution of s in [s0, s1] with the chord outside the disc
 SPHBI_HD void edge_outside3f(double pv1, double rg1, double Ds, double D2, double s0, double x0, double s1,
                              double x1, double& V, double& Gn, double& Gt) {
@@ -1063,7 +1072,7 @@ SPHBI_HD void edge_outside3f(double pv1, double rg1, double Ds, double D2, doubl
   Gn = fma(rg1, s1 * ix1 - s0 * ix0, Gn);
   Gt = fma(rg1 * Ds, ix0 - ix1, Gt);
 }
-SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
+SPHBI_HDNI void edge_sum3f_general(const KernelConsts& K, const P2* v, double* raw3) {
   const int N = K.deg;
   const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
   // the three edges through one copy of the code: (a, b, c) rotate in registers
@@ -1091,7 +1100,7 @@ SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
     // origin on the edge line (incl. on an end point): zero-area origin
     // triangle, as integrate_edges. Plain products: a x b is exactly zero then.
     if (a.x * b.y - a.y * b.x == 0.0) continue;
-    const double Ds = (a.x * ey - a.y * ex) * iL;
+    const double Ds = cross_exact(a, b) * iL;
     if (Ds == 0.0) continue;
     const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
     const double D = fabs(Ds), D2 = Ds * Ds;
@@ -1141,6 +1150,94 @@ SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
     Gx += fma(Gn, ty, Gt * tx);   // n = (t.y, -t.x)
     Gy += fma(Gt, ty, -(Gn * tx));
   }
+  raw3[0] = V;
+  raw3[1] = Gx;
+  raw3[2] = Gy;
+}
+
+// The same sum with the outside parts folded away (v: canonical order, i.e.
+// counter-clockwise). Over the closed triangle the full-edge angles add up to
+// 2 pi (origin inside: all three Ds > 0) or 0 and the full-edge gradient terms
+// of the disc's constant cancel (a closed loop of unit vectors), so only the
+// chord parts INSIDE the disc contribute:
+//   V = [origin inside] 2 pi Pv(1) + sum_e ( Ds dPv - sign(Ds) Pv(1) dtheta_e )
+//   G = sum_e n ( Ds^2 dGn - Rg(1) [s / x] ) + t Ds ( [Q(x)] + Rg(1) [1 / x] )
+// with [.] between the inside part's two ends (x = 1 on the circle, |vertex|
+// at a vertex inside) and dtheta_e = atan2(D (shi - slo), D^2 + slo shi). An
+// edge that misses the disc costs its geometry only. Pairs with the origin
+// exactly on an edge line or a vertex (a x b == 0: the folded terms are then
+// not 0 / 2 pi) take the general form above.
+SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
+  P2 a = v[0], b = v[1], c = v[2];
+  if (a.x * b.y - a.y * b.x == 0.0 || b.x * c.y - b.y * c.x == 0.0 || c.x * a.y - c.y * a.x == 0.0) {
+    edge_sum3f_general(K, v, raw3);
+    return;
+  }
+  const int N = K.deg;
+  const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
+  double ra = sqrt(fma(a.x, a.x, a.y * a.y)), rb = sqrt(fma(b.x, b.x, b.y * b.y)),
+         rc = sqrt(fma(c.x, c.x, c.y * c.y));
+  double V = 0.0, Gx = 0.0, Gy = 0.0;
+  int npos = 0;
+#pragma unroll 1
+  for (int e = 0; e < 3; ++e) {
+    if (e > 0) {
+      const P2 t = a;
+      a = b;
+      b = c;
+      c = t;
+      const double tr = ra;
+      ra = rb;
+      rb = rc;
+      rc = tr;
+    }
+    const double ex = b.x - a.x, ey = b.y - a.y;
+    const double iL = 1.0 / sqrt(fma(ex, ex, ey * ey));
+    const double tx = ex * iL, ty = ey * iL;
+    const double Ds = cross_exact(a, b) * iL;
+    if (Ds == 0.0) {  // exactly on the edge line after all
+      edge_sum3f_general(K, v, raw3);
+      return;
+    }
+    npos += Ds > 0.0 ? 1 : 0;
+    const double D = fabs(Ds);
+    if (!(D < 1.0)) continue;
+    const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
+    const double sc = sqrt((1.0 - D) * (1.0 + D));
+    if (!(sa < sc && sb > -sc)) continue;
+    const double D2 = Ds * Ds;
+    const bool clo = sa < -sc, chi = sb > sc;  // the end lies outside the disc: clamp onto the circle
+    const double slo = clo ? -sc : sa, shi = chi ? sc : sb;
+    const double xlo = clo ? 1.0 : ra, xhi = chi ? 1.0 : rb;
+    const double ixlo = 1.0 / xlo, ixhi = 1.0 / xhi;
+    const double nh = shi >= 0.0 ? xhi + shi : D2 / (xhi - shi);
+    const double nl = slo >= 0.0 ? xlo + slo : D2 / (xlo - slo);
+    double um2 = log(nh / nl), um1 = shi - slo;
+    double aPv = K.wpv[1].hi * um1;
+    double aGn = fma(K.wgn[0], um2, K.wgn[1] * um1);
+    double ph = shi, pl = slo;
+    for (int m = 2; m <= N + 1; ++m) {
+      ph *= xhi;
+      pl *= xlo;
+      const double um = fma(K.dfac[m - 2], ph - pl, (double)(m - 1) * D2 * um2);
+      aPv = fma(K.wpv[m].hi, um, aPv);
+      aGn = fma(K.wgn[m], um, aGn);
+      um2 = um1;
+      um1 = um;
+    }
+    double qh = K.qg[N], ql = K.qg[N];
+    for (int k = N - 1; k >= 0; --k) {
+      qh = fma(qh, xhi, K.qg[k]);
+      ql = fma(ql, xlo, K.qg[k]);
+    }
+    const double ang = atan2(D * (shi - slo), fma(slo, shi, D2));
+    V += fma(Ds, aPv, -(pv1 * (Ds < 0.0 ? -ang : ang)));
+    const double Gn = fma(D2, aGn, -(rg1 * (shi * ixhi - slo * ixlo)));
+    const double Gt = Ds * ((qh - ql) + rg1 * (ixhi - ixlo));
+    Gx += fma(Gn, ty, Gt * tx);  // n = (t.y, -t.x)
+    Gy += fma(Gt, ty, -(Gn * tx));
+  }
+  if (npos == 3) V += 2.0 * kPiHi * pv1;
   raw3[0] = V;
   raw3[1] = Gx;
   raw3[2] = Gy;

@@ -26,7 +26,7 @@ METRICS = ["gpu__time_duration.sum",
            "smsp__thread_inst_executed_per_inst_executed.ratio",
            "sm__warps_active.avg.pct_of_peak_sustained_active",
            "dram__bytes_read.sum", "dram__bytes_write.sum"]
-K4 = ("k_pre_class", "k_sig_", "k_pipe_")
+K4 = ("k_pre_class", "k_sig_", "k_pipe_", "k_edge_pairs")
 
 
 def num(s):
