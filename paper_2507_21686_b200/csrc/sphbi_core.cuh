@@ -1072,7 +1072,7 @@ SPHBI_HD void edge_outside3f(double pv1, double rg1, double Ds, double D2, doubl
   Gn = fma(rg1, s1 * ix1 - s0 * ix0, Gn);
   Gt = fma(rg1 * Ds, ix0 - ix1, Gt);
 }
-SPHBI_HDNI void edge_sum3f_general(const KernelConsts& K, const P2* v, double* raw3) {
+SPHBI_HD void edge_sum3f_general(const KernelConsts& K, const P2* v, double* raw3) {
   const int N = K.deg;
   const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
   // the three edges through one copy of the code: (a, b, c) rotate in registers
@@ -1164,55 +1164,44 @@ SPHBI_HDNI void edge_sum3f_general(const KernelConsts& K, const P2* v, double* r
 //   G = sum_e n ( Ds^2 dGn - Rg(1) [s / x] ) + t Ds ( [Q(x)] + Rg(1) [1 / x] )
 // with [.] between the inside part's two ends (x = 1 on the circle, |vertex|
 // at a vertex inside) and dtheta_e = atan2(D (shi - slo), D^2 + slo shi). An
-// edge that misses the disc costs its geometry only. Pairs with the origin
-// exactly on an edge line or a vertex (a x b == 0: the folded terms are then
-// not 0 / 2 pi) take the general form above.
-SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
-  P2 a = v[0], b = v[1], c = v[2];
-  if (a.x * b.y - a.y * b.x == 0.0 || b.x * c.y - b.y * c.x == 0.0 || c.x * a.y - c.y * a.x == 0.0) {
-    edge_sum3f_general(K, v, raw3);
-    return;
-  }
+// edge that misses the disc costs its geometry only. With the origin exactly
+// on an edge line or a vertex (a x b == 0: cfg2's d = 0 placements) the folded
+// terms are not 0 / 2 pi; such a pair skips its zero-area origin triangles and
+// adds the remaining edges' full-edge terms explicitly (edge_sum3f_general's
+// sum, regrouped), one more atan2 per edge.
+// one edge a -> b of the sum (cab = a x b, ra = |a|, ira = 1 / |a|, ...)
+SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double ra, double rb, double ira,
+                          double irb, bool deg, int& npos, double& V, double& Gx, double& Gy) {
+  if (cab == 0.0) return;  // origin on this edge's line: zero-area origin triangle
   const int N = K.deg;
   const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
-  double ra = sqrt(fma(a.x, a.x, a.y * a.y)), rb = sqrt(fma(b.x, b.x, b.y * b.y)),
-         rc = sqrt(fma(c.x, c.x, c.y * c.y));
-  double V = 0.0, Gx = 0.0, Gy = 0.0;
-  int npos = 0;
-#pragma unroll 1
-  for (int e = 0; e < 3; ++e) {
-    if (e > 0) {
-      const P2 t = a;
-      a = b;
-      b = c;
-      c = t;
-      const double tr = ra;
-      ra = rb;
-      rb = rc;
-      rc = tr;
-    }
-    const double ex = b.x - a.x, ey = b.y - a.y;
-    const double iL = 1.0 / sqrt(fma(ex, ex, ey * ey));
-    const double tx = ex * iL, ty = ey * iL;
-    const double Ds = cross_exact(a, b) * iL;
-    if (Ds == 0.0) {  // exactly on the edge line after all
-      edge_sum3f_general(K, v, raw3);
-      return;
-    }
-    npos += Ds > 0.0 ? 1 : 0;
-    const double D = fabs(Ds);
-    if (!(D < 1.0)) continue;
-    const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
-    const double sc = sqrt((1.0 - D) * (1.0 + D));
-    if (!(sa < sc && sb > -sc)) continue;
-    const double D2 = Ds * Ds;
+  const double ex = b.x - a.x, ey = b.y - a.y;
+  const double iL = fast_rsqrt(fma(ex, ex, ey * ey));
+  const double tx = ex * iL, ty = ey * iL;
+  const double Ds = cab * iL;
+  npos += Ds > 0.0 ? 1 : 0;
+  const double D = fabs(Ds), D2 = Ds * Ds;
+  const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
+  double Ve = 0.0, Gn = 0.0, Gt = 0.0;
+  if (deg) {  // full-edge terms, explicitly
+    const double ang = atan2(D * (sb - sa), fma(sa, sb, D2));
+    Ve = pv1 * (Ds < 0.0 ? -ang : ang);
+    Gn = rg1 * (sb * irb - sa * ira);
+    Gt = rg1 * Ds * (ira - irb);
+  }
+  const double sc = D < 1.0 ? sqrt((1.0 - D) * (1.0 + D)) : 0.0;
+  if (D < 1.0 && sa < sc && sb > -sc) {
     const bool clo = sa < -sc, chi = sb > sc;  // the end lies outside the disc: clamp onto the circle
     const double slo = clo ? -sc : sa, shi = chi ? sc : sb;
     const double xlo = clo ? 1.0 : ra, xhi = chi ? 1.0 : rb;
-    const double ixlo = 1.0 / xlo, ixhi = 1.0 / xhi;
-    const double nh = shi >= 0.0 ? xhi + shi : D2 / (xhi - shi);
-    const double nl = slo >= 0.0 ? xlo + slo : D2 / (xlo - slo);
-    double um2 = log(nh / nl), um1 = shi - slo;
+    const double ixlo = clo ? 1.0 : ira, ixhi = chi ? 1.0 : irb;
+    // (x + s) at the two ends, without cancellation on the far side of the
+    // foot (x + s = D^2 / (x - s)); their quotient by one reciprocal
+    const double nh = shi >= 0.0 ? xhi + shi : D2;
+    const double dh = shi >= 0.0 ? 1.0 : xhi - shi;
+    const double nl = slo >= 0.0 ? xlo + slo : D2;
+    const double dl = slo >= 0.0 ? 1.0 : xlo - slo;
+    double um2 = log((nh * dl) * fast_rcp(nl * dh)), um1 = shi - slo;
     double aPv = K.wpv[1].hi * um1;
     double aGn = fma(K.wgn[0], um2, K.wgn[1] * um1);
     double ph = shi, pl = slo;
@@ -1231,13 +1220,29 @@ SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
       ql = fma(ql, xlo, K.qg[k]);
     }
     const double ang = atan2(D * (shi - slo), fma(slo, shi, D2));
-    V += fma(Ds, aPv, -(pv1 * (Ds < 0.0 ? -ang : ang)));
-    const double Gn = fma(D2, aGn, -(rg1 * (shi * ixhi - slo * ixlo)));
-    const double Gt = Ds * ((qh - ql) + rg1 * (ixhi - ixlo));
-    Gx += fma(Gn, ty, Gt * tx);  // n = (t.y, -t.x)
-    Gy += fma(Gt, ty, -(Gn * tx));
+    Ve += fma(Ds, aPv, -(pv1 * (Ds < 0.0 ? -ang : ang)));
+    Gn += fma(D2, aGn, -(rg1 * (shi * ixhi - slo * ixlo)));
+    Gt += Ds * ((qh - ql) + rg1 * (ixhi - ixlo));
   }
-  if (npos == 3) V += 2.0 * kPiHi * pv1;
+  V += Ve;
+  Gx += fma(Gn, ty, Gt * tx);  // n = (t.y, -t.x)
+  Gy += fma(Gt, ty, -(Gn * tx));
+}
+SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
+  const P2 a = v[0], b = v[1], c = v[2];
+  const double cab = cross_exact(a, b), cbc = cross_exact(b, c), cca = cross_exact(c, a);
+  const bool deg = cab == 0.0 || cbc == 0.0 || cca == 0.0;
+  const double qa = fma(a.x, a.x, a.y * a.y), qb = fma(b.x, b.x, b.y * b.y), qc = fma(c.x, c.x, c.y * c.y);
+  // |v| and 1 / |v| (a vertex on the particle: its edges are skipped, cab == 0)
+  const double ira = qa > 0.0 ? fast_rsqrt(qa) : 0.0, irb = qb > 0.0 ? fast_rsqrt(qb) : 0.0,
+               irc = qc > 0.0 ? fast_rsqrt(qc) : 0.0;
+  const double ra = qa * ira, rb = qb * irb, rc = qc * irc;
+  double V = 0.0, Gx = 0.0, Gy = 0.0;
+  int npos = 0;
+  edge_term3f(K, a, b, cab, ra, rb, ira, irb, deg, npos, V, Gx, Gy);
+  edge_term3f(K, b, c, cbc, rb, rc, irb, irc, deg, npos, V, Gx, Gy);
+  edge_term3f(K, c, a, cca, rc, ra, irc, ira, deg, npos, V, Gx, Gy);
+  if (!deg && npos == 3) V += 2.0 * kPiHi * K.pv1.hi;
   raw3[0] = V;
   raw3[1] = Gx;
   raw3[2] = Gy;

@@ -542,6 +542,21 @@ struct SceneSrc {  // particle pp[k] vs triangle pt[k]
 #pragma unroll
     for (int j = 0; j < 3; ++j) a3[j] = vals ? __ldg(vals + 3 * (int64_t)t + j) : 1.0;
   }
+  // geometry only, triangle by three 16-byte loads (48-byte records, 16-byte aligned array)
+  __device__ void load_geom(int64_t k, double& qx, double& qy, double* t6) const {
+    const int i = pp[k], t = pt[k];
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    qx = p.x;
+    qy = p.y;
+    const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
+    const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    t6[0] = a.x;
+    t6[1] = a.y;
+    t6[2] = b.x;
+    t6[3] = b.y;
+    t6[4] = c.x;
+    t6[5] = c.y;
+  }
   __device__ void load_vals(int64_t k, double* a3) const {
     if (!vals) {
       a3[0] = a3[1] = a3[2] = 1.0;
@@ -564,6 +579,12 @@ struct DirectSrc {  // query, triangle, values per item
     for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
 #pragma unroll
     for (int j = 0; j < 3; ++j) a3[j] = vals ? vals[3 * k + j] : 1.0;
+  }
+  __device__ void load_geom(int64_t k, double& qx, double& qy, double* t6) const {
+    qx = q[2 * k];
+    qy = q[2 * k + 1];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) t6[j] = tri[6 * k + j];
   }
   __device__ void load_vals(int64_t k, double* a3) const {
 #pragma unroll
@@ -1340,11 +1361,26 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
                    double* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  double qx, qy, t6[6], a3[3];
-  src.load(k, qx, qy, t6, a3);
-  P2 nv[3];
-  int perm[3];
-  normalized_pair(qx, qy, h, t6, nv, perm);
+  double qx, qy, t6[6];
+  src.load_geom(k, qx, qy, t6);
+  // canonicalize (lexicographic lead vertex, then counter-clockwise:
+  // triangle_integrator.hpp:680-694) and normalize, in registers
+  P2 v0{t6[0], t6[1]}, v1{t6[2], t6[3]}, v2{t6[4], t6[5]};
+  {
+    const bool l1 = v1.x < v0.x || (v1.x == v0.x && v1.y < v0.y);
+    const P2 vl = l1 ? v1 : v0;
+    const bool l2 = v2.x < vl.x || (v2.x == vl.x && v2.y < vl.y);
+    const int lead = l2 ? 2 : (l1 ? 1 : 0);
+    const P2 w0 = lead == 0 ? v0 : (lead == 1 ? v1 : v2);
+    const P2 w1 = lead == 0 ? v1 : (lead == 1 ? v2 : v0);
+    const P2 w2 = lead == 0 ? v2 : (lead == 1 ? v0 : v1);
+    const bool cw = signed_area(w0, w1, w2) < 0.0;
+    v0 = w0;
+    v1 = cw ? w2 : w1;
+    v2 = cw ? w1 : w2;
+  }
+  const P2 nv[3] = {P2{(v0.x - qx) / h, (v0.y - qy) / h}, P2{(v1.x - qx) / h, (v1.y - qy) / h},
+                    P2{(v2.x - qx) / h, (v2.y - qy) / h}};
   double o[4] = {0.0, 0.0, 0.0, 0.0};
   if (!(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes_nondeg(nv)) {
     double raw[3];

@@ -211,6 +211,36 @@ SPHBI_HD void dsincos(double x, double* s, double* c) {
 #endif
 }
 
+// 1 / x and 1 / sqrt(x) for the FP64 constant-field path (positive, normal x):
+// the hardware's approximate seed (about 20 bits) refined by two Newton steps
+// -- within 1-2 ulp, not correctly rounded, a third of the instructions of the
+// IEEE division / square root the compiler emits for `1.0 / x`. The geometry
+// that replicates the reference's IEEE operation order never uses these.
+SPHBI_HD double fast_rcp(double x) {
+#if defined(__CUDA_ARCH__)
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+#else
+  return 1.0 / x;
+#endif
+}
+SPHBI_HD double fast_rsqrt(double x) {
+#if defined(__CUDA_ARCH__)
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);      // 1 - x y^2
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, e, y);
+#else
+  return 1.0 / sqrt(x);
+#endif
+}
+
 // atan2, out of line on the device (3 call sites in the decomposition).
 SPHBI_HDNI double d_atan2(double y, double x) { return atan2(y, x); }
 
