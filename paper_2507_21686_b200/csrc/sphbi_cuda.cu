@@ -2082,32 +2082,52 @@ __global__ void __launch_bounds__(256)
                     const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
                     const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2,
                     int* __restrict__ pp, int* __restrict__ pt) {
+  // A warp takes 32 consecutive particles. Staged rows (<= kFindStage hits from
+  // a short cell list) are copied by the whole warp, one row per step: lane l
+  // moves the row's l-th hit, so the staging reads and the pair-list writes are
+  // contiguous (a thread-per-particle copy ran 2 of 32 lanes on average).
+  const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= p_count) return;
-  const int i = p_begin + static_cast<int>(r);
-  const unsigned long long o = off[i] - base, n = off[i + 1] - off[i];
-  const unsigned c = pcell[i];
-  const unsigned long long cb = cell_start[c], ce = cell_start[c + 1];
-  // staged by the count pass: short lists (lane walk) with <= kFindStage hits
-  if (n <= static_cast<unsigned long long>(kFindStage) && ce - cb <= kFindLaneMax) {
-    const int* src = stage + static_cast<int64_t>(i) * kFindStage;
-    for (unsigned long long q = 0; q < n; ++q) {
-      pp[o + q] = i;
-      pt[o + q] = src[q];
-    }
-    return;
+  const bool valid = r < p_count;
+  const int i = p_begin + static_cast<int>(valid ? r : 0);
+  unsigned long long o = 0, n = 0, cb = 0, ce = 0;
+  if (valid) {
+    o = off[i] - base;
+    n = off[i + 1] - off[i];
+    const unsigned c = pcell[i];
+    cb = cell_start[c];
+    ce = cell_start[c + 1];
   }
-  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
-  unsigned long long m = 0;
-  for (unsigned long long k = cb; k < ce; ++k) {
-    const int t = __ldg(cell_tris + k);
-    double tv[6];
-    load_tri6(tri, t, tv);
-    if (pair_dist2(p.x, p.y, tv) < h2) {
-      pp[o + m] = i;
-      pt[o + m] = t;
-      ++m;
+  const bool staged = n <= static_cast<unsigned long long>(kFindStage) && ce - cb <= kFindLaneMax;
+  unsigned todo = __ballot_sync(0xffffffffu, valid && n > 0 && staged);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int qi = __shfl_sync(0xffffffffu, i, src);
+    const unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
+    const int qn = static_cast<int>(__shfl_sync(0xffffffffu, n, src));
+    if (lane < qn) {
+      pp[qo + lane] = qi;
+      pt[qo + lane] = stage[static_cast<int64_t>(qi) * kFindStage + lane];
     }
+  }
+  // rows with more hits than slots, or from a long cell list (walked by the
+  // whole warp in the count pass, not staged): the warp walks the list again
+  unsigned redo = __ballot_sync(0xffffffffu, valid && n > 0 && !staged);
+  double px = 0.0, py = 0.0;
+  if (redo & (1u << lane)) {
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    px = p.x;
+    py = p.y;
+  }
+  while (redo) {
+    const int src = __ffs(redo) - 1;
+    redo &= redo - 1;
+    const double qx = __shfl_sync(0xffffffffu, px, src), qy = __shfl_sync(0xffffffffu, py, src);
+    const unsigned long long qb = __shfl_sync(0xffffffffu, cb, src), qe = __shfl_sync(0xffffffffu, ce, src);
+    const unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
+    const int qi = __shfl_sync(0xffffffffu, i, src);
+    walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, 1, pp, pt);
   }
 }
 
@@ -3553,12 +3573,16 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     }
     // chunk boundaries (particle index, pair offset), computed on the device
     std::vector<long long> cb;
-    if (total_pairs > kMaxChunkPairs) {
-      const int max_chunks = static_cast<int>(std::min<int64_t>(n_particles, 2 * (total_pairs / kMaxChunkPairs) + 8));
+    // the FP64 edge kernel needs no per-pair scratch: 32 Mi-pair chunks (only
+    // the per-chunk D2H overlap of the host-memory path wants chunks at all)
+    const int64_t chunk_pairs = (c->fp64_now && !c->fp64_pieces && !pieces) ? (int64_t(1) << 25) : int64_t(kMaxChunkPairs);
+    if (total_pairs > chunk_pairs) {
+      const int max_chunks = static_cast<int>(std::min<int64_t>(n_particles, 2 * (total_pairs / chunk_pairs) + 8));
       long long* dbounds;
       if ((st = scratch_t(c, kBufGeneric0, 2 * (size_t)max_chunks + 4, &dbounds)) != SPHBI_OK) return st;
       int* dn = reinterpret_cast<int*>(dbounds + 2 * max_chunks + 2);
-      k_chunk_bounds<<<1, 1, 0, s>>>(static_cast<int>(n_particles), poff, kMaxChunkPairs, max_chunks, dbounds, dn);
+      k_chunk_bounds<<<1, 1, 0, s>>>(static_cast<int>(n_particles), poff, static_cast<unsigned long long>(chunk_pairs),
+                                     max_chunks, dbounds, dn);
       if ((st = check_launch(c, "k_chunk_bounds")) != SPHBI_OK) return st;
       int nch = 0;
       cb.resize(2 * (size_t)max_chunks + 2);
