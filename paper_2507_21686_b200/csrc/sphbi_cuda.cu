@@ -148,6 +148,7 @@ enum ScratchSlot {
   kBufPieceOut,
   kBufPieceFlag,
   kBufStage,
+  kBufPartStart,
   kNumBufs
 };
 
@@ -197,6 +198,7 @@ struct sphbi_ctx {
   cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  bool no_tile_find = true;     // SPHBI_FIND=tile selects the cell-tile finder (k_find_tile); default: lane-per-particle walk (measured faster on cfg5: 9.7 vs 10.6 ms)
   bool no_sparse_find = false;  // SPHBI_NO_SPARSE_FIND=1: always walk all particles in cell order
   int stream_chunk_log2 = 0;    // SPHBI_STREAM_CHUNK_LOG2: equal chunks of 2^L particles (0: the ramp)
   std::vector<double> stream_ramp{1, 2, 3, 4, 3, 2, 1};  // SPHBI_STREAM_RAMP: relative chunk sizes
@@ -2131,6 +2133,171 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cell-tile pair finding (dense scenes: most particles share their cell's list
+// with ~15 neighbours). One warp per grid cell: the cell's candidate triangles
+// are staged in shared memory with cp.async (16-byte asynchronous copies: the
+// list is a gather by triangle id, so no bulk copy applies), 96 at a time;
+// then for each particle of the cell (cell-sorted order) the 32 lanes test 32
+// staged candidates at once and a ballot records the hits. A particle's hit
+// pattern over its first 96 candidates is kept as a 96-bit mask (pmask), its
+// count goes to the scan; the fill (k_expand_masks) turns masks into pairs
+// without touching a triangle again. Against the lane-per-particle walk this
+// keeps all 32 lanes on one list (no ragged tails, no idle lanes on empty
+// cells) and reads each triangle once per cell instead of once per particle.
+// Cells with more than 96 candidates are counted here batch by batch and
+// re-walked by the fill (mask flag).
+// ---------------------------------------------------------------------------
+constexpr int kTileBatch = 96, kTileWarps = 8;
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32 * kTileWarps, 3)
+    k_find_tile(int ncells, const unsigned long long* __restrict__ pstart, const int* __restrict__ sorder,
+                const double* __restrict__ pxy, const unsigned long long* __restrict__ cell_start,
+                const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2,
+                unsigned long long* __restrict__ pcount, uint4* __restrict__ pmask, unsigned long long row_limit,
+                unsigned* __restrict__ row_flag) {
+  __shared__ double2 sv[kTileWarps][3][kTileBatch];  // vertex k of staged triangle j: sv[w][k][j]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * kTileWarps + w;
+  if (c >= ncells) return;
+  const unsigned long long ps = pstart[c], pe = pstart[c + 1];
+  const unsigned long long cb = cell_start[c], ce = cell_start[c + 1];
+  if (ps == pe || cb == ce) return;  // counts were zeroed beforehand
+  const unsigned flag_long = ce - cb > static_cast<unsigned long long>(kTileBatch) ? 1u : 0u;
+  for (unsigned long long b0 = cb; b0 < ce; b0 += kTileBatch) {
+    const int nb = static_cast<int>(ce - b0 < static_cast<unsigned long long>(kTileBatch) ? ce - b0 : kTileBatch);
+    __syncwarp();  // the previous batch has been read
+#pragma unroll
+    for (int r = 0; r < kTileBatch / 32; ++r) {
+      const int j = 32 * r + lane;
+      if (j < nb) {
+        const int t = __ldg(cell_tris + b0 + j);
+        const double2* src = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
+        cp_async16(&sv[w][0][j], src);
+        cp_async16(&sv[w][1][j], src + 1);
+        cp_async16(&sv[w][2][j], src + 2);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (unsigned long long p0 = ps; p0 < pe; p0 += 32) {
+      // 32 particles of the cell at a time: lane l holds particle p0 + l
+      const bool have = p0 + lane < pe;
+      const int mi = have ? sorder[p0 + lane] : 0;
+      double2 mp = make_double2(0.0, 0.0);
+      if (have) mp = __ldg(reinterpret_cast<const double2*>(pxy) + mi);
+      unsigned m0 = 0u, m1 = 0u, m2 = 0u;
+      const int np = static_cast<int>(pe - p0 < 32 ? pe - p0 : 32);
+      for (int q = 0; q < np; ++q) {
+        const double qx = __shfl_sync(0xffffffffu, mp.x, q), qy = __shfl_sync(0xffffffffu, mp.y, q);
+        unsigned hm[kTileBatch / 32];
+#pragma unroll
+        for (int r = 0; r < kTileBatch / 32; ++r) {
+          const int j = 32 * r + lane;
+          bool hit = false;
+          if (32 * r < nb) {  // warp-uniform: skip empty rounds
+            const int jj = j < nb ? j : 0;
+            const double2 a = sv[w][0][jj], b = sv[w][1][jj], cc = sv[w][2][jj];
+            const double tv[6] = {a.x, a.y, b.x, b.y, cc.x, cc.y};
+            hit = j < nb && pair_dist2(qx, qy, tv) < h2;
+          }
+          hm[r] = __ballot_sync(0xffffffffu, hit);
+        }
+        if (lane == q) {
+          m0 = hm[0];
+          m1 = hm[1];
+          m2 = hm[2];
+        }
+      }
+      if (have) {
+        const unsigned long long n = static_cast<unsigned long long>(__popc(m0) + __popc(m1) + __popc(m2));
+        if (b0 == cb) {
+          pcount[mi] = n;
+          pmask[mi] = make_uint4(m0, m1, m2, flag_long);
+        } else {
+          pcount[mi] += n;  // this warp owns the cell's particles
+        }
+        if (row_limit && b0 + kTileBatch >= ce && pcount[mi] > row_limit) atomicOr(row_flag, 8u);
+      }
+    }
+  }
+}
+
+// Fill from the hit masks: a warp takes 32 consecutive particles (index
+// order); each particle with hits is expanded by the whole warp, lane l
+// testing bit l of the three mask words, so a row's pairs are written
+// contiguously in ascending list position (= ascending triangle id).
+__global__ void __launch_bounds__(256)
+    k_expand_masks(int p_begin, int p_count, const uint4* __restrict__ pmask,
+                   const unsigned long long* __restrict__ off, long long base, const double* __restrict__ pxy,
+                   const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
+                   const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2,
+                   int* __restrict__ pp, int* __restrict__ pt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool valid = r < p_count;
+  const int i = p_begin + static_cast<int>(valid ? r : 0);
+  unsigned long long o = 0, n = 0, cb = 0, ce = 0;
+  uint4 m = make_uint4(0u, 0u, 0u, 0u);
+  if (valid) {
+    o = off[i] - base;
+    n = off[i + 1] - off[i];
+    if (n > 0) {
+      m = pmask[i];
+      const unsigned c = pcell[i];
+      cb = cell_start[c];
+      ce = cell_start[c + 1];
+    }
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, valid && n > 0 && m.w == 0u);
+  const unsigned below = (1u << lane) - 1u;
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int qi = __shfl_sync(0xffffffffu, i, src);
+    const unsigned long long qo = __shfl_sync(0xffffffffu, o, src), qb = __shfl_sync(0xffffffffu, cb, src);
+    const unsigned q0 = __shfl_sync(0xffffffffu, m.x, src), q1 = __shfl_sync(0xffffffffu, m.y, src),
+                   q2 = __shfl_sync(0xffffffffu, m.z, src);
+    if ((q0 >> lane) & 1u) {
+      const unsigned long long d = qo + __popc(q0 & below);
+      pp[d] = qi;
+      pt[d] = __ldg(cell_tris + qb + lane);
+    }
+    if ((q1 >> lane) & 1u) {
+      const unsigned long long d = qo + __popc(q0) + __popc(q1 & below);
+      pp[d] = qi;
+      pt[d] = __ldg(cell_tris + qb + 32 + lane);
+    }
+    if ((q2 >> lane) & 1u) {
+      const unsigned long long d = qo + __popc(q0) + __popc(q1) + __popc(q2 & below);
+      pp[d] = qi;
+      pt[d] = __ldg(cell_tris + qb + 64 + lane);
+    }
+  }
+  // cells with more than kTileBatch candidates: the warp walks the list again
+  unsigned redo = __ballot_sync(0xffffffffu, valid && n > 0 && m.w != 0u);
+  double px = 0.0, py = 0.0;
+  if (redo & (1u << lane)) {
+    const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+    px = p.x;
+    py = p.y;
+  }
+  while (redo) {
+    const int src = __ffs(redo) - 1;
+    redo &= redo - 1;
+    const double qx = __shfl_sync(0xffffffffu, px, src), qy = __shfl_sync(0xffffffffu, py, src);
+    const unsigned long long qb = __shfl_sync(0xffffffffu, cb, src), qe = __shfl_sync(0xffffffffu, ce, src);
+    const unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
+    const int qi = __shfl_sync(0xffffffffu, i, src);
+    walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, 1, pp, pt);
+  }
+}
+
 // Piecewise kernels: the pairs of an inner piece with
 // support h_j <= h are the chunk's pairs that pass the same exact predicate at
 // h_j (so its pair list is bit-identical to a separate pass at h_j).
@@ -2873,6 +3040,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
       if (!w.empty()) c->stream_ramp = w;
     }
     if (const char* fp = std::getenv("SPHBI_FP64_PIECES"); fp && fp[0] == '1') c->fp64_pieces = true;
+    if (const char* ff = std::getenv("SPHBI_FIND"); ff && *ff) c->no_tile_find = std::string(ff) != "tile";
     if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
       const std::string v(pm);
       if (v == "dd") c->precision = SPHBI_PRECISION_DD;
@@ -3532,12 +3700,30 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
                           : (sparse ? std::min(find_grid(np), 8 * c->sms) : find_grid(np));
     int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
-    if (!wpp && (st = scratch_t(c, kBufStage, static_cast<size_t>(np) * kFindStage, &stage)) != SPHBI_OK) return st;
-    k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
-                                              nullptr, nullptr, dactive_n, wpp, stage,
-                                              row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull,
-                                              dflags + 1);
-    if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
+    uint4* pmask = nullptr;  // cell-tile finder: 96-bit hit masks, the fill expands them
+    const bool tile = !sparse && !wpp && !c->no_tile_find;
+    const unsigned long long rl = row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull;
+    if (tile) {
+      // dense scenes: one warp per cell, candidates staged in shared memory (k_find_tile)
+      unsigned long long* pstart;
+      if ((st = scratch_t(c, kBufPartStart, (size_t)ncells + 1, &pstart)) != SPHBI_OK) return st;
+      if ((st = scratch_t(c, kBufStage, static_cast<size_t>(np), &pmask)) != SPHBI_OK) return st;
+      const unsigned* pcs = static_cast<const unsigned*>(c->buf[c->bank * kNumBufs + kBufKeysA]);  // cell keys, sorted
+      if (np < ncells)
+        k_cell_start_bs<<<grid_for((int64_t)ncells + 1, 256), 256, 0, s>>>((int64_t)np, pcs, ncells, pstart);
+      else
+        k_cell_start<<<grid_for((int64_t)np + 1, 256), 256, 0, s>>>((int64_t)np, pcs, ncells, pstart);
+      if ((st = check_launch(c, "k_cell_start(particles)")) != SPHBI_OK) return st;
+      SPHBI_CUDA_TRY(zero_async(c, pcount, 8 * (static_cast<size_t>(np) + 1), s));
+      k_find_tile<<<(ncells + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, s>>>(
+          ncells, pstart, sorder, dp, cell_start, vb, dt, h2, pcount, pmask, rl, dflags + 1);
+      if ((st = check_launch(c, "k_find_tile")) != SPHBI_OK) return st;
+    } else {
+      if (!wpp && (st = scratch_t(c, kBufStage, static_cast<size_t>(np) * kFindStage, &stage)) != SPHBI_OK) return st;
+      k_find_pairs<<<fgrid, kFindBlock, 0, s>>>(np, sorder, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount, 0,
+                                                nullptr, nullptr, dactive_n, wpp, stage, rl, dflags + 1);
+      if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
+    }
     SPHBI_CUDA_TRY(cudaMemsetAsync(pcount + n_particles, 0, 8, s));
     {
       size_t tmp = 0;
@@ -3603,7 +3789,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if (resident && total_pairs > 0) {
       if ((st = scratch_t(c, kBufPairP, total_pairs, &gpp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPairT, total_pairs, &gpt)) != SPHBI_OK) return st;
-      if (stage)
+      if (pmask)
+        k_expand_masks<<<grid_for(np, 256), 256, 0, s>>>(0, np, pmask, poff, 0, dp, pcell, cell_start, vb, dt, h2,
+                                                         gpp, gpt);
+      else if (stage)
         k_stage_compact<<<grid_for(np, 256), 256, 0, s>>>(0, np, stage, poff, 0, dp, pcell, cell_start, vb, dt, h2,
                                                           gpp, gpt);
       else
@@ -3668,7 +3857,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           if ((st = scratch_t(c, kBufPairT, cnt, &pt)) != SPHBI_OK) return st;
           const int cgrid = wpp ? static_cast<int>((static_cast<int64_t>(p1 - p0) * 32 + kFindBlock - 1) / kFindBlock)
                                 : find_grid(p1 - p0);
-          if (stage)
+          if (pmask)
+            k_expand_masks<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, pmask, poff, (long long)base, dp,
+                                                                  pcell, cell_start, vb, dt, h2, pp, pt);
+          else if (stage)
             k_stage_compact<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, stage, poff, (long long)base, dp,
                                                                    pcell, cell_start, vb, dt, h2, pp, pt);
           else
