@@ -1553,9 +1553,9 @@ __global__ void __launch_bounds__(128)
 // K5: per-particle fixed-order reduction (pairs sorted by particle, then
 // triangle id), vectorised double2 gradient stores.
 // ---------------------------------------------------------------------------
-__global__ void k_iota(int n, int* __restrict__ out) {
+__global__ void k_iota(int n, int* __restrict__ out, int base = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = i;
+  if (i < n) out[i] = base + i;
 }
 
 // Row pointers by binary search, one thread per row: balanced when most
@@ -3360,6 +3360,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     std::memset(stats, 0, sizeof(*stats));
     cudaEventRecord(c->ev[0], s);
   }
+  const auto t_call = std::chrono::steady_clock::now();
+  auto tl_mark = [&](const char* what) {  // SPHBI_TIMELINE=1: host time at the call's synchronisation points
+    if (c->timeline)
+      std::fprintf(stderr, "[sphbi timeline] %-28s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count());
+  };
   // constant-field arithmetic (sphbi_ctx_set_precision): FP64 when no row of
   // the pair list is longer than row_limit, decided where the rows are known
   c->fp64_now = false;
@@ -3389,14 +3395,43 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // unsorted pair list: fall through to the general path (which sorts)
   }
   // ---- inputs on the device
+  int up_chunks = 1;       // particle upload chunks in flight on c->h2d (1: everything is on the device / on s)
+  int64_t up_chunk = 0;    // particles per upload chunk
+  auto wait_uploads = [&](cudaStream_t st_) -> sphbi_status {  // the stream sees every particle
+    if (up_chunks > 1) SPHBI_CUDA_TRY(cudaStreamWaitEvent(st_, c->sev[0][up_chunks - 1], 0));
+    return SPHBI_OK;
+  };
   const double *dp = particle_xy, *dt = tri_xy, *dv = tri_values;
   double *dov = out_value, *dog = out_grad;
   if (mem == SPHBI_MEM_HOST) {
     double *a, *b, *v;
     if ((st = scratch_t(c, kBufPxy, 2 * n_particles, &a)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufTri, 6 * n_triangles, &b)) != SPHBI_OK) return st;
-    if (n_particles) SPHBI_CUDA_TRY(cudaMemcpyAsync(a, particle_xy, 16 * n_particles, cudaMemcpyHostToDevice, s));
-    if (n_triangles) SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, s));
+    // The mesh first (the cell list needs nothing else): for a cell-list call
+    // from pinned memory the particles follow on the copy stream, behind the
+    // triangle binning (K1: bounding box, counts, fill, sort, cell starts).
+    const bool stream_up = n_pairs < 0 && n_triangles > 0 && n_particles >= (int64_t(1) << 22) &&
+                           is_pinned(particle_xy) && is_pinned(tri_xy);
+    if (stream_up) {
+      // one copy stream, in order: the mesh, then the particle chunks (copies
+      // on two streams share the link and would all finish together)
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, c->h2d));
+      SPHBI_CUDA_TRY(cudaEventRecord(c->sev[2][0], c->h2d));
+      SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[2][0], 0));
+    } else if (n_triangles) {
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(b, tri_xy, 48 * n_triangles, cudaMemcpyHostToDevice, s));
+    }
+    if (stream_up) {
+      up_chunk = std::max<int64_t>(int64_t(1) << 21, (n_particles + 31) / 32);
+      up_chunks = static_cast<int>((n_particles + up_chunk - 1) / up_chunk);
+      for (int k = 0; k < up_chunks; ++k) {
+        const int64_t p0 = k * up_chunk, cnt = std::min(up_chunk, n_particles - p0);
+        SPHBI_CUDA_TRY(cudaMemcpyAsync(a + 2 * p0, particle_xy + 2 * p0, 16 * cnt, cudaMemcpyHostToDevice, c->h2d));
+        SPHBI_CUDA_TRY(cudaEventRecord(c->sev[0][k], c->h2d));
+      }
+    } else if (n_particles) {
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(a, particle_xy, 16 * n_particles, cudaMemcpyHostToDevice, s));
+    }
     dp = a;
     dt = b;
     if (tri_values) {
@@ -3572,11 +3607,14 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     const int nb = 296;
     double* partial;
     if ((st = scratch_t(c, kBufBBox, 4 * nb, &partial)) != SPHBI_OK) return st;
-    k_bbox<<<nb, 256, 0, s>>>(n_particles, dp, 3 * n_triangles, dt, partial);
+    // the grid covers the triangles' h-expanded boxes (plus a border of empty
+    // cells); particles beyond it clamp into the border and pair with nothing
+    k_bbox<<<nb, 256, 0, s>>>(0, dp, 3 * n_triangles, dt, partial);
     if ((st = check_launch(c, "k_bbox")) != SPHBI_OK) return st;
     std::vector<double> hb(4 * nb);
     SPHBI_CUDA_TRY(cudaMemcpyAsync(hb.data(), partial, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    tl_mark("bounding box");
     double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     for (int b = 0; b < nb; ++b) {
       mnx = std::min(mnx, hb[4 * b]);
@@ -3617,6 +3655,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     unsigned long long n_entries = 0;
     SPHBI_CUDA_TRY(cudaMemcpyAsync(&n_entries, toff + n_triangles, 8, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    tl_mark("cell-list entry count");
     if (n_entries >= (1ull << 31)) return fail(SPHBI_ERR_OUT_OF_MEMORY, "cell list exceeds 2^31 entries");
     unsigned *ka, *kb;
     int *va, *vb;
@@ -3657,6 +3696,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     int* sorder;
     int* dactive_n = nullptr;
     if (sparse) {
+      if ((st = wait_uploads(s)) != SPHBI_OK) return st;
       unsigned char* act;
       if ((st = scratch_t(c, kBufPieceFlag, n_particles, &act)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPartOrder, n_particles + 2, &sorder)) != SPHBI_OK) return st;
@@ -3671,19 +3711,33 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch(c, kBufCubTemp2, tmp, &dtmp)) != SPHBI_OK) return st;
       cub::DeviceSelect::Flagged(dtmp, tmp, ids, act, sorder, dactive_n, (int)n_particles, s);
       if ((st = check_launch(c, "select active particles")) != SPHBI_OK) return st;
-    } else {
-    k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
-    if ((st = check_launch(c, "k_particle_cell")) != SPHBI_OK) return st;
-    // particles in cell order (the finder walks them so)
-    {
+    }
+    // K3 regime. Long cell lists (mean entries per cell > 512, e.g. cfg2 mode B)
+    // are walked one warp per particle, short ones one lane per particle.
+    const double h2 = h * h;
+    const int np = static_cast<int>(n_particles);
+    const int wpp = !sparse && n_entries > 512ull * static_cast<unsigned long long>(ncells) ? 1 : 0;
+    const bool tile = !sparse && !wpp && !c->no_tile_find;
+    const unsigned long long rl = row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull;
+    int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
+    uint4* pmask = nullptr;  // cell-tile finder: 96-bit hit masks, the fill expands them
+    if (!sparse) {
+      // particles in cell order (the finder walks them so: neighbouring lanes
+      // share cell lists). One global sort once every particle is on the
+      // device: sorting and counting each upload chunk as it arrives was
+      // measured slower (a chunk of randomly ordered particles has ~2 per cell,
+      // the lanes' candidate loads stop sharing cache lines: count 5.5 -> 10 ms).
+      if ((st = wait_uploads(s)) != SPHBI_OK) return st;
       unsigned* pcell_sorted;
       int* piota;
       if ((st = scratch_t(c, kBufKeysA, n_particles, &pcell_sorted)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufValsA, n_particles, &piota)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPartOrder, n_particles, &sorder)) != SPHBI_OK) return st;
-      k_iota<<<grid_for(n_particles, 256), 256, 0, s>>>((int)n_particles, piota);
       int bits = 1;
       while ((1ll << bits) < ncells) ++bits;
+      k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
+      k_iota<<<grid_for(n_particles, 256), 256, 0, s>>>((int)n_particles, piota);
+      if ((st = check_launch(c, "k_particle_cell", 2)) != SPHBI_OK) return st;
       size_t tmp = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
       void* dtmp;
@@ -3691,18 +3745,8 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       cub::DeviceRadixSort::SortPairs(dtmp, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
       if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
     }
-    }
-    // K3: count, scan. Long cell lists (mean entries per cell > 512, e.g. cfg2
-    // mode B) are walked one warp per particle, short ones one lane per particle.
-    const double h2 = h * h;
-    const int np = static_cast<int>(n_particles);
-    const int wpp = !sparse && n_entries > 512ull * static_cast<unsigned long long>(ncells) ? 1 : 0;
     const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
                           : (sparse ? std::min(find_grid(np), 8 * c->sms) : find_grid(np));
-    int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
-    uint4* pmask = nullptr;  // cell-tile finder: 96-bit hit masks, the fill expands them
-    const bool tile = !sparse && !wpp && !c->no_tile_find;
-    const unsigned long long rl = row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull;
     if (tile) {
       // dense scenes: one warp per cell, candidates staged in shared memory (k_find_tile)
       unsigned long long* pstart;
@@ -3739,6 +3783,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
     if (row_limit > 0) SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+    tl_mark("pair counts scanned");
     total_pairs = static_cast<int64_t>(*htot);
     c->fp64_now = row_limit > 0 && !(c->h_flags[1] & kFlagLongRow);
     if (counts_out) {  // sphbi_pair_counts: the count pass only
@@ -3946,6 +3991,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   }
   SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+  tl_mark("done");
   if (c->h_flags[1] & 4u) {
     c->overflowed = true;
     return SPHBI_ERR_INTERNAL;

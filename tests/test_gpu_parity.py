@@ -270,6 +270,31 @@ def test_sparse_and_dense_pair_finders_agree(S, ctx):
     assert np.array_equal(v1, v2) and np.array_equal(g1, g2)
 
 
+def test_tile_finder_matches_walk(S, ctx):
+    """The cell-tile finder (SPHBI_FIND=tile: warp per cell, candidates staged in
+    shared memory with cp.async, hit masks) returns the walk finder's pair list
+    bit for bit -- on a cfg5-like scene (short cell lists) and on one whose cell
+    lists exceed the 96-candidate mask (batched count, re-walked fill)."""
+    import os
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5(n_particles=60_000, n_discs=6, target_tris=20_000, domain=12.0)
+    dense = scenes.cfg5(n_particles=20_000, n_discs=2, target_tris=40_000, domain=6.0, spacing=0.02)
+    os.environ["SPHBI_FIND"] = "tile"
+    try:
+        ct = S.Context(0)
+    finally:
+        os.environ.pop("SPHBI_FIND", None)
+    for scn in (sc, dense):
+        k = scn.kernels[0]
+        v1, g1, st1, pl1 = S.evaluate(scn.particles, scn.h, scn.triangles, table_of(S, k), ctx=ctx, return_pairs=True)
+        v2, g2, st2, pl2 = S.evaluate(scn.particles, scn.h, scn.triangles, table_of(S, k), ctx=ct, return_pairs=True)
+        assert st1.n_pairs == st2.n_pairs > 10000
+        assert np.array_equal(pl1, pl2)
+        assert np.array_equal(v1, v2) and np.array_equal(g1, g2)
+    assert np.bincount(pl1[:, 0]).max() > 96  # the dense scene's rows are longer than a mask
+    ct.close()
+
+
 @pytest.mark.parametrize("kernel", ["wendland_c2", "cubic_spline"])
 def test_cfg5_reduced_scene(S, ctx, O, kernel):
     """cfg5 structure (Delaunay obstacle discs, uniform particles, h = 0.1) at
