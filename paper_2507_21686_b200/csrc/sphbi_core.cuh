@@ -1170,10 +1170,13 @@ SPHBI_HD void edge_sum3f_general(const KernelConsts& K, const P2* v, double* raw
 // adds the remaining edges' full-edge terms explicitly (edge_sum3f_general's
 // sum, regrouped), one more atan2 per edge.
 // one edge a -> b of the sum (cab = a x b, ra = |a|, ira = 1 / |a|, ...)
+// NT: the kernel's degree when known at compile time (the chain and Horner
+// loops unroll, their weights become constant-bank operands), -1: K.deg
+template <int NT>
 SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double ra, double rb, double ira,
                           double irb, bool deg, int& npos, double& V, double& Gx, double& Gy) {
   if (cab == 0.0) return;  // origin on this edge's line: zero-area origin triangle
-  const int N = K.deg;
+  const int N = NT >= 0 ? NT : K.deg;
   const double pv1 = K.pv1.hi, rg1 = K.rg1.hi;
   const double ex = b.x - a.x, ey = b.y - a.y;
   const double iL = fast_rsqrt(fma(ex, ex, ey * ey));
@@ -1205,16 +1208,20 @@ SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double 
     double aPv = K.wpv[1].hi * um1;
     double aGn = fma(K.wgn[0], um2, K.wgn[1] * um1);
     double ph = shi, pl = slo;
+    double fm = 1.0;  // m - 1
+#pragma unroll
     for (int m = 2; m <= N + 1; ++m) {
       ph *= xhi;
       pl *= xlo;
-      const double um = fma(K.dfac[m - 2], ph - pl, (double)(m - 1) * D2 * um2);
+      const double um = fma(K.dfac[m - 2], ph - pl, fm * D2 * um2);
       aPv = fma(K.wpv[m].hi, um, aPv);
       aGn = fma(K.wgn[m], um, aGn);
       um2 = um1;
       um1 = um;
+      fm += 1.0;
     }
     double qh = K.qg[N], ql = K.qg[N];
+#pragma unroll
     for (int k = N - 1; k >= 0; --k) {
       qh = fma(qh, xhi, K.qg[k]);
       ql = fma(ql, xlo, K.qg[k]);
@@ -1228,6 +1235,7 @@ SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double 
   Gx += fma(Gn, ty, Gt * tx);  // n = (t.y, -t.x)
   Gy += fma(Gt, ty, -(Gn * tx));
 }
+template <int NT = -1>
 SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
   const P2 a = v[0], b = v[1], c = v[2];
   const double cab = cross_exact(a, b), cbc = cross_exact(b, c), cca = cross_exact(c, a);
@@ -1239,9 +1247,9 @@ SPHBI_HD void edge_sum3f(const KernelConsts& K, const P2* v, double* raw3) {
   const double ra = qa * ira, rb = qb * irb, rc = qc * irc;
   double V = 0.0, Gx = 0.0, Gy = 0.0;
   int npos = 0;
-  edge_term3f(K, a, b, cab, ra, rb, ira, irb, deg, npos, V, Gx, Gy);
-  edge_term3f(K, b, c, cbc, rb, rc, irb, irc, deg, npos, V, Gx, Gy);
-  edge_term3f(K, c, a, cca, rc, ra, irc, ira, deg, npos, V, Gx, Gy);
+  edge_term3f<NT>(K, a, b, cab, ra, rb, ira, irb, deg, npos, V, Gx, Gy);
+  edge_term3f<NT>(K, b, c, cbc, rb, rc, irb, irc, deg, npos, V, Gx, Gy);
+  edge_term3f<NT>(K, c, a, cca, rc, ra, irc, ira, deg, npos, V, Gx, Gy);
   if (!deg && npos == 3) V += 2.0 * kPiHi * K.pv1.hi;
   raw3[0] = V;
   raw3[1] = Gx;

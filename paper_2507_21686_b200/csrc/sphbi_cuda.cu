@@ -1357,7 +1357,7 @@ __global__ void __launch_bounds__(128)
 // result is bitwise independent of the triangle's vertex order), same
 // degenerate-triangle rule (integrate_normalized :640 / hat planes :255-269).
 // ---------------------------------------------------------------------------
-template <class Src>
+template <class Src, int NT>
 __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
     k_edge_pairs_f(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h, int stride,
                    double* __restrict__ out) {
@@ -1381,12 +1381,15 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
     v1 = cw ? w2 : w1;
     v2 = cw ? w1 : w2;
   }
-  const P2 nv[3] = {P2{(v0.x - qx) / h, (v0.y - qy) / h}, P2{(v1.x - qx) / h, (v1.y - qy) / h},
-                    P2{(v2.x - qx) / h, (v2.y - qy) / h}};
+  // (v - q) / h by one reciprocal (this path owns its rounding: no other
+  // path's normalized coordinates need to match bit for bit)
+  const double ih = 1.0 / h;
+  const P2 nv[3] = {P2{(v0.x - qx) * ih, (v0.y - qy) * ih}, P2{(v1.x - qx) * ih, (v1.y - qy) * ih},
+                    P2{(v2.x - qx) * ih, (v2.y - qy) * ih}};
   double o[4] = {0.0, 0.0, 0.0, 0.0};
   if (!(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes_nondeg(nv)) {
     double raw[3];
-    edge_sum3f(K, nv, raw);
+    edge_sum3f<NT>(K, nv, raw);
     finalize(raw, K.c2, h, o);
   }
   for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
@@ -1597,6 +1600,25 @@ __global__ void k_reduce_rows(int p_begin, int p_count, const int64_t* __restric
     gx = out_g[2 * (int64_t)(p_begin + j)];
     gy = out_g[2 * (int64_t)(p_begin + j) + 1];
   }
+  for (int64_t k = b; k < e; ++k) {
+    v += pair_out3[3 * k];
+    gx += pair_out3[3 * k + 1];
+    gy += pair_out3[3 * k + 2];
+  }
+  out_v[p_begin + j] = v;
+  reinterpret_cast<double2*>(out_g)[p_begin + j] = make_double2(gx, gy);
+}
+
+// The same sums with the rows taken from the pair finder's scanned offsets
+// (cell-list path: off[i] - base is particle i's first pair of the chunk), so
+// no row pointers are rebuilt from the pair list.
+__global__ void k_reduce_rows_off(int p_begin, int p_count, const unsigned long long* __restrict__ off,
+                                  unsigned long long base, const double* __restrict__ pair_out3,
+                                  double* __restrict__ out_v, double* __restrict__ out_g) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p_count) return;
+  const int64_t b = static_cast<int64_t>(off[p_begin + j] - base), e = static_cast<int64_t>(off[p_begin + j + 1] - base);
+  double v = 0.0, gx = 0.0, gy = 0.0;
   for (int64_t k = b; k < e; ++k) {
     v += pair_out3[3 * k];
     gx += pair_out3[3 * k + 1];
@@ -2610,7 +2632,13 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   const bool f1 = mode == 0 && src.vals == nullptr;
   if (f1 && c->fp64_now && !c->fp64_pieces) {
     // FP64 constant-field path: the whole pair in one kernel (edge form)
-    k_edge_pairs_f<<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
+    // the degrees of the named kernels (Wendland C2 / C4) are compiled in
+    if (K.deg == 5)
+      k_edge_pairs_f<Src, 5><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
+    else if (K.deg == 8)
+      k_edge_pairs_f<Src, 8><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
+    else
+      k_edge_pairs_f<Src, -1><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
     return check_launch(c, "k_edge_pairs_f");
   }
   const int64_t cap = slot_chunk(mode, f1);
@@ -3940,10 +3968,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
           p0 = p1;
           continue;
         }
-        if ((st = scratch_t(c, kBufRowPtr, (p1 - p0) + 1, &row_ptr)) != SPHBI_OK) return st;
-        launch_row_ptr(cnt, pp, p0, p1 - p0, row_ptr, s);
-        if ((st = check_launch(c, "k_row_ptr")) != SPHBI_OK) return st;
-        k_reduce_rows<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, row_ptr, pout, dov, dog, 0);
+        k_reduce_rows_off<<<grid_for(p1 - p0, 256), 256, 0, s>>>(p0, p1 - p0, poff, base, pout, dov, dog);
         if ((st = check_launch(c, "k_reduce_rows")) != SPHBI_OK) return st;
       }
       if (chunk_d2h && p1 > p0) {
