@@ -1187,7 +1187,7 @@ SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double 
   const double sa = fma(a.x, tx, a.y * ty), sb = fma(b.x, tx, b.y * ty);
   double Ve = 0.0, Gn = 0.0, Gt = 0.0;
   if (deg) {  // full-edge terms, explicitly
-    const double ang = atan2(D * (sb - sa), fma(sa, sb, D2));
+    const double ang = fast_atan2_pos(D * (sb - sa), fma(sa, sb, D2));
     Ve = pv1 * (Ds < 0.0 ? -ang : ang);
     Gn = rg1 * (sb * irb - sa * ira);
     Gt = rg1 * Ds * (ira - irb);
@@ -1204,7 +1204,7 @@ SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double 
     const double dh = shi >= 0.0 ? 1.0 : xhi - shi;
     const double nl = slo >= 0.0 ? xlo + slo : D2;
     const double dl = slo >= 0.0 ? 1.0 : xlo - slo;
-    double um2 = log((nh * dl) * fast_rcp(nl * dh)), um1 = shi - slo;
+    double um2 = fast_log((nh * dl) * fast_rcp(nl * dh)), um1 = shi - slo;
     double aPv = K.wpv[1].hi * um1;
     double aGn = fma(K.wgn[0], um2, K.wgn[1] * um1);
     double ph = shi, pl = slo;
@@ -1226,7 +1226,7 @@ SPHBI_HD void edge_term3f(const KernelConsts& K, P2 a, P2 b, double cab, double 
       qh = fma(qh, xhi, K.qg[k]);
       ql = fma(ql, xlo, K.qg[k]);
     }
-    const double ang = atan2(D * (shi - slo), fma(slo, shi, D2));
+    const double ang = fast_atan2_pos(D * (shi - slo), fma(slo, shi, D2));
     Ve += fma(Ds, aPv, -(pv1 * (Ds < 0.0 ? -ang : ang)));
     Gn += fma(D2, aGn, -(rg1 * (shi * ixhi - slo * ixlo)));
     Gt += Ds * ((qh - ql) + rg1 * (ixhi - ixlo));

@@ -241,6 +241,75 @@ SPHBI_HD double fast_rsqrt(double x) {
 #endif
 }
 
+// log and atan2 of the FP64 constant-field path (edge_term3f), for the
+// arguments that occur there: r > 0 finite; y >= 0 with (x, y) != (0, 0).
+// libdevice's versions spend most of their instructions on special cases and
+// on building each polynomial coefficient in registers (two uniform moves per
+// 64-bit constant); these keep the coefficients in constant memory, where an
+// FP64 instruction reads them as an operand. Absolute error ~2e-16 (atanh /
+// arctangent series on arguments reduced to |u| <= 0.172, |z| <= 1/16).
+#if defined(__CUDACC__)
+__constant__ double kLogC[10] = {2.0 / 3.0,  2.0 / 5.0,  2.0 / 7.0,  2.0 / 9.0,  2.0 / 11.0,
+                                 2.0 / 13.0, 2.0 / 15.0, 2.0 / 17.0, 2.0 / 19.0, 2.0 / 21.0};
+__constant__ double kAtanC[7] = {-1.0 / 3.0, 1.0 / 5.0, -1.0 / 7.0, 1.0 / 9.0, -1.0 / 11.0, 1.0 / 13.0, -1.0 / 15.0};
+// atan(i / 8), i = 0 .. 8
+__constant__ double kAtanTab[9] = {0.0,
+                                   0.12435499454676143816,
+                                   0.24497866312686415417,
+                                   0.35877067027057222040,
+                                   0.46364760900080611621,
+                                   0.55859931534356243597,
+                                   0.64350110879328438680,
+                                   0.71882999962162450542,
+                                   0.78539816339744830962};
+#endif
+SPHBI_HD double fast_log(double r) {
+#if defined(__CUDA_ARCH__)
+  int hi = __double2hiint(r);
+  const int lo = __double2loint(r);
+  int e = (hi >> 20) - 1023;
+  if (e <= -1023 || e >= 1024) return log(r);  // zero / subnormal / inf / nan: not on the hot path
+  hi = (hi & 0x000fffff) | 0x3ff00000;
+  double m = __hiloint2double(hi, lo);  // [1, 2)
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const double u = (m - 1.0) * fast_rcp(m + 1.0);  // log m = 2 atanh u, |u| <= 0.1716
+  const double u2 = u * u;
+  double p = kLogC[9];
+#pragma unroll
+  for (int k = 8; k >= 0; --k) p = fma(p, u2, kLogC[k]);
+  const double fe = static_cast<double>(e);
+  return fma(fe, 6.93147180559945286227e-01, fma(u * u2, p, 2.0 * u)) + fe * 2.31904681384629955842e-17;
+#else
+  return ::log(r);
+#endif
+}
+// atan2(y, x) for y >= 0: the angle in [0, pi]
+SPHBI_HD double fast_atan2_pos(double y, double x) {
+#if defined(__CUDA_ARCH__)
+  const double ax = fabs(x);
+  const bool sw = y > ax;
+  const double num = sw ? ax : y, den = sw ? y : ax;
+  if (!(den > 0.0)) return 0.0;
+  const double t = num * fast_rcp(den);  // [0, 1]
+  const int i = static_cast<int>(fma(t, 8.0, 0.5));
+  const double c = 0.125 * static_cast<double>(i);
+  const double z = (t - c) * fast_rcp(fma(t, c, 1.0));  // atan t = atan c + atan z, |z| <= 1/16
+  const double z2 = z * z;
+  double p = kAtanC[6];
+#pragma unroll
+  for (int k = 5; k >= 0; --k) p = fma(p, z2, kAtanC[k]);
+  double a = kAtanTab[i] + fma(z * z2, p, z);
+  if (sw) a = (kHalfPiHi - a) + kHalfPiLo;
+  if (x < 0.0) a = (kPiHi - a) + kPiLo;
+  return a;
+#else
+  return ::atan2(y, x);
+#endif
+}
+
 // atan2, out of line on the device (3 call sites in the decomposition).
 SPHBI_HDNI double d_atan2(double y, double x) { return atan2(y, x); }
 
