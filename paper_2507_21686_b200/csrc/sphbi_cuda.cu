@@ -1817,6 +1817,68 @@ __host__ __device__ __forceinline__ double pair_dist2(double px, double py, cons
   return fmin(d0, fmin(d1, d2));
 }
 
+// The pair predicate decided in FP32 wherever FP32 can decide it: the exact
+// test above costs ~150 instructions with three IEEE double divisions per
+// candidate and bounds the pair finder on the FP64 pipe. In coordinates
+// relative to the particle (|.| <= scale), FP32 gets the squared distance to
+// ~2.4e-6 scale^2 (rounded coordinates 6e-8 scale, projection parameter 5e-7);
+// outside a band of 2e-5 scale^2 around h^2 its verdict is the exact test's
+// (whose own rounding is ~1e-15), inside the band -- or when a half-plane sign
+// is not certain (within 8e-6 of the products' size: the particle next to an
+// edge LINE, e.g. beyond the end of a sliver), the support is tiny against the
+// triangle, or anything is not finite -- the exact test decides. The pair
+// lists stay bit-identical with the CPU finder's (tests: every scene test
+// compares them).
+// returns 1 hit, 0 miss, -1 undecided
+__device__ __forceinline__ int pair_classify_f32(double px, double py, const double* t, float h2f, float hf) {
+  const float ax = static_cast<float>(t[0] - px), ay = static_cast<float>(t[1] - py);
+  const float bx = static_cast<float>(t[2] - px), by = static_cast<float>(t[3] - py);
+  const float cx = static_cast<float>(t[4] - px), cy = static_cast<float>(t[5] - py);
+  const float scale = fmaxf(fmaxf(fmaxf(fabsf(ax), fabsf(ay)), fmaxf(fabsf(bx), fabsf(by))),
+                            fmaxf(fmaxf(fabsf(cx), fabsf(cy)), hf));
+  if (!(hf > 1e-3f * scale)) return -1;  // also: not finite
+  const float e0x = bx - ax, e0y = by - ay, e1x = cx - bx, e1y = cy - by, e2x = ax - cx, e2y = ay - cy;
+  // half-plane signs cross(e_k, p - v_k), p = 0
+  const float p0 = e0y * ax, q0 = e0x * ay, p1 = e1y * bx, q1 = e1x * by, p2 = e2y * cx, q2 = e2x * cy;
+  const float s0 = p0 - q0, s1 = p1 - q1, s2 = p2 - q2;
+  const float ts = 8e-6f;
+  if (!(fabsf(s0) > ts * (fabsf(p0) + fabsf(q0)) && fabsf(s1) > ts * (fabsf(p1) + fabsf(q1)) &&
+        fabsf(s2) > ts * (fabsf(p2) + fabsf(q2))))
+    return -1;
+  if ((s0 > 0.f && s1 > 0.f && s2 > 0.f) || (s0 < 0.f && s1 < 0.f && s2 < 0.f)) return 1;  // strictly inside
+  // certainly outside: squared distance to the three edges
+  float m;
+  {
+    const float t0 = __saturatef(__fdividef(-(ax * e0x + ay * e0y), e0x * e0x + e0y * e0y));
+    const float dx = fmaf(t0, e0x, ax), dy = fmaf(t0, e0y, ay);
+    m = dx * dx + dy * dy;
+  }
+  {
+    const float t1 = __saturatef(__fdividef(-(bx * e1x + by * e1y), e1x * e1x + e1y * e1y));
+    const float dx = fmaf(t1, e1x, bx), dy = fmaf(t1, e1y, by);
+    m = fminf(m, dx * dx + dy * dy);
+  }
+  {
+    const float t2 = __saturatef(__fdividef(-(cx * e2x + cy * e2y), e2x * e2x + e2y * e2y));
+    const float dx = fmaf(t2, e2x, cx), dy = fmaf(t2, e2y, cy);
+    m = fminf(m, dx * dx + dy * dy);
+  }
+  const float tol2 = 2e-5f * scale * scale;
+  if (m < h2f - tol2) return 1;
+  if (m > h2f + tol2) return 0;
+  return -1;
+}
+struct PairTest {  // d(p, closed triangle) < h, the exact predicate's verdict
+  double h2;
+  float h2f, hf;
+  __device__ __forceinline__ explicit PairTest(double h2_) : h2(h2_), h2f(static_cast<float>(h2_)), hf(sqrtf(static_cast<float>(h2_))) {}
+  __device__ __forceinline__ bool operator()(double px, double py, const double* t) const {
+    const int c = pair_classify_f32(px, py, t, h2f, hf);
+    if (c >= 0) return c != 0;
+    return pair_dist2(px, py, t) < h2;
+  }
+};
+
 __device__ __forceinline__ int cell_coord(double v, double o, double cell, int n) {
   const double f = floor((v - o) / cell);
   int c = f < 0.0 ? 0 : (f >= (double)(n - 1) ? n - 1 : (int)f);
@@ -1949,7 +2011,7 @@ __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy
 // Either way a particle's pairs come out in ascending triangle id (stably
 // sorted cell lists) -- the CPU finder's list.
 constexpr int kFindBlock = 256;
-constexpr unsigned long long kFindLaneMax = 96;
+constexpr unsigned long long kFindLaneMax = 128;
 __device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
   const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
   const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -1976,7 +2038,7 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
       t = __ldg(cell_tris + k);
       double tv[6];
       load_tri6(tri, t, tv);
-      hit = pair_dist2(qx, qy, tv) < h2;
+      hit = PairTest(h2)(qx, qy, tv);
     }
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (fill && hit) {
@@ -1994,7 +2056,7 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
 // particle-major staging area, so the fill becomes a compaction
 // (k_stage_compact) instead of a second walk over every candidate; particles
 // with more hits than slots are walked again there.
-constexpr int kFindStage = 32;
+constexpr int kFindStage = 64;  // cfg5's interior rows hold ~27 pairs, up to ~45: 32 slots sent a sixth of them to the re-walk
 
 // 32 consecutive list positions (one warp; see k_find_pairs)
 __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int* __restrict__ order, int p0,
@@ -2026,7 +2088,7 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
       const int t = __ldg(cell_tris + k);
       double tv[6];
       load_tri6(tri, t, tv);
-      if (pair_dist2(px, py, tv) < h2) {
+      if (PairTest(h2)(px, py, tv)) {
         if (fill) {
           pp[o + n] = i;
           pt[o + n] = t;
@@ -2130,9 +2192,9 @@ __global__ void __launch_bounds__(256)
     const int qi = __shfl_sync(0xffffffffu, i, src);
     const unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
     const int qn = static_cast<int>(__shfl_sync(0xffffffffu, n, src));
-    if (lane < qn) {
-      pp[qo + lane] = qi;
-      pt[qo + lane] = stage[static_cast<int64_t>(qi) * kFindStage + lane];
+    for (int l = lane; l < qn; l += 32) {
+      pp[qo + l] = qi;
+      pt[qo + l] = stage[static_cast<int64_t>(qi) * kFindStage + l];
     }
   }
   // rows with more hits than slots, or from a long cell list (walked by the
@@ -2226,7 +2288,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, 3)
             const int jj = j < nb ? j : 0;
             const double2 a = sv[w][0][jj], b = sv[w][1][jj], cc = sv[w][2][jj];
             const double tv[6] = {a.x, a.y, b.x, b.y, cc.x, cc.y};
-            hit = j < nb && pair_dist2(qx, qy, tv) < h2;
+            hit = j < nb && PairTest(h2)(qx, qy, tv);
           }
           hm[r] = __ballot_sync(0xffffffffu, hit);
         }
