@@ -2012,6 +2012,7 @@ __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy
 // sorted cell lists) -- the CPU finder's list.
 constexpr int kFindBlock = 256;
 constexpr unsigned long long kFindLaneMax = 128;
+constexpr int kFindStage = 64;  // staged hits per particle (see find_group); cfg5's interior rows hold ~27 pairs, up to ~45
 __device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
   const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
   const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -2028,7 +2029,8 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
                                                         unsigned long long qe, unsigned long long qo, int qi,
                                                         const int* __restrict__ cell_tris,
                                                         const double* __restrict__ tri, double h2, int fill,
-                                                        int* __restrict__ pp, int* __restrict__ pt) {
+                                                        int* __restrict__ pp, int* __restrict__ pt,
+                                                        int* __restrict__ stage = nullptr) {
   unsigned long long n = 0;
   for (unsigned long long k0 = qb; k0 < qe; k0 += 32) {
     const unsigned long long k = k0 + lane;
@@ -2041,10 +2043,14 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
       hit = PairTest(h2)(qx, qy, tv);
     }
     const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (fill && hit) {
-      const unsigned long long q = qo + n + __popc(m & ((1u << lane) - 1u));
-      pp[q] = qi;
-      pt[q] = t;
+    if (hit) {
+      const unsigned long long r = n + __popc(m & ((1u << lane) - 1u));
+      if (fill) {
+        pp[qo + r] = qi;
+        pt[qo + r] = t;
+      } else if (stage && r < static_cast<unsigned long long>(kFindStage)) {
+        stage[static_cast<int64_t>(qi) * kFindStage + r] = t;  // count pass: staged like the lane walk's hits
+      }
     }
     n += __popc(m);
   }
@@ -2056,7 +2062,6 @@ __device__ __forceinline__ unsigned long long walk_warp(int lane, double qx, dou
 // particle-major staging area, so the fill becomes a compaction
 // (k_stage_compact) instead of a second walk over every candidate; particles
 // with more hits than slots are walked again there.
-constexpr int kFindStage = 64;  // cfg5's interior rows hold ~27 pairs, up to ~45: 32 slots sent a sixth of them to the re-walk
 
 // 32 consecutive list positions (one warp; see k_find_pairs)
 __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int* __restrict__ order, int p0,
@@ -2112,7 +2117,7 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
     const unsigned long long qb = __shfl_sync(0xffffffffu, b, src), qe = __shfl_sync(0xffffffffu, e, src);
     unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
     const int qi = __shfl_sync(0xffffffffu, i, src);
-    const unsigned long long n = walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, fill, pp, pt);
+    const unsigned long long n = walk_warp(lane, qx, qy, qb, qe, qo, qi, cell_tris, tri, h2, fill, pp, pt, stage);
     if (!fill && lane == src) {
       count_or_offset[qi] = n;
       if (row_limit && n > row_limit) atomicOr(row_flag, 8u);
@@ -2180,11 +2185,13 @@ __global__ void __launch_bounds__(256)
   if (valid) {
     o = off[i] - base;
     n = off[i + 1] - off[i];
+  }
+  const bool staged = n <= static_cast<unsigned long long>(kFindStage);  // either walk of the count pass staged it
+  if (valid && n > 0 && !staged) {  // only the re-walked rows need their cell list
     const unsigned c = pcell[i];
     cb = cell_start[c];
     ce = cell_start[c + 1];
   }
-  const bool staged = n <= static_cast<unsigned long long>(kFindStage) && ce - cb <= kFindLaneMax;
   unsigned todo = __ballot_sync(0xffffffffu, valid && n > 0 && staged);
   while (todo) {
     const int src = __ffs(todo) - 1;
