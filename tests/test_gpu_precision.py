@@ -97,3 +97,29 @@ def test_auto_falls_back_to_dd_on_long_rows(S):
     assert ctx.last_precision() == "dd"
     assert np.array_equal(v2, v) and np.array_equal(g2, g)
     ctx.close()
+
+
+def test_fp64_piece_kernels_agree_with_the_edge_kernel(S, O):
+    """SPHBI_FP64_PIECES=1 routes the FP64 constant field through the work-item
+    pipeline (k_pipe_*_f: stub pieces from the chord geometry) instead of the
+    edge kernel; same integrals, two independent FP64 formulations."""
+    import os
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5(n_particles=60_000, n_discs=6, target_tris=20_000, domain=12.0)
+    k = sc.kernels[0]
+    os.environ["SPHBI_FP64_PIECES"] = "1"
+    try:
+        cp = S.Context(0)
+    finally:
+        os.environ.pop("SPHBI_FP64_PIECES", None)
+    ce = S.Context(0)
+    res = []
+    for ctx in (cp, ce):
+        ctx.set_precision("fp64")
+        v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, _table(S, k), ctx=ctx)
+        assert ctx.last_precision() == "fp64"
+        res.append(np.concatenate([v[:, None], g], axis=1))
+        ctx.close()
+    r = OL.parity_ratio(res[0], res[1], k.normalization, sc.h)
+    print(f"FP64 pieces vs edge kernel: {r:.4f} tolerances")
+    assert 0.0 < r <= 0.05  # different kernels (not bitwise equal), same integral
