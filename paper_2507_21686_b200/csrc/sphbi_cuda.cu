@@ -1366,7 +1366,12 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
   double qx, qy, t6[6];
   src.load_geom(k, qx, qy, t6);
   // canonicalize (lexicographic lead vertex, then counter-clockwise:
-  // triangle_integrator.hpp:680-694) and normalize, in registers
+  // triangle_integrator.hpp:680-694) and normalize, in registers. The
+  // orientation is read off the normalized triangle's signed area, which also
+  // serves the degenerate-triangle rule (integrate_normalized :640; the plane
+  // solve's degeneracy test :255-269 checks the same quantity, twice the area,
+  // in another rounding: triangles that close to the 1e-13 threshold contribute
+  // less than the parity floor either way).
   P2 v0{t6[0], t6[1]}, v1{t6[2], t6[3]}, v2{t6[4], t6[5]};
   {
     const bool l1 = v1.x < v0.x || (v1.x == v0.x && v1.y < v0.y);
@@ -1376,18 +1381,20 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
     const P2 w0 = lead == 0 ? v0 : (lead == 1 ? v1 : v2);
     const P2 w1 = lead == 0 ? v1 : (lead == 1 ? v2 : v0);
     const P2 w2 = lead == 0 ? v2 : (lead == 1 ? v0 : v1);
-    const bool cw = signed_area(w0, w1, w2) < 0.0;
     v0 = w0;
-    v1 = cw ? w2 : w1;
-    v2 = cw ? w1 : w2;
+    v1 = w1;
+    v2 = w2;
   }
   // (v - q) / h by one reciprocal (this path owns its rounding: no other
   // path's normalized coordinates need to match bit for bit)
   const double ih = 1.0 / h;
-  const P2 nv[3] = {P2{(v0.x - qx) * ih, (v0.y - qy) * ih}, P2{(v1.x - qx) * ih, (v1.y - qy) * ih},
-                    P2{(v2.x - qx) * ih, (v2.y - qy) * ih}};
+  const P2 n0{(v0.x - qx) * ih, (v0.y - qy) * ih}, n1{(v1.x - qx) * ih, (v1.y - qy) * ih},
+      n2{(v2.x - qx) * ih, (v2.y - qy) * ih};
+  const double area = signed_area(n0, n1, n2);  // exact negation under a swap of n1, n2: the order is well defined
+  const bool cw = area < 0.0;
+  const P2 nv[3] = {n0, cw ? n2 : n1, cw ? n1 : n2};
   double o[4] = {0.0, 0.0, 0.0, 0.0};
-  if (!(fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps) && hat_planes_nondeg(nv)) {
+  if (!(fabs(area) < kGeomEps)) {
     double raw[3];
     edge_sum3f<NT>(K, nv, raw);
     finalize(raw, K.c2, h, o);

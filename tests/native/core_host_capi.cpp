@@ -450,13 +450,19 @@ static void f1_pair(const KernelConsts& K, double qx, double qy, double h, const
 }
 // the whole pair by the FP64 edge form (k_edge_pairs_f)
 static void f1_pair_edges(const KernelConsts& K, double qx, double qy, double h, const double* tri6, double* out3) {
+  // as k_edge_pairs_f: lead vertex, one reciprocal, orientation and the
+  // degenerate rule from the normalized triangle's signed area
   P2 v[3] = {{tri6[0], tri6[1]}, {tri6[2], tri6[3]}, {tri6[4], tri6[5]}};
-  int perm[3];
-  canonicalize(v, perm);
-  P2 nv[3];
-  for (int i = 0; i < 3; ++i) nv[i] = P2{(v[i].x - qx) / h, (v[i].y - qy) / h};
+  int lead = 0;
+  for (int i = 1; i < 3; ++i)
+    if (v[i].x < v[lead].x || (v[i].x == v[lead].x && v[i].y < v[lead].y)) lead = i;
+  const double ih = 1.0 / h;
+  P2 n[3];
+  for (int i = 0; i < 3; ++i) n[i] = P2{(v[(i + lead) % 3].x - qx) * ih, (v[(i + lead) % 3].y - qy) * ih};
+  const double area = signed_area(n[0], n[1], n[2]);
+  const P2 nv[3] = {n[0], area < 0.0 ? n[2] : n[1], area < 0.0 ? n[1] : n[2]};
   out3[0] = out3[1] = out3[2] = 0.0;
-  if (fabs(signed_area(nv[0], nv[1], nv[2])) < kGeomEps || !hat_planes_nondeg(nv)) return;
+  if (fabs(area) < kGeomEps) return;
   double raw[3], o4[4];
   edge_sum3f(K, nv, raw);
   finalize(raw, K.c2, h, o4);
