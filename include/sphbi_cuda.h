@@ -94,7 +94,10 @@ typedef struct sphbi_stats {
 /* ---- context -------------------------------------------------------- */
 sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out);
 sphbi_status sphbi_ctx_destroy(sphbi_ctx* ctx);
-/* Use a caller-owned cudaStream_t (NULL = the context's own stream). */
+/* Use a caller-owned cudaStream_t, so that the context's work is ordered with
+ * the caller's copies and kernels on that stream. NULL = the context's own
+ * (non-blocking) stream: a caller working on the default stream passes
+ * cudaStreamLegacy / cudaStreamPerThread, not NULL. */
 sphbi_status sphbi_ctx_set_stream(sphbi_ctx* ctx, void* cuda_stream);
 sphbi_status sphbi_ctx_synchronize(sphbi_ctx* ctx);
 /* Branch-route counters on the device (off by default: they cost atomics). */

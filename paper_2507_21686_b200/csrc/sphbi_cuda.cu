@@ -198,6 +198,7 @@ struct sphbi_ctx {
   cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  bool debug_sync = false;      // SPHBI_DEBUG_SYNC=1: synchronise after every launch (diagnosis)
   bool no_tile_find = true;     // SPHBI_FIND=tile selects the cell-tile finder (k_find_tile); default: lane-per-particle walk (measured faster on cfg5: 9.7 vs 10.6 ms)
   bool no_sparse_find = false;  // SPHBI_NO_SPARSE_FIND=1: always walk all particles in cell order
   int stream_chunk_log2 = 0;    // SPHBI_STREAM_CHUNK_LOG2: equal chunks of 2^L particles (0: the ramp)
@@ -253,7 +254,8 @@ sphbi_status scratch_t(sphbi_ctx* c, int slot, size_t count, T** out) {
 // n: kernels launched since the previous check (c->launches counts kernels)
 sphbi_status check_launch(sphbi_ctx* c, const char* what, int n = 1) {
   c->launches += n;
-  const cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && c->debug_sync) e = cudaStreamSynchronize(c->stream);  // SPHBI_DEBUG_SYNC=1: name the failing kernel
   if (e != cudaSuccess) return fail(SPHBI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return SPHBI_OK;
 }
@@ -1888,9 +1890,11 @@ struct PairTest {  // d(p, closed triangle) < h, the exact predicate's verdict
 
 __device__ __forceinline__ int cell_coord(double v, double o, double cell, int n) {
   const double f = floor((v - o) / cell);
-  int c = f < 0.0 ? 0 : (f >= (double)(n - 1) ? n - 1 : (int)f);
+  // written so that a NaN lands in cell 0 (never an out-of-range index)
+  int c = !(f >= 0.0) ? 0 : (f >= (double)(n - 1) ? n - 1 : (int)f);
   return c;
 }
+constexpr unsigned kFlagBadParticle = 16u;  // dflags[1]: a non-finite particle coordinate
 
 // bounding box of particles and triangle vertices: per-block partials
 __global__ void k_bbox(int64_t n_pts, const double* __restrict__ pxy, int64_t n_tri_pts,
@@ -1924,10 +1928,13 @@ __global__ void k_bbox(int64_t n_pts, const double* __restrict__ pxy, int64_t n_
 }
 
 __global__ void k_tri_cell_count(int64_t n_tris, const double* __restrict__ tri, Grid g,
-                                 unsigned* __restrict__ count) {
+                                 unsigned* __restrict__ count, unsigned* __restrict__ flags) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n_tris) return;
   const double* v = tri + 6 * t;
+  // (fmin / fmax drop NaNs: the bounding box alone would not show one)
+  if (!isfinite(v[0]) || !isfinite(v[1]) || !isfinite(v[2]) || !isfinite(v[3]) || !isfinite(v[4]) || !isfinite(v[5]))
+    atomicOr(flags, kFlagBadParticle);
   const double mnx = fmin(v[0], fmin(v[2], v[4])) - g.pad, mxx = fmax(v[0], fmax(v[2], v[4])) + g.pad;
   const double mny = fmin(v[1], fmin(v[3], v[5])) - g.pad, mxy = fmax(v[1], fmax(v[3], v[5])) + g.pad;
   const int cx0 = cell_coord(mnx, g.x0, g.cell, g.nx), cx1 = cell_coord(mxx, g.x0, g.cell, g.nx);
@@ -1976,11 +1983,14 @@ __global__ void k_cell_start(int64_t n_entries, const unsigned* __restrict__ key
   for (long long c = prev + 1; c <= cur; ++c) cell_start[c] = static_cast<unsigned long long>(k);
 }
 
-__global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid g, unsigned* __restrict__ cell) {
+__global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid g, unsigned* __restrict__ cell,
+                                unsigned* __restrict__ flags) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int cx = cell_coord(pxy[2 * i], g.x0, g.cell, g.nx);
-  const int cy = cell_coord(pxy[2 * i + 1], g.y0, g.cell, g.ny);
+  const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+  if (!isfinite(p.x) || !isfinite(p.y)) atomicOr(flags, kFlagBadParticle);  // reported as INVALID_ARGUMENT
+  const int cx = cell_coord(p.x, g.x0, g.cell, g.nx);
+  const int cy = cell_coord(p.y, g.y0, g.cell, g.ny);
   cell[i] = static_cast<unsigned>(cy * g.nx + cx);
 }
 // Sparse scenes (few cells hold triangles, e.g. a boundary strip around a
@@ -1989,10 +1999,12 @@ __global__ void k_particle_cell(int64_t n, const double* __restrict__ pxy, Grid 
 // particles are walked, in index order (no particle sort).
 __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy, Grid g,
                                        const unsigned long long* __restrict__ cell_start, unsigned* __restrict__ cell,
-                                       unsigned char* __restrict__ active, unsigned long long* __restrict__ count) {
+                                       unsigned char* __restrict__ active, unsigned long long* __restrict__ count,
+                                       unsigned* __restrict__ flags) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double2 p = __ldg(reinterpret_cast<const double2*>(pxy) + i);
+  if (!isfinite(p.x) || !isfinite(p.y)) atomicOr(flags, kFlagBadParticle);
   const int cx = cell_coord(p.x, g.x0, g.cell, g.nx);
   const int cy = cell_coord(p.y, g.y0, g.cell, g.ny);
   const unsigned c = static_cast<unsigned>(cy * g.nx + cx);
@@ -3145,6 +3157,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
     }
     if (const char* fp = std::getenv("SPHBI_FP64_PIECES"); fp && fp[0] == '1') c->fp64_pieces = true;
     if (const char* ff = std::getenv("SPHBI_FIND"); ff && *ff) c->no_tile_find = std::string(ff) != "tile";
+    if (const char* ds = std::getenv("SPHBI_DEBUG_SYNC"); ds && ds[0] == '1') c->debug_sync = true;
     if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
       const std::string v(pm);
       if (v == "dd") c->precision = SPHBI_PRECISION_DD;
@@ -3745,7 +3758,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     unsigned long long* toff;
     if ((st = scratch_t(c, kBufTriCount, n_triangles + 1, &tcount)) != SPHBI_OK) return st;
     if ((st = scratch_t(c, kBufTriOffset, n_triangles + 1, &toff)) != SPHBI_OK) return st;
-    k_tri_cell_count<<<grid_for(n_triangles, 256), 256, 0, s>>>(n_triangles, dt, g, tcount);
+    k_tri_cell_count<<<grid_for(n_triangles, 256), 256, 0, s>>>(n_triangles, dt, g, tcount, dflags + 1);
     if ((st = check_launch(c, "k_tri_cell_count")) != SPHBI_OK) return st;
     SPHBI_CUDA_TRY(cudaMemsetAsync(tcount + n_triangles, 0, 4, s));
     {
@@ -3758,8 +3771,11 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     }
     unsigned long long n_entries = 0;
     SPHBI_CUDA_TRY(cudaMemcpyAsync(&n_entries, toff + n_triangles, 8, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     tl_mark("cell-list entry count");
+    if (c->h_flags[1] & kFlagBadParticle)
+      return fail(SPHBI_ERR_INVALID_ARGUMENT, "non-finite particle or vertex coordinates");
     if (n_entries >= (1ull << 31)) return fail(SPHBI_ERR_OUT_OF_MEMORY, "cell list exceeds 2^31 entries");
     unsigned *ka, *kb;
     int *va, *vb;
@@ -3806,7 +3822,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPartOrder, n_particles + 2, &sorder)) != SPHBI_OK) return st;
       dactive_n = sorder + n_particles;
       k_particle_cell_active<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, cell_start, pcell, act,
-                                                                        pcount);
+                                                                        pcount, dflags + 1);
       if ((st = check_launch(c, "k_particle_cell_active")) != SPHBI_OK) return st;
       size_t tmp = 0;
       cub::CountingInputIterator<int> ids(0);
@@ -3839,7 +3855,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPartOrder, n_particles, &sorder)) != SPHBI_OK) return st;
       int bits = 1;
       while ((1ll << bits) < ncells) ++bits;
-      k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell);
+      k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell, dflags + 1);
       k_iota<<<grid_for(n_particles, 256), 256, 0, s>>>((int)n_particles, piota);
       if ((st = check_launch(c, "k_particle_cell", 2)) != SPHBI_OK) return st;
       size_t tmp = 0;
@@ -3885,9 +3901,11 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // the pairs need more than one evaluation chunk (chunk boundaries)
     unsigned long long* htot = reinterpret_cast<unsigned long long*>(c->h_flags + 32);
     SPHBI_CUDA_TRY(cudaMemcpyAsync(htot, poff + n_particles, 8, cudaMemcpyDeviceToHost, s));
-    if (row_limit > 0) SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
+    SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags + 1, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
     SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
     tl_mark("pair counts scanned");
+    if (c->h_flags[1] & kFlagBadParticle)  // (the grid is sized from the mesh alone: particles are checked here)
+      return fail(SPHBI_ERR_INVALID_ARGUMENT, "non-finite particle or vertex coordinates");
     total_pairs = static_cast<int64_t>(*htot);
     c->fp64_now = row_limit > 0 && !(c->h_flags[1] & kFlagLongRow);
     if (counts_out) {  // sphbi_pair_counts: the count pass only

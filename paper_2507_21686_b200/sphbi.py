@@ -303,7 +303,18 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: int | None):
-        _raise(self.lib.sphbi_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)))
+        """Run this context's work on a caller's CUDA stream (its handle as an
+        int), so that it is ordered with the caller's copies and kernels on that
+        stream. None restores the context's own stream. A handle of 0 is the
+        legacy default stream -- what torch.cuda.current_stream().cuda_stream
+        returns unless a stream was set -- and is passed on as cudaStreamLegacy:
+        the C-ABI reads NULL as "own stream", which would leave the calls
+        unordered with work the caller queued on the default stream."""
+        if stream_ptr is None:
+            handle = 0
+        else:
+            handle = int(stream_ptr) or 1  # cudaStreamLegacy
+        _raise(self.lib.sphbi_ctx_set_stream(self.handle, ctypes.c_void_p(handle)))
 
     def enable_counters(self, enable: bool = True):
         _raise(self.lib.sphbi_ctx_enable_counters(self.handle, 1 if enable else 0))

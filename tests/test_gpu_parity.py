@@ -270,6 +270,26 @@ def test_sparse_and_dense_pair_finders_agree(S, ctx):
     assert np.array_equal(v1, v2) and np.array_equal(g1, g2)
 
 
+def test_non_finite_coordinates_are_rejected(S, ctx):
+    """A NaN / inf particle or vertex coordinate is an InvalidArgument, not a
+    wild cell index (the grid is sized from the mesh; particles are checked
+    when they are binned)."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5(n_particles=20_000, n_discs=3, target_tris=6_000, domain=8.0)
+    k = sc.kernels[0]
+    for bad in (np.nan, np.inf):
+        P = sc.particles.copy()
+        P[1234, 1] = bad
+        with pytest.raises(S.InvalidArgument):
+            S.evaluate(P, sc.h, sc.triangles, table_of(S, k), ctx=ctx)
+        T = sc.triangles.copy()
+        T[17, 3] = bad
+        with pytest.raises(S.InvalidArgument):
+            S.evaluate(sc.particles, sc.h, T, table_of(S, k), ctx=ctx)
+    v, g, st = S.evaluate(sc.particles, sc.h, sc.triangles, table_of(S, k), ctx=ctx)  # the context is still usable
+    assert st.n_pairs > 1000 and np.isfinite(v).all()
+
+
 def test_tile_finder_matches_walk(S, ctx):
     """The cell-tile finder (SPHBI_FIND=tile: warp per cell, candidates staged in
     shared memory with cp.async, hit masks) returns the walk finder's pair list
