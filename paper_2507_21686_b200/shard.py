@@ -159,6 +159,7 @@ class ShardedScene:
 
         out = torch.zeros(max(e - b, 1), dtype=torch.int64, device=self.device)
         if e > b:
+            self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)  # ordered with `out`'s zeroing
             stats = N.Stats()
             lib = self.ctx.lib
             p = self.particles[b:e]
@@ -203,6 +204,11 @@ class ShardedScene:
         from . import _native as N
         from .sphbi import _raise
 
+        import torch
+
+        # the inputs and the all-gather buffer are torch tensors: run on torch's
+        # current stream so the call is ordered with whatever produced them
+        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         stats = N.Stats()
         desc = self.table.desc()
         lib = self.ctx.lib
