@@ -339,6 +339,11 @@ def secondary_configs(ctx, names):
             sc = scenes.subsample(scenes.cfg2(), 16384, seed=2)
             sc.pairs = None
             note = "full cell-list pairing (mode B, ~12.5k pairs per particle) on a seeded 16,384-particle subsample"
+        elif name == "cfg5cubic":
+            sc = scenes.cfg5()
+            note = ("cfg5 scene with the 2-piece cubic spline in one pass (sphbi_evaluate_piecewise: one pair search "
+                    "at h, inner piece on the pairs within h/2); pairs = pair evaluations over both pieces; CPU: the "
+                    "outer piece's pairs through the reference")
         elif name == "cfg3":
             sc = scenes.cfg3()
             note = "1M particles, boundary strip: pair finding dominates"
@@ -346,7 +351,11 @@ def secondary_configs(ctx, names):
             sc = scenes.cfg4()
             note = "4M particles, P3 (cubic) field, degree-12 kernel"
         k = sc.kernels[0]
-        r = BC.run_device(ctx, sc, k, sc.h, 3, pairs=pairs, repeat=repeat)
+        pieces = None
+        if name == "cfg5cubic":
+            pieces = sc.kernels[1:]
+            k = pieces[0]
+        r = BC.run_device(ctx, sc, k, sc.h, 3, pairs=pairs, repeat=repeat, pieces=pieces)
         dev_ms = r["ms_pairs"] + r["ms_eval"] + r["ms_reduce"]
         row = {"pairs": r["pairs"], "ms_device": dev_ms, "ms_pair_finding": r["ms_pairs"],
                "value": r["pairs"] / (dev_ms * 1e-3), "unit": UNIT, "kernel": k.name, "h": sc.h,
@@ -386,7 +395,7 @@ def main():
     ap.add_argument("--balance", default="pairs", choices=["pairs", "count"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--configs", default="cfg1,cfg2a,cfg2b,cfg3,cfg4",
+    ap.add_argument("--configs", default="cfg1,cfg2a,cfg2b,cfg3,cfg4,cfg5cubic",
                     help="secondary BASELINE.json configs measured in the same run at N = 1 ('' for none)")
     args = ap.parse_args()
     if args.impl == "ours":

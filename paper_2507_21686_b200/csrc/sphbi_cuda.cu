@@ -2720,9 +2720,11 @@ sphbi_status run_pipeline(sphbi_ctx* c, const KernelConsts& K, double h, const S
   const bool f1 = mode == 0 && src.vals == nullptr;
   if (f1 && c->fp64_now && !c->fp64_pieces) {
     // FP64 constant-field path: the whole pair in one kernel (edge form)
-    // the degrees of the named kernels (Wendland C2 / C4) are compiled in
+    // the degrees of the named kernels (cubic spline pieces, Wendland C2 / C4) are compiled in
     if (K.deg == 5)
       k_edge_pairs_f<Src, 5><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
+    else if (K.deg == 3)
+      k_edge_pairs_f<Src, 3><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
     else if (K.deg == 8)
       k_edge_pairs_f<Src, 8><<<grid_for(n, 128), 128, 0, c->stream>>>(K, src, n, h, stride, dout);
     else
