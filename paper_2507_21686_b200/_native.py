@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
-LIB_PATH = LIB_DIR / "libsphbi_cuda.so"
+# SPHBI_LIB: a variant build of the same library (tools/build_variant.sh; code-shape sweeps)
+LIB_PATH = Path(os.environ["SPHBI_LIB"]) if os.environ.get("SPHBI_LIB") else LIB_DIR / "libsphbi_cuda.so"
 
 MAX_COEFFICIENTS = 17
 NUM_COUNTERS = 19

@@ -81,8 +81,11 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
+#ifndef SPHBI_MINB_FIND
+#define SPHBI_MINB_FIND 4
+#endif
 #ifndef SPHBI_MINB_EDGE
-#define SPHBI_MINB_EDGE 6
+#define SPHBI_MINB_EDGE 7
 #endif
 #ifndef SPHBI_MINB_STUBF
 #define SPHBI_MINB_STUBF 6
@@ -2144,7 +2147,7 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
   }
 }
 
-__global__ void __launch_bounds__(kFindBlock)
+__global__ void __launch_bounds__(kFindBlock, SPHBI_MINB_FIND)
     k_find_pairs(int64_t count, const int* __restrict__ order, int p0, const double* __restrict__ pxy,
                  const unsigned* __restrict__ pcell, const unsigned long long* __restrict__ cell_start,
                  const int* __restrict__ cell_tris, const double* __restrict__ tri, double h2, int fill,
