@@ -201,6 +201,7 @@ struct sphbi_ctx {
   cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  int upload_groups = 3;        // SPHBI_UPLOAD_GROUPS: sort + count groups behind the particle upload (host-memory path)
   bool debug_sync = false;      // SPHBI_DEBUG_SYNC=1: synchronise after every launch (diagnosis)
   bool no_tile_find = true;     // SPHBI_FIND=tile selects the cell-tile finder (k_find_tile); default: lane-per-particle walk (measured faster on cfg5: 9.7 vs 10.6 ms)
   bool no_sparse_find = false;  // SPHBI_NO_SPARSE_FIND=1: always walk all particles in cell order
@@ -3163,6 +3164,7 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
     if (const char* fp = std::getenv("SPHBI_FP64_PIECES"); fp && fp[0] == '1') c->fp64_pieces = true;
     if (const char* ff = std::getenv("SPHBI_FIND"); ff && *ff) c->no_tile_find = std::string(ff) != "tile";
     if (const char* ds = std::getenv("SPHBI_DEBUG_SYNC"); ds && ds[0] == '1') c->debug_sync = true;
+    if (const char* ug = std::getenv("SPHBI_UPLOAD_GROUPS"); ug && *ug) c->upload_groups = std::max(1, std::atoi(ug));
     if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
       const std::string v(pm);
       if (v == "dd") c->precision = SPHBI_PRECISION_DD;
@@ -3846,13 +3848,15 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     const unsigned long long rl = row_limit > 0 ? static_cast<unsigned long long>(row_limit) : 0ull;
     int* stage = nullptr;  // staged hits (short lists): the fill is a compaction
     uint4* pmask = nullptr;  // cell-tile finder: 96-bit hit masks, the fill expands them
+    bool counted = false;  // the count pass already ran (per upload group)
     if (!sparse) {
       // particles in cell order (the finder walks them so: neighbouring lanes
-      // share cell lists). One global sort once every particle is on the
-      // device: sorting and counting each upload chunk as it arrives was
-      // measured slower (a chunk of randomly ordered particles has ~2 per cell,
-      // the lanes' candidate loads stop sharing cache lines: count 5.5 -> 10 ms).
-      if ((st = wait_uploads(s)) != SPHBI_OK) return st;
+      // share cell lists). With the particle upload in flight the particles are
+      // sorted and counted in a few groups (default 3, SPHBI_UPLOAD_GROUPS), so
+      // each group's sort + count pass runs behind the next group's copy (cfg5
+      // e2e 25.6 -> 23.0 ms). Finer groups were measured slower than they hide: a group of randomly
+      // ordered particles has n_group / n_cells per cell, the lanes' candidate
+      // loads stop sharing cache lines (eight groups: count 5.5 -> 10 ms).
       unsigned* pcell_sorted;
       int* piota;
       if ((st = scratch_t(c, kBufKeysA, n_particles, &pcell_sorted)) != SPHBI_OK) return st;
@@ -3860,19 +3864,43 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPartOrder, n_particles, &sorder)) != SPHBI_OK) return st;
       int bits = 1;
       while ((1ll << bits) < ncells) ++bits;
-      k_particle_cell<<<grid_for(n_particles, 256), 256, 0, s>>>(n_particles, dp, g, pcell, dflags + 1);
-      k_iota<<<grid_for(n_particles, 256), 256, 0, s>>>((int)n_particles, piota);
-      if ((st = check_launch(c, "k_particle_cell", 2)) != SPHBI_OK) return st;
+      const bool grouped = up_chunks >= 4 && !tile && c->upload_groups > 1;
+      const int ngroups = grouped ? std::min(c->upload_groups, up_chunks) : 1;
+      if (!grouped && (st = wait_uploads(s)) != SPHBI_OK) return st;
+      if (grouped && !wpp &&
+          (st = scratch_t(c, kBufStage, static_cast<size_t>(np) * kFindStage, &stage)) != SPHBI_OK)
+        return st;
       size_t tmp = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
       void* dtmp;
       if ((st = scratch(c, kBufCubTemp2, tmp, &dtmp)) != SPHBI_OK) return st;
-      cub::DeviceRadixSort::SortPairs(dtmp, tmp, pcell, pcell_sorted, piota, sorder, (int)n_particles, 0, bits, s);
-      if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
+      for (int gi = 0; gi < ngroups; ++gi) {
+        // group gi: upload chunks [k0, k1) = particles [p0, p0 + cnt)
+        const int k0 = grouped ? gi * up_chunks / ngroups : 0, k1 = grouped ? (gi + 1) * up_chunks / ngroups : 1;
+        const int64_t p0 = grouped ? k0 * up_chunk : 0;
+        const int64_t cnt = grouped ? std::min<int64_t>(k1 * up_chunk, n_particles) - p0 : n_particles;
+        if (grouped) SPHBI_CUDA_TRY(cudaStreamWaitEvent(s, c->sev[0][k1 - 1], 0));
+        k_particle_cell<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, dp + 2 * p0, g, pcell + p0, dflags + 1);
+        k_iota<<<grid_for(cnt, 256), 256, 0, s>>>((int)cnt, piota + p0, (int)p0);
+        if ((st = check_launch(c, "k_particle_cell", 2)) != SPHBI_OK) return st;
+        size_t t2 = tmp;
+        cub::DeviceRadixSort::SortPairs(dtmp, t2, pcell + p0, pcell_sorted + p0, piota + p0, sorder + p0, (int)cnt, 0,
+                                        bits, s);
+        if ((st = check_launch(c, "radix sort particle cells")) != SPHBI_OK) return st;
+        if (grouped) {
+          const int cgrid = wpp ? static_cast<int>((cnt * 32 + kFindBlock - 1) / kFindBlock) : find_grid(cnt);
+          k_find_pairs<<<cgrid, kFindBlock, 0, s>>>(cnt, sorder + p0, 0, dp, pcell, cell_start, vb, dt, h2, 0, pcount,
+                                                    0, nullptr, nullptr, nullptr, wpp, stage, rl, dflags + 1);
+          if ((st = check_launch(c, "k_find_pairs(count)")) != SPHBI_OK) return st;
+        }
+      }
+      counted = grouped;
     }
     const int fgrid = wpp ? static_cast<int>((static_cast<int64_t>(np) * 32 + kFindBlock - 1) / kFindBlock)
                           : (sparse ? std::min(find_grid(np), 8 * c->sms) : find_grid(np));
-    if (tile) {
+    if (counted) {
+      // per upload group above
+    } else if (tile) {
       // dense scenes: one warp per cell, candidates staged in shared memory (k_find_tile)
       unsigned long long* pstart;
       if ((st = scratch_t(c, kBufPartStart, (size_t)ncells + 1, &pstart)) != SPHBI_OK) return st;

@@ -270,6 +270,34 @@ def test_sparse_and_dense_pair_finders_agree(S, ctx):
     assert np.array_equal(v1, v2) and np.array_equal(g1, g2)
 
 
+def test_pinned_host_upload_path_is_bitwise_identical(S, ctx):
+    """sphbi_evaluate(MEM_HOST) from PINNED buffers (>= 2^22 particles) uploads
+    the mesh first and the particles in chunks on the copy stream, sorting and
+    counting them in groups behind the upload; results equal the pageable-host
+    call's bit for bit (rows and their order do not depend on the grouping)."""
+    import ctypes
+    import torch
+    from paper_2507_21686_b200 import scenes, _native as N
+    sc = scenes.cfg5(n_particles=4_500_000, n_discs=20, target_tris=80_000, domain=20.0)
+    k = sc.kernels[0]
+    tab = table_of(S, k)
+    v0, g0, st0 = S.evaluate(sc.particles, sc.h, sc.triangles, tab, ctx=ctx)
+    n, T = sc.particles.shape[0], sc.triangles.shape[0]
+    p_h = torch.from_numpy(sc.particles).pin_memory()
+    t_h = torch.from_numpy(sc.triangles).pin_memory()
+    ov = torch.empty(n, dtype=torch.float64).pin_memory()
+    og = torch.empty((n, 2), dtype=torch.float64).pin_memory()
+    desc = tab.desc()
+    vp = ctypes.c_void_p
+    for _ in range(2):
+        ov.fill_(-1.0)
+        S._raise(ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), sc.h, n, vp(p_h.data_ptr()), T,
+                                        vp(t_h.data_ptr()), None, -1, None, None, vp(ov.data_ptr()),
+                                        vp(og.data_ptr()), None, None, None, N.MEM_HOST), "evaluate")
+        assert np.array_equal(ov.numpy(), v0) and np.array_equal(og.numpy(), g0)
+    assert st0.n_pairs > 1_000_000
+
+
 def test_non_finite_coordinates_are_rejected(S, ctx):
     """A NaN / inf particle or vertex coordinate is an InvalidArgument, not a
     wild cell index (the grid is sized from the mesh; particles are checked
