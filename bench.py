@@ -52,7 +52,7 @@ UNIT = "pair-evals/s"
 PROFILES = ROOT / "profiles"
 # ncu FP64 instruction counts of the K4 kernels (tools/ncu_fp64.py); the frozen
 # first-kernel F_pair of BASELINE.md §5 stays in F_pair.json
-FP64_PROFILE = {"cfg5": PROFILES / "r02ae_fp64_cfg5.json", "cfg2a": PROFILES / "r02ae_fp64_cfg2a.json"}
+FP64_PROFILE = {"cfg5": PROFILES / "r02af_fp64_cfg5.json", "cfg2a": PROFILES / "r02af_fp64_cfg2a.json"}
 F_PAIR_FILE = PROFILES / "F_pair.json"
 
 
@@ -286,7 +286,7 @@ def run_reference(args, rank, world):
 
 def fp64_roofline(workload, pairs, k4_ms, fp64_peak):
     """Roofline of the K4 pipeline from the ncu FP64 instruction counts of the
-    same kernels (profiles/r02ae_fp64_<workload>.json): achieved = measured flops
+    same kernels (profiles/r02af_fp64_<workload>.json): achieved = measured flops
     per pair x pairs / live K4 time; also the ncu time-weighted FP64-pipe
     fraction and the BASELINE.md frozen-F_pair fraction."""
     roof = {"bound": "fp64", "peak": fp64_peak, "unit": "TFLOP/s", "kernel_ms": k4_ms,

@@ -49,3 +49,7 @@ def dev_stats():
 for name, f in (("host", host_stats), ("device", dev_stats)):
     t = timed(f)
     print(name, "total ms", t, "phases: pairs", stats.ms_pairs, "eval", stats.ms_eval, "reduce", stats.ms_reduce)
+def host_no_out():
+    S._raise(ctx.lib.sphbi_evaluate(ctx.handle, ctypes.byref(desc), sc.h, n, vp(p_h.data_ptr()), T, vp(t_h.data_ptr()), None, -1, None, None,
+                                    None, None, None, None, None, N.MEM_HOST), "evaluate")
+print("evaluate MEM_HOST without outputs ms", timed(host_no_out))
