@@ -493,6 +493,16 @@ int core_host_eval_pairs_f1(int64_t npairs, const int64_t* pp, const int64_t* pt
   for (auto& th : pool) th.join();
   return 0;
 }
+// the two FP64 edge forms on normalized, counter-clockwise vertices nv6:
+// out6 = general (explicit outside parts) then folded (winding term)
+int core_host_edge_forms(const double* coef, int ncoef, const double* nv6, double* out6) {
+  KernelConsts K;
+  if (!build_kernel_consts(coef, ncoef, 1.0, &K)) return -1;
+  const P2 v[3] = {{nv6[0], nv6[1]}, {nv6[2], nv6[3]}, {nv6[4], nv6[5]}};
+  edge_sum3f_general(K, v, out6);
+  edge_sum3f(K, v, out6 + 3);
+  return 0;
+}
 double core_host_kappa(const double* coef, int ncoef) {
   KernelConsts K;
   if (!build_kernel_consts(coef, ncoef, 1.0, &K)) return -1.0;

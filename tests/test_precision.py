@@ -85,3 +85,41 @@ def test_fp64_path_against_dd_and_reference(C, name):
     # §3.3); these reduced scenes have none above the tolerance
     assert OL.parity_ratio(sdd, want, c2, h) <= 1.0
     assert OL.parity_ratio(sf, want, c2, h) <= 1.0
+
+
+def test_folded_edge_form_equals_the_general_one(C):
+    """edge_sum3f folds the chord parts outside the disc away (winding term,
+    closed loop of unit vectors); edge_sum3f_general integrates them explicitly.
+    Same integral: random triangles in every position relative to the disc
+    (enclosing it, inside it, crossing, missing), a vertex 1e-12 from the
+    particle, the particle exactly on a vertex / an edge line (the general
+    terms of the folded form)."""
+    C.core_host_edge_forms.argtypes = [P, ctypes.c_int, P, P]
+    rng = np.random.default_rng(99)
+    coef = OL.arr(list(scenes.wendland_c4().coefficients))
+    worst = 0.0
+    n_deg = 0
+    for it in range(20000):
+        scale = 10.0 ** rng.uniform(-1.5, 1.2)
+        nv = rng.uniform(-1.0, 1.0, (3, 2)) * scale + rng.uniform(-1.0, 1.0, 2) * rng.choice([0.0, 1.0, 3.0])
+        kind = it % 8
+        if kind == 1:
+            nv[1] = rng.uniform(-1e-12, 1e-12, 2)       # a vertex next to the particle
+        elif kind == 2:
+            nv[2] = 0.0                                  # the particle on a vertex
+        elif kind == 3:
+            t = rng.uniform(0.1, 0.9)
+            nv[1] = -nv[0] * t / (1.0 - t)               # the particle on the line of edge 0-1
+        area = (nv[1, 0] - nv[0, 0]) * (nv[2, 1] - nv[0, 1]) - (nv[1, 1] - nv[0, 1]) * (nv[2, 0] - nv[0, 0])
+        if abs(area) < 1e-9 * scale * scale:
+            continue
+        if area < 0:
+            nv = nv[[0, 2, 1]]
+        out = np.zeros(6)
+        assert C.core_host_edge_forms(OL.ptr(coef), coef.shape[0], OL.ptr(OL.arr(nv)), OL.ptr(out)) == 0
+        assert np.isfinite(out).all(), (nv, out)
+        n_deg += kind in (2, 3)
+        worst = max(worst, abs(out[:3] - out[3:]).max())
+    assert n_deg > 1000
+    kappa = np.abs(coef).sum()
+    assert worst <= 8.0 * 2.0 ** -53 * kappa, worst / (2.0 ** -53 * kappa)
