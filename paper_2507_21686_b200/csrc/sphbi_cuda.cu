@@ -201,6 +201,7 @@ struct sphbi_ctx {
   cudaEvent_t count_src_ev = nullptr;  // the counts are final on the compute stream
   int64_t count_n = 0;            // pairs of the call h_counts belongs to (0: none pending)
   bool no_sig_sort = false;     // SPHBI_NO_SIG_SORT=1: emit in pair order (experiment)
+  int fp64_chunk_log2 = 0;      // SPHBI_FP64_CHUNK_LOG2: pairs per chunk on the FP64 edge path (0: 2^23 with host outputs, the per-chunk D2H overlap's grain, else 2^25)
   int upload_groups = 3;        // SPHBI_UPLOAD_GROUPS: sort + count groups behind the particle upload (host-memory path)
   bool debug_sync = false;      // SPHBI_DEBUG_SYNC=1: synchronise after every launch (diagnosis)
   bool no_tile_find = true;     // SPHBI_FIND=tile selects the cell-tile finder (k_find_tile); default: lane-per-particle walk (measured faster on cfg5: 9.7 vs 10.6 ms)
@@ -3164,6 +3165,8 @@ sphbi_status sphbi_ctx_create(int device, sphbi_ctx** out) {
     if (const char* fp = std::getenv("SPHBI_FP64_PIECES"); fp && fp[0] == '1') c->fp64_pieces = true;
     if (const char* ff = std::getenv("SPHBI_FIND"); ff && *ff) c->no_tile_find = std::string(ff) != "tile";
     if (const char* ds = std::getenv("SPHBI_DEBUG_SYNC"); ds && ds[0] == '1') c->debug_sync = true;
+    if (const char* cl = std::getenv("SPHBI_FP64_CHUNK_LOG2"); cl && *cl)
+      c->fp64_chunk_log2 = std::min(26, std::max(16, std::atoi(cl)));
     if (const char* ug = std::getenv("SPHBI_UPLOAD_GROUPS"); ug && *ug) c->upload_groups = std::max(1, std::atoi(ug));
     if (const char* pm = std::getenv("SPHBI_PRECISION"); pm && *pm) {
       const std::string v(pm);
@@ -3961,7 +3964,12 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     std::vector<long long> cb;
     // the FP64 edge kernel needs no per-pair scratch: 32 Mi-pair chunks (only
     // the per-chunk D2H overlap of the host-memory path wants chunks at all)
-    const int64_t chunk_pairs = (c->fp64_now && !c->fp64_pieces && !pieces) ? (int64_t(1) << 25) : int64_t(kMaxChunkPairs);
+    // Host outputs: 8 Mi-pair chunks -- the last chunk's download is the exposed
+    // tail (cfg5 e2e, B200: 22.9 ms with 32 Mi, 22.3 with 16 Mi, 21.75 with 8 Mi
+    // and 4 Mi; the device-resident call loses 0.1 ms per halving, so it keeps 32 Mi)
+    const int fp64_log2 = c->fp64_chunk_log2 ? c->fp64_chunk_log2 : (mem == SPHBI_MEM_HOST ? 23 : 25);
+    const int64_t chunk_pairs =
+        (c->fp64_now && !c->fp64_pieces && !pieces) ? (int64_t(1) << fp64_log2) : int64_t(kMaxChunkPairs);
     if (total_pairs > chunk_pairs) {
       const int max_chunks = static_cast<int>(std::min<int64_t>(n_particles, 2 * (total_pairs / chunk_pairs) + 8));
       long long* dbounds;
