@@ -2426,7 +2426,7 @@ __global__ void k_piece_flags(int64_t n, const int* __restrict__ pp, const int* 
   const int64_t t = pt[k];
 #pragma unroll
   for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * t + j);
-  flag[k] = pair_dist2(p.x, p.y, tv) < hj2 ? 1 : 0;
+  flag[k] = PairTest(hj2)(p.x, p.y, tv) ? 1 : 0;  // the exact predicate's verdict (FP32-classified, see PairTest)
 }
 __global__ void k_piece_gather(int64_t m, const int* __restrict__ idx, const int* __restrict__ pp,
                                const int* __restrict__ pt, int* __restrict__ qp, int* __restrict__ qt) {
@@ -3969,7 +3969,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // and 4 Mi; the device-resident call loses 0.1 ms per halving, so it keeps 32 Mi)
     const int fp64_log2 = c->fp64_chunk_log2 ? c->fp64_chunk_log2 : (mem == SPHBI_MEM_HOST ? 23 : 25);
     const int64_t chunk_pairs =
-        (c->fp64_now && !c->fp64_pieces && !pieces) ? (int64_t(1) << fp64_log2) : int64_t(kMaxChunkPairs);
+        (c->fp64_now && !c->fp64_pieces) ? (int64_t(1) << fp64_log2) : int64_t(kMaxChunkPairs);
     if (total_pairs > chunk_pairs) {
       const int max_chunks = static_cast<int>(std::min<int64_t>(n_particles, 2 * (total_pairs / chunk_pairs) + 8));
       long long* dbounds;
