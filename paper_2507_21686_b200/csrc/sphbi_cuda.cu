@@ -3579,9 +3579,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
   // basis cache, 9 per pair into the cache at pair offset `at`)
   auto eval_chunk = [&](const int* cpp, const int* cpt, int64_t cnt, double* pout, unsigned* dflags,
                         unsigned long long* ctr, int64_t at) -> sphbi_status {
+    const cudaStream_t cs = c->stream;  // the chunk's stream (the chunk loop alternates banks)
     if (bc) {
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pp + at, cpp, 4 * cnt, cudaMemcpyDeviceToDevice, s));
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pt + at, cpt, 4 * cnt, cudaMemcpyDeviceToDevice, s));
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pp + at, cpp, 4 * cnt, cudaMemcpyDeviceToDevice, cs));
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(bc->pt + at, cpt, 4 * cnt, cudaMemcpyDeviceToDevice, cs));
       const SceneSrc src{cpp, cpt, dp, dt, nullptr};
       return run_pipeline(c, K, h, src, cnt, 1, 9, bc->bases + 9 * at, dflags, ctr, nullptr);
     }
@@ -3601,29 +3602,29 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPieceFlag, cnt + 16, &flag)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPieceIdx, cnt + 1, &idx)) != SPHBI_OK) return st;
       dnum = reinterpret_cast<int*>(flag + ((cnt + 3) & ~3ll));
-      k_piece_flags<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, cpp, cpt, dp, dt, pieces->h[j] * pieces->h[j], flag);
+      k_piece_flags<<<grid_for(cnt, 256), 256, 0, cs>>>(cnt, cpp, cpt, dp, dt, pieces->h[j] * pieces->h[j], flag);
       if ((st = check_launch(c, "k_piece_flags")) != SPHBI_OK) return st;
       size_t tmp = 0;
       cub::CountingInputIterator<int> ci(0);
-      cub::DeviceSelect::Flagged(nullptr, tmp, ci, flag, idx, dnum, (int)cnt, s);
+      cub::DeviceSelect::Flagged(nullptr, tmp, ci, flag, idx, dnum, (int)cnt, cs);
       void* dtmp;
       if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
-      cub::DeviceSelect::Flagged(dtmp, tmp, ci, flag, idx, dnum, (int)cnt, s);
+      cub::DeviceSelect::Flagged(dtmp, tmp, ci, flag, idx, dnum, (int)cnt, cs);
       if ((st = check_launch(c, "select piece pairs")) != SPHBI_OK) return st;
       int m = 0;
-      SPHBI_CUDA_TRY(cudaMemcpyAsync(&m, dnum, 4, cudaMemcpyDeviceToHost, s));
-      SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
+      SPHBI_CUDA_TRY(cudaMemcpyAsync(&m, dnum, 4, cudaMemcpyDeviceToHost, cs));
+      SPHBI_CUDA_TRY(cudaStreamSynchronize(cs));
       piece_pairs += m;
       if (m == 0) continue;
       if ((st = scratch_t(c, kBufPiecePP, m, &qp)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPiecePT, m, &qt)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPieceOut, 3 * (size_t)m, &po)) != SPHBI_OK) return st;
-      k_piece_gather<<<grid_for(m, 256), 256, 0, s>>>(m, idx, cpp, cpt, qp, qt);
+      k_piece_gather<<<grid_for(m, 256), 256, 0, cs>>>(m, idx, cpp, cpt, qp, qt);
       if ((st = check_launch(c, "k_piece_gather")) != SPHBI_OK) return st;
       const SceneSrc sj{qp, qt, dp, dt, dv};
       if ((st = run_pipeline(c, pieces->K[j], pieces->h[j], sj, m, 0, 3, po, dflags, ctr, nullptr)) != SPHBI_OK)
         return st;
-      k_piece_add<<<grid_for(m, 256), 256, 0, s>>>(m, idx, po, pout);
+      k_piece_add<<<grid_for(m, 256), 256, 0, cs>>>(m, idx, po, pout);
       if ((st = check_launch(c, "k_piece_add")) != SPHBI_OK) return st;
     }
     return SPHBI_OK;
@@ -4013,7 +4014,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     // scratch bank, so one chunk's latency-bound geometry pass and kernel
     // tails overlap the next chunk's FP64-bound piece kernels (the e2e
     // streamed path does the same, evaluate_streamed).
-    const int nbanks = (!cb.empty() && !bc && !pieces && !pair_list_out)
+    const int nbanks = (!cb.empty() && !bc && !pair_list_out)
                            ? std::max(1, std::min(c->stream_banks, static_cast<int>(sphbi_ctx::kBanks)))
                            : 1;
     cudaStream_t cs2[sphbi_ctx::kBanks] = {s, c->aux[0], c->aux[1]};
