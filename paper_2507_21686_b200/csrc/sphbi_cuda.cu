@@ -1364,14 +1364,9 @@ __global__ void __launch_bounds__(128)
 // result is bitwise independent of the triangle's vertex order), same
 // degenerate-triangle rule (integrate_normalized :640 / hat planes :255-269).
 // ---------------------------------------------------------------------------
-template <class Src, int NT>
-__global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
-    k_edge_pairs_f(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h, int stride,
-                   double* __restrict__ out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double qx, qy, t6[6];
-  src.load_geom(k, qx, qy, t6);
+template <int NT>
+__device__ __forceinline__ void edge_pair_f(const KernelConsts& K, double qx, double qy, const double* t6, double h,
+                                            double* o) {
   // canonicalize (lexicographic lead vertex, then counter-clockwise:
   // triangle_integrator.hpp:680-694) and normalize, in registers. The
   // orientation is read off the normalized triangle's signed area, which also
@@ -1400,13 +1395,50 @@ __global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
   const double area = signed_area(n0, n1, n2);  // exact negation under a swap of n1, n2: the order is well defined
   const bool cw = area < 0.0;
   const P2 nv[3] = {n0, cw ? n2 : n1, cw ? n1 : n2};
-  double o[4] = {0.0, 0.0, 0.0, 0.0};
+  o[0] = o[1] = o[2] = o[3] = 0.0;
   if (!(fabs(area) < kGeomEps)) {
     double raw[3];
     edge_sum3f<NT>(K, nv, raw);
     finalize(raw, K.c2, h, o);
   }
+}
+template <class Src, int NT>
+__global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
+    k_edge_pairs_f(const __grid_constant__ KernelConsts K, Src src, int64_t n, double h, int stride,
+                   double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6];
+  src.load_geom(k, qx, qy, t6);
+  double o[4];
+  edge_pair_f<NT>(K, qx, qy, t6, h, o);
   for (int q = 0; q < stride; ++q) out[stride * k + q] = o[q];
+}
+
+// An inner piece of a piecewise kernel on the FP64 edge path: thread k takes
+// the k-th selected pair of the chunk (idx: DeviceSelect's output, *dcount of
+// them: the grid is sized for the chunk, surplus blocks leave), evaluates it
+// with the piece's kernel and support and adds to the pair's result. No
+// gathered pair list, no separate add pass, no host round trip for the count
+// (total: the call's inner-piece evaluations, for the statistics).
+template <int NT>
+__global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
+    k_edge_piece_add_f(const __grid_constant__ KernelConsts K, SceneSrc src, const int* __restrict__ idx,
+                       const int* __restrict__ dcount, double h, double* __restrict__ pair_out3,
+                       unsigned long long* __restrict__ total) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int m = *dcount;
+  if (k == 0) atomicAdd(total, static_cast<unsigned long long>(m));
+  if (k >= m) return;
+  const int64_t j = idx[k];
+  double qx, qy, t6[6];
+  src.load_geom(j, qx, qy, t6);
+  double o[4];
+  edge_pair_f<NT>(K, qx, qy, t6, h, o);
+  double* q = pair_out3 + 3 * j;
+  q[0] += o[0];
+  q[1] += o[1];
+  q[2] += o[2];
 }
 
 // combine, vertex-basis mode: per pair and vertex i (original order) the
@@ -3611,6 +3643,23 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
       cub::DeviceSelect::Flagged(dtmp, tmp, ci, flag, idx, dnum, (int)cnt, cs);
       if ((st = check_launch(c, "select piece pairs")) != SPHBI_OK) return st;
+      if (!dv && c->fp64_now && !c->fp64_pieces && !c->force_exact && !c->two_pass) {
+        // FP64 edge path: the selected pairs are evaluated and added in place
+        const KernelConsts& Kj = pieces->K[j];
+        const SceneSrc sj{cpp, cpt, dp, dt, nullptr};
+        unsigned long long* tot = reinterpret_cast<unsigned long long*>(dflags + 4);
+        const int pgrid = grid_for(cnt, 128);
+        if (Kj.deg == 5)
+          k_edge_piece_add_f<5><<<pgrid, 128, 0, cs>>>(Kj, sj, idx, dnum, pieces->h[j], pout, tot);
+        else if (Kj.deg == 3)
+          k_edge_piece_add_f<3><<<pgrid, 128, 0, cs>>>(Kj, sj, idx, dnum, pieces->h[j], pout, tot);
+        else if (Kj.deg == 8)
+          k_edge_piece_add_f<8><<<pgrid, 128, 0, cs>>>(Kj, sj, idx, dnum, pieces->h[j], pout, tot);
+        else
+          k_edge_piece_add_f<-1><<<pgrid, 128, 0, cs>>>(Kj, sj, idx, dnum, pieces->h[j], pout, tot);
+        if ((st = check_launch(c, "k_edge_piece_add_f")) != SPHBI_OK) return st;
+        continue;
+      }
       int m = 0;
       SPHBI_CUDA_TRY(cudaMemcpyAsync(&m, dnum, 4, cudaMemcpyDeviceToHost, cs));
       SPHBI_CUDA_TRY(cudaStreamSynchronize(cs));
@@ -4150,9 +4199,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
     if (out_value) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_value, dov, 8 * n_particles, cudaMemcpyDeviceToHost, s));
     if (out_grad) SPHBI_CUDA_TRY(cudaMemcpyAsync(out_grad, dog, 16 * n_particles, cudaMemcpyDeviceToHost, s));
   }
-  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 8, cudaMemcpyDeviceToHost, s));
+  SPHBI_CUDA_TRY(cudaMemcpyAsync(c->h_flags, dflags, 32, cudaMemcpyDeviceToHost, s));
   SPHBI_CUDA_TRY(cudaStreamSynchronize(s));
   tl_mark("done");
+  piece_pairs += static_cast<int64_t>(*reinterpret_cast<const unsigned long long*>(c->h_flags + 4));  // counted on the device
   if (c->h_flags[1] & 4u) {
     c->overflowed = true;
     return SPHBI_ERR_INTERNAL;
