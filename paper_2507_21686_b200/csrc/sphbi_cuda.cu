@@ -2460,6 +2460,24 @@ __global__ void k_piece_flags(int64_t n, const int* __restrict__ pp, const int* 
   for (int j = 0; j < 6; ++j) tv[j] = __ldg(tri + 6 * t + j);
   flag[k] = PairTest(hj2)(p.x, p.y, tv) ? 1 : 0;  // the exact predicate's verdict (FP32-classified, see PairTest)
 }
+// The outer piece on the FP64 edge path with the inner piece's membership
+// flags as a by-product (two-piece kernels: the pair's geometry is in
+// registers already, so the separate flag pass over the pair list goes away).
+template <int NT>
+__global__ void __launch_bounds__(128, SPHBI_MINB_EDGE)
+    k_edge_pairs_flag_f(const __grid_constant__ KernelConsts K, SceneSrc src, int64_t n, double h, double hj2,
+                        double* __restrict__ out, unsigned char* __restrict__ flag) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double qx, qy, t6[6];
+  src.load_geom(k, qx, qy, t6);
+  flag[k] = PairTest(hj2)(qx, qy, t6) ? 1 : 0;
+  double o[4];
+  edge_pair_f<NT>(K, qx, qy, t6, h, o);
+  out[3 * k] = o[0];
+  out[3 * k + 1] = o[1];
+  out[3 * k + 2] = o[2];
+}
 __global__ void k_piece_gather(int64_t m, const int* __restrict__ idx, const int* __restrict__ pp,
                                const int* __restrict__ pt, int* __restrict__ qp, int* __restrict__ qt) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -3624,7 +3642,26 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       return run_pipeline(c, K, h, src, cnt, 3, 3, pout, dflags, ctr, nullptr, &job);
     }
     const SceneSrc src{cpp, cpt, dp, dt, dv};
-    if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) return st;
+    // two pieces on the FP64 edge path: the outer piece's kernel also flags the inner piece's pairs
+    const bool edge_pieces = pieces && !dv && c->fp64_now && !c->fp64_pieces && !c->force_exact && !c->two_pass;
+    const bool flag_fused = edge_pieces && pieces->n == 2 && cnt > 0;
+    unsigned char* flag0 = nullptr;
+    if (flag_fused) {
+      if ((st = scratch_t(c, kBufPieceFlag, cnt + 16, &flag0)) != SPHBI_OK) return st;
+      const double hj2 = pieces->h[1] * pieces->h[1];
+      const int g0 = grid_for(cnt, 128);
+      if (K.deg == 5)
+        k_edge_pairs_flag_f<5><<<g0, 128, 0, cs>>>(K, src, cnt, h, hj2, pout, flag0);
+      else if (K.deg == 3)
+        k_edge_pairs_flag_f<3><<<g0, 128, 0, cs>>>(K, src, cnt, h, hj2, pout, flag0);
+      else if (K.deg == 8)
+        k_edge_pairs_flag_f<8><<<g0, 128, 0, cs>>>(K, src, cnt, h, hj2, pout, flag0);
+      else
+        k_edge_pairs_flag_f<-1><<<g0, 128, 0, cs>>>(K, src, cnt, h, hj2, pout, flag0);
+      if ((st = check_launch(c, "k_edge_pairs_flag_f")) != SPHBI_OK) return st;
+    } else if ((st = run_pipeline(c, K, h, src, cnt, 0, 3, pout, dflags, ctr, nullptr)) != SPHBI_OK) {
+      return st;
+    }
     // inner pieces: the subset of the chunk's pairs within h_j, one pipeline
     // run each, added per pair (outer + inner) before the per-particle sums
     for (int j = 1; pieces && j < pieces->n; ++j) {
@@ -3634,8 +3671,10 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch_t(c, kBufPieceFlag, cnt + 16, &flag)) != SPHBI_OK) return st;
       if ((st = scratch_t(c, kBufPieceIdx, cnt + 1, &idx)) != SPHBI_OK) return st;
       dnum = reinterpret_cast<int*>(flag + ((cnt + 3) & ~3ll));
-      k_piece_flags<<<grid_for(cnt, 256), 256, 0, cs>>>(cnt, cpp, cpt, dp, dt, pieces->h[j] * pieces->h[j], flag);
-      if ((st = check_launch(c, "k_piece_flags")) != SPHBI_OK) return st;
+      if (!flag_fused) {
+        k_piece_flags<<<grid_for(cnt, 256), 256, 0, cs>>>(cnt, cpp, cpt, dp, dt, pieces->h[j] * pieces->h[j], flag);
+        if ((st = check_launch(c, "k_piece_flags")) != SPHBI_OK) return st;
+      }
       size_t tmp = 0;
       cub::CountingInputIterator<int> ci(0);
       cub::DeviceSelect::Flagged(nullptr, tmp, ci, flag, idx, dnum, (int)cnt, cs);
@@ -3643,7 +3682,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       if ((st = scratch(c, kBufCubTemp, tmp, &dtmp)) != SPHBI_OK) return st;
       cub::DeviceSelect::Flagged(dtmp, tmp, ci, flag, idx, dnum, (int)cnt, cs);
       if ((st = check_launch(c, "select piece pairs")) != SPHBI_OK) return st;
-      if (!dv && c->fp64_now && !c->fp64_pieces && !c->force_exact && !c->two_pass) {
+      if (edge_pieces) {
         // FP64 edge path: the selected pairs are evaluated and added in place
         const KernelConsts& Kj = pieces->K[j];
         const SceneSrc sj{cpp, cpt, dp, dt, nullptr};

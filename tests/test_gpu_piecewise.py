@@ -76,6 +76,34 @@ def test_cubic_spline_one_pass_cfg5_reduced(S, O):
     assert OL.parity_ratio(got, np.concatenate([tv[:, None], tg], axis=1), ks[0].normalization, sc.h) <= 1.0
 
 
+def test_cubic_spline_many_chunks_on_two_streams_is_bitwise_identical(S, monkeypatch):
+    """The chunked form of the one-pass path (chunks of 2^16 pairs alternating
+    between the two compute streams, the inner piece evaluated and added in place
+    per chunk, its pairs counted on the device) against the single-chunk call;
+    device-resident and host-memory outputs use different default chunk sizes."""
+    from paper_2507_21686_b200 import scenes
+    sc = scenes.cfg5(n_particles=60_000, n_discs=6, target_tris=20_000, domain=12.0)
+    pcs = pieces_of(S, sc.kernels[1:])
+    v0, g0, st0 = S.evaluate_piecewise(sc.particles, sc.h, sc.triangles, pcs)
+    assert st0.status_bits == 0
+    monkeypatch.setenv("SPHBI_FP64_CHUNK_LOG2", "16")
+    ctx = S.Context(0)
+    monkeypatch.delenv("SPHBI_FP64_CHUNK_LOG2")
+    try:
+        assert st0.n_pairs > 4 * (1 << 16)  # several chunks
+        v1, g1, st1 = S.evaluate_piecewise(sc.particles, sc.h, sc.triangles, pcs, ctx=ctx)
+        assert st1.n_pairs == st0.n_pairs and st1.status_bits == 0
+        assert np.array_equal(v0, v1) and np.array_equal(g0, g1)
+        # single kernel through the same chunking
+        k = sc.kernels[0]
+        a0, b0, s0 = S.evaluate(sc.particles, sc.h, sc.triangles, tab(S, k))
+        a1, b1, s1 = S.evaluate(sc.particles, sc.h, sc.triangles, tab(S, k), ctx=ctx)
+        assert s0.n_pairs == s1.n_pairs
+        assert np.array_equal(a0, a1) and np.array_equal(b0, b1)
+    finally:
+        ctx.close()
+
+
 def test_piecewise_explicit_pairs_and_single_piece(S, O):
     """Explicit (unsorted, own-triangle) pairs; a single piece equals evaluate()."""
     from paper_2507_21686_b200 import scenes
