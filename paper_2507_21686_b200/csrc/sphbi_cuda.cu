@@ -2249,15 +2249,39 @@ __global__ void __launch_bounds__(256)
     ce = cell_start[c + 1];
   }
   unsigned todo = __ballot_sync(0xffffffffu, valid && n > 0 && staged);
+  // four rows per step: their staging reads (two per row: kFindStage = 64 slots)
+  // are all in flight before the first store (one row per step left the copy
+  // latency-bound: IPC 0.63)
+  static_assert(kFindStage <= 64, "two lane passes cover a staged row");
   while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const int qi = __shfl_sync(0xffffffffu, i, src);
-    const unsigned long long qo = __shfl_sync(0xffffffffu, o, src);
-    const int qn = static_cast<int>(__shfl_sync(0xffffffffu, n, src));
-    for (int l = lane; l < qn; l += 32) {
-      pp[qo + l] = qi;
-      pt[qo + l] = stage[static_cast<int64_t>(qi) * kFindStage + l];
+    int qi[4], qn[4], v0[4], v1[4];
+    unsigned long long qo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int src = todo ? __ffs(todo) - 1 : 0;
+      const bool have = todo != 0;
+      todo &= todo - 1;
+      qi[u] = __shfl_sync(0xffffffffu, i, src);
+      qo[u] = __shfl_sync(0xffffffffu, o, src);
+      const int rn = static_cast<int>(__shfl_sync(0xffffffffu, n, src));
+      qn[u] = have ? rn : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int* row = stage + static_cast<int64_t>(qi[u]) * kFindStage;
+      v0[u] = lane < qn[u] ? row[lane] : 0;
+      v1[u] = lane + 32 < qn[u] ? row[lane + 32] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (lane < qn[u]) {
+        pp[qo[u] + lane] = qi[u];
+        pt[qo[u] + lane] = v0[u];
+      }
+      if (lane + 32 < qn[u]) {
+        pp[qo[u] + lane + 32] = qi[u];
+        pt[qo[u] + lane + 32] = v1[u];
+      }
     }
   }
   // rows with more hits than slots, or from a long cell list (walked by the
