@@ -81,6 +81,9 @@ constexpr int kEvalBlock = 128;
 #ifndef SPHBI_MINB_STUB
 #define SPHBI_MINB_STUB 5
 #endif
+#ifndef SPHBI_COMPACT_ROWS
+#define SPHBI_COMPACT_ROWS 4
+#endif
 #ifndef SPHBI_MINB_FIND
 #define SPHBI_MINB_FIND 4
 #endif
@@ -2067,6 +2070,7 @@ __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy
 // Either way a particle's pairs come out in ascending triangle id (stably
 // sorted cell lists) -- the CPU finder's list.
 constexpr int kFindBlock = 256;
+constexpr int kCompactRows = SPHBI_COMPACT_ROWS;  // staged rows per step of the fill (k_stage_compact)
 constexpr unsigned long long kFindLaneMax = 128;
 constexpr int kFindStage = 64;  // staged hits per particle (see find_group); cfg5's interior rows hold ~27 pairs, up to ~45
 __device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
@@ -2249,15 +2253,15 @@ __global__ void __launch_bounds__(256)
     ce = cell_start[c + 1];
   }
   unsigned todo = __ballot_sync(0xffffffffu, valid && n > 0 && staged);
-  // four rows per step: their staging reads (two per row: kFindStage = 64 slots)
+  // kCompactRows rows per step: their staging reads (two per row: kFindStage = 64 slots)
   // are all in flight before the first store (one row per step left the copy
   // latency-bound: IPC 0.63)
   static_assert(kFindStage <= 64, "two lane passes cover a staged row");
   while (todo) {
-    int qi[4], qn[4], v0[4], v1[4];
-    unsigned long long qo[4];
+    int qi[kCompactRows], qn[kCompactRows], v0[kCompactRows], v1[kCompactRows];
+    unsigned long long qo[kCompactRows];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCompactRows; ++u) {
       const int src = todo ? __ffs(todo) - 1 : 0;
       const bool have = todo != 0;
       todo &= todo - 1;
@@ -2267,13 +2271,13 @@ __global__ void __launch_bounds__(256)
       qn[u] = have ? rn : 0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCompactRows; ++u) {
       const int* row = stage + static_cast<int64_t>(qi[u]) * kFindStage;
       v0[u] = lane < qn[u] ? row[lane] : 0;
       v1[u] = lane + 32 < qn[u] ? row[lane + 32] : 0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCompactRows; ++u) {
       if (lane < qn[u]) {
         pp[qo[u] + lane] = qi[u];
         pt[qo[u] + lane] = v0[u];
