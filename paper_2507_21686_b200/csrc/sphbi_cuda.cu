@@ -2530,28 +2530,38 @@ __global__ void k_piece_add(int64_t m, const int* __restrict__ idx, const double
 // to the host. out[2k] = p_k, out[2k + 1] = off[p_k]; *nchunks = K.
 __global__ void k_chunk_bounds(int np, const unsigned long long* __restrict__ off, unsigned long long budget,
                                int max_chunks, long long* __restrict__ out, int* __restrict__ nchunks) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  // one warp; each boundary by a 32-ary search over the (non-decreasing) offsets:
+  // five dependent rounds of loads per boundary instead of a binary search's 24
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   int p0 = 0, k = 0;
-  out[0] = 0;
-  out[1] = static_cast<long long>(off[0]);
+  if (lane == 0) {
+    out[0] = 0;
+    out[1] = static_cast<long long>(off[0]);
+  }
   while (p0 < np && k < max_chunks) {
     const unsigned long long lim = off[p0] + budget;
-    int lo = p0 + 1, hi = np;  // largest p in [p0 + 1, np] with off[p] <= lim (else p0 + 1)
-    if (off[lo] > lim) {
-      hi = lo;
-    } else {
-      while (lo < hi) {
-        const int mid = lo + (hi - lo + 1) / 2;
-        if (off[mid] <= lim) lo = mid; else hi = mid - 1;
+    long long lo = p0 + 1, hi = np;  // largest p in [p0 + 1, np] with off[p] <= lim (else p0 + 1)
+    if (off[lo] <= lim) {
+      while (hi > lo) {
+        // probes lo < q_0 <= ... <= q_31 = hi; off[q] <= lim holds for a prefix of the lanes
+        const long long span = hi - lo;
+        const long long q = lo + (span * (lane + 1) + 31) / 32;
+        const int c = __popc(__ballot_sync(0xffffffffu, off[q] <= lim));
+        const long long nlo = c ? lo + (span * c + 31) / 32 : lo;
+        const long long nhi = c < 32 ? lo + (span * (c + 1) + 31) / 32 - 1 : hi;
+        lo = nlo;
+        hi = nhi;
       }
-      hi = lo;
     }
-    p0 = hi;
+    p0 = static_cast<int>(lo);
     ++k;
-    out[2 * k] = p0;
-    out[2 * k + 1] = static_cast<long long>(off[p0]);
+    if (lane == 0) {
+      out[2 * k] = p0;
+      out[2 * k + 1] = static_cast<long long>(off[p0]);
+    }
   }
-  *nchunks = p0 < np ? -1 : k;
+  if (lane == 0) *nchunks = p0 < np ? -1 : k;
 }
 // row pointers of a particle-sorted pair list: per pair (dense rows) or per
 // row by binary search (sparse rows)
@@ -4092,7 +4102,7 @@ static sphbi_status evaluate_impl(sphbi_ctx* c, const sphbi_kernel_desc* kernel,
       long long* dbounds;
       if ((st = scratch_t(c, kBufGeneric0, 2 * (size_t)max_chunks + 4, &dbounds)) != SPHBI_OK) return st;
       int* dn = reinterpret_cast<int*>(dbounds + 2 * max_chunks + 2);
-      k_chunk_bounds<<<1, 1, 0, s>>>(static_cast<int>(n_particles), poff, static_cast<unsigned long long>(chunk_pairs),
+      k_chunk_bounds<<<1, 32, 0, s>>>(static_cast<int>(n_particles), poff, static_cast<unsigned long long>(chunk_pairs),
                                      max_chunks, dbounds, dn);
       if ((st = check_launch(c, "k_chunk_bounds")) != SPHBI_OK) return st;
       int nch = 0;
