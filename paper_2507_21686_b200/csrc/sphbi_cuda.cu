@@ -2072,7 +2072,14 @@ __global__ void k_particle_cell_active(int64_t n, const double* __restrict__ pxy
 constexpr int kFindBlock = 256;
 constexpr int kCompactRows = SPHBI_COMPACT_ROWS;  // staged rows per step of the fill (k_stage_compact)
 constexpr unsigned long long kFindLaneMax = 128;
-constexpr int kFindStage = 64;  // staged hits per particle (see find_group); cfg5's interior rows hold ~27 pairs, up to ~45
+#ifndef SPHBI_FIND_STAGE
+#define SPHBI_FIND_STAGE 64
+#endif
+#ifndef SPHBI_FIND_SMEM_SLOTS
+#define SPHBI_FIND_SMEM_SLOTS 32
+#endif
+constexpr int kFindSmemSlots = SPHBI_FIND_SMEM_SLOTS;  // hits per particle collected in shared memory by the count pass
+constexpr int kFindStage = SPHBI_FIND_STAGE;  // staged hits per particle (see find_group); cfg5's interior rows hold ~27 pairs, up to ~45
 __device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
   const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
   const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -2131,7 +2138,7 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
                                            double h2, int fill, unsigned long long* __restrict__ count_or_offset,
                                            long long base, int* __restrict__ pp, int* __restrict__ pt, int lane,
                                            int* __restrict__ stage, unsigned long long row_limit,
-                                           unsigned* __restrict__ row_flag) {
+                                           unsigned* __restrict__ row_flag, int* sw = nullptr) {
   const bool valid = pos < count;
   int i = 0;
   double px = 0.0, py = 0.0;
@@ -2147,6 +2154,7 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
     if (fill) o = count_or_offset[i] - base;
   }
   // short lists: one lane per particle
+  int ns = 0;  // this lane's hits held in the warp's shared-memory rows
   if (valid && e - b <= kFindLaneMax) {
     unsigned long long n = 0;
     for (unsigned long long k = b; k < e; ++k) {
@@ -2157,8 +2165,11 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
         if (fill) {
           pp[o + n] = i;
           pt[o + n] = t;
-        } else if (stage && n < kFindStage) {
-          stage[static_cast<int64_t>(i) * kFindStage + n] = t;
+        } else if (stage) {
+          if (sw && n < kFindSmemSlots)
+            sw[static_cast<int>(n) * 33 + lane] = t;  // slot-major, stride 33: conflict-free flush below
+          else if (n < kFindStage)
+            stage[static_cast<int64_t>(i) * kFindStage + n] = t;
         }
         ++n;
       }
@@ -2167,6 +2178,21 @@ __device__ __forceinline__ void find_group(int64_t pos, int64_t count, const int
       count_or_offset[i] = n;
       if (row_limit && n > row_limit) atomicOr(row_flag, 8u);  // a row too long for the FP64 path
     }
+    ns = static_cast<int>(n < kFindSmemSlots ? n : kFindSmemSlots);
+  }
+  // the warp's shared-memory rows go to the staging area row by row: lane l
+  // writes the row's l-th hit, whole sectors (a lane writing its own row hit by
+  // hit cost the count pass 1.2 of its 4.4 ms on cfg5: 14 sectors per store
+  // request, partial-sector writes read back from DRAM)
+  if (!fill && stage && sw) {
+    __syncwarp();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int nr = __shfl_sync(0xffffffffu, ns, r);
+      const int ir = __shfl_sync(0xffffffffu, i, r);
+      if (lane < nr) stage[static_cast<int64_t>(ir) * kFindStage + lane] = sw[lane * 33 + r];
+    }
+    __syncwarp();
   }
   // long lists: the whole warp per particle
   unsigned todo = __ballot_sync(0xffffffffu, valid && e - b > kFindLaneMax);
@@ -2216,10 +2242,12 @@ __global__ void __launch_bounds__(kFindBlock, SPHBI_MINB_FIND)
   // grid-stride over groups of 32 list positions: the sparse path's list
   // length is known only on the device, so its grid is capped (a grid sized
   // for every particle was mostly empty blocks)
+  __shared__ int s_hits[kFindBlock / 32][kFindSmemSlots * 33];
+  int* sw = s_hits[threadIdx.x >> 5];
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t pos0 = pos; (pos0 & ~31ll) < count; pos0 += stride) {
     find_group(pos0, count, order, p0, pxy, pcell, cell_start, cell_tris, tri, h2, fill, count_or_offset, base, pp,
-               pt, lane, stage, row_limit, row_flag);
+               pt, lane, stage, row_limit, row_flag, sw);
   }
 }
 
