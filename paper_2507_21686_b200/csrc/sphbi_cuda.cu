@@ -2076,9 +2076,10 @@ constexpr unsigned long long kFindLaneMax = 128;
 #define SPHBI_FIND_STAGE 64
 #endif
 #ifndef SPHBI_FIND_SMEM_SLOTS
-#define SPHBI_FIND_SMEM_SLOTS 32
+#define SPHBI_FIND_SMEM_SLOTS 20  // cfg5: 8: 6.75 ms, 12: 6.65, 16: 6.59, 20: 6.55, 24: 6.56, 32: 6.84 (shared memory taken from L1)
 #endif
 constexpr int kFindSmemSlots = SPHBI_FIND_SMEM_SLOTS;  // hits per particle collected in shared memory by the count pass
+static_assert(kFindSmemSlots >= 1 && kFindSmemSlots <= 32, "one lane per shared-memory slot in the flush");
 constexpr int kFindStage = SPHBI_FIND_STAGE;  // staged hits per particle (see find_group); cfg5's interior rows hold ~27 pairs, up to ~45
 __device__ __forceinline__ void load_tri6(const double* __restrict__ tri, int t, double* tv) {
   const double2* q = reinterpret_cast<const double2*>(tri + 6 * static_cast<int64_t>(t));
